@@ -1,0 +1,364 @@
+// fft.cuh — FP32 complex FFT building blocks for sm_100a.
+//
+// Replaces the reference's RadixTwoRealFft (roomsim/fft.hpp:57-169) on the
+// device.  Design:
+//   * a real transform of size N is a complex transform of size M = N/2 of
+//     the packed signal z[k] = x[2k] + i x[2k+1] (the reference's packing,
+//     fft.hpp:51-56, :92), plus a pairing pass over (k, M-k);
+//   * the complex transform is a Stockham autosort FFT: every pass reads R
+//     strided elements per butterfly from shared memory into registers,
+//     applies twiddles, runs an in-register radix-R DFT (R <= 16) and writes
+//     the autosorted result back, so input and output are both in natural
+//     order and no bit-reversal pass exists;
+//   * shared-memory index i is stored at PAD(i) = i + i/16 so the stride-R
+//     writes of the first passes are bank-conflict free;
+//   * twiddles come from FP64-accurate tables (rounded once to FP32).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rsg {
+
+// ---- complex helpers ---------------------------------------------------------
+__device__ __forceinline__ float2 c_add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ float2 c_mulc(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ float2 c_conj(float2 a) { return make_float2(a.x, -a.y); }
+__device__ __forceinline__ float2 c_scale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+// multiply by -i (forward) or +i (inverse)
+template <bool INV>
+__device__ __forceinline__ float2 c_rot(float2 a) {
+  return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
+}
+// multiply by exp(-+ i pi/4) (forward -, inverse +)
+template <bool INV>
+__device__ __forceinline__ float2 c_w8(float2 a) {
+  const float c = 0.70710678118654752f;
+  return INV ? make_float2(c * (a.x - a.y), c * (a.x + a.y)) : make_float2(c * (a.x + a.y), c * (a.y - a.x));
+}
+// multiply by exp(-+ 3 i pi/4)
+template <bool INV>
+__device__ __forceinline__ float2 c_w83(float2 a) {
+  const float c = 0.70710678118654752f;
+  return INV ? make_float2(-c * (a.x + a.y), c * (a.x - a.y)) : make_float2(c * (a.y - a.x), -c * (a.x + a.y));
+}
+
+// ---- in-register DFTs, natural order in and out -----------------------------
+template <int R, bool INV>
+struct Dft;
+
+template <bool INV>
+struct Dft<1, INV> {
+  __device__ __forceinline__ static void run(float2*) {}
+};
+
+template <bool INV>
+struct Dft<2, INV> {
+  __device__ __forceinline__ static void run(float2* v) {
+    const float2 a = v[0], b = v[1];
+    v[0] = c_add(a, b);
+    v[1] = c_sub(a, b);
+  }
+};
+
+template <bool INV>
+struct Dft<4, INV> {
+  __device__ __forceinline__ static void run(float2* v) {
+    const float2 t0 = c_add(v[0], v[2]), t1 = c_sub(v[0], v[2]);
+    const float2 t2 = c_add(v[1], v[3]), t3 = c_rot<INV>(c_sub(v[1], v[3]));
+    v[0] = c_add(t0, t2);
+    v[2] = c_sub(t0, t2);
+    v[1] = c_add(t1, t3);
+    v[3] = c_sub(t1, t3);
+  }
+};
+
+template <bool INV>
+struct Dft<8, INV> {
+  // 8 = 4 (inner, over n1 with n = 2 n1 + n2) x 2 (outer).
+  __device__ __forceinline__ static void run(float2* v) {
+    float2 e[4] = {v[0], v[2], v[4], v[6]};
+    float2 o[4] = {v[1], v[3], v[5], v[7]};
+    Dft<4, INV>::run(e);
+    Dft<4, INV>::run(o);
+    o[1] = c_w8<INV>(o[1]);
+    o[2] = c_rot<INV>(o[2]);
+    o[3] = c_w83<INV>(o[3]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = c_add(e[k], o[k]);
+      v[k + 4] = c_sub(e[k], o[k]);
+    }
+  }
+};
+
+template <bool INV>
+struct Dft<16, INV> {
+  // 16 = 4 x 4: n = 4 n1 + n2, k = k1 + 4 k2.
+  __device__ __forceinline__ static void run(float2* v) {
+    float2 y[4][4];
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) {
+#pragma unroll
+      for (int n1 = 0; n1 < 4; ++n1) y[n2][n1] = v[4 * n1 + n2];
+      Dft<4, INV>::run(y[n2]);
+    }
+    // twiddles W16^(n2 k1)
+    const float c1 = 0.92387953251128674f, s1 = 0.38268343236508978f;
+    const float2 w1 = make_float2(c1, INV ? s1 : -s1);
+    const float2 w3 = make_float2(s1, INV ? c1 : -c1);
+    y[1][1] = c_mul(y[1][1], w1);
+    y[1][2] = c_w8<INV>(y[1][2]);
+    y[1][3] = c_mul(y[1][3], w3);
+    y[2][1] = c_w8<INV>(y[2][1]);
+    y[2][2] = c_rot<INV>(y[2][2]);
+    y[2][3] = c_w83<INV>(y[2][3]);
+    y[3][1] = c_mul(y[3][1], w3);
+    y[3][2] = c_w83<INV>(y[3][2]);
+    // W16^9 = -W16^1
+    y[3][3] = c_mul(y[3][3], make_float2(-w1.x, -w1.y));
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      float2 z[4] = {y[0][k1], y[1][k1], y[2][k1], y[3][k1]};
+      Dft<4, INV>::run(z);
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = z[k2];
+    }
+  }
+};
+
+// ---- compile-time plan of an M-point complex FFT ----------------------------
+__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
+
+template <int M>
+struct Plan {
+  static constexpr int LOG = ilog2(M);
+  // complex elements per thread: whole transform for M < 16, else 16 (32 for
+  // the two largest sizes so that T <= 512 threads keeps 128 registers).
+  static constexpr int E = M < 16 ? M : (M >= 8192 ? 32 : 16);
+  static constexpr int T = M / E;                          // threads per transform
+  static constexpr int NP = LOG == 0 ? 1 : (LOG + 3) / 4;  // Stockham passes
+  static constexpr int PADDED = M + M / 16;                // smem float2 slots per transform
+  __host__ __device__ static constexpr int radix(int p) {
+    return p < NP - 1 ? 16 : (1 << (LOG - 4 * (NP - 1)));
+  }
+  __host__ __device__ static constexpr int ns(int p) { return p == 0 ? 1 : ns(p - 1) * radix(p - 1); }
+  // offset (in float2) of pass p's twiddle table: tables of passes 1..p-1 precede it
+  __host__ __device__ static constexpr int tw_off(int p) {
+    return p <= 1 ? 0 : tw_off(p - 1) + ns(p - 1) * radix(p - 1);
+  }
+  // total pass-twiddle table size, then the pairing table W^k, k in [0, M/2]
+  static constexpr int TW_PASS = NP >= 2 ? tw_off(NP) : 0;
+  static constexpr int TW_TOTAL = TW_PASS + M / 2 + 1;
+};
+
+__host__ __device__ __forceinline__ constexpr int PAD(int i) { return i + (i >> 4); }
+
+// smem slot of element base + r*STEP.  When STEP is a multiple of 16 the
+// padding distributes over the sum, so every r is a compile-time offset from
+// one base register (no per-element address arithmetic).
+template <int STEP>
+__device__ __forceinline__ float2& slot(float2* s, int base, int r) {
+  if constexpr (STEP % 16 == 0)
+    return s[PAD(base) + r * PAD(STEP)];
+  else
+    return s[PAD(base + r * STEP)];
+}
+
+// Twiddle load that the compiler may not hoist out of the round loop (keeps
+// register pressure bounded for the large transforms).
+__device__ __forceinline__ float2 ld_tw(const float2* p) {
+  float2 v;
+  asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+
+#ifndef RSG_TW_LOAD
+#define RSG_TW_LOAD(p) ld_tw(p)
+#endif
+
+// One Stockham pass (p > 0) of a transform stored in smem `s`, executed by the
+// T threads of a group (t = thread index within the group).  The caller
+// synchronises before the pass; the pass synchronises between its reads and
+// writes (in-place) and after its writes.
+//
+// Thread t runs butterflies j = t + q*T (q < NB).  All smem and twiddle
+// addresses are one base register per pass plus compile-time offsets:
+//   read   slot(j + r*STRIDE)            = PAD(t) + q*PAD(T) + r*PAD(STRIDE)
+//   write  slot((j-k)*R + k + r*NS), k = j mod NS, which is either the same k
+//          for every q (NS | T) or k = j (NS >= M/R, the last pass).
+template <int M, int P, bool INV>
+__device__ __forceinline__ void stockham_pass(float2* s, int t, const float2* __restrict__ tw,
+                                              bool active) {
+  using PL = Plan<M>;
+  constexpr int R = PL::radix(P), NS = PL::ns(P), T = PL::T, NB = PL::E / R, STRIDE = M / R;
+  static_assert(NB == 1 || T % NS == 0 || NS >= STRIDE, "unsupported pass shape");
+  constexpr bool LIN = (NB == 1) || (T % 16 == 0);  // padding distributes over q*T
+  constexpr bool SAME_K = (NB == 1) || (T % NS == 0);
+  float2 v[NB][R];
+  const int kt = t % NS;  // k of butterfly q = 0
+  if (active) {
+    const float2* sr = s + PAD(t);
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if constexpr (STRIDE % 16 == 0 && LIN)
+          v[q][r] = sr[q * PAD(T) + r * PAD(STRIDE)];
+        else
+          v[q][r] = s[PAD(t + q * T + r * STRIDE)];
+      }
+      if constexpr (NS > 1) {
+        const float2* w = tw + PL::tw_off(P) + (SAME_K ? kt : t) * R + (SAME_K ? 0 : q * T * R);
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          const float2 wr = RSG_TW_LOAD(w + r);
+          v[q][r] = INV ? c_mulc(v[q][r], wr) : c_mul(v[q][r], wr);
+        }
+      }
+      Dft<R, INV>::run(v[q]);
+    }
+  }
+  __syncthreads();
+  if (active) {
+    if constexpr (NS == 1 && R == 16 && NB == 1) {
+      float2* sw = s + 17 * t;  // PAD(16 t + r) = 17 t + r
+#pragma unroll
+      for (int r = 0; r < R; ++r) sw[r] = v[0][r];
+    } else {
+      // base of q = 0; for q > 0 the base moves by q*T*R (same k) or q*T (k = j)
+      const int base0 = SAME_K ? (t - kt) * R + kt : t;
+      constexpr int QSTEP = SAME_K ? T * R : T;
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if constexpr (NS % 16 == 0 && QSTEP % 16 == 0 && LIN)
+            s[PAD(base0) + q * PAD(QSTEP) + r * PAD(NS)] = v[q][r];
+          else
+            s[PAD(base0 + q * QSTEP + r * NS)] = v[q][r];
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Pass 0 of a forward transform whose packed input z[c] = (x[2c], x[2c+1])
+// comes straight from global memory: x points at the block start, elements
+// at or beyond `take` are the zero padding.  Writes smem, then syncs.
+template <int M, class Src>
+__device__ __forceinline__ void first_pass(float2* s, int t, bool active, const Src* x, int take) {
+  using PL = Plan<M>;
+  constexpr int R = PL::radix(0), T = PL::T, NB = PL::E / R, STRIDE = M / R;
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      const int j = t + q * T;
+      const Src* xb = x + 2 * j;
+      const int lim = take - 2 * j;
+      float2 v[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int off = 2 * r * STRIDE;
+        v[r].x = off < lim ? static_cast<float>(xb[off]) : 0.f;
+        v[r].y = off + 1 < lim ? static_cast<float>(xb[off + 1]) : 0.f;
+      }
+      Dft<R, false>::run(v);
+      if constexpr (R == 16) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) s[17 * j + r] = v[r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) s[PAD(j * R + r)] = v[r];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Remaining forward passes 1..NP-1.
+template <int M, int P = 1>
+__device__ __forceinline__ void forward_rest(float2* s, int t, const float2* tw, bool active) {
+  if constexpr (P < Plan<M>::NP) {
+    stockham_pass<M, P, false>(s, t, tw, active);
+    forward_rest<M, P + 1>(s, t, tw, active);
+  }
+}
+
+// All inverse passes 0..NP-1 from smem to smem (unnormalised, conj twiddles).
+template <int M, int P = 0>
+__device__ __forceinline__ void inverse_all(float2* s, int t, const float2* tw, bool active) {
+  if constexpr (P < Plan<M>::NP) {
+    stockham_pass<M, P, true>(s, t, tw, active);
+    inverse_all<M, P + 1>(s, t, tw, active);
+  }
+}
+
+// OLA spectral step for one transform held in smem (natural order Z = FFT(z)):
+// untangle the packed real spectrum (fft.hpp:152-161), multiply by the
+// pre-scaled RIR spectrum G = H / (4M) (bins 0..M), and repack for the inverse
+// (fft.hpp:104-110).  Per pair (k, M-k), with a = Z[k], b = conj(Z[M-k]):
+//   S = a + b, D = -i (a - b), X2 = S + W^k D = 2 X[k], X2m = S - W^k D = 2 conj(X[M-k])
+//   P = X2 G[k], Q = X2m conj(G[M-k]), U = P + Q, V = (P - Q) conj(W^k)
+//   Z'[k] = U + i V,  Z'[M-k] = conj(U) + i conj(V).
+// W^k = exp(-2 pi i k / N) comes from the plan's pairing table.
+template <int M>
+__device__ __forceinline__ void spectral_multiply(float2* s, int t, const float2* __restrict__ G,
+                                                  const float2* __restrict__ W, bool active) {
+  constexpr int T = Plan<M>::T;
+  if (active) {
+#pragma unroll 2
+    for (int k = 1 + t; k < M / 2; k += T) {  // k in [1, M/2)
+      const float2 a = s[PAD(k)];
+      const float2 b = c_conj(s[PAD(M - k)]);
+      const float2 w = ld_tw(W + k);
+      const float2 S = c_add(a, b);
+      const float2 D = c_rot<false>(c_sub(a, b));
+      const float2 wD = c_mul(w, D);
+      const float2 X2 = c_add(S, wD), X2m = c_sub(S, wD);
+      const float2 P = c_mul(X2, ld_tw(G + k));
+      const float2 Q = c_mulc(X2m, ld_tw(G + (M - k)));
+      const float2 U = c_add(P, Q);
+      const float2 V = c_mulc(c_sub(P, Q), w);
+      s[PAD(k)] = make_float2(U.x - V.y, U.y + V.x);
+      s[PAD(M - k)] = make_float2(U.x + V.y, V.x - U.y);
+    }
+    if (t == 0) {
+      {  // k = 0 (partner bin M of G)
+        const float2 a = s[0];
+        const float2 S = make_float2(2.f * a.x, 0.f), D = make_float2(2.f * a.y, 0.f);
+        const float2 X2 = c_add(S, D), X2m = c_sub(S, D);
+        const float2 P = c_mul(X2, ld_tw(G + 0));
+        const float2 Q = c_mulc(X2m, ld_tw(G + M));
+        const float2 U = c_add(P, Q), V = c_sub(P, Q);
+        s[0] = make_float2(U.x - V.y, U.y + V.x);
+      }
+      if (M >= 2) {  // k = M/2, its own partner
+        const int k = M / 2;
+        const float2 a = s[PAD(k)];
+        const float2 b = c_conj(a);
+        const float2 w = ld_tw(W + k);
+        const float2 S = c_add(a, b);
+        const float2 D = c_rot<false>(c_sub(a, b));
+        const float2 wD = c_mul(w, D);
+        const float2 X2 = c_add(S, wD), X2m = c_sub(S, wD);
+        const float2 g = ld_tw(G + k);
+        const float2 P = c_mul(X2, g);
+        const float2 Q = c_mulc(X2m, g);
+        const float2 U = c_add(P, Q);
+        const float2 V = c_mulc(c_sub(P, Q), w);
+        s[PAD(k)] = make_float2(U.x - V.y, U.y + V.x);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace rsg

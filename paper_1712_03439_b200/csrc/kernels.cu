@@ -1,0 +1,642 @@
+// kernels.cu — the sm_100a kernels of the room-simulation hot path.
+//
+//   K1 rir_synth_kernel     synthesize_rir        roomsim/room_model.hpp:141-174 (FP64, bit-exact)
+//   K2 rir_cut_kernel       power_threshold/cutoff_index/truncate_rir  room_model.hpp:177-213
+//   K3 rir_spectrum_kernel  the RIR transform of convolve_ola         convolution.hpp:238-239
+//   K4 ola_kernel           the OLA block loop + Σy^2                 convolution.hpp:242-253,
+//                                                                     audio_buffer.hpp:66-75
+//   K5 gain_kernel          SPEC compute_gain
+//   K6 mix_kernel           SPEC render sum
+//   rfft_*_kernel           RealFftEngine seam                        fft.hpp:38-49
+#include <cmath>
+#include <cstdio>
+
+#include "fft.cuh"
+#include "kernels.cuh"
+
+#ifndef RSG_OLA_MINB
+#define RSG_OLA_MINB 2
+#endif
+
+namespace rsg {
+
+// ============================================================================
+// K1: image-method RIR synthesis, bit-exact against the reference.
+//
+// One CTA per (pair, slice of delay bins).  The RIR slice lives in shared
+// memory as FP64.  Images are processed in enumeration order (nx -> ny -> nz,
+// room_model.hpp:118-120) in chunks of 512; every bin must receive its
+// contributions sequentially in that order (rir[delay] += amp, :170), so the
+// chunk is resolved by "owner" warps: warp o owns the bins with
+// (bin & 15) == o, walks the 16 compute warps' entries in order, and per
+// compute warp lets the first lane of each equal-delay group (match_any)
+// fold the group in lane order.  All arithmetic uses _rn intrinsics so no
+// FMA contraction can change a bit; r^g comes from the host's std::pow.
+// ============================================================================
+__global__ void __launch_bounds__(kSynthThreads) rir_synth_kernel(SynthArgs a, int slice_cap) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const SynthItem it = a.items[blockIdx.x];
+  const PairMeta& pm = a.pair[it.pair];
+  const UttMeta& um = a.utt[pm.utt];
+  const int K = um.order, W = 2 * K + 1;
+  double* bins = reinterpret_cast<double*>(sm);
+  double* ax = bins + slice_cap;      // [3][W] squared per-axis offsets
+  double* rg = ax + 3 * W;            // [3K+1]
+  double* ent_a = rg + (3 * K + 1);   // [512]
+  int* ent_d = reinterpret_cast<int*>(ent_a + kSynthThreads);  // [512]
+  unsigned* mask = reinterpret_cast<unsigned*>(ent_d + kSynthThreads);  // [16][16]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lo = it.slice_lo, len = it.slice_len;
+
+  for (int l = tid; l < len; l += kSynthThreads) bins[l] = 0.0;
+  for (int idx = tid; idx < 3 * W; idx += kSynthThreads) {
+    const int axis = idx / W, n = idx - axis * W - K;
+    const double L = um.dims[axis], s = pm.src[axis];
+    // room_model.hpp:126-127: mirrored = n even ? s : L - s; pos = n*L + mirrored
+    const double mirrored = (n % 2 == 0) ? s : __dsub_rn(L, s);
+    const double pos = __dadd_rn(__dmul_rn(static_cast<double>(n), L), mirrored);
+    const double diff = __dsub_rn(pos, pm.mic[axis]);  // room_model.hpp:37 (a - b)
+    ax[idx] = __dmul_rn(diff, diff);                    // :43 v.x * v.x
+  }
+  for (int g = tid; g <= 3 * K; g += kSynthThreads) rg[g] = a.rg[um.rg_off + g];
+  __syncthreads();
+
+  const long long V = static_cast<long long>(W) * W * W;
+  const unsigned WW = static_cast<unsigned>(W);
+  unsigned long long max_d = 0;
+  int geo = 0;
+  for (long long base = 0; base < V; base += kSynthThreads) {
+    const long long i = base + tid;
+    int rel_bin = -1;
+    double amp = 0.0;
+    if (i < V) {
+      const unsigned ui = static_cast<unsigned>(i);
+      const unsigned iz = ui % WW, t2 = ui / WW;
+      const unsigned iy = t2 % WW, ix = t2 / WW;
+      // norm: sqrt((x*x + y*y) + z*z), room_model.hpp:43
+      const double d2 = __dadd_rn(__dadd_rn(ax[ix], ax[W + iy]), ax[2 * W + iz]);
+      const double d = __dsqrt_rn(d2);
+      if (d <= 0.0) geo = 1;  // :157-158
+      const double dl = ceil(__dmul_rn(d, um.spm));  // :159-160
+      const unsigned long long D = static_cast<unsigned long long>(dl);
+      max_d = D > max_d ? D : max_d;
+      const long long rel = static_cast<long long>(D) - lo;
+      if (rel >= 0 && rel < len) {
+        const int g = abs(static_cast<int>(ix) - K) + abs(static_cast<int>(iy) - K) +
+                      abs(static_cast<int>(iz) - K);
+        amp = __ddiv_rn(rg[g], d);  // :161-162 pow(r, g) / d
+        rel_bin = static_cast<int>(rel);
+      }
+    }
+    ent_d[tid] = rel_bin;
+    ent_a[tid] = amp;
+    const int owner = rel_bin >= 0 ? (rel_bin & 15) : -1;
+#pragma unroll
+    for (int o = 0; o < 16; ++o) {
+      const unsigned m = __ballot_sync(0xffffffffu, owner == o);
+      if (lane == o) mask[warp * 16 + o] = m;
+    }
+    __syncthreads();
+    // Ordered scatter: owner warp `warp` walks compute warps 0..15 in order.
+    for (int cw = 0; cw < kSynthThreads / 32; ++cw) {
+      const unsigned m = mask[cw * 16 + warp];
+      if (m == 0u) continue;
+      if ((m >> lane) & 1u) {
+        const int b = ent_d[cw * 32 + lane];
+        const unsigned grp = __match_any_sync(m, b);
+        if (lane == __ffs(grp) - 1) {
+          double acc = bins[b];
+          unsigned gg = grp;
+          while (gg) {
+            const int src = __ffs(gg) - 1;
+            gg &= gg - 1;
+            acc = __dadd_rn(acc, ent_a[cw * 32 + src]);
+          }
+          bins[b] = acc;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  double* out = a.rir + pm.rir_off + lo;
+  for (int l = tid; l < len; l += kSynthThreads) out[l] = bins[l];
+  // max delay / geometry flag over the CTA
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, max_d, o);
+    max_d = other > max_d ? other : max_d;
+    geo |= __shfl_xor_sync(0xffffffffu, geo, o);
+  }
+  if (lane == 0) {
+    atomicMax(&a.out[it.pair].max_delay, max_d);
+    if (geo) atomicOr(&a.out[it.pair].flags, 1);
+  }
+}
+
+size_t synth_smem_bytes(int max_order, int slice) {
+  const int W = 2 * max_order + 1;
+  return sizeof(double) * (static_cast<size_t>(slice) + 3 * W + 3 * max_order + 1 + kSynthThreads) +
+         sizeof(int) * kSynthThreads + sizeof(unsigned) * 256;
+}
+
+cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice,
+                         cudaStream_t s) {
+  if (n_items == 0) return cudaSuccess;
+  const size_t smem = synth_smem_bytes(max_order, slice);
+  cudaError_t e = cudaFuncSetAttribute(rir_synth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  rir_synth_kernel<<<n_items, kSynthThreads, smem, s>>>(a, slice);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// K2: -eta dB tail cut.  One CTA per pair: exact FP64 max of h^2 and the last
+// index with h^2 >= p_th (max reductions are order independent, so the result
+// equals the reference's sequential scans bit for bit).
+// ============================================================================
+__global__ void __launch_bounds__(256) rir_cut_kernel(CutArgs a) {
+  const int p = blockIdx.x;
+  const PairMeta& pm = a.pair[p];
+  const UttMeta& um = a.utt[pm.utt];
+  PairRir& r = a.out[p];
+  __shared__ double red_d[8];
+  __shared__ long long red_i[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  long long len = static_cast<long long>(r.max_delay) + 1;
+  if (um.max_taps > 0 && um.max_taps < len) len = um.max_taps;
+  if (r.flags & 1) len = 0;
+  const double* h = a.rir + pm.rir_off;
+  if (a.eta_factor <= 0.0 || len == 0) {
+    if (tid == 0) {
+      r.len = len;
+      r.keep = len;
+      r.cutoff = -1;
+    }
+    return;
+  }
+  double mx = 0.0;
+  for (long long n = tid; n < len; n += 256) mx = fmax(mx, __dmul_rn(h[n], h[n]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red_d[warp] = mx;
+  __syncthreads();
+  mx = red_d[0];
+  for (int w = 1; w < 8; ++w) mx = fmax(mx, red_d[w]);
+  const double th = __dmul_rn(mx, a.eta_factor);  // room_model.hpp:184
+  long long last = -1;
+  for (long long n = tid; n < len; n += 256)
+    if (__dmul_rn(h[n], h[n]) >= th) last = n;  // room_model.hpp:193-195
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long other = __shfl_xor_sync(0xffffffffu, last, o);
+    last = other > last ? other : last;
+  }
+  if (lane == 0) red_i[warp] = last;
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 0; w < 8; ++w) last = red_i[w] > last ? red_i[w] : last;
+    const long long nc = last < 0 ? 0 : last;
+    r.len = len;
+    r.threshold = th;
+    r.cutoff = nc;
+    r.keep = nc + 2 < len ? nc + 2 : len;  // room_model.hpp:209
+    if (mx == 0.0) r.flags |= 2;
+  }
+}
+
+cudaError_t launch_cut(const CutArgs& a, int n_pairs, cudaStream_t s) {
+  if (n_pairs == 0) return cudaSuccess;
+  rir_cut_kernel<<<n_pairs, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// FFT sizing helpers
+// ============================================================================
+__host__ __device__ constexpr int cta_threads_of(int log2m) {
+  // T = M / E threads per transform (E = 16, or 32 for M >= 8192); >= 256 per CTA.
+  return log2m <= 4 ? 256 : (log2m >= 13 ? (1 << log2m) / 32 : ((1 << log2m) / 16 > 256 ? (1 << log2m) / 16 : 256));
+}
+int cta_threads(int log2m) { return cta_threads_of(log2m); }
+
+template <int M>
+__host__ __device__ constexpr int groups_of() {
+  return cta_threads_of(Plan<M>::LOG) / Plan<M>::T;
+}
+
+size_t ola_smem_bytes(int log2m) {
+  const int M = 1 << log2m;
+  const int E = M < 16 ? M : (M >= 8192 ? 32 : 16);
+  const int T = M / E;
+  const int G = cta_threads_of(log2m) / T;
+  return static_cast<size_t>(G) * (M + M / 16) * sizeof(float2);
+}
+
+template <int M>
+static int tw_total_t() { return Plan<M>::TW_TOTAL; }
+
+int tw_total(int log2m) {
+  switch (log2m) {
+#define RSG_CASE(L) case L: return Plan<(1 << L)>::TW_TOTAL;
+    RSG_CASE(0) RSG_CASE(1) RSG_CASE(2) RSG_CASE(3) RSG_CASE(4) RSG_CASE(5) RSG_CASE(6)
+    RSG_CASE(7) RSG_CASE(8) RSG_CASE(9) RSG_CASE(10) RSG_CASE(11) RSG_CASE(12) RSG_CASE(13)
+    RSG_CASE(14)
+#undef RSG_CASE
+  }
+  return 0;
+}
+
+template <int M>
+static void fill_twiddles_t(float2* h) {
+  using PL = Plan<M>;
+  const double pi = 3.14159265358979323846;
+  for (int p = 1; p < PL::NP; ++p) {
+    const int R = PL::radix(p), NS = PL::ns(p);
+    const long long span = static_cast<long long>(NS) * R;
+    for (int k = 0; k < NS; ++k)
+      for (int r = 0; r < R; ++r) {
+        const long long e = (static_cast<long long>(r) * k) % span;
+        const double ang = -2.0 * pi * static_cast<double>(e) / static_cast<double>(span);
+        h[PL::tw_off(p) + k * R + r] = make_float2(static_cast<float>(std::cos(ang)),
+                                                   static_cast<float>(std::sin(ang)));
+      }
+  }
+  // pairing table W^k = exp(-2 pi i k / N), N = 2M, k in [0, M/2]
+  for (int k = 0; k <= M / 2; ++k) {
+    const double ang = -2.0 * pi * static_cast<double>(k) / (2.0 * M);
+    h[PL::TW_PASS + k] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+  }
+}
+
+void fill_twiddles(int log2m, float2* host) {
+  switch (log2m) {
+#define RSG_CASE(L) case L: fill_twiddles_t<(1 << L)>(host); break;
+    RSG_CASE(0) RSG_CASE(1) RSG_CASE(2) RSG_CASE(3) RSG_CASE(4) RSG_CASE(5) RSG_CASE(6)
+    RSG_CASE(7) RSG_CASE(8) RSG_CASE(9) RSG_CASE(10) RSG_CASE(11) RSG_CASE(12) RSG_CASE(13)
+    RSG_CASE(14)
+#undef RSG_CASE
+  }
+}
+
+// W^k for k in [0, M] from the pairing table (k <= M/2 stored; W^k = -conj(W^(M-k)) above).
+template <int M>
+__device__ __forceinline__ float2 pair_twiddle(const float2* W, int k) {
+  if (k <= M / 2) return __ldg(W + k);
+  const float2 w = __ldg(W + (M - k));
+  return make_float2(-w.x, w.y);
+}
+
+// ============================================================================
+// K3: RIR spectrum.  G[k] = H[k] / (4M) for k = 0..M, H the real FFT of the
+// truncated RIR zero-padded to N (convolution.hpp:238-239; untangle as
+// fft.hpp:152-161).  The 1/(4M) folds the inverse's 1/M and the two 1/2's of
+// the untangle/repack into the filter, so K4 needs no scaling pass.
+// ============================================================================
+template <int M>
+__global__ void __launch_bounds__(cta_threads_of(Plan<M>::LOG)) rir_spectrum_kernel(SpecArgs a) {
+  using PL = Plan<M>;
+  extern __shared__ __align__(16) float2 smem[];
+  constexpr int G = groups_of<M>();
+  const int g = threadIdx.x / PL::T, t = threadIdx.x % PL::T;
+  const int item = blockIdx.x * G + g;
+  const bool active = item < a.count;
+  float2* s = smem + g * PL::PADDED;
+  const int p = active ? a.list[item] : 0;
+  const PairPlan& pl = a.plan[p];
+  const double* h = a.rir + a.pair[p].rir_off;
+  const long long nh = pl.nh;
+  first_pass<M>(s, t, active, h, static_cast<int>(nh));
+  forward_rest<M>(s, t, a.tw, active);
+  if (active) {
+    const float2* W = a.tw + PL::TW_PASS;
+    const float scale = 1.0f / (8.0f * M);
+    float2* out = a.spec + pl.spec_off;
+    for (int k = t; k <= M; k += PL::T) {
+      const float2 za = s[PAD(k & (M - 1))];
+      const float2 zb = c_conj(s[PAD((M - k) & (M - 1))]);
+      const float2 S = c_add(za, zb);
+      const float2 D = c_rot<false>(c_sub(za, zb));
+      const float2 X2 = c_add(S, c_mul(pair_twiddle<M>(W, k), D));
+      out[k] = c_scale(X2, scale);
+    }
+  }
+}
+
+// ============================================================================
+// K4: the OLA filter.  One CTA per (source, mic) pair; the CTA runs G
+// transforms of size M = N/2 at a time (G consecutive OLA blocks), each on T
+// threads: forward Stockham FFT of the packed block (loaded straight from the
+// FP32 source signal), spectral multiply with the pair's G, inverse FFT, then
+// a CTA-wide deterministic overlap-add into the pair's output (exclusive
+// ownership: no atomics, fixed summation order) and the FP64 Σy^2 of every
+// sample once it is final.  Reference: convolve_ola, convolution.hpp:219-255.
+// ============================================================================
+template <int M>
+__global__ void __launch_bounds__(cta_threads_of(Plan<M>::LOG), (M >= 8192 ? 1 : RSG_OLA_MINB)) ola_kernel(OlaArgs a) {
+  using PL = Plan<M>;
+  extern __shared__ __align__(16) float2 smem[];
+  constexpr int G = groups_of<M>();
+  constexpr int CTA = cta_threads_of(PL::LOG);
+  constexpr int N = 2 * M;
+  const int g = threadIdx.x / PL::T, t = threadIdx.x % PL::T;
+  const int p = a.list[blockIdx.x];
+  const PairPlan pl = a.plan[p];
+  const PairMeta& pm = a.pair[p];
+  const float* __restrict__ x = a.signals + pm.sig_off;
+  const long long nx = pm.nx;
+  const float2* __restrict__ Gs = a.spec + pl.spec_off;
+  const float2* W = a.tw + PL::TW_PASS;
+  float* __restrict__ y = a.y + pl.y_off;
+  const int L = static_cast<int>(pl.L);
+  const int B = static_cast<int>(pl.B);
+  const int out_len = static_cast<int>(pl.out_len);
+  float2* s = smem + g * PL::PADDED;
+  double pw = 0.0;
+
+#pragma unroll 1
+  for (int b0 = 0; b0 < B; b0 += G) {
+    const int b = b0 + g;
+    const bool active = b < B;
+    const long long start = static_cast<long long>(b) * L;
+    const long long take = active ? (nx - start < L ? nx - start : L) : 0;
+    first_pass<M>(s, t, active, x + start, static_cast<int>(take));
+    forward_rest<M>(s, t, a.tw, active);
+    spectral_multiply<M>(s, t, Gs, W, active);
+    inverse_all<M>(s, t, a.tw, active);
+    // ---- deterministic overlap-add of this round's blocks ----
+    const int nact = (B - b0) < G ? (B - b0) : G;
+    const int P0 = b0 * L;
+    const long long p1 = static_cast<long long>(b0 + nact - 1) * L + N;
+    const int P1 = p1 < out_len ? static_cast<int>(p1) : out_len;
+    const long long fl = b0 == 0 ? 0 : static_cast<long long>(b0 - 1) * L + N;
+    const long long fh = (b0 + nact == B) ? out_len : static_cast<long long>(b0 + nact) * L;
+    for (int n = P0 + static_cast<int>(threadIdx.x); n < P1; n += CTA) {
+      const int rel = n - P0;
+      int ghi = rel / L;
+      ghi = ghi < nact - 1 ? ghi : nact - 1;
+      const int glo = rel >= N ? (rel - N) / L + 1 : 0;
+      float acc = (n >= fl) ? 0.f : y[n];
+#pragma unroll 1
+      for (int gg = glo; gg <= ghi; ++gg) {
+        const int i = rel - gg * L;
+        const float2 v = smem[gg * PL::PADDED + PAD(i >> 1)];
+        acc += (i & 1) ? v.y : v.x;
+      }
+      y[n] = acc;
+      if (n < fh) pw = fma(static_cast<double>(acc), static_cast<double>(acc), pw);
+    }
+    __syncthreads();
+  }
+  // Σ y^2 over the CTA (fixed order: deterministic)
+  __shared__ double red[CTA / 32];
+  for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pw;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < CTA / 32; ++w) tot += red[w];
+    a.sumsq[p] = tot;
+  }
+}
+
+// ============================================================================
+// Seam kernels: natural-order real FFTs (RadixTwoRealFft::forward/inverse).
+// ============================================================================
+template <int M>
+__global__ void __launch_bounds__(cta_threads_of(Plan<M>::LOG))
+rfft_forward_kernel(const float* in, float2* out, int count, const float2* tw) {
+  using PL = Plan<M>;
+  extern __shared__ __align__(16) float2 smem[];
+  constexpr int G = groups_of<M>();
+  const int g = threadIdx.x / PL::T, t = threadIdx.x % PL::T;
+  const int item = blockIdx.x * G + g;
+  const bool active = item < count;
+  float2* s = smem + g * PL::PADDED;
+  const float* x = in + static_cast<long long>(active ? item : 0) * (2 * M);
+  first_pass<M>(s, t, active, x, 2 * M);
+  forward_rest<M>(s, t, tw, active);
+  if (active) {
+    const float2* W = tw + PL::TW_PASS;
+    float2* o = out + static_cast<long long>(item) * (M + 1);
+    for (int k = t; k <= M; k += PL::T) {
+      const float2 za = s[PAD(k & (M - 1))];
+      const float2 zb = c_conj(s[PAD((M - k) & (M - 1))]);
+      const float2 S = c_add(za, zb);
+      const float2 D = c_rot<false>(c_sub(za, zb));
+      o[k] = c_scale(c_add(S, c_mul(pair_twiddle<M>(W, k), D)), 0.5f);
+    }
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(cta_threads_of(Plan<M>::LOG))
+rfft_inverse_kernel(const float2* in, float* out, int count, const float2* tw) {
+  using PL = Plan<M>;
+  extern __shared__ __align__(16) float2 smem[];
+  constexpr int G = groups_of<M>();
+  const int g = threadIdx.x / PL::T, t = threadIdx.x % PL::T;
+  const int item = blockIdx.x * G + g;
+  const bool active = item < count;
+  float2* s = smem + g * PL::PADDED;
+  const float2* X = in + static_cast<long long>(active ? item : 0) * (M + 1);
+  const float2* W = tw + PL::TW_PASS;
+  if (active) {
+    // fft.hpp:104-110: Z[k] = Ye + i Yo, Ye = (X[k] + conj(X[M-k]))/2,
+    // Yo = (X[k] - conj(X[M-k]))/2 * conj(W^k)
+    for (int k = t; k < M; k += PL::T) {
+      const float2 xa = X[k], xb = c_conj(X[M - k]);
+      const float2 e = c_scale(c_add(xa, xb), 0.5f);
+      const float2 o = c_mulc(c_scale(c_sub(xa, xb), 0.5f), pair_twiddle<M>(W, k));
+      s[PAD(k)] = make_float2(e.x - o.y, e.y + o.x);
+    }
+  }
+  __syncthreads();
+  inverse_all<M>(s, t, tw, active);
+  if (active) {
+    float* o = out + static_cast<long long>(item) * (2 * M);
+    const float sc = 1.0f / M;
+    for (int k = t; k < M; k += PL::T) {
+      const float2 v = s[PAD(k)];
+      o[2 * k] = v.x * sc;
+      o[2 * k + 1] = v.y * sc;
+    }
+  }
+}
+
+// ---- dispatch over M ----------------------------------------------------------
+template <int M>
+static cudaError_t set_attrs() {
+  const int smem = static_cast<int>(ola_smem_bytes(Plan<M>::LOG));
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(ola_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(rir_spectrum_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(rfft_forward_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(rfft_inverse_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  return cudaSuccess;
+}
+
+cudaError_t kernels_init() {
+  cudaError_t e = cudaSuccess;
+#define RSG_CASE(L) if (e == cudaSuccess) e = set_attrs<(1 << L)>();
+  RSG_CASE(0) RSG_CASE(1) RSG_CASE(2) RSG_CASE(3) RSG_CASE(4) RSG_CASE(5) RSG_CASE(6)
+  RSG_CASE(7) RSG_CASE(8) RSG_CASE(9) RSG_CASE(10) RSG_CASE(11) RSG_CASE(12) RSG_CASE(13)
+  RSG_CASE(14)
+#undef RSG_CASE
+  return e;
+}
+
+template <int M>
+static cudaError_t spectrum_t(const SpecArgs& a, cudaStream_t s) {
+  constexpr int G = groups_of<M>();
+  const int grid = (a.count + G - 1) / G;
+  rir_spectrum_kernel<M><<<grid, cta_threads_of(Plan<M>::LOG), ola_smem_bytes(Plan<M>::LOG), s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int M>
+static cudaError_t ola_t(const OlaArgs& a, cudaStream_t s) {
+  ola_kernel<M><<<a.count, cta_threads_of(Plan<M>::LOG), ola_smem_bytes(Plan<M>::LOG), s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int M>
+static cudaError_t rfft_t(bool inverse, const float* in_real, const float2* in_spec,
+                          float* out_real, float2* out_spec, int count, const float2* tw,
+                          cudaStream_t s) {
+  constexpr int G = groups_of<M>();
+  const int grid = (count + G - 1) / G;
+  const size_t smem = ola_smem_bytes(Plan<M>::LOG);
+  if (inverse)
+    rfft_inverse_kernel<M><<<grid, cta_threads_of(Plan<M>::LOG), smem, s>>>(in_spec, out_real, count, tw);
+  else
+    rfft_forward_kernel<M><<<grid, cta_threads_of(Plan<M>::LOG), smem, s>>>(in_real, out_spec, count, tw);
+  return cudaGetLastError();
+}
+
+#define RSG_DISPATCH(L, CALL)                                                             \
+  switch (L) {                                                                            \
+    case 0: { constexpr int M = 1; return CALL; }                                         \
+    case 1: { constexpr int M = 2; return CALL; }                                         \
+    case 2: { constexpr int M = 4; return CALL; }                                         \
+    case 3: { constexpr int M = 8; return CALL; }                                         \
+    case 4: { constexpr int M = 16; return CALL; }                                        \
+    case 5: { constexpr int M = 32; return CALL; }                                        \
+    case 6: { constexpr int M = 64; return CALL; }                                        \
+    case 7: { constexpr int M = 128; return CALL; }                                       \
+    case 8: { constexpr int M = 256; return CALL; }                                       \
+    case 9: { constexpr int M = 512; return CALL; }                                       \
+    case 10: { constexpr int M = 1024; return CALL; }                                     \
+    case 11: { constexpr int M = 2048; return CALL; }                                     \
+    case 12: { constexpr int M = 4096; return CALL; }                                     \
+    case 13: { constexpr int M = 8192; return CALL; }                                     \
+    case 14: { constexpr int M = 16384; return CALL; }                                    \
+  }                                                                                       \
+  return cudaErrorInvalidValue;
+
+cudaError_t launch_spectrum(int log2m, const SpecArgs& a, cudaStream_t s) {
+  if (a.count == 0) return cudaSuccess;
+  RSG_DISPATCH(log2m, spectrum_t<M>(a, s))
+}
+
+cudaError_t launch_ola(int log2m, const OlaArgs& a, cudaStream_t s) {
+  if (a.count == 0) return cudaSuccess;
+  RSG_DISPATCH(log2m, ola_t<M>(a, s))
+}
+
+cudaError_t launch_rfft(int log2m, bool inverse, const float* in_real, const float2* in_spec,
+                        float* out_real, float2* out_spec, int count, const float2* tw,
+                        cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  RSG_DISPATCH(log2m, rfft_t<M>(inverse, in_real, in_spec, out_real, out_spec, count, tw, s))
+}
+
+// ============================================================================
+// K5: SNR gains.  alpha_ij = sqrt(P_0j / (P_ij 10^(snr_i/10)))
+// with P = mean_power (audio_buffer.hpp:66-75) = Σy^2 / len; alpha_0j = 1.
+// ============================================================================
+__global__ void gain_kernel(GainArgs a) {
+  const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (p >= a.n_pairs) return;
+  const PairMeta& pm = a.pair[p];
+  const long long p0 = a.utt_pair0[pm.utt] + pm.mic_local;  // target pair at mic j
+  const double P = a.sumsq[p] / static_cast<double>(a.plan[p].out_len);
+  a.power[p] = P;
+  if (pm.src_local == 0) {
+    a.gain[p] = 1.0;
+    if (!(P > 0.0)) a.flags[p] |= 4;
+    return;
+  }
+  const double Pt = a.sumsq[p0] / static_cast<double>(a.plan[p0].out_len);
+  if (!(P > 0.0) || !(Pt > 0.0)) {
+    a.flags[p] |= 4;
+    a.gain[p] = 0.0;
+    return;
+  }
+  a.gain[p] = sqrt(Pt / (P * a.snr_lin[pm.src_idx]));
+}
+
+cudaError_t launch_gain(const GainArgs& a, cudaStream_t s) {
+  if (a.n_pairs == 0) return cudaSuccess;
+  gain_kernel<<<static_cast<unsigned>((a.n_pairs + 255) / 256), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// K6: the mix y_j[n] = Σ_i alpha_ij (h_ij * x_i)[n], zero-padded, summed in
+// source order in FP64, stored FP32.
+// ============================================================================
+__global__ void __launch_bounds__(256) mix_kernel(MixArgs a) {
+  const long long ch = blockIdx.y;
+  const long long u = a.chan_utt[ch];
+  const int j = a.chan_mic[ch];
+  const long long len = a.utt_len[u];
+  const long long stride = a.utt_stride[u];
+  const long long n0 = blockIdx.x * a.tile;
+  if (n0 >= stride) return;
+  const long long n1 = n0 + a.tile < stride ? n0 + a.tile : stride;
+  const int I = a.utt_I[u], J = a.utt_J[u];
+  const long long pair0 = a.utt_pair0[u];
+  float* out = a.out + a.chan_out[ch];
+  for (long long n = n0 + threadIdx.x; n < n1; n += blockDim.x) {
+    double acc = 0.0;
+    if (n < len) {
+      for (int i = 0; i < I; ++i) {
+        const long long p = pair0 + static_cast<long long>(i) * J + j;
+        const PairPlan& pl = a.plan[p];
+        if (n < pl.out_len) acc = fma(a.gain[p], static_cast<double>(__ldg(a.y + pl.y_off + n)), acc);
+      }
+    }
+    out[n] = static_cast<float>(acc);
+  }
+}
+
+cudaError_t launch_mix(const MixArgs& a, int64_t n_chan, int64_t max_len, cudaStream_t s) {
+  if (n_chan == 0 || max_len == 0) return cudaSuccess;
+  dim3 grid(static_cast<unsigned>((max_len + a.tile - 1) / a.tile), static_cast<unsigned>(n_chan));
+  mix_kernel<<<grid, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ---- conversions -------------------------------------------------------------
+__global__ void d2f_kernel(const double* in, float* out, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<float>(in[i]);
+}
+__global__ void f2d_kernel(const float* in, double* out, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<double>(in[i]);
+}
+cudaError_t launch_convert_d2f(const double* in, float* out, int64_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int grid = static_cast<int>((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+  d2f_kernel<<<grid, 256, 0, s>>>(in, out, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_convert_f2d(const float* in, double* out, int64_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int grid = static_cast<int>((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+  f2d_kernel<<<grid, 256, 0, s>>>(in, out, n);
+  return cudaGetLastError();
+}
+
+}  // namespace rsg

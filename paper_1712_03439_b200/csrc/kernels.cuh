@@ -1,0 +1,158 @@
+// kernels.cuh — device-side data layout shared by the kernels and the host
+// orchestration (api.cu).  See DESIGN.md §"Data layout in HBM".
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rsg {
+
+// Per utterance (room) — RoomConfig (roomsim/room_model.hpp:49-72) plus the
+// host-computed constants that must match glibc bit for bit.
+struct UttMeta {
+  double dims[3];
+  double spm;        // samples_per_meter = fs / c0 (room_model.hpp:150), host FP64
+  int32_t order;     // K
+  int32_t rg_off;    // offset of the r^g table (g = 0..3K, std::pow on the host)
+  int64_t max_taps;  // horizon cap (0 = none)
+};
+
+// Per (source, mic) pair.
+struct PairMeta {
+  double src[3];
+  double mic[3];
+  int32_t utt;
+  int32_t src_idx;   // global source index (signal, snr)
+  int32_t mic_local; // j
+  int32_t src_local; // i
+  int64_t sig_off;   // offset of x_i in the signal buffer
+  int64_t nx;        // N_x
+  int64_t rir_off;   // FP64 RIR region (synth output) [rir_cap]
+  int64_t rir_cap;
+};
+
+// Per pair, produced on device by K1/K2, consumed by the planner.
+struct PairRir {
+  unsigned long long max_delay;  // K1 atomicMax over images
+  int64_t len;                   // min(max_delay + 1, horizon)
+  int64_t keep;                  // after truncate_rir
+  int64_t cutoff;                // n_c
+  double threshold;              // p_th (room_model.hpp:184)
+  int32_t flags;                 // 1: geometry error (d <= 0), 2: degenerate (all-zero)
+  int32_t pad;
+};
+
+// Per pair, written by the host planner (after K2) and consumed by K3/K4/mix.
+struct PairPlan {
+  int64_t spec_off;  // float2 offset of G (M+1 bins)
+  int64_t y_off;     // float offset of the reverberant pair signal
+  int64_t nh;        // N_h (truncated)
+  int64_t L;         // block length N - N_h + 1
+  int64_t B;         // block count
+  int64_t out_len;   // N_x + N_h - 1
+  int32_t log2n;     // N = 2^log2n
+  int32_t pad;
+};
+
+// K1 work item: one (pair, bin-slice).
+struct SynthItem {
+  int32_t pair;
+  int32_t slice_lo;  // first bin of the slice
+  int32_t slice_len; // bins in the slice
+  int32_t pad;
+};
+
+struct SynthArgs {
+  const UttMeta* utt;
+  const PairMeta* pair;
+  const double* rg;
+  const SynthItem* items;
+  double* rir;
+  PairRir* out;
+};
+
+struct CutArgs {
+  const PairMeta* pair;
+  const UttMeta* utt;
+  const double* rir;
+  PairRir* out;
+  double eta_factor;  // pow(10, -eta/10), host std::pow; <= 0: no truncation
+};
+
+struct SpecArgs {
+  const int32_t* list;  // pairs of this FFT size
+  int32_t count;
+  const PairMeta* pair;
+  const PairPlan* plan;
+  const double* rir;
+  float2* spec;
+  const float2* tw;     // twiddle tables of this M
+};
+
+struct OlaArgs {
+  const int32_t* list;
+  int32_t count;
+  const PairMeta* pair;
+  const PairPlan* plan;
+  const float* signals;
+  const float2* spec;
+  float* y;             // reverberant pair signals
+  double* sumsq;        // per pair Σ y^2 (FP64)
+  const float2* tw;
+};
+
+struct MixArgs {
+  const int64_t* chan_utt;    // per output channel: utterance
+  const int32_t* chan_mic;    // j
+  const int64_t* chan_out;    // float offset of the channel in `out`
+  const int64_t* utt_len;     // output length per utterance
+  const int64_t* utt_stride;  // channel stride per utterance (tail zero-filled)
+  const int64_t* utt_pair0;   // first pair of the utterance
+  const int32_t* utt_I;
+  const int32_t* utt_J;
+  const PairPlan* plan;
+  const float* y;
+  const double* gain;
+  float* out;
+  int64_t tile;               // samples per CTA
+};
+
+struct GainArgs {
+  const PairMeta* pair;
+  const PairPlan* plan;
+  const int64_t* utt_pair0;
+  const int32_t* utt_J;
+  const double* sumsq;
+  const double* snr_lin;      // per global source: pow(10, snr/10) (host std::pow)
+  double* gain;
+  double* power;
+  int32_t* flags;
+  int64_t n_pairs;
+};
+
+// ---- launchers (kernels.cu) --------------------------------------------------
+constexpr int kMaxLog2M = 14;  // M <= 16384  (N <= 32768) in one CTA
+int cta_threads(int log2m);
+size_t ola_smem_bytes(int log2m);
+int tw_total(int log2m);       // float2 entries of the twiddle table of 2^log2m
+void fill_twiddles(int log2m, float2* host);  // host, FP64 -> FP32
+cudaError_t kernels_init();    // smem attributes
+
+constexpr int kSynthThreads = 512;
+constexpr int kSynthSlice = 12288;  // FP64 bins per K1 CTA (96 KB)
+size_t synth_smem_bytes(int max_order, int slice);
+
+cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice,
+                         cudaStream_t s);
+cudaError_t launch_cut(const CutArgs& a, int n_pairs, cudaStream_t s);
+cudaError_t launch_spectrum(int log2m, const SpecArgs& a, cudaStream_t s);
+cudaError_t launch_ola(int log2m, const OlaArgs& a, cudaStream_t s);
+cudaError_t launch_gain(const GainArgs& a, cudaStream_t s);
+cudaError_t launch_mix(const MixArgs& a, int64_t n_chan, int64_t max_len, cudaStream_t s);
+// Seam kernels (RealFftEngine): count transforms of size 2^(log2m+1).
+cudaError_t launch_rfft(int log2m, bool inverse, const float* in_real, const float2* in_spec,
+                        float* out_real, float2* out_spec, int count, const float2* tw,
+                        cudaStream_t s);
+cudaError_t launch_convert_d2f(const double* in, float* out, int64_t n, cudaStream_t s);
+cudaError_t launch_convert_f2d(const float* in, double* out, int64_t n, cudaStream_t s);
+
+}  // namespace rsg

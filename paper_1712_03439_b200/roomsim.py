@@ -1,0 +1,408 @@
+"""Python mirror of the reference ``roomsim`` C++ API over the CUDA C-ABI.
+
+Names, argument meaning and error behaviour follow the reference headers
+(/root/reference/proj/include/roomsim/*.hpp) so parity tests read like the
+reference's own: ``synthesize_rir`` (room_model.hpp:141), ``truncate_rir``
+(:203), ``power_threshold``/``cutoff_index`` (:177/:188), ``cost_*``,
+``plan_for``, ``choose_plan`` (convolution.hpp:89-161), ``convolve_ola``
+(:219), ``convolve_full_fft`` (:182), ``convolve`` (:258), the
+``RealFftEngine`` concept (fft.hpp:38-49) as ``CudaRealFft``, and SPEC
+``render`` as ``render_batch``.  Errors raise the classes of
+roomsim/errors.hpp:22-68.
+
+Every compute call runs on the GPU through ``_lib/libroomsim_gpu.so``; there
+is no CPU fallback — importing on a machine without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libroomsim_gpu.so")
+
+DIRECT, FULL_FFT, OVERLAP_ADD = 0, 1, 2
+PLAN_CHOOSE, PLAN_FORCED, PLAN_POW2_TWICE = 0, 1, 2
+
+
+# ---- error taxonomy (roomsim/errors.hpp:22-68) --------------------------------
+class Error(RuntimeError):
+    """roomsim::Error"""
+
+
+class PlacementError(Error):
+    pass
+
+
+class GeometryError(Error):
+    pass
+
+
+class DegenerateInputError(Error):
+    pass
+
+
+class PlanError(Error):
+    pass
+
+
+class ConfigError(Error):
+    pass
+
+
+class FormatError(Error):
+    pass
+
+
+class IoError(Error):
+    pass
+
+
+class DeviceError(Error):
+    """CUDA / allocation failure (no reference analogue)."""
+
+
+class UnsupportedError(Error):
+    """Size outside what the device kernels implement."""
+
+
+_CODES = {1: PlacementError, 2: GeometryError, 3: DegenerateInputError, 4: PlanError,
+          5: ConfigError, 6: FormatError, 7: IoError, 16: DeviceError, 17: DeviceError,
+          18: UnsupportedError}
+
+
+class RsSceneBatch(C.Structure):
+    _fields_ = [
+        ("n_utt", C.c_int64), ("src_begin", C.c_void_p), ("mic_begin", C.c_void_p),
+        ("room_dims", C.c_void_p), ("reflection", C.c_void_p), ("sample_rate", C.c_void_p),
+        ("speed_of_sound", C.c_void_p), ("image_order", C.c_void_p), ("max_taps", C.c_void_p),
+        ("src_pos", C.c_void_p), ("mic_pos", C.c_void_p), ("snr_db", C.c_void_p),
+        ("sig_off", C.c_void_p), ("sig_len", C.c_void_p), ("signals", C.c_void_p),
+        ("eta_db", C.c_double), ("plan_rule", C.c_int32), ("forced_fft_size", C.c_int64),
+    ]
+
+
+LAYOUT_DTYPE = np.dtype([("rir_len", np.int64), ("rir_keep", np.int64), ("cutoff", np.int64),
+                         ("fft_size", np.int64), ("block_len", np.int64), ("n_blocks", np.int64),
+                         ("out_len", np.int64), ("strategy", np.int32), ("flags", np.int32)])
+
+# Every symbol include/roomsim_gpu.h declares (checked by tests/test_abi.py).
+ABI_SYMBOLS = [
+    "rs_last_error", "rs_version", "rs_ctx_create", "rs_ctx_destroy", "rs_ctx_set_stream",
+    "rs_ctx_synchronize", "rs_ctx_last_timing", "rs_ctx_set_profiling", "rs_cost_direct",
+    "rs_cost_full_fft", "rs_cost_ola", "rs_ola_block_count", "rs_plan_for", "rs_choose_plan",
+    "rs_rfft_forward", "rs_rfft_inverse", "rs_synthesize_rir", "rs_truncate_rir",
+    "rs_convolve_ola", "rs_convolve_full_fft", "rs_convolve", "rs_batch_num_pairs",
+    "rs_render_batch", "rs_render_batch_device", "rs_last_pair_signal", "rs_last_pair_rir",
+]
+
+_lib = None
+
+
+def load_library() -> C.CDLL:
+    """Load the CUDA library (raises if it was not built: no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built (run `make` / __graft_entry__.build())")
+    L = C.CDLL(LIB_PATH)
+    d, sz, i64, vp = C.c_double, C.c_size_t, C.c_int64, C.c_void_p
+    dp = C.POINTER(C.c_double)
+    szp = C.POINTER(C.c_size_t)
+    sig = {
+        "rs_last_error": (C.c_char_p, []),
+        "rs_version": (C.c_char_p, []),
+        "rs_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+        "rs_ctx_destroy": (C.c_int, [vp]),
+        "rs_ctx_set_stream": (C.c_int, [vp, vp]),
+        "rs_ctx_synchronize": (C.c_int, [vp]),
+        "rs_ctx_last_timing": (C.c_int, [vp, dp, dp, dp, C.POINTER(i64)]),
+        "rs_ctx_set_profiling": (C.c_int, [vp, C.c_int]),
+        "rs_cost_direct": (d, [d, d, sz, sz]),
+        "rs_cost_full_fft": (d, [d, d, sz, sz, sz]),
+        "rs_cost_ola": (d, [d, d, sz, sz, sz]),
+        "rs_ola_block_count": (sz, [sz, sz, sz]),
+        "rs_plan_for": (C.c_int, [d, d, sz, sz, C.c_int, C.POINTER(C.c_int), szp, dp]),
+        "rs_choose_plan": (C.c_int, [d, d, sz, sz, C.POINTER(C.c_int), szp, dp]),
+        "rs_rfft_forward": (C.c_int, [vp, sz, sz, vp, vp]),
+        "rs_rfft_inverse": (C.c_int, [vp, sz, sz, vp, vp]),
+        "rs_synthesize_rir": (C.c_int, [vp, vp, d, d, d, C.c_int, vp, vp, i64, vp, sz, szp]),
+        "rs_truncate_rir": (C.c_int, [vp, vp, sz, d, szp, szp, dp]),
+        "rs_convolve_ola": (C.c_int, [vp, vp, sz, vp, sz, sz, vp]),
+        "rs_convolve_full_fft": (C.c_int, [vp, vp, sz, vp, sz, vp]),
+        "rs_convolve": (C.c_int, [vp, vp, sz, vp, sz, C.c_int, sz, vp]),
+        "rs_batch_num_pairs": (i64, [vp]),
+        "rs_render_batch": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "rs_render_batch_device": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "rs_last_pair_signal": (C.c_int, [vp, i64, vp, sz, szp]),
+        "rs_last_pair_rir": (C.c_int, [vp, i64, vp, sz, szp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(st: int) -> None:
+    if st != 0:
+        msg = load_library().rs_last_error().decode()
+        raise _CODES.get(st, Error)(msg)
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+# ---- planner (host side; exact mirror of convolution.hpp) ----------------------
+@dataclass
+class ConvolutionPlan:
+    """roomsim::ConvolutionPlan (convolution.hpp:64-68)."""
+
+    strategy: int = DIRECT
+    fft_size: Optional[int] = None
+    predicted_cost: float = 0.0
+
+
+def cost_direct(I, J, nx, nh) -> float:
+    v = load_library().rs_cost_direct(I, J, nx, nh)
+    if np.isnan(v):
+        _check(5)
+    return v
+
+
+def cost_full_fft(I, J, nx, nh, n) -> float:
+    v = load_library().rs_cost_full_fft(I, J, nx, nh, n)
+    if np.isnan(v):
+        raise (PlanError if "FFT" in load_library().rs_last_error().decode() else ConfigError)(
+            load_library().rs_last_error().decode())
+    return v
+
+
+def cost_ola(I, J, nx, nh, n) -> float:
+    v = load_library().rs_cost_ola(I, J, nx, nh, n)
+    if np.isnan(v):
+        raise (PlanError if "FFT" in load_library().rs_last_error().decode() else ConfigError)(
+            load_library().rs_last_error().decode())
+    return v
+
+
+def ola_block_count(nx, nh, n) -> int:
+    return int(load_library().rs_ola_block_count(nx, nh, n))
+
+
+def plan_for(I, J, nx, nh, strategy) -> ConvolutionPlan:
+    s, n, c = C.c_int(), C.c_size_t(), C.c_double()
+    _check(load_library().rs_plan_for(I, J, nx, nh, strategy, C.byref(s), C.byref(n), C.byref(c)))
+    return ConvolutionPlan(s.value, n.value if s.value != DIRECT else None, c.value)
+
+
+def choose_plan(I, J, nx, nh) -> ConvolutionPlan:
+    s, n, c = C.c_int(), C.c_size_t(), C.c_double()
+    _check(load_library().rs_choose_plan(I, J, nx, nh, C.byref(s), C.byref(n), C.byref(c)))
+    return ConvolutionPlan(s.value, n.value if s.value != DIRECT else None, c.value)
+
+
+# ---- device context -------------------------------------------------------------
+class Context:
+    """rs_ctx: one device, one stream, one arena.  Not shareable across threads."""
+
+    def __init__(self, device: int = 0):
+        L = load_library()
+        h = C.c_void_p()
+        _check(L.rs_ctx_create(int(device), C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            load_library().rs_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_handle: int) -> None:
+        _check(load_library().rs_ctx_set_stream(self.h, C.c_void_p(stream_handle)))
+
+    def set_profiling(self, on: bool) -> None:
+        _check(load_library().rs_ctx_set_profiling(self.h, int(on)))
+
+    def synchronize(self) -> None:
+        _check(load_library().rs_ctx_synchronize(self.h))
+
+    def last_timing(self):
+        ms, fl, by = C.c_double(), C.c_double(), C.c_double()
+        n = C.c_int64()
+        _check(load_library().rs_ctx_last_timing(self.h, C.byref(ms), C.byref(fl), C.byref(by), C.byref(n)))
+        return {"ola_ms": ms.value, "ola_flops": fl.value, "alg_bytes": by.value, "launches": n.value}
+
+
+_default: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None:
+        _default = Context(0)
+    return _default
+
+
+# ---- room model ------------------------------------------------------------------
+def synthesize_rir(room, reflection, image_order, src, mic, *, sample_rate=16000.0,
+                   speed_of_sound=343.0, max_taps=0, ctx: Optional[Context] = None) -> np.ndarray:
+    """roomsim::synthesize_rir (room_model.hpp:141-174), FP64 bit-exact on device."""
+    ctx = ctx or default_context()
+    room = np.ascontiguousarray(room, np.float64)
+    src = np.ascontiguousarray(src, np.float64)
+    mic = np.ascontiguousarray(mic, np.float64)
+    ext = (abs(int(image_order)) + 2) * room
+    cap = int(np.ceil(np.sqrt((ext ** 2).sum()) * sample_rate / speed_of_sound)) + 4
+    if max_taps:
+        cap = min(cap, int(max_taps))
+    out = np.zeros(max(cap, 1))
+    n = C.c_size_t()
+    _check(load_library().rs_synthesize_rir(ctx.h, _ptr(room), float(reflection), float(sample_rate),
+                                            float(speed_of_sound), int(image_order), _ptr(src), _ptr(mic),
+                                            int(max_taps), _ptr(out), out.size, C.byref(n)))
+    return out[: n.value].copy()
+
+
+def truncate_rir(h, eta_db, ctx: Optional[Context] = None):
+    """roomsim::truncate_rir (room_model.hpp:203-213) -> (taps, n_c, p_th)."""
+    ctx = ctx or default_context()
+    h = np.ascontiguousarray(h, np.float64)
+    keep, nc, th = C.c_size_t(), C.c_size_t(), C.c_double()
+    _check(load_library().rs_truncate_rir(ctx.h, _ptr(h), h.size, float(eta_db), C.byref(keep),
+                                          C.byref(nc), C.byref(th)))
+    return h[: keep.value].copy(), nc.value, th.value
+
+
+def power_threshold(h, eta_db, ctx: Optional[Context] = None) -> float:
+    return truncate_rir(h, eta_db, ctx)[2]
+
+
+# ---- FFT engine seam (fft.hpp:38-49) ------------------------------------------------
+class CudaRealFft:
+    """RealFftEngine on the device: forward -> N/2+1 bins, inverse includes 1/N."""
+
+    def __init__(self, size: int, ctx: Optional[Context] = None):
+        if size < 2 or size & (size - 1):
+            raise PlanError("FFT size must be a power of two >= 2")
+        self._n = int(size)
+        self.ctx = ctx or default_context()
+
+    def size(self) -> int:
+        return self._n
+
+    def spectrum_size(self) -> int:
+        return self._n // 2 + 1
+
+    def forward(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.float64).reshape(-1, self._n)
+        out = np.zeros((x.shape[0], 2 * self.spectrum_size()))
+        _check(load_library().rs_rfft_forward(self.ctx.h, self._n, x.shape[0], _ptr(x), _ptr(out)))
+        res = out[:, 0::2] + 1j * out[:, 1::2]
+        return res[0] if res.shape[0] == 1 else res
+
+    def inverse(self, spec: np.ndarray) -> np.ndarray:
+        spec = np.asarray(spec, np.complex128).reshape(-1, self.spectrum_size())
+        inp = np.zeros((spec.shape[0], 2 * self.spectrum_size()))
+        inp[:, 0::2] = spec.real
+        inp[:, 1::2] = spec.imag
+        out = np.zeros((spec.shape[0], self._n))
+        _check(load_library().rs_rfft_inverse(self.ctx.h, self._n, spec.shape[0], _ptr(inp), _ptr(out)))
+        return out[0] if out.shape[0] == 1 else out
+
+
+# ---- convolution ---------------------------------------------------------------------
+def _conv(fn, x, h, *extra, ctx=None):
+    ctx = ctx or default_context()
+    x = np.ascontiguousarray(x, np.float64)
+    h = np.ascontiguousarray(h, np.float64)
+    out = np.zeros(max(x.size + h.size - 1, 1))
+    _check(fn(ctx.h, _ptr(x), x.size, _ptr(h), h.size, *extra, _ptr(out)))
+    return out[: x.size + h.size - 1]
+
+
+def convolve_ola(x, h, fft_size, ctx: Optional[Context] = None) -> np.ndarray:
+    """roomsim::convolve_ola (convolution.hpp:219-255)."""
+    return _conv(load_library().rs_convolve_ola, x, h, int(fft_size), ctx=ctx)
+
+
+def convolve_full_fft(x, h, ctx: Optional[Context] = None) -> np.ndarray:
+    """roomsim::convolve_full_fft (convolution.hpp:182-212)."""
+    return _conv(load_library().rs_convolve_full_fft, x, h, ctx=ctx)
+
+
+def convolve(x, h, plan: ConvolutionPlan, ctx: Optional[Context] = None) -> np.ndarray:
+    """roomsim::convolve (convolution.hpp:258-271)."""
+    return _conv(load_library().rs_convolve, x, h, int(plan.strategy), int(plan.fft_size or 0), ctx=ctx)
+
+
+# ---- batched render --------------------------------------------------
+@dataclass
+class RenderResult:
+    out: object               # host np.float32 array or device tensor
+    out_len: np.ndarray       # [n_utt]
+    layout: np.ndarray        # [n_pairs] LAYOUT_DTYPE
+    gains: np.ndarray         # [n_pairs] alpha_ij
+    power: np.ndarray         # [n_pairs] mean power of each reverberant pair signal
+
+
+def render_batch(batch, *, ctx: Optional[Context] = None, out: Optional[np.ndarray] = None,
+                 device_signals_ptr: Optional[int] = None, device_out_ptr: Optional[int] = None) -> RenderResult:
+    """Render a ``scenes.SceneBatch``.
+
+    Host mode (default): signals/out are host arrays, H2D/D2H inside the call.
+    Device mode: pass ``device_signals_ptr`` and ``device_out_ptr`` (e.g. torch
+    ``data_ptr()``); nothing large crosses PCIe."""
+    ctx = ctx or default_context()
+    L = load_library()
+    device = device_signals_ptr is not None
+    b, keep = batch.as_struct(RsSceneBatch, signals_ptr=device_signals_ptr)
+    out_off = np.ascontiguousarray(batch.out_off, np.int64)
+    out_stride = np.ascontiguousarray(batch.out_stride, np.int64)
+    out_len = np.zeros(batch.n_utt, np.int64)
+    layout = np.zeros(batch.n_pairs, LAYOUT_DTYPE)
+    gains = np.zeros(batch.n_pairs)
+    power = np.zeros(batch.n_pairs)
+    if device:
+        assert device_out_ptr is not None
+        st = L.rs_render_batch_device(ctx.h, C.byref(b), C.c_void_p(device_out_ptr), _ptr(out_off),
+                                      _ptr(out_stride), _ptr(out_len), _ptr(layout), _ptr(gains), _ptr(power))
+        res_out = None
+    else:
+        if out is None:
+            out = np.zeros(batch.out_total, np.float32)
+        st = L.rs_render_batch(ctx.h, C.byref(b), _ptr(out), _ptr(out_off), _ptr(out_stride),
+                               _ptr(out_len), _ptr(layout), _ptr(gains), _ptr(power))
+        res_out = out
+    del keep
+    _check(st)
+    return RenderResult(res_out, out_len, layout, gains, power)
+
+
+def last_pair_signal(pair: int, cap: int, ctx: Optional[Context] = None) -> np.ndarray:
+    ctx = ctx or default_context()
+    out = np.zeros(cap, np.float32)
+    n = C.c_size_t()
+    _check(load_library().rs_last_pair_signal(ctx.h, int(pair), _ptr(out), cap, C.byref(n)))
+    return out[: n.value]
+
+
+def last_pair_rir(pair: int, cap: int, ctx: Optional[Context] = None) -> np.ndarray:
+    ctx = ctx or default_context()
+    out = np.zeros(cap)
+    n = C.c_size_t()
+    _check(load_library().rs_last_pair_rir(ctx.h, int(pair), _ptr(out), cap, C.byref(n)))
+    return out[: n.value]

@@ -1,0 +1,293 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * RIR taps (FP64), cut indices, truncated lengths, N / L / B: bit-exact;
+  * waveforms: max|gpu - oracle| <= 1e-5 * peak|oracle| per utterance (FP32);
+  * achieved SNR within 1e-6 dB.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+WAVE_TOL = 1e-5  # relative to each utterance's peak, written per north_star
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+def rel_err(got, want):
+    return np.abs(np.asarray(got, np.float64) - want).max() / max(np.abs(want).max(), 1e-300)
+
+
+# ---- K1 / K2 ------------------------------------------------------------------------
+def test_rir_single_tap(rs, ctx):
+    h = rs.synthesize_rir([5, 5, 5], 0.5, 0, [1, 1, 1], [2, 1, 1], ctx=ctx)
+    assert h.size == 48 and h[47] == 1.0 and not h[:47].any()
+
+
+def test_rir_bitexact_random(rs, ctx, port):
+    rng = np.random.default_rng(10)
+    for t in range(60):
+        room = rng.uniform([3, 3, 2.5], [10, 8, 6])
+        src, mic = rng.uniform(0.5, room - 0.5), rng.uniform(0.5, room - 0.5)
+        k, r = int(rng.integers(0, 18)), rng.uniform(0.2, 0.95)
+        mt = int(rng.choice([0, 700, 4000, 20000]))
+        want = port.synthesize_rir(room, r, k, src, mic, max_taps=mt)
+        got = rs.synthesize_rir(room, r, k, src, mic, max_taps=mt, ctx=ctx)
+        assert got.size == want.size, t
+        assert (bits(got) == bits(want)).all(), t
+
+
+def test_rir_bitexact_long_sliced(rs, ctx, port):
+    # K large enough that the RIR exceeds one K1 slice (12288 bins)
+    room, src, mic = [4.0, 3.5, 2.8], [1.1, 2.0, 1.3], [2.9, 1.0, 1.7]
+    want = port.synthesize_rir(room, 0.9, 40, src, mic, max_taps=30000)
+    got = rs.synthesize_rir(room, 0.9, 40, src, mic, max_taps=30000, ctx=ctx)
+    assert want.size > 12288 and (bits(got) == bits(want)).all()
+
+
+def test_truncate_bitexact(rs, ctx, port):
+    rng = np.random.default_rng(11)
+    for _ in range(50):
+        n = int(rng.integers(1, 20000))
+        h = rng.random(n) * np.exp(-rng.random() * 12 * np.linspace(0, 1, n))
+        for eta in (5.0, 20.0, 60.0):
+            a = port.truncate_rir(h, eta)
+            b = rs.truncate_rir(h, eta, ctx=ctx)
+            assert (a[1], a[0].size, a[2]) == (b[1], b[0].size, b[2])
+    t, nc, _ = rs.truncate_rir(0.9 ** np.arange(60), 20, ctx=ctx)
+    assert nc == 21
+
+
+def test_errors(rs, ctx):
+    with pytest.raises(rs.PlacementError):
+        rs.synthesize_rir([5, 5, 5], 0.5, 2, [0, 1, 1], [2, 2, 2], ctx=ctx)
+    with pytest.raises(rs.ConfigError):
+        rs.synthesize_rir([5, 5, 5], 1.5, 2, [1, 1, 1], [2, 2, 2], ctx=ctx)
+    with pytest.raises(rs.GeometryError):
+        rs.synthesize_rir([5, 5, 5], 0.5, 0, [1, 1, 1], [1, 1, 1], ctx=ctx)
+    with pytest.raises(rs.PlanError):
+        rs.convolve_ola(np.ones(10), np.ones(8), 4, ctx=ctx)
+    with pytest.raises(rs.DegenerateInputError):
+        rs.convolve_ola(np.ones(0), np.ones(8), 16, ctx=ctx)
+    with pytest.raises(rs.DegenerateInputError):
+        rs.truncate_rir(np.zeros(10), 20, ctx=ctx)
+
+
+# ---- FFT seam ---------------------------------------------------------------------
+@pytest.mark.parametrize("n", [2 ** k for k in range(1, 16)])
+def test_rfft_engine(rs, ctx, port, n):
+    rng = np.random.default_rng(n)
+    eng = rs.CudaRealFft(n, ctx=ctx)
+    assert eng.spectrum_size() == n // 2 + 1
+    x = rng.standard_normal((3, n))
+    got = eng.forward(x)
+    for i in range(3):
+        want = port.rfft_forward(x[i])
+        assert np.abs(got[i] - want).max() <= 1e-5 * np.abs(want).max() + 1e-6
+    back = eng.inverse(got)
+    assert np.abs(back - x).max() <= 1e-5 * np.abs(x).max()
+    for i in range(3):
+        want = port.rfft_inverse(got[i], n)
+        assert np.abs(back[i] - want).max() <= 1e-5 * np.abs(want).max()
+
+
+# ---- K3 + K4 single pair ----------------------------------------------------------------
+def test_convolve_kats(rs, ctx):
+    np.testing.assert_allclose(rs.convolve_ola([1, 2, 3], [1], 2, ctx=ctx), [1, 2, 3], atol=1e-6)
+    np.testing.assert_allclose(rs.convolve_ola([1, 1], [1, 1], 2, ctx=ctx), [1, 2, 1], atol=1e-6)
+    np.testing.assert_allclose(rs.convolve_ola([2, 0, -1], [0.5, 0.25], 4, ctx=ctx),
+                               [1, 0.5, -0.5, -0.25], atol=1e-6)
+    np.testing.assert_allclose(rs.convolve_full_fft([1, 2, 3], [1], ctx=ctx), [1, 2, 3], atol=1e-6)
+    assert np.abs(rs.convolve_ola(np.zeros(50), np.ones(5), 8, ctx=ctx)).max() == 0
+
+
+def test_convolve_random_vs_oracle(rs, ctx, port):
+    rng = np.random.default_rng(12)
+    for _ in range(120):
+        nx, nh = int(rng.integers(1, 6000)), int(rng.integers(1, 700))
+        x, h = rng.standard_normal(nx), rng.standard_normal(nh)
+        lo = max(1, (nh - 1).bit_length())
+        n = 1 << int(rng.integers(lo, min(16, lo + 5)))
+        want = port.convolve_ola(x, h, n)
+        got = rs.convolve_ola(x, h, n, ctx=ctx)
+        assert got.size == want.size
+        assert rel_err(got, want) <= WAVE_TOL, (nx, nh, n)
+
+
+def test_ola_block_boundaries(rs, ctx, port):
+    rng = np.random.default_rng(13)
+    h = rng.standard_normal(8)
+    for nx in (9, 17, 18, 16, 1, 2, 900):
+        x = rng.standard_normal(nx)
+        assert rel_err(rs.convolve_ola(x, h, 16, ctx=ctx), port.convolve_ola(x, h, 16)) <= WAVE_TOL
+    x, h = rng.standard_normal(777), rng.standard_normal(64)
+    assert rel_err(rs.convolve_ola(x, h, 64, ctx=ctx), port.convolve_ola(x, h, 64)) <= WAVE_TOL  # L=1
+
+
+@pytest.mark.parametrize("n", [2 ** k for k in range(1, 16)])
+def test_every_fft_size(rs, ctx, port, n):
+    rng = np.random.default_rng(100 + n)
+    nh = max(1, n // 2 - 3) if n > 2 else 1
+    x, h = rng.standard_normal(5 * n + 7), rng.standard_normal(nh)
+    assert rel_err(rs.convolve_ola(x, h, n, ctx=ctx), port.convolve_ola(x, h, n)) <= WAVE_TOL
+
+
+def test_config1(rs, ctx, port):
+    from paper_1712_03439_b200 import scenes
+
+    x, h, n = scenes.config1()
+    assert rs.ola_block_count(x.size, h.size, n) == 20 and n - h.size + 1 == 4097
+    got = rs.convolve_ola(x.astype(np.float64), h, n, ctx=ctx)
+    want = port.convolve_ola(x.astype(np.float64), h, n)
+    assert rel_err(got, want) <= WAVE_TOL
+    t = ctx.last_timing()
+    assert t["launches"] >= 2
+
+
+# ---- the batched render -------------------------------------------------------------
+def _render_both(rs, ctx, port, b):
+    g = rs.render_batch(b, ctx=ctx)
+    o_out, o_len, o_lay, o_gain, o_pow = port.render_batch(b, threads=8)
+    return g, (o_out, o_len, o_lay, o_gain, o_pow)
+
+
+def _check_render(b, g, o):
+    o_out, o_len, o_lay, o_gain, o_pow = o
+    assert (g.out_len == o_len).all()
+    for f in ("rir_len", "rir_keep", "cutoff", "fft_size", "block_len", "n_blocks", "out_len"):
+        assert (g.layout[f] == o_lay[f]).all(), f
+    np.testing.assert_allclose(g.gains, o_gain, rtol=1e-5)
+    np.testing.assert_allclose(g.power, o_pow, rtol=1e-5)
+    J = np.diff(b.mic_begin)
+    for u in range(b.n_utt):
+        want = np.concatenate([b.channel(o_out, u, j, o_len[u]) for j in range(J[u])])
+        got = np.concatenate([b.channel(g.out, u, j, o_len[u]) for j in range(J[u])])
+        assert rel_err(got, want) <= WAVE_TOL, u
+        # tail beyond out_len is zero-filled
+        for j in range(J[u]):
+            o = int(b.out_off[u] + j * b.out_stride[u])
+            assert not g.out[o + o_len[u]: o + b.out_stride[u]].any()
+
+
+def test_render_config3_subset(rs, ctx, port):
+    from paper_1712_03439_b200 import scenes
+
+    b = scenes.config3(n_utt=6, seed=21)
+    g, o = _render_both(rs, ctx, port, b)
+    _check_render(b, g, o)
+
+
+def test_render_config4_subset(rs, ctx, port):
+    from paper_1712_03439_b200 import scenes
+
+    b = scenes.config4(n_utt=4, seed=22)
+    g, o = _render_both(rs, ctx, port, b)
+    _check_render(b, g, o)
+
+
+def test_render_config2_subset(rs, ctx, port):
+    from paper_1712_03439_b200 import scenes
+
+    b = scenes.config2(n_utt=4, seed=23)
+    g, o = _render_both(rs, ctx, port, b)
+    _check_render(b, g, o)
+
+
+def test_render_config5_subset(rs, ctx, port):
+    from paper_1712_03439_b200 import scenes
+
+    b = scenes.config5(n_utt=1, seed=24)
+    g, o = _render_both(rs, ctx, port, b)
+    assert (g.layout["fft_size"] == 32768).all()
+    _check_render(b, g, o)
+
+
+def test_render_kats(rs, ctx):
+    """SPEC.md:354-355 with K = 0, d = 1 m (a single unit tap at 47)."""
+    from paper_1712_03439_b200 import scenes
+
+    x = np.random.default_rng(5).standard_normal(1000).astype(np.float32)
+
+    def batch(n_src):
+        return scenes.SceneBatch(
+            src_begin=np.array([0, n_src]), mic_begin=np.array([0, 1]),
+            room_dims=np.array([[5.0, 5.0, 5.0]]), reflection=np.array([0.5]),
+            sample_rate=np.array([16000.0]), speed_of_sound=np.array([343.0]),
+            image_order=np.array([0], np.int32), max_taps=np.array([0]),
+            src_pos=np.tile([1.0, 1.0, 1.0], (n_src, 1)), mic_pos=np.array([[2.0, 1.0, 1.0]]),
+            snr_db=np.zeros(n_src), sig_off=np.zeros(n_src, np.int64), sig_len=np.full(n_src, 1000),
+            signals=x, plan_rule=scenes.PLAN_CHOOSE)
+
+    b = batch(1)
+    r = rs.render_batch(b, ctx=ctx)
+    y = b.channel(r.out, 0, 0, r.out_len[0])
+    assert r.out_len[0] == 1047
+    np.testing.assert_allclose(y[47:], x, atol=1e-6)
+    assert np.abs(y[:47]).max() < 1e-6
+    b = batch(2)
+    r = rs.render_batch(b, ctx=ctx)
+    y = b.channel(r.out, 0, 0, r.out_len[0])
+    assert r.gains[1] == pytest.approx(1.0, rel=1e-12)
+    np.testing.assert_allclose(y[47:], 2 * x, atol=1e-5)
+
+
+def test_snr_fidelity(rs, ctx):
+    """10 log10(P_target / P_scaled_noise) = snr within 1e-6 dB."""
+    from paper_1712_03439_b200 import scenes
+
+    b = scenes.config3(n_utt=3, seed=31)
+    r = rs.render_batch(b, ctx=ctx)
+    pb = b.pair_begin
+    for u in range(b.n_utt):
+        I, J = int(np.diff(b.src_begin)[u]), int(np.diff(b.mic_begin)[u])
+        for j in range(J):
+            t = rs.last_pair_signal(pb[u] + j, 1 << 22, ctx=ctx).astype(np.float64)
+            pt = np.mean(t * t)
+            for i in range(1, I):
+                p = pb[u] + i * J + j
+                n = rs.last_pair_signal(p, 1 << 22, ctx=ctx).astype(np.float64) * r.gains[p]
+                snr = 10 * math.log10(pt / np.mean(n * n))
+                assert abs(snr - b.snr_db[b.src_begin[u] + i]) <= 1e-6
+
+
+def test_determinism(rs, ctx):
+    from paper_1712_03439_b200 import scenes
+
+    b = scenes.config4(n_utt=8, seed=41)
+    a = rs.render_batch(b, ctx=ctx).out.copy()
+    c = rs.render_batch(b, ctx=ctx).out.copy()
+    assert (a.view(np.uint32) == c.view(np.uint32)).all()
+
+
+def test_device_mode_matches_host(rs, ctx):
+    import torch
+
+    from paper_1712_03439_b200 import scenes
+
+    b = scenes.config4(n_utt=5, seed=42)
+    host = rs.render_batch(b, ctx=ctx)
+    sig = torch.from_numpy(b.signals).cuda()
+    out = torch.zeros(b.out_total, dtype=torch.float32, device="cuda")
+    dev = rs.render_batch(b, ctx=ctx, device_signals_ptr=sig.data_ptr(), device_out_ptr=out.data_ptr())
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy().view(np.uint32) == host.out.view(np.uint32)).all()
+    assert (dev.layout == host.layout).all()
+
+
+def test_render_errors(rs, ctx):
+    from paper_1712_03439_b200 import scenes
+
+    b = scenes.config3(n_utt=2, seed=51)
+    b.src_pos[1] = [0.0, 1.0, 1.0]
+    with pytest.raises(rs.PlacementError):
+        rs.render_batch(b, ctx=ctx)
+    b = scenes.config3(n_utt=2, seed=51)
+    b.plan_rule, b.forced_fft_size = scenes.PLAN_FORCED, 16
+    with pytest.raises(rs.PlanError):
+        rs.render_batch(b, ctx=ctx)
