@@ -261,8 +261,10 @@ class _Lib:
         layout = np.zeros(scene.n_pairs, LAYOUT_DTYPE)
         gains = np.zeros(scene.n_pairs)
         power = np.zeros(scene.n_pairs)
-        st = self.render_batch_raw(C.byref(b), out.ctypes.data, scene.out_off.ctypes.data,
-                                   scene.out_stride.ctypes.data, out_len.ctypes.data,
+        out_off = np.ascontiguousarray(scene.out_off, np.int64)  # keep alive across the call
+        out_stride = np.ascontiguousarray(scene.out_stride, np.int64)
+        st = self.render_batch_raw(C.byref(b), out.ctypes.data, out_off.ctypes.data,
+                                   out_stride.ctypes.data, out_len.ctypes.data,
                                    layout.ctypes.data, gains.ctypes.data, power.ctypes.data,
                                    int(threads))
         del keep

@@ -45,9 +45,9 @@ def test_rir_bitexact_random(rs, ctx, port):
 
 def test_rir_bitexact_long_sliced(rs, ctx, port):
     # K large enough that the RIR exceeds one K1 slice (12288 bins)
-    room, src, mic = [4.0, 3.5, 2.8], [1.1, 2.0, 1.3], [2.9, 1.0, 1.7]
-    want = port.synthesize_rir(room, 0.9, 40, src, mic, max_taps=30000)
-    got = rs.synthesize_rir(room, 0.9, 40, src, mic, max_taps=30000, ctx=ctx)
+    room, src, mic = [10.0, 8.0, 6.0], [1.1, 2.0, 1.3], [2.9, 1.0, 1.7]
+    want = port.synthesize_rir(room, 0.9, 30, src, mic, max_taps=30000)
+    got = rs.synthesize_rir(room, 0.9, 30, src, mic, max_taps=30000, ctx=ctx)
     assert want.size > 12288 and (bits(got) == bits(want)).all()
 
 
