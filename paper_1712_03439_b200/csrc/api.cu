@@ -191,7 +191,7 @@ struct rs_ctx {
   float2* tw[kMaxLog2M + 1] = {};
   DevBuf tw_all;
   // arena
-  DevBuf utt, pair, rg, items, rir, rirout, plan, lists, spec, y, sumsq, gain, power, flags,
+  DevBuf utt, pair, rg, items, olaitems, rir, rirout, plan, lists, spec, y, sumsq, gain, power, flags,
       snr, chan_utt, chan_mic, chan_out, utt_len, utt_stride, utt_pair0, utt_I, utt_J, sig, out,
       scratch_a, scratch_b;
   // last render (debug fetch)
@@ -242,8 +242,10 @@ double pair_flops(const PairPlan& p) {
 }
 
 // ---- stage B: spectrum + OLA over planned pairs (shared by render/convolve) ----
-// Pairs are bucketed by transform size; buckets run largest work first.
-int run_filter(rs_ctx* c, const std::vector<PairPlan>& plans, const float* d_signals,
+// Pairs are bucketed by transform size; buckets run largest work first.  Each
+// pair's blocks are split into runs (K4 work items) long enough that the
+// recomputed overlap blocks cost <= ~6%, short enough to fill the GPU.
+int run_filter(rs_ctx* c, std::vector<PairPlan>& plans, const float* d_signals,
                const double* d_rir, double* flops_out) {
   const int64_t n_pairs = static_cast<int64_t>(plans.size());
   std::vector<std::vector<int32_t>> bucket(kMaxLog2M + 1);
@@ -257,7 +259,9 @@ int run_filter(rs_ctx* c, const std::vector<PairPlan>& plans, const float* d_sig
     flops += work[p];
   }
   std::vector<int32_t> lists;
-  std::vector<std::pair<int, int64_t>> spans;  // (log2m, offset in lists)
+  std::vector<OlaItem> items;
+  struct Span { int l; int64_t list_off, list_n, item_off, item_n; };
+  std::vector<Span> spans;
   std::vector<int> order(kMaxLog2M + 1);
   std::iota(order.begin(), order.end(), 0);
   std::vector<double> bucket_work(kMaxLog2M + 1, 0.0);
@@ -269,11 +273,37 @@ int run_filter(rs_ctx* c, const std::vector<PairPlan>& plans, const float* d_sig
     if (v.empty()) continue;
     // largest pairs first (LPT) so the tail of the launch is short
     std::stable_sort(v.begin(), v.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
-    spans.emplace_back(l, static_cast<int64_t>(lists.size()));
+    int64_t total_blocks = 0;
+    int64_t max_pre = 1;
+    for (int32_t p : v) {
+      total_blocks += plans[p].B;
+      const int64_t n = int64_t(1) << plans[p].log2n;
+      max_pre = std::max<int64_t>(max_pre, (n - plans[p].L + plans[p].L - 1) / plans[p].L);
+    }
+    const int64_t slots = 148LL * 2 * ola_groups(l);
+    int64_t run = std::max<int64_t>((total_blocks + 4 * slots - 1) / (4 * slots), 16 * max_pre);
+    Span sp{l, static_cast<int64_t>(lists.size()), static_cast<int64_t>(v.size()),
+            static_cast<int64_t>(items.size()), 0};
+    for (int32_t p : v) {
+      PairPlan& pl = plans[p];
+      const int64_t n = int64_t(1) << pl.log2n;
+      const int64_t pre = (n - pl.L + pl.L - 1) / pl.L;  // ceil((N_h - 1) / L)
+      pl.item0 = static_cast<int64_t>(items.size());
+      pl.nitems = 0;
+      for (int64_t r0 = 0; r0 < pl.B; r0 += run) {
+        const int64_t r1 = std::min<int64_t>(pl.B, r0 + run);
+        const int64_t b0 = r0 == 0 ? 0 : std::max<int64_t>(0, r0 - pre);
+        items.push_back(OlaItem{p, static_cast<int32_t>(b0), static_cast<int32_t>(r0), static_cast<int32_t>(r1)});
+        ++pl.nitems;
+      }
+    }
+    sp.item_n = static_cast<int64_t>(items.size()) - sp.item_off;
+    spans.push_back(sp);
     lists.insert(lists.end(), v.begin(), v.end());
   }
   RS_TRY(upload(c, c->lists, lists));
   RS_TRY(upload(c, c->plan, plans));
+  RS_TRY(upload(c, c->olaitems, items));
   int64_t spec_total = 0, y_total = 0;
   for (const auto& p : plans) {
     spec_total = std::max<int64_t>(spec_total, p.spec_off + (int64_t(1) << (p.log2n - 1)) + 1);
@@ -281,20 +311,20 @@ int run_filter(rs_ctx* c, const std::vector<PairPlan>& plans, const float* d_sig
   }
   RS_TRY(c->spec.ensure(std::max<int64_t>(spec_total, 1) * sizeof(float2)));
   RS_TRY(c->y.ensure(std::max<int64_t>(y_total, 1) * sizeof(float)));
-  RS_TRY(c->sumsq.ensure(std::max<int64_t>(n_pairs, 1) * sizeof(double)));
+  RS_TRY(c->sumsq.ensure(std::max<size_t>(items.size(), 1) * sizeof(double)));
   const int32_t* d_lists = c->lists.as<int32_t>();
-  for (auto& [l, off] : spans) {
-    SpecArgs a{d_lists + off, static_cast<int32_t>(bucket[l].size()), c->pair.as<PairMeta>(),
-               c->plan.as<PairPlan>(), d_rir, c->spec.as<float2>(), c->tw[l]};
-    RS_CUDA(launch_spectrum(l, a, c->stream));
+  for (const Span& sp : spans) {
+    SpecArgs a{d_lists + sp.list_off, static_cast<int32_t>(sp.list_n), c->pair.as<PairMeta>(),
+               c->plan.as<PairPlan>(), d_rir, c->spec.as<float2>(), c->tw[sp.l]};
+    RS_CUDA(launch_spectrum(sp.l, a, c->stream));
     ++c->launches;
   }
   if (c->profiling) RS_CUDA(cudaEventRecord(c->ev0, c->stream));
-  for (auto& [l, off] : spans) {
-    OlaArgs a{d_lists + off, static_cast<int32_t>(bucket[l].size()), c->pair.as<PairMeta>(),
-              c->plan.as<PairPlan>(), d_signals, c->spec.as<float2>(), c->y.as<float>(),
-              c->sumsq.as<double>(), c->tw[l]};
-    RS_CUDA(launch_ola(l, a, c->stream));
+  for (const Span& sp : spans) {
+    OlaArgs a{c->olaitems.as<OlaItem>() + sp.item_off, static_cast<int32_t>(sp.item_n),
+              c->pair.as<PairMeta>(), c->plan.as<PairPlan>(), d_signals, c->spec.as<float2>(),
+              c->y.as<float>(), c->sumsq.as<double>() + sp.item_off, c->tw[sp.l]};
+    RS_CUDA(launch_ola(sp.l, a, c->stream));
     ++c->launches;
   }
   if (c->profiling) RS_CUDA(cudaEventRecord(c->ev1, c->stream));
@@ -591,14 +621,15 @@ int convolve_host(rs_ctx* c, const double* x, size_t nx, const double* h, size_t
   pm.rir_cap = static_cast<int64_t>(nh);
   std::vector<PairMeta> pv{pm};
   RS_TRY(upload(c, c->pair, pv));
-  PairPlan pl{};
+  std::vector<PairPlan> plv(1);
+  PairPlan& pl = plv[0];
   pl.log2n = log2_exact(n);
   pl.nh = static_cast<int64_t>(nh);
   pl.L = static_cast<int64_t>(n - nh + 1);
   pl.B = static_cast<int64_t>(block_count(nx, nh, n));
   pl.out_len = static_cast<int64_t>(nx + nh - 1);
   double flops = 0;
-  RS_TRY(run_filter(c, {pl}, c->sig.as<float>(), c->rir.as<double>(), &flops));
+  RS_TRY(run_filter(c, plv, c->sig.as<float>(), c->rir.as<double>(), &flops));
   const size_t ol = nx + nh - 1;
   RS_TRY(c->scratch_b.ensure(ol * sizeof(double)));
   RS_CUDA(launch_convert_f2d(c->y.as<float>(), c->scratch_b.as<double>(), static_cast<int64_t>(ol), c->stream));
@@ -637,7 +668,7 @@ int rs_ctx_destroy(rs_ctx* c) {
   if (!c) return RS_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  DevBuf* bufs[] = {&c->tw_all, &c->utt, &c->pair, &c->rg, &c->items, &c->rir, &c->rirout,
+  DevBuf* bufs[] = {&c->tw_all, &c->utt, &c->pair, &c->rg, &c->items, &c->olaitems, &c->rir, &c->rirout,
                     &c->plan, &c->lists, &c->spec, &c->y, &c->sumsq, &c->gain, &c->power,
                     &c->flags, &c->snr, &c->chan_utt, &c->chan_mic, &c->chan_out, &c->utt_len,
                     &c->utt_stride, &c->utt_pair0, &c->utt_I, &c->utt_J, &c->sig, &c->out,
@@ -737,10 +768,9 @@ int rs_synthesize_rir(rs_ctx* c, const double room_dims[3], double reflection, d
                       int64_t max_taps, double* out, size_t cap, size_t* len) {
   RS_TRY(check_ctx(c));
   // A one-utterance, one-pair batch through K1 + K2 (no truncation).
-  int64_t sb[2] = {0, 1}, mb[2] = {0, 1};
-  double fs = sample_rate, c0 = speed_of_sound, r = reflection, snr = 0.0;
-  int32_t K = image_order;
-  int64_t mt = max_taps, so = 0, sl = 1;
+  const double fs = sample_rate, c0 = speed_of_sound, r = reflection;
+  const int32_t K = image_order;
+  const int64_t mt = max_taps;
   RS_TRY(room_validate(room_dims, r, fs, c0, K));
   if (!strictly_inside(room_dims, src)) return fail(RS_ERR_PLACEMENT, "source must lie strictly inside the room");
   if (!strictly_inside(room_dims, mic)) return fail(RS_ERR_PLACEMENT, "microphone must lie strictly inside the room");
@@ -774,7 +804,6 @@ int rs_synthesize_rir(rs_ctx* c, const double room_dims[3], double reflection, d
     items.push_back(SynthItem{0, static_cast<int32_t>(lo), static_cast<int32_t>(l), 0});
     slice = std::max<int>(slice, static_cast<int>(l));
   }
-  (void)sb; (void)mb; (void)snr; (void)so; (void)sl;
   RS_TRY(upload(c, c->utt, std::vector<UttMeta>{um}));
   RS_TRY(upload(c, c->pair, std::vector<PairMeta>{pm}));
   RS_TRY(upload(c, c->rg, rg));

@@ -193,9 +193,13 @@ __device__ __forceinline__ float2 ld_tw(const float2* p) {
 //   read   slot(j + r*STRIDE)            = PAD(t) + q*PAD(T) + r*PAD(STRIDE)
 //   write  slot((j-k)*R + k + r*NS), k = j mod NS, which is either the same k
 //          for every q (NS | T) or k = j (NS >= M/R, the last pass).
-template <int M, int P, bool INV>
+struct CtaBar {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+
+template <int M, int P, bool INV, class Bar = CtaBar>
 __device__ __forceinline__ void stockham_pass(float2* s, int t, const float2* __restrict__ tw,
-                                              bool active) {
+                                              bool active, Bar bar = Bar()) {
   using PL = Plan<M>;
   constexpr int R = PL::radix(P), NS = PL::ns(P), T = PL::T, NB = PL::E / R, STRIDE = M / R;
   static_assert(NB == 1 || T % NS == 0 || NS >= STRIDE, "unsupported pass shape");
@@ -225,7 +229,7 @@ __device__ __forceinline__ void stockham_pass(float2* s, int t, const float2* __
       Dft<R, INV>::run(v[q]);
     }
   }
-  __syncthreads();
+  bar();
   if (active) {
     if constexpr (NS == 1 && R == 16 && NB == 1) {
       float2* sw = s + 17 * t;  // PAD(16 t + r) = 17 t + r
@@ -247,14 +251,15 @@ __device__ __forceinline__ void stockham_pass(float2* s, int t, const float2* __
       }
     }
   }
-  __syncthreads();
+  bar();
 }
 
 // Pass 0 of a forward transform whose packed input z[c] = (x[2c], x[2c+1])
 // comes straight from global memory: x points at the block start, elements
 // at or beyond `take` are the zero padding.  Writes smem, then syncs.
-template <int M, class Src>
-__device__ __forceinline__ void first_pass(float2* s, int t, bool active, const Src* x, int take) {
+template <int M, class Src, class Bar = CtaBar>
+__device__ __forceinline__ void first_pass(float2* s, int t, bool active, const Src* x, int take,
+                                           Bar bar = Bar()) {
   using PL = Plan<M>;
   constexpr int R = PL::radix(0), T = PL::T, NB = PL::E / R, STRIDE = M / R;
   if (active) {
@@ -280,24 +285,76 @@ __device__ __forceinline__ void first_pass(float2* s, int t, bool active, const 
       }
     }
   }
-  __syncthreads();
+  bar();
 }
 
 // Remaining forward passes 1..NP-1.
-template <int M, int P = 1>
-__device__ __forceinline__ void forward_rest(float2* s, int t, const float2* tw, bool active) {
+template <int M, int P = 1, class Bar = CtaBar>
+__device__ __forceinline__ void forward_rest(float2* s, int t, const float2* tw, bool active,
+                                             Bar bar = Bar()) {
   if constexpr (P < Plan<M>::NP) {
-    stockham_pass<M, P, false>(s, t, tw, active);
-    forward_rest<M, P + 1>(s, t, tw, active);
+    stockham_pass<M, P, false>(s, t, tw, active, bar);
+    forward_rest<M, P + 1>(s, t, tw, active, bar);
   }
 }
 
 // All inverse passes 0..NP-1 from smem to smem (unnormalised, conj twiddles).
-template <int M, int P = 0>
-__device__ __forceinline__ void inverse_all(float2* s, int t, const float2* tw, bool active) {
+template <int M, int P = 0, class Bar = CtaBar>
+__device__ __forceinline__ void inverse_all(float2* s, int t, const float2* tw, bool active,
+                                            Bar bar = Bar()) {
   if constexpr (P < Plan<M>::NP) {
-    stockham_pass<M, P, true>(s, t, tw, active);
-    inverse_all<M, P + 1>(s, t, tw, active);
+    stockham_pass<M, P, true>(s, t, tw, active, bar);
+    inverse_all<M, P + 1>(s, t, tw, active, bar);
+  }
+}
+
+// Inverse passes 0..NP-2 (smem -> smem); the last pass is stockham_emit_pass.
+template <int M, int P = 0, class Bar = CtaBar>
+__device__ __forceinline__ void inverse_but_last(float2* s, int t, const float2* tw, bool active,
+                                                 Bar bar = Bar()) {
+  if constexpr (P + 1 < Plan<M>::NP) {
+    stockham_pass<M, P, true>(s, t, tw, active, bar);
+    inverse_but_last<M, P + 1>(s, t, tw, active, bar);
+  }
+}
+
+// Last inverse pass: reads smem, twiddles, DFT, then a barrier (smem may be
+// reused) and hands every output element to `emit(c, v)` in registers,
+// c = complex index in natural order (c = j + r*M/R).
+template <int M, class Bar, class Emit>
+__device__ __forceinline__ void stockham_emit_pass(float2* s, int t, const float2* __restrict__ tw,
+                                                   bool active, Bar bar, Emit emit) {
+  using PL = Plan<M>;
+  constexpr int P = PL::NP - 1;
+  constexpr int R = PL::radix(P), NS = PL::ns(P), T = PL::T, NB = PL::E / R, STRIDE = M / R;
+  static_assert(NS == STRIDE, "last pass writes natural order");
+  constexpr bool LIN = (NB == 1) || (T % 16 == 0);
+  float2 v[NB][R];
+  if (active) {
+    const float2* sr = s + PAD(t);
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if constexpr (STRIDE % 16 == 0 && LIN)
+          v[q][r] = sr[q * PAD(T) + r * PAD(STRIDE)];
+        else
+          v[q][r] = s[PAD(t + q * T + r * STRIDE)];
+      }
+      if constexpr (NS > 1) {
+        const float2* w = tw + PL::tw_off(P) + t * R + q * T * R;  // k = j in the last pass
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[q][r] = c_mulc(v[q][r], RSG_TW_LOAD(w + r));
+      }
+      Dft<R, true>::run(v[q]);
+    }
+  }
+  bar();
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+#pragma unroll
+      for (int r = 0; r < R; ++r) emit(t + q * T + r * STRIDE, v[q][r]);
   }
 }
 
@@ -309,9 +366,10 @@ __device__ __forceinline__ void inverse_all(float2* s, int t, const float2* tw, 
 //   P = X2 G[k], Q = X2m conj(G[M-k]), U = P + Q, V = (P - Q) conj(W^k)
 //   Z'[k] = U + i V,  Z'[M-k] = conj(U) + i conj(V).
 // W^k = exp(-2 pi i k / N) comes from the plan's pairing table.
-template <int M>
+template <int M, class Bar = CtaBar>
 __device__ __forceinline__ void spectral_multiply(float2* s, int t, const float2* __restrict__ G,
-                                                  const float2* __restrict__ W, bool active) {
+                                                  const float2* __restrict__ W, bool active,
+                                                  Bar bar = Bar()) {
   constexpr int T = Plan<M>::T;
   if (active) {
 #pragma unroll 2
@@ -358,7 +416,7 @@ __device__ __forceinline__ void spectral_multiply(float2* s, int t, const float2
       }
     }
   }
-  __syncthreads();
+  bar();
 }
 
 }  // namespace rsg

@@ -321,25 +321,52 @@ __global__ void __launch_bounds__(cta_threads_of(Plan<M>::LOG)) rir_spectrum_ker
 }
 
 // ============================================================================
-// K4: the OLA filter.  One CTA per (source, mic) pair; the CTA runs G
-// transforms of size M = N/2 at a time (G consecutive OLA blocks), each on T
-// threads: forward Stockham FFT of the packed block (loaded straight from the
-// FP32 source signal), spectral multiply with the pair's G, inverse FFT, then
-// a CTA-wide deterministic overlap-add into the pair's output (exclusive
-// ownership: no atomics, fixed summation order) and the FP64 Σy^2 of every
-// sample once it is final.  Reference: convolve_ola, convolution.hpp:219-255.
+// K4: the OLA filter.  A CTA holds G independent groups of T threads; each
+// group takes one work item (a run of OLA blocks of one pair) and, per block,
+// runs the forward Stockham FFT of the packed block (loaded straight from the
+// FP32 source signal), the spectral multiply with the pair's G, and the
+// inverse FFT, whose last pass writes the block's N outputs from registers
+// into the pair's output: plain stores where the block is the first writer,
+// read-add-write (earlier blocks first, as convolution.hpp:251-252) on the
+// N_h - 1 overlap.  Groups synchronise with their own barrier (__syncwarp or
+// a named bar.sync), never with the whole CTA, and every sample's FP64 y^2 is
+// accumulated once, when it is final.  Reference: convolve_ola,
+// convolution.hpp:219-255; mean_power, audio_buffer.hpp:66-75.
 // ============================================================================
+template <int T>
+struct GroupBar {
+  int id;
+  __device__ __forceinline__ void operator()() const {
+    if constexpr (T == 1) {
+      // one thread per transform: no inter-thread exchange
+    } else if constexpr (T <= 32) {
+      __syncwarp();  // groups of a warp run convergent (uniform trip count)
+    } else {
+      asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(T) : "memory");
+    }
+  }
+};
+
+int ola_groups(int log2m) {
+  const int M = 1 << log2m;
+  const int E = M < 16 ? M : (M >= 8192 ? 32 : 16);
+  return cta_threads_of(log2m) / (M / E);
+}
+
 template <int M>
-__global__ void __launch_bounds__(cta_threads_of(Plan<M>::LOG), (M >= 8192 ? 1 : RSG_OLA_MINB)) ola_kernel(OlaArgs a) {
+__global__ void __launch_bounds__(cta_threads_of(Plan<M>::LOG), (M >= 8192 ? 1 : RSG_OLA_MINB))
+ola_kernel(OlaArgs a) {
   using PL = Plan<M>;
   extern __shared__ __align__(16) float2 smem[];
+  constexpr int T = PL::T;
   constexpr int G = groups_of<M>();
-  constexpr int CTA = cta_threads_of(PL::LOG);
   constexpr int N = 2 * M;
-  const int g = threadIdx.x / PL::T, t = threadIdx.x % PL::T;
-  const int p = a.list[blockIdx.x];
-  const PairPlan pl = a.plan[p];
-  const PairMeta& pm = a.pair[p];
+  const int g = threadIdx.x / T, t = threadIdx.x % T;
+  const int item = blockIdx.x * G + g;
+  const bool has = item < a.count;
+  const OlaItem it = a.items[has ? item : 0];
+  const PairPlan& pl = a.plan[it.pair];
+  const PairMeta& pm = a.pair[it.pair];
   const float* __restrict__ x = a.signals + pm.sig_off;
   const long long nx = pm.nx;
   const float2* __restrict__ Gs = a.spec + pl.spec_off;
@@ -348,52 +375,70 @@ __global__ void __launch_bounds__(cta_threads_of(Plan<M>::LOG), (M >= 8192 ? 1 :
   const int L = static_cast<int>(pl.L);
   const int B = static_cast<int>(pl.B);
   const int out_len = static_cast<int>(pl.out_len);
+  const int ovl = N - L;  // N_h - 1 samples overlap the next block
   float2* s = smem + g * PL::PADDED;
+  const GroupBar<T> bar{1 + g};
+  int trips = has ? it.b_end - it.b_begin : 0;
+  if constexpr (T < 32 && T > 1) trips = __reduce_max_sync(0xffffffffu, trips);
+  if constexpr (T == 1) trips = __reduce_max_sync(0xffffffffu, trips);
+  const long long own_lo = static_cast<long long>(it.b_own) * L;
+  const long long own_hi = it.b_end == B ? out_len : static_cast<long long>(it.b_end) * L;
   double pw = 0.0;
-
 #pragma unroll 1
-  for (int b0 = 0; b0 < B; b0 += G) {
-    const int b = b0 + g;
-    const bool active = b < B;
+  for (int k = 0; k < trips; ++k) {
+    const int b = it.b_begin + k;
+    const bool active = has && b < it.b_end;
     const long long start = static_cast<long long>(b) * L;
-    const long long take = active ? (nx - start < L ? nx - start : L) : 0;
-    first_pass<M>(s, t, active, x + start, static_cast<int>(take));
-    forward_rest<M>(s, t, a.tw, active);
-    spectral_multiply<M>(s, t, Gs, W, active);
-    inverse_all<M>(s, t, a.tw, active);
-    // ---- deterministic overlap-add of this round's blocks ----
-    const int nact = (B - b0) < G ? (B - b0) : G;
-    const int P0 = b0 * L;
-    const long long p1 = static_cast<long long>(b0 + nact - 1) * L + N;
-    const int P1 = p1 < out_len ? static_cast<int>(p1) : out_len;
-    const long long fl = b0 == 0 ? 0 : static_cast<long long>(b0 - 1) * L + N;
-    const long long fh = (b0 + nact == B) ? out_len : static_cast<long long>(b0 + nact) * L;
-    for (int n = P0 + static_cast<int>(threadIdx.x); n < P1; n += CTA) {
-      const int rel = n - P0;
-      int ghi = rel / L;
-      ghi = ghi < nact - 1 ? ghi : nact - 1;
-      const int glo = rel >= N ? (rel - N) / L + 1 : 0;
-      float acc = (n >= fl) ? 0.f : y[n];
-#pragma unroll 1
-      for (int gg = glo; gg <= ghi; ++gg) {
-        const int i = rel - gg * L;
-        const float2 v = smem[gg * PL::PADDED + PAD(i >> 1)];
-        acc += (i & 1) ? v.y : v.x;
+    const int take = active ? static_cast<int>(nx - start < L ? nx - start : L) : 0;
+    first_pass<M>(s, t, active, x + start, take, bar);
+#ifndef RSG_NO_FWD
+    forward_rest<M>(s, t, a.tw, active, bar);
+#endif
+#ifndef RSG_NO_MUL
+    spectral_multiply<M>(s, t, Gs, W, active, bar);
+#endif
+#ifndef RSG_NO_INV
+    inverse_but_last<M>(s, t, a.tw, active, bar);
+#endif
+    const bool rmw = b > it.b_begin;  // this item's previous block wrote the overlap
+    float* yb = y + start;
+    // element offsets e in [0, N) relative to the block start (32-bit)
+    const int lo = static_cast<int>(max(own_lo - start, -1ll));
+    const int hi = static_cast<int>(min(own_hi - start, static_cast<long long>(N)));
+    const int fe = (b == B - 1) ? N : L;  // e < fe: final after block b
+    const int rmw_end = rmw ? ovl : 0;
+    stockham_emit_pass<M>(s, t, a.tw, active, bar, [&](int c, float2 v) {
+#ifdef RSG_TRIVIAL_EMIT
+      yb[2 * c] = v.x; yb[2 * c + 1] = v.y;
+#else
+      const int e0 = 2 * c, e1 = e0 + 1;
+      if (e0 >= lo && e0 < hi) {
+        const float acc = e0 < rmw_end ? yb[e0] + v.x : v.x;
+        yb[e0] = acc;
+        if (e0 < fe) pw = fma(static_cast<double>(acc), static_cast<double>(acc), pw);
       }
-      y[n] = acc;
-      if (n < fh) pw = fma(static_cast<double>(acc), static_cast<double>(acc), pw);
-    }
-    __syncthreads();
+      if (e1 >= lo && e1 < hi) {
+        const float acc = e1 < rmw_end ? yb[e1] + v.y : v.y;
+        yb[e1] = acc;
+        if (e1 < fe) pw = fma(static_cast<double>(acc), static_cast<double>(acc), pw);
+      }
+#endif
+    });
   }
-  // Σ y^2 over the CTA (fixed order: deterministic)
-  __shared__ double red[CTA / 32];
-  for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pw;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double tot = 0.0;
-    for (int w = 0; w < CTA / 32; ++w) tot += red[w];
-    a.sumsq[p] = tot;
+  // Σ y^2 of the group (fixed order: deterministic) -> part[item]
+  if constexpr (T >= 32) {
+    __shared__ double red[cta_threads_of(PL::LOG) / 32];
+    for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pw;
+    bar();
+    if (t == 0 && has) {
+      double tot = 0.0;
+      for (int w = 0; w < T / 32; ++w) tot += red[g * (T / 32) + w];
+      a.part[item] = tot;
+    }
+  } else {
+    for (int o = T / 2; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
+    if (t == 0 && has) a.part[item] = pw;
   }
 }
 
@@ -493,7 +538,9 @@ static cudaError_t spectrum_t(const SpecArgs& a, cudaStream_t s) {
 
 template <int M>
 static cudaError_t ola_t(const OlaArgs& a, cudaStream_t s) {
-  ola_kernel<M><<<a.count, cta_threads_of(Plan<M>::LOG), ola_smem_bytes(Plan<M>::LOG), s>>>(a);
+  constexpr int G = groups_of<M>();
+  const int grid = (a.count + G - 1) / G;
+  ola_kernel<M><<<grid, cta_threads_of(Plan<M>::LOG), ola_smem_bytes(Plan<M>::LOG), s>>>(a);
   return cudaGetLastError();
 }
 
@@ -552,19 +599,26 @@ cudaError_t launch_rfft(int log2m, bool inverse, const float* in_real, const flo
 // K5: SNR gains.  alpha_ij = sqrt(P_0j / (P_ij 10^(snr_i/10)))
 // with P = mean_power (audio_buffer.hpp:66-75) = Σy^2 / len; alpha_0j = 1.
 // ============================================================================
+__device__ __forceinline__ double pair_sumsq(const GainArgs& a, long long p) {
+  const PairPlan& pl = a.plan[p];
+  double s = 0.0;
+  for (int k = 0; k < pl.nitems; ++k) s += a.part[pl.item0 + k];  // item order: deterministic
+  return s;
+}
+
 __global__ void gain_kernel(GainArgs a) {
   const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (p >= a.n_pairs) return;
   const PairMeta& pm = a.pair[p];
   const long long p0 = a.utt_pair0[pm.utt] + pm.mic_local;  // target pair at mic j
-  const double P = a.sumsq[p] / static_cast<double>(a.plan[p].out_len);
+  const double P = pair_sumsq(a, p) / static_cast<double>(a.plan[p].out_len);
   a.power[p] = P;
   if (pm.src_local == 0) {
     a.gain[p] = 1.0;
     if (!(P > 0.0)) a.flags[p] |= 4;
     return;
   }
-  const double Pt = a.sumsq[p0] / static_cast<double>(a.plan[p0].out_len);
+  const double Pt = pair_sumsq(a, p0) / static_cast<double>(a.plan[p0].out_len);
   if (!(P > 0.0) || !(Pt > 0.0)) {
     a.flags[p] |= 4;
     a.gain[p] = 0.0;

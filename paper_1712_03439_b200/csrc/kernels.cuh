@@ -50,7 +50,19 @@ struct PairPlan {
   int64_t B;         // block count
   int64_t out_len;   // N_x + N_h - 1
   int32_t log2n;     // N = 2^log2n
-  int32_t pad;
+  int32_t nitems;    // K4 work items of this pair (consecutive)
+  int64_t item0;     // global index of the pair's first work item
+};
+
+// K4 work item: a run of OLA blocks of one pair.  The item owns output
+// positions [b_own*L, b_end*L) (to out_len for the pair's last run) and also
+// recomputes blocks [b_begin, b_own) whose tails overlap that range, so runs
+// are independent: no seams, no atomics, deterministic.
+struct OlaItem {
+  int32_t pair;
+  int32_t b_begin;
+  int32_t b_own;
+  int32_t b_end;
 };
 
 // K1 work item: one (pair, bin-slice).
@@ -89,14 +101,14 @@ struct SpecArgs {
 };
 
 struct OlaArgs {
-  const int32_t* list;
+  const OlaItem* items;
   int32_t count;
   const PairMeta* pair;
   const PairPlan* plan;
   const float* signals;
   const float2* spec;
   float* y;             // reverberant pair signals
-  double* sumsq;        // per pair Σ y^2 (FP64)
+  double* part;         // per item Σ y^2 over its final samples (FP64)
   const float2* tw;
 };
 
@@ -121,7 +133,7 @@ struct GainArgs {
   const PairPlan* plan;
   const int64_t* utt_pair0;
   const int32_t* utt_J;
-  const double* sumsq;
+  const double* part;         // per K4 item Σ y^2; summed per pair in item order
   const double* snr_lin;      // per global source: pow(10, snr/10) (host std::pow)
   double* gain;
   double* power;
@@ -132,6 +144,7 @@ struct GainArgs {
 // ---- launchers (kernels.cu) --------------------------------------------------
 constexpr int kMaxLog2M = 14;  // M <= 16384  (N <= 32768) in one CTA
 int cta_threads(int log2m);
+int ola_groups(int log2m);     // K4 work items per CTA
 size_t ola_smem_bytes(int log2m);
 int tw_total(int log2m);       // float2 entries of the twiddle table of 2^log2m
 void fill_twiddles(int log2m, float2* host);  // host, FP64 -> FP32

@@ -23,7 +23,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libroomsim_gpu.so")
+LIB_PATH = os.environ.get("ROOMSIM_LIB") or os.path.join(_HERE, "_lib", "libroomsim_gpu.so")
 
 DIRECT, FULL_FFT, OVERLAP_ADD = 0, 1, 2
 PLAN_CHOOSE, PLAN_FORCED, PLAN_POW2_TWICE = 0, 1, 2
