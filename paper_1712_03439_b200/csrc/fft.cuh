@@ -141,17 +141,22 @@ struct Plan {
   static constexpr int LOG = ilog2(M);
   // complex elements per thread: whole transform for M < 16, else 16 (32 for
   // the two largest sizes so that T <= 512 threads keeps 128 registers).
-  static constexpr int E = M < 16 ? M : (M >= 8192 ? 32 : 16);
+#ifndef RSG_E
+#define RSG_E 8  // complex elements (max radix) per thread; measured best on B200
+#endif
+  static constexpr int E = M < RSG_E ? M : (M >= 8192 ? 32 : RSG_E);
   static constexpr int T = M / E;                          // threads per transform
-  static constexpr int NP = LOG == 0 ? 1 : (LOG + 3) / 4;  // Stockham passes
+  static constexpr int LE = ilog2(E < 16 ? E : 16);         // log2 of the max radix
+  static constexpr int NP = LOG == 0 ? 1 : (LOG + LE - 1) / LE;  // Stockham passes
   static constexpr int PADDED = M + M / 16;                // smem float2 slots per transform
   __host__ __device__ static constexpr int radix(int p) {
-    return p < NP - 1 ? 16 : (1 << (LOG - 4 * (NP - 1)));
+    return p < NP - 1 ? (1 << LE) : (1 << (LOG - LE * (NP - 1)));
   }
   __host__ __device__ static constexpr int ns(int p) { return p == 0 ? 1 : ns(p - 1) * radix(p - 1); }
-  // offset (in float2) of pass p's twiddle table: tables of passes 1..p-1 precede it
+  // offset (in float2) of pass p's twiddle-base table w_k = exp(-2 pi i k / (NS R)),
+  // k < NS: the tables of passes 1..p-1 precede it
   __host__ __device__ static constexpr int tw_off(int p) {
-    return p <= 1 ? 0 : tw_off(p - 1) + ns(p - 1) * radix(p - 1);
+    return p <= 1 ? 0 : tw_off(p - 1) + ns(p - 1);
   }
   // total pass-twiddle table size, then the pairing table W^k, k in [0, M/2]
   static constexpr int TW_PASS = NP >= 2 ? tw_off(NP) : 0;
@@ -193,6 +198,34 @@ __device__ __forceinline__ float2 ld_tw(const float2* p) {
 //   read   slot(j + r*STRIDE)            = PAD(t) + q*PAD(T) + r*PAD(STRIDE)
 //   write  slot((j-k)*R + k + r*NS), k = j mod NS, which is either the same k
 //          for every q (NS | T) or k = j (NS >= M/R, the last pass).
+// Multiply v[r] by w^r (forward) or conj(w)^r (inverse), r = 1..R-1, with the
+// powers generated from the single loaded base w by a shallow product tree
+// (at most 5 roundings deep): one coalesced load per butterfly instead of R-1.
+template <int R, bool INV>
+__device__ __forceinline__ void apply_twiddles(float2* v, float2 w1) {
+  auto mul = [](float2 a, float2 b) { return INV ? c_mulc(a, b) : c_mul(a, b); };
+  if constexpr (R == 2) {
+    v[1] = mul(v[1], w1);
+  } else if constexpr (R == 4) {
+    const float2 w2 = c_mul(w1, w1), w3 = c_mul(w2, w1);
+    v[1] = mul(v[1], w1); v[2] = mul(v[2], w2); v[3] = mul(v[3], w3);
+  } else if constexpr (R == 8) {
+    const float2 w2 = c_mul(w1, w1), w3 = c_mul(w2, w1), w4 = c_mul(w2, w2);
+    v[1] = mul(v[1], w1); v[2] = mul(v[2], w2); v[3] = mul(v[3], w3); v[4] = mul(v[4], w4);
+    v[5] = mul(v[5], c_mul(w4, w1)); v[6] = mul(v[6], c_mul(w4, w2)); v[7] = mul(v[7], c_mul(w4, w3));
+  } else if constexpr (R == 16) {
+    const float2 w2 = c_mul(w1, w1), w3 = c_mul(w2, w1), w4 = c_mul(w2, w2);
+    v[1] = mul(v[1], w1); v[2] = mul(v[2], w2); v[3] = mul(v[3], w3); v[4] = mul(v[4], w4);
+    v[5] = mul(v[5], c_mul(w4, w1)); v[6] = mul(v[6], c_mul(w4, w2)); v[7] = mul(v[7], c_mul(w4, w3));
+    const float2 w8 = c_mul(w4, w4);
+    v[8] = mul(v[8], w8);
+    v[9] = mul(v[9], c_mul(w8, w1)); v[10] = mul(v[10], c_mul(w8, w2)); v[11] = mul(v[11], c_mul(w8, w3));
+    const float2 w12 = c_mul(w8, w4);
+    v[12] = mul(v[12], w12);
+    v[13] = mul(v[13], c_mul(w12, w1)); v[14] = mul(v[14], c_mul(w12, w2)); v[15] = mul(v[15], c_mul(w12, w3));
+  }
+}
+
 struct CtaBar {
   __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
@@ -219,12 +252,8 @@ __device__ __forceinline__ void stockham_pass(float2* s, int t, const float2* __
           v[q][r] = s[PAD(t + q * T + r * STRIDE)];
       }
       if constexpr (NS > 1) {
-        const float2* w = tw + PL::tw_off(P) + (SAME_K ? kt : t) * R + (SAME_K ? 0 : q * T * R);
-#pragma unroll
-        for (int r = 1; r < R; ++r) {
-          const float2 wr = RSG_TW_LOAD(w + r);
-          v[q][r] = INV ? c_mulc(v[q][r], wr) : c_mul(v[q][r], wr);
-        }
+        const float2 w1 = RSG_TW_LOAD(tw + PL::tw_off(P) + (SAME_K ? kt : t + q * T));
+        apply_twiddles<R, INV>(v[q], w1);
       }
       Dft<R, INV>::run(v[q]);
     }
@@ -342,9 +371,8 @@ __device__ __forceinline__ void stockham_emit_pass(float2* s, int t, const float
           v[q][r] = s[PAD(t + q * T + r * STRIDE)];
       }
       if constexpr (NS > 1) {
-        const float2* w = tw + PL::tw_off(P) + t * R + q * T * R;  // k = j in the last pass
-#pragma unroll
-        for (int r = 1; r < R; ++r) v[q][r] = c_mulc(v[q][r], RSG_TW_LOAD(w + r));
+        const float2 w1 = RSG_TW_LOAD(tw + PL::tw_off(P) + t + q * T);  // k = j in the last pass
+        apply_twiddles<R, true>(v[q], w1);
       }
       Dft<R, true>::run(v[q]);
     }

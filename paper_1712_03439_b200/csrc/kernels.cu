@@ -14,6 +14,10 @@
 #include "fft.cuh"
 #include "kernels.cuh"
 
+#ifndef RSG_E
+#define RSG_E 8  // complex elements (max radix) per thread; measured best on B200
+#endif
+
 #ifndef RSG_OLA_MINB
 #define RSG_OLA_MINB 2
 #endif
@@ -213,7 +217,9 @@ cudaError_t launch_cut(const CutArgs& a, int n_pairs, cudaStream_t s) {
 // ============================================================================
 __host__ __device__ constexpr int cta_threads_of(int log2m) {
   // T = M / E threads per transform (E = 16, or 32 for M >= 8192); >= 256 per CTA.
-  return log2m <= 4 ? 256 : (log2m >= 13 ? (1 << log2m) / 32 : ((1 << log2m) / 16 > 256 ? (1 << log2m) / 16 : 256));
+  return log2m <= ilog2(RSG_E) ? 256
+                               : (log2m >= 13 ? (1 << log2m) / 32
+                                              : ((1 << log2m) / RSG_E > 256 ? (1 << log2m) / RSG_E : 256));
 }
 int cta_threads(int log2m) { return cta_threads_of(log2m); }
 
@@ -224,7 +230,7 @@ __host__ __device__ constexpr int groups_of() {
 
 size_t ola_smem_bytes(int log2m) {
   const int M = 1 << log2m;
-  const int E = M < 16 ? M : (M >= 8192 ? 32 : 16);
+  const int E = M < RSG_E ? M : (M >= 8192 ? 32 : RSG_E);
   const int T = M / E;
   const int G = cta_threads_of(log2m) / T;
   return static_cast<size_t>(G) * (M + M / 16) * sizeof(float2);
@@ -250,14 +256,11 @@ static void fill_twiddles_t(float2* h) {
   const double pi = 3.14159265358979323846;
   for (int p = 1; p < PL::NP; ++p) {
     const int R = PL::radix(p), NS = PL::ns(p);
-    const long long span = static_cast<long long>(NS) * R;
-    for (int k = 0; k < NS; ++k)
-      for (int r = 0; r < R; ++r) {
-        const long long e = (static_cast<long long>(r) * k) % span;
-        const double ang = -2.0 * pi * static_cast<double>(e) / static_cast<double>(span);
-        h[PL::tw_off(p) + k * R + r] = make_float2(static_cast<float>(std::cos(ang)),
-                                                   static_cast<float>(std::sin(ang)));
-      }
+    const double span = static_cast<double>(NS) * R;
+    for (int k = 0; k < NS; ++k) {  // base w_k; powers are generated in registers
+      const double ang = -2.0 * pi * static_cast<double>(k) / span;
+      h[PL::tw_off(p) + k] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+    }
   }
   // pairing table W^k = exp(-2 pi i k / N), N = 2M, k in [0, M/2]
   for (int k = 0; k <= M / 2; ++k) {
@@ -349,7 +352,7 @@ struct GroupBar {
 
 int ola_groups(int log2m) {
   const int M = 1 << log2m;
-  const int E = M < 16 ? M : (M >= 8192 ? 32 : 16);
+  const int E = M < RSG_E ? M : (M >= 8192 ? 32 : RSG_E);
   return cta_threads_of(log2m) / (M / E);
 }
 
@@ -511,6 +514,9 @@ template <int M>
 static cudaError_t set_attrs() {
   const int smem = static_cast<int>(ola_smem_bytes(Plan<M>::LOG));
   cudaError_t e;
+  const int carve = cudaSharedmemCarveoutMaxShared;
+  if ((e = cudaFuncSetAttribute(ola_kernel<M>, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
+  if ((e = cudaFuncSetAttribute(rir_spectrum_kernel<M>, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
   if ((e = cudaFuncSetAttribute(ola_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(rir_spectrum_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(rfft_forward_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
