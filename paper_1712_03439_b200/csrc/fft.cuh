@@ -348,7 +348,7 @@ __device__ __forceinline__ void inverse_but_last(float2* s, int t, const float2*
 }
 
 // Last inverse pass: reads smem, twiddles, DFT, then a barrier (smem may be
-// reused) and hands every output element to `emit(c, v)` in registers,
+// reused) and hands every output element to `emit(q, r, c, v)` in registers,
 // c = complex index in natural order (c = j + r*M/R).
 template <int M, class Bar, class Emit>
 __device__ __forceinline__ void stockham_emit_pass(float2* s, int t, const float2* __restrict__ tw,
@@ -382,7 +382,7 @@ __device__ __forceinline__ void stockham_emit_pass(float2* s, int t, const float
 #pragma unroll
     for (int q = 0; q < NB; ++q)
 #pragma unroll
-      for (int r = 0; r < R; ++r) emit(t + q * T + r * STRIDE, v[q][r]);
+      for (int r = 0; r < R; ++r) emit(q, r, t + q * T + r * STRIDE, v[q][r]);
   }
 }
 
@@ -394,10 +394,11 @@ __device__ __forceinline__ void stockham_emit_pass(float2* s, int t, const float
 //   P = X2 G[k], Q = X2m conj(G[M-k]), U = P + Q, V = (P - Q) conj(W^k)
 //   Z'[k] = U + i V,  Z'[M-k] = conj(U) + i conj(V).
 // W^k = exp(-2 pi i k / N) comes from the plan's pairing table.
-template <int M, class Bar = CtaBar>
+template <int M, class Bar = CtaBar, bool G_SMEM = false>
 __device__ __forceinline__ void spectral_multiply(float2* s, int t, const float2* __restrict__ G,
                                                   const float2* __restrict__ W, bool active,
                                                   Bar bar = Bar()) {
+  auto ldg = [](const float2* p) { return G_SMEM ? *p : ld_tw(p); };
   constexpr int T = Plan<M>::T;
   if (active) {
 #pragma unroll 2
@@ -409,8 +410,8 @@ __device__ __forceinline__ void spectral_multiply(float2* s, int t, const float2
       const float2 D = c_rot<false>(c_sub(a, b));
       const float2 wD = c_mul(w, D);
       const float2 X2 = c_add(S, wD), X2m = c_sub(S, wD);
-      const float2 P = c_mul(X2, ld_tw(G + k));
-      const float2 Q = c_mulc(X2m, ld_tw(G + (M - k)));
+      const float2 P = c_mul(X2, ldg(G + k));
+      const float2 Q = c_mulc(X2m, ldg(G + (M - k)));
       const float2 U = c_add(P, Q);
       const float2 V = c_mulc(c_sub(P, Q), w);
       s[PAD(k)] = make_float2(U.x - V.y, U.y + V.x);
@@ -421,8 +422,8 @@ __device__ __forceinline__ void spectral_multiply(float2* s, int t, const float2
         const float2 a = s[0];
         const float2 S = make_float2(2.f * a.x, 0.f), D = make_float2(2.f * a.y, 0.f);
         const float2 X2 = c_add(S, D), X2m = c_sub(S, D);
-        const float2 P = c_mul(X2, ld_tw(G + 0));
-        const float2 Q = c_mulc(X2m, ld_tw(G + M));
+        const float2 P = c_mul(X2, ldg(G + 0));
+        const float2 Q = c_mulc(X2m, ldg(G + M));
         const float2 U = c_add(P, Q), V = c_sub(P, Q);
         s[0] = make_float2(U.x - V.y, U.y + V.x);
       }
@@ -435,7 +436,7 @@ __device__ __forceinline__ void spectral_multiply(float2* s, int t, const float2
         const float2 D = c_rot<false>(c_sub(a, b));
         const float2 wD = c_mul(w, D);
         const float2 X2 = c_add(S, wD), X2m = c_sub(S, wD);
-        const float2 g = ld_tw(G + k);
+        const float2 g = ldg(G + k);
         const float2 P = c_mul(X2, g);
         const float2 Q = c_mulc(X2m, g);
         const float2 U = c_add(P, Q);

@@ -356,6 +356,148 @@ int ola_groups(int log2m) {
   return cta_threads_of(log2m) / (M / E);
 }
 
+// ---- small/medium transforms (M <= 4096): everything a block needs is in
+// shared memory.  Per group: the transform buffer, the pair's filter spectrum
+// G (staged once per work item), the N_h - 1 sample overlap carried from the
+// previous block (so the output is written once, final, never re-read), and
+// the next block's input, prefetched with cp.async while the current block is
+// transformed.
+constexpr int kSmallMaxLog2M = 12;
+
+template <int M>
+struct SmallLayout {  // float2 offsets inside one group's region
+  static constexpr int FFT = 0;
+  static constexpr int GS = Plan<M>::PADDED;
+  static constexpr int CARRY = GS + M + 2;        // N floats
+  static constexpr int STAGE = CARRY + M;         // N floats
+  static constexpr int TOTAL = STAGE + M;
+};
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+template <int M>
+__global__ void __launch_bounds__(cta_threads_of(Plan<M>::LOG), (Plan<M>::T > 256 ? 1 : RSG_OLA_MINB))
+ola_small_kernel(OlaArgs a) {
+  using PL = Plan<M>;
+  using LY = SmallLayout<M>;
+  extern __shared__ __align__(16) float2 smem[];
+  constexpr int T = PL::T;
+  constexpr int G = groups_of<M>();
+  constexpr int N = 2 * M;
+  const int g = threadIdx.x / T, t = threadIdx.x % T;
+  const int item = blockIdx.x * G + g;
+  const bool has = item < a.count;
+  const OlaItem it = a.items[has ? item : 0];
+  const PairPlan& pl = a.plan[it.pair];
+  const PairMeta& pm = a.pair[it.pair];
+  const float* __restrict__ x = a.signals + pm.sig_off;
+  const long long nx = pm.nx;
+  const float2* W = a.tw + PL::TW_PASS;
+  float* __restrict__ y = a.y + pl.y_off;
+  const int L = static_cast<int>(pl.L);
+  const int B = static_cast<int>(pl.B);
+  const int out_len = static_cast<int>(pl.out_len);
+  const int ovl = N - L;  // N_h - 1 samples overlap the next block
+  float2* base = smem + g * LY::TOTAL;
+  float2* s = base + LY::FFT;
+  float2* gs = base + LY::GS;
+  float* carry = reinterpret_cast<float*>(base + LY::CARRY);
+  float* stage = reinterpret_cast<float*>(base + LY::STAGE);
+  const GroupBar<T> bar{1 + g};
+  int trips = has ? it.b_end - it.b_begin : 0;
+  if constexpr (T < 32) trips = __reduce_max_sync(0xffffffffu, trips);
+  const int own_lo = it.b_own * L;
+  const int own_hi = it.b_end == B ? out_len : it.b_end * L;
+  auto prefetch = [&](int b) {  // block b's samples -> stage (4-byte cp.async: any alignment)
+    const long long st = static_cast<long long>(b) * L;
+    const int take = static_cast<int>(nx - st < L ? nx - st : L);
+    for (int i = t; i < take; i += T) cp_async4(stage + i, x + st + i);
+  };
+  if (has) {
+    const float2* Gsrc = a.spec + pl.spec_off;
+    for (int k = t; k <= M; k += T) cp_async8(gs + k, Gsrc + k);
+    for (int i = t; i < N; i += T) carry[i] = 0.f;
+    prefetch(it.b_begin);
+  }
+  double pw = 0.0;
+#pragma unroll 1
+  for (int k = 0; k < trips; ++k) {
+    const int b = it.b_begin + k;
+    const bool active = has && b < it.b_end;
+    const long long start = static_cast<long long>(b) * L;
+    const int take = active ? static_cast<int>(nx - start < L ? nx - start : L) : 0;
+    cp_async_wait_all();
+    bar();
+    first_pass<M>(s, t, active, stage, take, bar);
+    if (active && b + 1 < it.b_end) prefetch(b + 1);  // lands while this block is transformed
+    forward_rest<M>(s, t, a.tw, active, bar);
+    spectral_multiply<M, GroupBar<T>, true>(s, t, gs, W, active, bar);
+    inverse_but_last<M>(s, t, a.tw, active, bar);
+    // emit: e < L -> final output (carry + v), e >= L -> carry for block b+1
+    float* yb = y + start;
+    const int lo = own_lo - static_cast<int>(start);
+    const int hi = own_hi - static_cast<int>(start);
+    const bool last = b == B - 1;
+    constexpr int NB = PL::E / PL::radix(PL::NP - 1);
+    constexpr int R = PL::radix(PL::NP - 1);
+    float2 cin[NB][R];  // carry values of this thread's elements, read before the barrier
+    if (active) {
+#pragma unroll
+      for (int q = 0; q < NB; ++q)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int e0 = 2 * (t + q * T + r * (M / R));
+          cin[q][r].x = e0 < ovl ? carry[e0] : 0.f;
+          cin[q][r].y = e0 + 1 < ovl ? carry[e0 + 1] : 0.f;
+        }
+    }
+    stockham_emit_pass<M>(s, t, a.tw, active, bar, [&](int q, int r, int c, float2 v) {
+      const float2 acc = make_float2(cin[q][r].x + v.x, cin[q][r].y + v.y);
+      const int e0 = 2 * c;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = e0 + h;
+        const float val = h ? acc.y : acc.x;
+        if (e < L || last) {  // final sample
+          if (e >= lo && e < hi) {
+            yb[e] = val;
+            pw = fma(static_cast<double>(val), static_cast<double>(val), pw);
+          }
+        } else {
+          carry[e - L] = val;  // partial sum for the next block
+        }
+      }
+    });
+    // (N_h - 1 > L, three or more overlapping blocks, needs no extra step: the
+    // old carry at e in [L, ovl) was read into cin before the emit barrier.)
+  }
+  // Σ y^2 of the group (fixed order: deterministic) -> part[item]
+  if constexpr (T >= 32) {
+    __shared__ double red[cta_threads_of(PL::LOG) / 32];
+    for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pw;
+    bar();
+    if (t == 0 && has) {
+      double tot = 0.0;
+      for (int w = 0; w < T / 32; ++w) tot += red[g * (T / 32) + w];
+      a.part[item] = tot;
+    }
+  } else {
+    for (int o = T / 2; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
+    if (t == 0 && has) a.part[item] = pw;
+  }
+}
+
 template <int M>
 __global__ void __launch_bounds__(cta_threads_of(Plan<M>::LOG), (M >= 8192 ? 1 : RSG_OLA_MINB))
 ola_kernel(OlaArgs a) {
@@ -410,7 +552,7 @@ ola_kernel(OlaArgs a) {
     const int hi = static_cast<int>(min(own_hi - start, static_cast<long long>(N)));
     const int fe = (b == B - 1) ? N : L;  // e < fe: final after block b
     const int rmw_end = rmw ? ovl : 0;
-    stockham_emit_pass<M>(s, t, a.tw, active, bar, [&](int c, float2 v) {
+    stockham_emit_pass<M>(s, t, a.tw, active, bar, [&](int, int, int c, float2 v) {
 #ifdef RSG_TRIVIAL_EMIT
       yb[2 * c] = v.x; yb[2 * c + 1] = v.y;
 #else
@@ -510,14 +652,28 @@ rfft_inverse_kernel(const float2* in, float* out, int count, const float2* tw) {
 }
 
 // ---- dispatch over M ----------------------------------------------------------
+size_t k4_smem_bytes(int log2m) {
+  if (log2m > kSmallMaxLog2M) return ola_smem_bytes(log2m);
+  const int M = 1 << log2m;
+  const int per_group = (M + M / 16) + (M + 2) + M + M;  // SmallLayout<M>::TOTAL
+  return static_cast<size_t>(ola_groups(log2m)) * per_group * sizeof(float2);
+}
+
 template <int M>
 static cudaError_t set_attrs() {
   const int smem = static_cast<int>(ola_smem_bytes(Plan<M>::LOG));
   cudaError_t e;
   const int carve = cudaSharedmemCarveoutMaxShared;
-  if ((e = cudaFuncSetAttribute(ola_kernel<M>, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
+  if constexpr (Plan<M>::LOG <= kSmallMaxLog2M) {
+    static_assert(SmallLayout<M>::TOTAL == (M + M / 16) + (M + 2) + M + M, "layout");
+    if ((e = cudaFuncSetAttribute(ola_small_kernel<M>, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
+    if ((e = cudaFuncSetAttribute(ola_small_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(k4_smem_bytes(Plan<M>::LOG))))) return e;
+  } else {
+    if ((e = cudaFuncSetAttribute(ola_kernel<M>, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
+    if ((e = cudaFuncSetAttribute(ola_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  }
   if ((e = cudaFuncSetAttribute(rir_spectrum_kernel<M>, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
-  if ((e = cudaFuncSetAttribute(ola_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(rir_spectrum_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(rfft_forward_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(rfft_inverse_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
@@ -546,7 +702,10 @@ template <int M>
 static cudaError_t ola_t(const OlaArgs& a, cudaStream_t s) {
   constexpr int G = groups_of<M>();
   const int grid = (a.count + G - 1) / G;
-  ola_kernel<M><<<grid, cta_threads_of(Plan<M>::LOG), ola_smem_bytes(Plan<M>::LOG), s>>>(a);
+  if constexpr (Plan<M>::LOG <= kSmallMaxLog2M)
+    ola_small_kernel<M><<<grid, cta_threads_of(Plan<M>::LOG), k4_smem_bytes(Plan<M>::LOG), s>>>(a);
+  else
+    ola_kernel<M><<<grid, cta_threads_of(Plan<M>::LOG), k4_smem_bytes(Plan<M>::LOG), s>>>(a);
   return cudaGetLastError();
 }
 
