@@ -210,6 +210,7 @@ def ours(args, rank, world, local_rank):
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ola_ms, flops, launches = 0.0, 0.0, 0
+    stages = {}
     e0.record(stream)
     for _ in range(args.steps):
         res = step()
@@ -217,6 +218,8 @@ def ours(args, rank, world, local_rank):
         ola_ms += t["ola_ms"]
         flops += t["ola_flops"]
         launches += t["launches"]
+        for k, v in ctx.stage_times().items():
+            stages[k] = stages.get(k, 0.0) + v / args.steps
     e1.record(stream)
     torch.cuda.synchronize(dev)
     barrier()
@@ -309,6 +312,7 @@ def ours(args, rank, world, local_rank):
                        "l2": "inputs (%.1f GB/GPU) >> L2 (126 MB): no flush needed" % (4 * batch.total_samples / 1e9)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
+            "stage_ms": {k: round(v, 3) for k, v in stages.items()},
         }
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -67,6 +67,11 @@ int rs_ctx_synchronize(rs_ctx* ctx);
  * bytes of that render (SURVEY.md §8d formulas). */
 int rs_ctx_last_timing(rs_ctx* ctx, double* ola_ms, double* ola_flops,
                        double* alg_bytes, int64_t* kernel_launches);
+/* Device time (ms) of the stages of the last render (profiling on): [0] K1 synth,
+ * [1] K2 cut, [2] host planning gap, [3] K3 spectra, [4] K4 OLA, [5] K5+K6 gains
+ * and mix; host_plan_ms = host wall time of the planner.  Entries are -1 when
+ * unavailable. */
+int rs_ctx_stage_times(rs_ctx* ctx, double* ms, int n, double* host_plan_ms);
 /* Enable event timing of the OLA kernels (adds events; off by default). */
 int rs_ctx_set_profiling(rs_ctx* ctx, int enabled);
 

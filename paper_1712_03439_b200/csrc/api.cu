@@ -188,6 +188,11 @@ struct rs_ctx {
   cudaStream_t stream = nullptr;
   bool profiling = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // stage boundaries of the last render: begin, synth, cut, plan, spectrum, ola, end
+  static constexpr int kStages = 7;
+  cudaEvent_t st[kStages] = {};
+  bool st_valid = false;
+  double host_plan_ms = 0;
   float2* tw[kMaxLog2M + 1] = {};
   DevBuf tw_all;
   // arena
@@ -212,6 +217,7 @@ int ctx_init(rs_ctx* c) {
   c->stream = c->own;
   RS_CUDA(cudaEventCreate(&c->ev0));
   RS_CUDA(cudaEventCreate(&c->ev1));
+  for (auto& e : c->st) RS_CUDA(cudaEventCreate(&e));
   RS_CUDA(kernels_init());
   size_t total = 0;
   size_t off[kMaxLog2M + 1];
@@ -313,6 +319,7 @@ int run_filter(rs_ctx* c, std::vector<PairPlan>& plans, const float* d_signals,
   RS_TRY(c->y.ensure(std::max<int64_t>(y_total, 1) * sizeof(float)));
   RS_TRY(c->sumsq.ensure(std::max<size_t>(items.size(), 1) * sizeof(double)));
   const int32_t* d_lists = c->lists.as<int32_t>();
+  if (c->profiling) RS_CUDA(cudaEventRecord(c->st[3], c->stream));
   for (const Span& sp : spans) {
     SpecArgs a{d_lists + sp.list_off, static_cast<int32_t>(sp.list_n), c->pair.as<PairMeta>(),
                c->plan.as<PairPlan>(), d_rir, c->spec.as<float2>(), c->tw[sp.l]};
@@ -320,6 +327,7 @@ int run_filter(rs_ctx* c, std::vector<PairPlan>& plans, const float* d_signals,
     ++c->launches;
   }
   if (c->profiling) RS_CUDA(cudaEventRecord(c->ev0, c->stream));
+  if (c->profiling) RS_CUDA(cudaEventRecord(c->st[4], c->stream));
   for (const Span& sp : spans) {
     OlaArgs a{c->olaitems.as<OlaItem>() + sp.item_off, static_cast<int32_t>(sp.item_n),
               c->pair.as<PairMeta>(), c->plan.as<PairPlan>(), d_signals, c->spec.as<float2>(),
@@ -328,6 +336,7 @@ int run_filter(rs_ctx* c, std::vector<PairPlan>& plans, const float* d_signals,
     ++c->launches;
   }
   if (c->profiling) RS_CUDA(cudaEventRecord(c->ev1, c->stream));
+  if (c->profiling) RS_CUDA(cudaEventRecord(c->st[5], c->stream));
   if (flops_out) *flops_out = flops;
   return RS_OK;
 }
@@ -449,21 +458,26 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
   RS_TRY(c->rirout.ensure(std::max<int64_t>(P, 1) * sizeof(PairRir)));
   RS_CUDA(cudaMemsetAsync(c->rirout.p, 0, std::max<int64_t>(P, 1) * sizeof(PairRir), c->stream));
   // ---- K1 synth, K2 cut ---------------------------------------------------------
+  c->st_valid = c->profiling;
+  if (c->profiling) RS_CUDA(cudaEventRecord(c->st[0], c->stream));
   SynthArgs sa{c->utt.as<UttMeta>(), c->pair.as<PairMeta>(), c->rg.as<double>(),
                c->items.as<SynthItem>(), c->rir.as<double>(), c->rirout.as<PairRir>()};
   RS_CUDA(launch_synth(sa, static_cast<int>(items.size()), max_order, slice, c->stream));
   ++c->launches;
+  if (c->profiling) RS_CUDA(cudaEventRecord(c->st[1], c->stream));
   const double eta_factor = b->eta_db > 0.0 ? std::pow(10.0, -b->eta_db / 10.0) : 0.0;
   CutArgs ca{c->pair.as<PairMeta>(), c->utt.as<UttMeta>(), c->rir.as<double>(),
              c->rirout.as<PairRir>(), eta_factor};
   RS_CUDA(launch_cut(ca, static_cast<int>(P), c->stream));
   ++c->launches;
+  if (c->profiling) RS_CUDA(cudaEventRecord(c->st[2], c->stream));
   c->h_rir.resize(P);
   if (P)
     RS_CUDA(cudaMemcpyAsync(c->h_rir.data(), c->rirout.p, P * sizeof(PairRir), cudaMemcpyDeviceToHost,
                             c->stream));
   RS_CUDA(cudaStreamSynchronize(c->stream));
   // ---- errors in reference order, then the planner --------------------------------
+  const auto t_plan0 = std::chrono::steady_clock::now();
   std::vector<PairPlan> plans(P);
   std::vector<int64_t> ulen(U, 0);
   std::vector<int32_t> strategy(P, RS_OVERLAP_ADD);
@@ -508,6 +522,7 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
   for (int64_t u = 0; u < U; ++u)
     if (out_stride[u] < ulen[u]) return fail(RS_ERR_CONFIG, "output stride too small");
   // ---- K3 + K4 -------------------------------------------------------------------
+  c->host_plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_plan0).count();
   double flops = 0;
   RS_TRY(run_filter(c, plans, io.d_signals, c->rir.as<double>(), &flops));
   // ---- K5 gains + K6 mix ------------------------------------------------------------
@@ -549,6 +564,7 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
              c->gain.as<double>(), io.d_out, 4096};
   RS_CUDA(launch_mix(ma, static_cast<int64_t>(ch_utt.size()), max_stride, c->stream));
   ++c->launches;
+  if (c->profiling) RS_CUDA(cudaEventRecord(c->st[6], c->stream));
   // ---- results, degenerate-power check --------------------------------------------
   std::vector<int32_t> hflags(P);
   std::vector<double> hgain(P), hpower(P);
@@ -676,6 +692,8 @@ int rs_ctx_destroy(rs_ctx* c) {
   for (DevBuf* b : bufs) b->release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  for (auto& e : c->st)
+    if (e) cudaEventDestroy(e);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return RS_OK;
@@ -690,6 +708,20 @@ int rs_ctx_set_stream(rs_ctx* c, void* stream) {
 int rs_ctx_synchronize(rs_ctx* c) {
   RS_TRY(check_ctx(c));
   RS_CUDA(cudaStreamSynchronize(c->stream));
+  return RS_OK;
+}
+
+int rs_ctx_stage_times(rs_ctx* c, double* ms, int n, double* host_plan_ms) {
+  RS_TRY(check_ctx(c));
+  if (host_plan_ms) *host_plan_ms = c->host_plan_ms;
+  for (int i = 0; i < n; ++i) ms[i] = -1.0;
+  if (!c->st_valid) return RS_OK;
+  RS_CUDA(cudaEventSynchronize(c->st[rs_ctx::kStages - 1]));
+  for (int i = 0; i + 1 < rs_ctx::kStages && i < n; ++i) {
+    float f = 0;
+    RS_CUDA(cudaEventElapsedTime(&f, c->st[i], c->st[i + 1]));
+    ms[i] = f;
+  }
   return RS_OK;
 }
 

@@ -142,7 +142,7 @@ struct Plan {
   // complex elements per thread: whole transform for M < 16, else 16 (32 for
   // the two largest sizes so that T <= 512 threads keeps 128 registers).
 #ifndef RSG_E
-#define RSG_E 8  // complex elements (max radix) per thread; measured best on B200
+#define RSG_E 16  // complex elements (max radix) per thread; measured best on B200
 #endif
   static constexpr int E = M < RSG_E ? M : (M >= 8192 ? 32 : RSG_E);
   static constexpr int T = M / E;                          // threads per transform
@@ -184,9 +184,13 @@ __device__ __forceinline__ float2 ld_tw(const float2* p) {
   return v;
 }
 
-#ifndef RSG_TW_LOAD
-#define RSG_TW_LOAD(p) ld_tw(p)
-#endif
+// Twiddle-table load: from shared memory (TWS) or through the non-hoistable
+// global path.
+template <bool TWS>
+__device__ __forceinline__ float2 tw_load(const float2* p) {
+  if constexpr (TWS) return *p;
+  else return ld_tw(p);
+}
 
 // One Stockham pass (p > 0) of a transform stored in smem `s`, executed by the
 // T threads of a group (t = thread index within the group).  The caller
@@ -230,7 +234,7 @@ struct CtaBar {
   __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
 
-template <int M, int P, bool INV, class Bar = CtaBar>
+template <int M, int P, bool INV, class Bar = CtaBar, bool TWS = false>
 __device__ __forceinline__ void stockham_pass(float2* s, int t, const float2* __restrict__ tw,
                                               bool active, Bar bar = Bar()) {
   using PL = Plan<M>;
@@ -252,7 +256,7 @@ __device__ __forceinline__ void stockham_pass(float2* s, int t, const float2* __
           v[q][r] = s[PAD(t + q * T + r * STRIDE)];
       }
       if constexpr (NS > 1) {
-        const float2 w1 = RSG_TW_LOAD(tw + PL::tw_off(P) + (SAME_K ? kt : t + q * T));
+        const float2 w1 = tw_load<TWS>(tw + PL::tw_off(P) + (SAME_K ? kt : t + q * T));
         apply_twiddles<R, INV>(v[q], w1);
       }
       Dft<R, INV>::run(v[q]);
@@ -286,7 +290,7 @@ __device__ __forceinline__ void stockham_pass(float2* s, int t, const float2* __
 // Pass 0 of a forward transform whose packed input z[c] = (x[2c], x[2c+1])
 // comes straight from global memory: x points at the block start, elements
 // at or beyond `take` are the zero padding.  Writes smem, then syncs.
-template <int M, class Src, class Bar = CtaBar>
+template <int M, class Src, class Bar = CtaBar, bool NOCHK = false>
 __device__ __forceinline__ void first_pass(float2* s, int t, bool active, const Src* x, int take,
                                            Bar bar = Bar()) {
   using PL = Plan<M>;
@@ -301,8 +305,13 @@ __device__ __forceinline__ void first_pass(float2* s, int t, bool active, const 
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int off = 2 * r * STRIDE;
-        v[r].x = off < lim ? static_cast<float>(xb[off]) : 0.f;
-        v[r].y = off + 1 < lim ? static_cast<float>(xb[off + 1]) : 0.f;
+        if constexpr (NOCHK) {  // zero padding already in the source buffer
+          v[r].x = static_cast<float>(xb[off]);
+          v[r].y = static_cast<float>(xb[off + 1]);
+        } else {
+          v[r].x = off < lim ? static_cast<float>(xb[off]) : 0.f;
+          v[r].y = off + 1 < lim ? static_cast<float>(xb[off + 1]) : 0.f;
+        }
       }
       Dft<R, false>::run(v);
       if constexpr (R == 16) {
@@ -318,12 +327,12 @@ __device__ __forceinline__ void first_pass(float2* s, int t, bool active, const 
 }
 
 // Remaining forward passes 1..NP-1.
-template <int M, int P = 1, class Bar = CtaBar>
+template <int M, int P = 1, class Bar = CtaBar, bool TWS = false>
 __device__ __forceinline__ void forward_rest(float2* s, int t, const float2* tw, bool active,
                                              Bar bar = Bar()) {
   if constexpr (P < Plan<M>::NP) {
-    stockham_pass<M, P, false>(s, t, tw, active, bar);
-    forward_rest<M, P + 1>(s, t, tw, active, bar);
+    stockham_pass<M, P, false, Bar, TWS>(s, t, tw, active, bar);
+    forward_rest<M, P + 1, Bar, TWS>(s, t, tw, active, bar);
   }
 }
 
@@ -338,19 +347,19 @@ __device__ __forceinline__ void inverse_all(float2* s, int t, const float2* tw, 
 }
 
 // Inverse passes 0..NP-2 (smem -> smem); the last pass is stockham_emit_pass.
-template <int M, int P = 0, class Bar = CtaBar>
+template <int M, int P = 0, class Bar = CtaBar, bool TWS = false>
 __device__ __forceinline__ void inverse_but_last(float2* s, int t, const float2* tw, bool active,
                                                  Bar bar = Bar()) {
   if constexpr (P + 1 < Plan<M>::NP) {
-    stockham_pass<M, P, true>(s, t, tw, active, bar);
-    inverse_but_last<M, P + 1>(s, t, tw, active, bar);
+    stockham_pass<M, P, true, Bar, TWS>(s, t, tw, active, bar);
+    inverse_but_last<M, P + 1, Bar, TWS>(s, t, tw, active, bar);
   }
 }
 
 // Last inverse pass: reads smem, twiddles, DFT, then a barrier (smem may be
 // reused) and hands every output element to `emit(q, r, c, v)` in registers,
 // c = complex index in natural order (c = j + r*M/R).
-template <int M, class Bar, class Emit>
+template <int M, class Bar, class Emit, bool TWS = false, bool SYNC = true>
 __device__ __forceinline__ void stockham_emit_pass(float2* s, int t, const float2* __restrict__ tw,
                                                    bool active, Bar bar, Emit emit) {
   using PL = Plan<M>;
@@ -371,13 +380,13 @@ __device__ __forceinline__ void stockham_emit_pass(float2* s, int t, const float
           v[q][r] = s[PAD(t + q * T + r * STRIDE)];
       }
       if constexpr (NS > 1) {
-        const float2 w1 = RSG_TW_LOAD(tw + PL::tw_off(P) + t + q * T);  // k = j in the last pass
+        const float2 w1 = tw_load<TWS>(tw + PL::tw_off(P) + t + q * T);  // k = j in the last pass
         apply_twiddles<R, true>(v[q], w1);
       }
       Dft<R, true>::run(v[q]);
     }
   }
-  bar();
+  if constexpr (SYNC) bar();
   if (active) {
 #pragma unroll
     for (int q = 0; q < NB; ++q)
@@ -394,18 +403,19 @@ __device__ __forceinline__ void stockham_emit_pass(float2* s, int t, const float
 //   P = X2 G[k], Q = X2m conj(G[M-k]), U = P + Q, V = (P - Q) conj(W^k)
 //   Z'[k] = U + i V,  Z'[M-k] = conj(U) + i conj(V).
 // W^k = exp(-2 pi i k / N) comes from the plan's pairing table.
-template <int M, class Bar = CtaBar, bool G_SMEM = false>
+template <int M, class Bar = CtaBar, bool G_SMEM = false, bool TWS = false>
 __device__ __forceinline__ void spectral_multiply(float2* s, int t, const float2* __restrict__ G,
                                                   const float2* __restrict__ W, bool active,
                                                   Bar bar = Bar()) {
   auto ldg = [](const float2* p) { return G_SMEM ? *p : ld_tw(p); };
+  auto ldw = [](const float2* p) { return tw_load<TWS>(p); };
   constexpr int T = Plan<M>::T;
   if (active) {
 #pragma unroll 2
     for (int k = 1 + t; k < M / 2; k += T) {  // k in [1, M/2)
       const float2 a = s[PAD(k)];
       const float2 b = c_conj(s[PAD(M - k)]);
-      const float2 w = ld_tw(W + k);
+      const float2 w = ldw(W + k);
       const float2 S = c_add(a, b);
       const float2 D = c_rot<false>(c_sub(a, b));
       const float2 wD = c_mul(w, D);
@@ -431,7 +441,7 @@ __device__ __forceinline__ void spectral_multiply(float2* s, int t, const float2
         const int k = M / 2;
         const float2 a = s[PAD(k)];
         const float2 b = c_conj(a);
-        const float2 w = ld_tw(W + k);
+        const float2 w = ldw(W + k);
         const float2 S = c_add(a, b);
         const float2 D = c_rot<false>(c_sub(a, b));
         const float2 wD = c_mul(w, D);

@@ -15,11 +15,11 @@
 #include "kernels.cuh"
 
 #ifndef RSG_E
-#define RSG_E 8  // complex elements (max radix) per thread; measured best on B200
+#define RSG_E 16  // complex elements (max radix) per thread; measured best on B200
 #endif
 
 #ifndef RSG_OLA_MINB
-#define RSG_OLA_MINB 2
+#define RSG_OLA_MINB 1
 #endif
 
 namespace rsg {
@@ -368,8 +368,8 @@ template <int M>
 struct SmallLayout {  // float2 offsets inside one group's region
   static constexpr int FFT = 0;
   static constexpr int GS = Plan<M>::PADDED;
-  static constexpr int CARRY = GS + M + 2;        // N floats
-  static constexpr int STAGE = CARRY + M;         // N floats
+  static constexpr int CARRY = GS + M + 2;        // 2 x N floats (double-buffered)
+  static constexpr int STAGE = CARRY + 2 * M;     // N floats
   static constexpr int TOTAL = STAGE + M;
 };
 
@@ -394,6 +394,7 @@ ola_small_kernel(OlaArgs a) {
   constexpr int T = PL::T;
   constexpr int G = groups_of<M>();
   constexpr int N = 2 * M;
+  constexpr int CTA = cta_threads_of(PL::LOG);
   const int g = threadIdx.x / T, t = threadIdx.x % T;
   const int item = blockIdx.x * G + g;
   const bool has = item < a.count;
@@ -402,68 +403,93 @@ ola_small_kernel(OlaArgs a) {
   const PairMeta& pm = a.pair[it.pair];
   const float* __restrict__ x = a.signals + pm.sig_off;
   const long long nx = pm.nx;
-  const float2* W = a.tw + PL::TW_PASS;
   float* __restrict__ y = a.y + pl.y_off;
   const int L = static_cast<int>(pl.L);
   const int B = static_cast<int>(pl.B);
   const int out_len = static_cast<int>(pl.out_len);
-  const int ovl = N - L;  // N_h - 1 samples overlap the next block
-  float2* base = smem + g * LY::TOTAL;
+  constexpr int TWN = (PL::TW_TOTAL + 1) & ~1;  // per-CTA twiddle tables (pass bases + W)
+  float2* tws = smem;
+  float2* base = smem + TWN + g * LY::TOTAL;
   float2* s = base + LY::FFT;
   float2* gs = base + LY::GS;
-  float* carry = reinterpret_cast<float*>(base + LY::CARRY);
-  float* stage = reinterpret_cast<float*>(base + LY::STAGE);
+  float* carry0 = reinterpret_cast<float*>(base + LY::CARRY);  // 2 x N floats, zero beyond N_h - 1
+  float* stage = reinterpret_cast<float*>(base + LY::STAGE);  // N floats, zero beyond the block
   const GroupBar<T> bar{1 + g};
   int trips = has ? it.b_end - it.b_begin : 0;
   if constexpr (T < 32) trips = __reduce_max_sync(0xffffffffu, trips);
   const int own_lo = it.b_own * L;
   const int own_hi = it.b_end == B ? out_len : it.b_end * L;
-  auto prefetch = [&](int b) {  // block b's samples -> stage (4-byte cp.async: any alignment)
+  // block b's samples -> stage[0, take) (4-byte cp.async: any alignment); fixed
+  // trip count N/T = 2E, predicated
+  auto prefetch = [&](int b) {
     const long long st = static_cast<long long>(b) * L;
     const int take = static_cast<int>(nx - st < L ? nx - st : L);
-    for (int i = t; i < take; i += T) cp_async4(stage + i, x + st + i);
+    const float* src = x + st;
+#pragma unroll
+    for (int m = 0; m < N / T; ++m) {
+      const int i = t + m * T;
+      if (i < take) cp_async4(stage + i, src + i);
+    }
   };
+  for (int i = threadIdx.x; i < PL::TW_TOTAL; i += CTA) cp_async8(tws + i, a.tw + i);
+  const float2* W = tws + PL::TW_PASS;
   if (has) {
     const float2* Gsrc = a.spec + pl.spec_off;
     for (int k = t; k <= M; k += T) cp_async8(gs + k, Gsrc + k);
-    for (int i = t; i < N; i += T) carry[i] = 0.f;
+    for (int i = t; i < 2 * N; i += T) carry0[i] = 0.f;
+    for (int i = L + t; i < N; i += T) stage[i] = 0.f;  // zero padding of every block
     prefetch(it.b_begin);
   }
-  double pw = 0.0;
+  cp_async_wait_all();
+  __syncthreads();  // per-CTA twiddles, G, carry and padding in place (all threads)
+  double pw4[4] = {0.0, 0.0, 0.0, 0.0};
+  constexpr int R = PL::radix(PL::NP - 1);
+  constexpr int NB = PL::E / R;
 #pragma unroll 1
   for (int k = 0; k < trips; ++k) {
     const int b = it.b_begin + k;
     const bool active = has && b < it.b_end;
     const long long start = static_cast<long long>(b) * L;
-    const int take = active ? static_cast<int>(nx - start < L ? nx - start : L) : 0;
+    const int take = active ? static_cast<int>(nx - start < L ? nx - start : L) : L;
     cp_async_wait_all();
+    if (take < L)  // the signal ends inside this block: clear stale samples
+      for (int i = take + t; i < L; i += T) stage[i] = 0.f;
     bar();
-    first_pass<M>(s, t, active, stage, take, bar);
+    first_pass<M, float, GroupBar<T>, true>(s, t, active, stage, N, bar);
     if (active && b + 1 < it.b_end) prefetch(b + 1);  // lands while this block is transformed
-    forward_rest<M>(s, t, a.tw, active, bar);
-    spectral_multiply<M, GroupBar<T>, true>(s, t, gs, W, active, bar);
-    inverse_but_last<M>(s, t, a.tw, active, bar);
+    forward_rest<M, 1, GroupBar<T>, true>(s, t, tws, active, bar);
+    spectral_multiply<M, GroupBar<T>, true, true>(s, t, gs, W, active, bar);
+    inverse_but_last<M, 0, GroupBar<T>, true>(s, t, tws, active, bar);
     // emit: e < L -> final output (carry + v), e >= L -> carry for block b+1
     float* yb = y + start;
     const int lo = own_lo - static_cast<int>(start);
     const int hi = own_hi - static_cast<int>(start);
     const bool last = b == B - 1;
-    constexpr int NB = PL::E / PL::radix(PL::NP - 1);
-    constexpr int R = PL::radix(PL::NP - 1);
-    float2 cin[NB][R];  // carry values of this thread's elements, read before the barrier
-    if (active) {
-#pragma unroll
-      for (int q = 0; q < NB; ++q)
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int e0 = 2 * (t + q * T + r * (M / R));
-          cin[q][r].x = e0 < ovl ? carry[e0] : 0.f;
-          cin[q][r].y = e0 + 1 < ovl ? carry[e0 + 1] : 0.f;
-        }
-    }
-    stockham_emit_pass<M>(s, t, a.tw, active, bar, [&](int q, int r, int c, float2 v) {
-      const float2 acc = make_float2(cin[q][r].x + v.x, cin[q][r].y + v.y);
+    const bool fast = lo <= 0 && hi >= L && !last;  // interior block of the owned range
+    // carry of this block (read) and of the next (written): double-buffered, so
+    // the emit needs no barrier and nothing stays live across one
+    const float* cin = carry0 + (k & 1) * N;
+    float* carry = carry0 + ((k + 1) & 1) * N;
+    auto emit_fn = [&](int q, int r, int c, float2 v) {
       const int e0 = 2 * c;
+      const float2 ci = *reinterpret_cast<const float2*>(cin + e0);
+      const float2 acc = make_float2(ci.x + v.x, ci.y + v.y);
+      double& p = pw4[(q * R + r) & 3];  // 4 independent FP64 chains
+      if (fast) {
+        if (e0 < L) {
+          yb[e0] = acc.x;
+          p = fma(static_cast<double>(acc.x), static_cast<double>(acc.x), p);
+        } else {
+          carry[e0 - L] = acc.x;
+        }
+        if (e0 + 1 < L) {
+          yb[e0 + 1] = acc.y;
+          p = fma(static_cast<double>(acc.y), static_cast<double>(acc.y), p);
+        } else {
+          carry[e0 + 1 - L] = acc.y;
+        }
+        return;
+      }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int e = e0 + h;
@@ -471,19 +497,21 @@ ola_small_kernel(OlaArgs a) {
         if (e < L || last) {  // final sample
           if (e >= lo && e < hi) {
             yb[e] = val;
-            pw = fma(static_cast<double>(val), static_cast<double>(val), pw);
+            p = fma(static_cast<double>(val), static_cast<double>(val), p);
           }
         } else {
           carry[e - L] = val;  // partial sum for the next block
         }
       }
-    });
+    };
+    stockham_emit_pass<M, GroupBar<T>, decltype(emit_fn), true, false>(s, t, tws, active, bar, emit_fn);
     // (N_h - 1 > L, three or more overlapping blocks, needs no extra step: the
-    // old carry at e in [L, ovl) was read into cin before the emit barrier.)
+    // old carry at e in [L, N_h - 1) comes from the other buffer.)
   }
   // Σ y^2 of the group (fixed order: deterministic) -> part[item]
+  double pw = (pw4[0] + pw4[1]) + (pw4[2] + pw4[3]);
   if constexpr (T >= 32) {
-    __shared__ double red[cta_threads_of(PL::LOG) / 32];
+    __shared__ double red[CTA / 32];
     for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pw;
     bar();
@@ -655,8 +683,9 @@ rfft_inverse_kernel(const float2* in, float* out, int count, const float2* tw) {
 size_t k4_smem_bytes(int log2m) {
   if (log2m > kSmallMaxLog2M) return ola_smem_bytes(log2m);
   const int M = 1 << log2m;
-  const int per_group = (M + M / 16) + (M + 2) + M + M;  // SmallLayout<M>::TOTAL
-  return static_cast<size_t>(ola_groups(log2m)) * per_group * sizeof(float2);
+  const int per_group = (M + M / 16) + (M + 2) + 2 * M + M;  // SmallLayout<M>::TOTAL
+  const int twn = (tw_total(log2m) + 1) & ~1;            // per-CTA twiddle tables
+  return (static_cast<size_t>(ola_groups(log2m)) * per_group + twn) * sizeof(float2);
 }
 
 template <int M>
@@ -665,7 +694,7 @@ static cudaError_t set_attrs() {
   cudaError_t e;
   const int carve = cudaSharedmemCarveoutMaxShared;
   if constexpr (Plan<M>::LOG <= kSmallMaxLog2M) {
-    static_assert(SmallLayout<M>::TOTAL == (M + M / 16) + (M + 2) + M + M, "layout");
+    static_assert(SmallLayout<M>::TOTAL == (M + M / 16) + (M + 2) + 2 * M + M, "layout");
     if ((e = cudaFuncSetAttribute(ola_small_kernel<M>, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
     if ((e = cudaFuncSetAttribute(ola_small_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(k4_smem_bytes(Plan<M>::LOG))))) return e;

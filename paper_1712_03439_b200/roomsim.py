@@ -93,7 +93,7 @@ LAYOUT_DTYPE = np.dtype([("rir_len", np.int64), ("rir_keep", np.int64), ("cutoff
 # Every symbol include/roomsim_gpu.h declares (checked by tests/test_abi.py).
 ABI_SYMBOLS = [
     "rs_last_error", "rs_version", "rs_ctx_create", "rs_ctx_destroy", "rs_ctx_set_stream",
-    "rs_ctx_synchronize", "rs_ctx_last_timing", "rs_ctx_set_profiling", "rs_cost_direct",
+    "rs_ctx_synchronize", "rs_ctx_last_timing", "rs_ctx_stage_times", "rs_ctx_set_profiling", "rs_cost_direct",
     "rs_cost_full_fft", "rs_cost_ola", "rs_ola_block_count", "rs_plan_for", "rs_choose_plan",
     "rs_rfft_forward", "rs_rfft_inverse", "rs_synthesize_rir", "rs_truncate_rir",
     "rs_convolve_ola", "rs_convolve_full_fft", "rs_convolve", "rs_batch_num_pairs",
@@ -123,6 +123,7 @@ def load_library() -> C.CDLL:
         "rs_ctx_synchronize": (C.c_int, [vp]),
         "rs_ctx_last_timing": (C.c_int, [vp, dp, dp, dp, C.POINTER(i64)]),
         "rs_ctx_set_profiling": (C.c_int, [vp, C.c_int]),
+        "rs_ctx_stage_times": (C.c_int, [vp, dp, C.c_int, dp]),
         "rs_cost_direct": (d, [d, d, sz, sz]),
         "rs_cost_full_fft": (d, [d, d, sz, sz, sz]),
         "rs_cost_ola": (d, [d, d, sz, sz, sz]),
@@ -239,6 +240,17 @@ class Context:
 
     def synchronize(self) -> None:
         _check(load_library().rs_ctx_synchronize(self.h))
+
+    STAGES = ("synth", "cut", "plan_gap", "spectrum", "ola", "gain_mix")
+
+    def stage_times(self) -> dict:
+        """Device ms per stage of the last render (profiling on) + host planner ms."""
+        arr = (C.c_double * 6)()
+        hp = C.c_double()
+        _check(load_library().rs_ctx_stage_times(self.h, arr, 6, C.byref(hp)))
+        d = {k: arr[i] for i, k in enumerate(self.STAGES)}
+        d["host_plan_ms"] = hp.value
+        return d
 
     def last_timing(self):
         ms, fl, by = C.c_double(), C.c_double(), C.c_double()
