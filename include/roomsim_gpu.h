@@ -2,7 +2,7 @@
  * roomsim_gpu.h — C-ABI of the B200 (sm_100a) room-simulation hot path.
  *
  * This is the drop-in boundary between the reference's C++ simulator API
- * (header-only library `roomsim`, /root/reference/proj/include/roomsim/*.hpp)
+ * (header-only library `roomsim`, /root/reference/proj/include/roomsim/X.hpp)
  * and the hand-written CUDA kernels in paper_1712_03439_b200/csrc/.  Every
  * entry point takes plain pointers and sizes; no CUDA or torch types appear
  * in the signatures (streams are passed as opaque `void*`).
@@ -67,10 +67,11 @@ int rs_ctx_synchronize(rs_ctx* ctx);
  * bytes of that render (SURVEY.md §8d formulas). */
 int rs_ctx_last_timing(rs_ctx* ctx, double* ola_ms, double* ola_flops,
                        double* alg_bytes, int64_t* kernel_launches);
-/* Device time (ms) of the stages of the last render (profiling on): [0] K1 synth,
- * [1] K2 cut, [2] host planning gap, [3] K3 spectra, [4] K4 OLA, [5] K5+K6 gains
- * and mix; host_plan_ms = host wall time of the planner.  Entries are -1 when
- * unavailable. */
+/* Device time (ms) of the stages of the last render (profiling on), summed over
+ * the render's chunks: [0] inputs + K1 synth + K2 cut (stream A), [4] K4 OLA,
+ * [5] K5 gains + K6 mix (stream B); [1..3] are 0 (the host planner and K3 run
+ * overlapped with the other stream); host_plan_ms = host wall time of the
+ * planner.  Entries are -1 when unavailable. */
 int rs_ctx_stage_times(rs_ctx* ctx, double* ms, int n, double* host_plan_ms);
 /* Enable event timing of the OLA kernels (adds events; off by default). */
 int rs_ctx_set_profiling(rs_ctx* ctx, int enabled);

@@ -75,6 +75,42 @@ struct DevBuf {
   }
 };
 
+// Page-locked host staging (bump allocator) so H2D/D2H copies are truly async.
+struct PinnedArena {
+  char* p = nullptr;
+  size_t cap = 0, used = 0;
+  int reserve(size_t bytes) {  // only call while no copy from this arena is pending
+    if (bytes <= cap) return RS_OK;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = bytes + bytes / 4 + 4096;
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p), want, cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      return fail(RS_ERR_OOM, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+    }
+    cap = want;
+    return RS_OK;
+  }
+  void reset() { used = 0; }
+  template <class T>
+  T* alloc(size_t n) {
+    used = (used + 63) & ~size_t(63);
+    T* r = reinterpret_cast<T*>(p + used);
+    used += std::max<size_t>(n, 1) * sizeof(T);
+    return used <= cap ? r : nullptr;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+template <class T>
+size_t staged_bytes(const std::vector<T>& v) { return ((std::max<size_t>(v.size(), 1) * sizeof(T) + 63) & ~size_t(63)) + 64; }
+
 size_t bit_ceil_sz(size_t n) {
   size_t p = 1;
   while (p < n) p <<= 1;
@@ -193,12 +229,15 @@ struct rs_ctx {
   cudaEvent_t st[kStages] = {};
   bool st_valid = false;
   double host_plan_ms = 0;
+  double stage_ms[6] = {};
+  bool stage_valid = false;
   float2* tw[kMaxLog2M + 1] = {};
   DevBuf tw_all;
   // arena
   DevBuf utt, pair, rg, items, olaitems, rir, rirout, plan, lists, spec, y, sumsq, gain, power, flags,
       snr, chan_utt, chan_mic, chan_out, utt_len, utt_stride, utt_pair0, utt_I, utt_J, sig, out,
       scratch_a, scratch_b;
+  struct rs_render_state* rs = nullptr;
   // last render (debug fetch)
   std::vector<PairPlan> h_plan;
   std::vector<PairMeta> h_pair;
@@ -247,97 +286,136 @@ double pair_flops(const PairPlan& p) {
   return (2.0 * static_cast<double>(p.B) + 1.0) * 5.0 * n * p.log2n;
 }
 
-// ---- stage B: spectrum + OLA over planned pairs (shared by render/convolve) ----
+// ---- stage B: spectrum + OLA over planned pairs --------------------------------
 // Pairs are bucketed by transform size; buckets run largest work first.  Each
 // pair's blocks are split into runs (K4 work items) long enough that the
 // recomputed overlap blocks cost <= ~6%, short enough to fill the GPU.
-int run_filter(rs_ctx* c, std::vector<PairPlan>& plans, const float* d_signals,
-               const double* d_rir, double* flops_out) {
+struct Span { int l; int64_t list_off, list_n, item_off, item_n; };
+
+struct FilterPlan {
+  std::vector<int32_t> lists;
+  std::vector<OlaItem> items;
+  std::vector<Span> spans;
+  int64_t spec_total = 0, y_total = 0;
+  double flops = 0;
+};
+
+int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
   const int64_t n_pairs = static_cast<int64_t>(plans.size());
   std::vector<std::vector<int32_t>> bucket(kMaxLog2M + 1);
   std::vector<double> work(n_pairs);
-  double flops = 0;
+  fp.flops = 0;
   for (int64_t p = 0; p < n_pairs; ++p) {
     const int l = plans[p].log2n - 1;
     if (l < 0 || l > kMaxLog2M) return fail(RS_ERR_UNSUPPORTED, "FFT size outside the supported range");
     bucket[l].push_back(static_cast<int32_t>(p));
     work[p] = pair_flops(plans[p]);
-    flops += work[p];
+    fp.flops += work[p];
   }
-  std::vector<int32_t> lists;
-  std::vector<OlaItem> items;
-  struct Span { int l; int64_t list_off, list_n, item_off, item_n; };
-  std::vector<Span> spans;
   std::vector<int> order(kMaxLog2M + 1);
   std::iota(order.begin(), order.end(), 0);
   std::vector<double> bucket_work(kMaxLog2M + 1, 0.0);
   for (int l = 0; l <= kMaxLog2M; ++l)
     for (int32_t p : bucket[l]) bucket_work[l] += work[p];
   std::sort(order.begin(), order.end(), [&](int a, int b) { return bucket_work[a] > bucket_work[b]; });
+  fp.lists.clear();
+  fp.items.clear();
+  fp.spans.clear();
   for (int l : order) {
     auto& v = bucket[l];
     if (v.empty()) continue;
     // largest pairs first (LPT) so the tail of the launch is short
     std::stable_sort(v.begin(), v.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
-    int64_t total_blocks = 0;
-    int64_t max_pre = 1;
+    int64_t total_blocks = 0, max_pre = 1;
     for (int32_t p : v) {
       total_blocks += plans[p].B;
       const int64_t n = int64_t(1) << plans[p].log2n;
       max_pre = std::max<int64_t>(max_pre, (n - plans[p].L + plans[p].L - 1) / plans[p].L);
     }
     const int64_t slots = 148LL * 2 * ola_groups(l);
-    int64_t run = std::max<int64_t>((total_blocks + 4 * slots - 1) / (4 * slots), 16 * max_pre);
-    Span sp{l, static_cast<int64_t>(lists.size()), static_cast<int64_t>(v.size()),
-            static_cast<int64_t>(items.size()), 0};
+    const int64_t run = std::max<int64_t>((total_blocks + 4 * slots - 1) / (4 * slots), 16 * max_pre);
+    Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
+            static_cast<int64_t>(fp.items.size()), 0};
     for (int32_t p : v) {
       PairPlan& pl = plans[p];
       const int64_t n = int64_t(1) << pl.log2n;
       const int64_t pre = (n - pl.L + pl.L - 1) / pl.L;  // ceil((N_h - 1) / L)
-      pl.item0 = static_cast<int64_t>(items.size());
+      pl.item0 = static_cast<int64_t>(fp.items.size());
       pl.nitems = 0;
       for (int64_t r0 = 0; r0 < pl.B; r0 += run) {
         const int64_t r1 = std::min<int64_t>(pl.B, r0 + run);
         const int64_t b0 = r0 == 0 ? 0 : std::max<int64_t>(0, r0 - pre);
-        items.push_back(OlaItem{p, static_cast<int32_t>(b0), static_cast<int32_t>(r0), static_cast<int32_t>(r1)});
+        fp.items.push_back(OlaItem{p, static_cast<int32_t>(b0), static_cast<int32_t>(r0), static_cast<int32_t>(r1)});
         ++pl.nitems;
       }
     }
-    sp.item_n = static_cast<int64_t>(items.size()) - sp.item_off;
-    spans.push_back(sp);
-    lists.insert(lists.end(), v.begin(), v.end());
+    sp.item_n = static_cast<int64_t>(fp.items.size()) - sp.item_off;
+    fp.spans.push_back(sp);
+    fp.lists.insert(fp.lists.end(), v.begin(), v.end());
   }
-  RS_TRY(upload(c, c->lists, lists));
-  RS_TRY(upload(c, c->plan, plans));
-  RS_TRY(upload(c, c->olaitems, items));
-  int64_t spec_total = 0, y_total = 0;
-  for (const auto& p : plans) {
-    spec_total = std::max<int64_t>(spec_total, p.spec_off + (int64_t(1) << (p.log2n - 1)) + 1);
-    y_total = std::max<int64_t>(y_total, p.y_off + p.out_len);
+  fp.spec_total = fp.y_total = 0;
+  for (const auto& q : plans) {
+    fp.spec_total = std::max<int64_t>(fp.spec_total, q.spec_off + (int64_t(1) << (q.log2n - 1)) + 1);
+    fp.y_total = std::max<int64_t>(fp.y_total, q.y_off + q.out_len);
   }
-  RS_TRY(c->spec.ensure(std::max<int64_t>(spec_total, 1) * sizeof(float2)));
-  RS_TRY(c->y.ensure(std::max<int64_t>(y_total, 1) * sizeof(float)));
-  RS_TRY(c->sumsq.ensure(std::max<size_t>(items.size(), 1) * sizeof(double)));
-  const int32_t* d_lists = c->lists.as<int32_t>();
-  if (c->profiling) RS_CUDA(cudaEventRecord(c->st[3], c->stream));
-  for (const Span& sp : spans) {
-    SpecArgs a{d_lists + sp.list_off, static_cast<int32_t>(sp.list_n), c->pair.as<PairMeta>(),
-               c->plan.as<PairPlan>(), d_rir, c->spec.as<float2>(), c->tw[sp.l]};
-    RS_CUDA(launch_spectrum(sp.l, a, c->stream));
+  return RS_OK;
+}
+
+// Device buffers of one filter stage (K3 + K4 + K5 + K6 of a chunk).
+struct FilterBufs {
+  DevBuf plan, lists, olaitems, spec, y, part;
+};
+
+// Async H2D of a host vector through a pinned arena (or synchronously staged
+// pageable memory when `arena` is null).
+template <class T>
+int upload_on(DevBuf& b, const std::vector<T>& v, cudaStream_t st, PinnedArena* arena) {
+  RS_TRY(b.ensure(std::max<size_t>(v.size(), 1) * sizeof(T)));
+  if (v.empty()) return RS_OK;
+  const void* src = v.data();
+  if (arena) {
+    T* h = arena->alloc<T>(v.size());
+    if (!h) return fail(RS_ERR_OOM, "pinned staging arena exhausted");
+    std::memcpy(h, v.data(), v.size() * sizeof(T));
+    src = h;
+  }
+  RS_CUDA(cudaMemcpyAsync(b.p, src, v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  return RS_OK;
+}
+
+int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<PairPlan>& plans,
+                  const PairMeta* d_pair, const double* d_rir, const float* d_signals, cudaStream_t st,
+                  PinnedArena* arena, cudaEvent_t ev_k4a, cudaEvent_t ev_k4b);
+
+template <class T>
+int upload(rs_ctx* c, DevBuf& b, const std::vector<T>& v);
+
+// K3 + K4 of a planned set of pairs on stream `st`.
+int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<PairPlan>& plans,
+                  const PairMeta* d_pair, const double* d_rir, const float* d_signals, cudaStream_t st,
+                  PinnedArena* arena, cudaEvent_t ev_k4a, cudaEvent_t ev_k4b) {
+  RS_TRY(upload_on(fb.lists, fp.lists, st, arena));
+  RS_TRY(upload_on(fb.plan, plans, st, arena));
+  RS_TRY(upload_on(fb.olaitems, fp.items, st, arena));
+  RS_TRY(fb.spec.ensure(std::max<int64_t>(fp.spec_total, 1) * sizeof(float2)));
+  RS_TRY(fb.y.ensure(std::max<int64_t>(fp.y_total, 1) * sizeof(float)));
+  RS_TRY(fb.part.ensure(std::max<size_t>(fp.items.size(), 1) * sizeof(double)));
+  const int32_t* d_lists = fb.lists.as<int32_t>();
+  for (const Span& sp : fp.spans) {
+    SpecArgs a{d_lists + sp.list_off, static_cast<int32_t>(sp.list_n), d_pair, fb.plan.as<PairPlan>(),
+               d_rir, fb.spec.as<float2>(), c->tw[sp.l]};
+    RS_CUDA(launch_spectrum(sp.l, a, st));
     ++c->launches;
   }
-  if (c->profiling) RS_CUDA(cudaEventRecord(c->ev0, c->stream));
-  if (c->profiling) RS_CUDA(cudaEventRecord(c->st[4], c->stream));
-  for (const Span& sp : spans) {
-    OlaArgs a{c->olaitems.as<OlaItem>() + sp.item_off, static_cast<int32_t>(sp.item_n),
-              c->pair.as<PairMeta>(), c->plan.as<PairPlan>(), d_signals, c->spec.as<float2>(),
-              c->y.as<float>(), c->sumsq.as<double>() + sp.item_off, c->tw[sp.l]};
-    RS_CUDA(launch_ola(sp.l, a, c->stream));
+  if (ev_k4a) RS_CUDA(cudaEventRecord(ev_k4a, st));
+  for (const Span& sp : fp.spans) {
+    OlaArgs a{fb.olaitems.as<OlaItem>() + sp.item_off, static_cast<int32_t>(sp.item_n), d_pair,
+              fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(),
+              fb.part.as<double>() + sp.item_off, c->tw[sp.l]};
+    RS_CUDA(launch_ola(sp.l, a, st));
     ++c->launches;
   }
-  if (c->profiling) RS_CUDA(cudaEventRecord(c->ev1, c->stream));
-  if (c->profiling) RS_CUDA(cudaEventRecord(c->st[5], c->stream));
-  if (flops_out) *flops_out = flops;
+  if (ev_k4b) RS_CUDA(cudaEventRecord(ev_k4b, st));
   return RS_OK;
 }
 
@@ -350,48 +428,100 @@ int finish_timing(rs_ctx* c) {
   return RS_OK;
 }
 
-// ---- the batched render ------------------------------------------------------
+// ---- the batched render: a chunked two-stream pipeline -----------------------
+// Utterances are processed in chunks.  Stream A runs chunk k's input upload,
+// K1 (synth) and K2 (cut) and returns the per-pair RIR summary to pinned host
+// memory; the host plans chunk k (reference planner) while the GPU is busy
+// with chunk k-1's filter on stream B; stream B then runs K3, K4, K5, K6 and
+// the output download of chunk k.  Chunks are independent (utterances share
+// nothing), so results do not depend on the chunking.
 struct RenderIO {
-  const float* d_signals;  // device signals (already offset so sig_off indexes it)
-  float* d_out;            // device output base
+  const float* d_signals;  // device signals (sig_off indexes them)
+  float* d_out;            // device output base (out_off indexes it)
+  const float* h_signals;  // host path: upload per chunk into d_signals
+  float* h_out;            // host path: download per chunk from d_out
 };
 
-int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const int64_t* out_off,
-                const int64_t* out_stride, int64_t* out_len, rs_pair_layout* layout,
-                double* gains, double* power) {
-  if (!b || b->n_utt < 0) return fail(RS_ERR_CONFIG, "invalid scene batch");
-  const int64_t U = b->n_utt;
-  c->launches = 0;
-  // ---- host validation + metadata -------------------------------------------
-  std::vector<UttMeta> utt(U);
+struct Chunk {
+  int64_t u0 = 0, u1 = 0, p0 = 0, P = 0;
+  std::vector<UttMeta> utt;
   std::vector<double> rg;
-  std::vector<PairMeta> pairs;
-  std::vector<int64_t> pair0(U + 1, 0);
-  std::vector<int32_t> uI(U), uJ(U);
-  std::vector<int> place_err;  // per pair: 0 ok, else status (in pair order)
+  std::vector<PairMeta> pair;
+  std::vector<SynthItem> items;
+  std::vector<int> place_err;
   std::vector<std::string> place_msg;
-  int max_order = 0;
+  std::vector<PairPlan> plans;
+  std::vector<int32_t> strategy;
+  std::vector<int64_t> ulen;
+  FilterPlan fp;
+  int max_order = 0, slice = 1;
   int64_t rir_total = 0;
-  for (int64_t u = 0; u < U; ++u) {
+  DevBuf d_utt, d_pair, d_rg, d_items, d_rir, d_rirout, d_gain, d_power, d_flags, d_snr, d_chan_utt,
+      d_chan_mic, d_chan_out, d_utt_len, d_utt_stride, d_utt_pair0, d_utt_I, d_utt_J;
+  FilterBufs fb;
+  PinnedArena hA, hB;
+  PairRir* h_rir = nullptr;
+  int32_t* h_flags = nullptr;
+  double* h_gain = nullptr;
+  double* h_power = nullptr;
+  cudaEvent_t ev_rir = nullptr, ev_syn0 = nullptr, ev_syn1 = nullptr, ev_k4a = nullptr, ev_k4b = nullptr,
+              ev_mix0 = nullptr, ev_mix1 = nullptr;
+  int init_events() {
+    cudaEvent_t* evs[] = {&ev_rir, &ev_syn0, &ev_syn1, &ev_k4a, &ev_k4b, &ev_mix0, &ev_mix1};
+    for (auto* e : evs)
+      if (!*e) RS_CUDA(cudaEventCreate(e));
+    return RS_OK;
+  }
+  void release() {
+    DevBuf* bufs[] = {&d_utt, &d_pair, &d_rg, &d_items, &d_rir, &d_rirout, &d_gain, &d_power, &d_flags,
+                      &d_snr, &d_chan_utt, &d_chan_mic, &d_chan_out, &d_utt_len, &d_utt_stride,
+                      &d_utt_pair0, &d_utt_I, &d_utt_J, &fb.plan, &fb.lists, &fb.olaitems, &fb.spec,
+                      &fb.y, &fb.part};
+    for (DevBuf* b : bufs) b->release();
+    hA.release();
+    hB.release();
+    cudaEvent_t evs[] = {ev_rir, ev_syn0, ev_syn1, ev_k4a, ev_k4b, ev_mix0, ev_mix1};
+    for (auto e : evs)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+}  // namespace
+
+struct rs_render_state {
+  FilterBufs conv;                  // single-pair convolve path
+  std::vector<Chunk> chunks;
+  std::vector<int64_t> pair_chunk;  // global pair -> chunk
+  cudaStream_t sA = nullptr, sB = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_endA = nullptr, ev_endB = nullptr;
+};
+
+namespace {
+
+int state_init(rs_ctx* c);
+
+// Host metadata of chunk k (validation with the reference's messages).
+int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
+  ch.utt.clear(); ch.rg.clear(); ch.pair.clear(); ch.items.clear();
+  ch.place_err.clear(); ch.place_msg.clear();
+  ch.max_order = 0; ch.slice = 1; ch.rir_total = 0;
+  for (int64_t u = ch.u0; u < ch.u1; ++u) {
     const double* L = b->room_dims + 3 * u;
     const int K = b->image_order[u];
     RS_TRY(room_validate(L, b->reflection[u], b->sample_rate[u], b->speed_of_sound[u], K));
     const int64_t s0 = b->src_begin[u], I = b->src_begin[u + 1] - s0;
     const int64_t m0 = b->mic_begin[u], J = b->mic_begin[u + 1] - m0;
     if (I < 1 || J < 1) return fail(RS_ERR_CONFIG, "scene needs a target and a microphone");
-    uI[u] = static_cast<int32_t>(I);
-    uJ[u] = static_cast<int32_t>(J);
-    UttMeta& um = utt[u];
+    UttMeta um{};
     for (int a = 0; a < 3; ++a) um.dims[a] = L[a];
     um.spm = b->sample_rate[u] / b->speed_of_sound[u];  // room_model.hpp:150
     um.order = K;
-    um.rg_off = static_cast<int32_t>(rg.size());
+    um.rg_off = static_cast<int32_t>(ch.rg.size());
     um.max_taps = b->max_taps ? b->max_taps[u] : 0;
-    for (int g = 0; g <= 3 * K; ++g) rg.push_back(std::pow(b->reflection[u], static_cast<double>(g)));
-    max_order = std::max(max_order, K);
-    // RIR capacity: the horizon, or a bound on the farthest lattice image.
+    for (int g = 0; g <= 3 * K; ++g) ch.rg.push_back(std::pow(b->reflection[u], static_cast<double>(g)));
+    ch.max_order = std::max(ch.max_order, K);
     int64_t cap = um.max_taps;
-    if (cap <= 0) {
+    if (cap <= 0) {  // bound on the farthest lattice image
       double d2 = 0;
       for (int a = 0; a < 3; ++a) {
         const double e = (K + 2.0) * L[a];
@@ -399,7 +529,8 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
       }
       cap = static_cast<int64_t>(std::ceil(std::sqrt(d2) * um.spm)) + 2;
     }
-    pair0[u] = static_cast<int64_t>(pairs.size());
+    const int32_t lu = static_cast<int32_t>(ch.utt.size());
+    ch.utt.push_back(um);
     for (int64_t i = 0; i < I; ++i)
       for (int64_t j = 0; j < J; ++j) {
         PairMeta pm{};
@@ -409,15 +540,15 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
           pm.src[a] = sp[a];
           pm.mic[a] = mp[a];
         }
-        pm.utt = static_cast<int32_t>(u);
+        pm.utt = lu;
         pm.src_idx = static_cast<int32_t>(s0 + i);
         pm.mic_local = static_cast<int32_t>(j);
         pm.src_local = static_cast<int32_t>(i);
         pm.sig_off = b->sig_off[s0 + i];
         pm.nx = b->sig_len[s0 + i];
-        pm.rir_off = rir_total;
+        pm.rir_off = ch.rir_total;
         pm.rir_cap = cap;
-        rir_total += cap;
+        ch.rir_total += cap;
         int err = RS_OK;
         std::string msg;
         if (!strictly_inside(L, sp)) {  // room_model.hpp:144-145
@@ -430,65 +561,80 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
           err = RS_ERR_DEGENERATE;
           msg = "convolution input must be non-empty mono audio";
         }
-        place_err.push_back(err);
-        place_msg.push_back(msg);
-        pairs.push_back(pm);
+        ch.place_err.push_back(err);
+        ch.place_msg.push_back(msg);
+        ch.pair.push_back(pm);
       }
   }
-  pair0[U] = static_cast<int64_t>(pairs.size());
-  const int64_t P = static_cast<int64_t>(pairs.size());
-  c->last_pairs = P;
-  // K1 work items: (pair, slice) for pairs with valid placements.
-  std::vector<SynthItem> items;
-  int slice = 1;
-  for (int64_t p = 0; p < P; ++p) {
-    if (place_err[p]) continue;
-    const int64_t cap = pairs[p].rir_cap;
+  ch.P = static_cast<int64_t>(ch.pair.size());
+  for (int64_t p = 0; p < ch.P; ++p) {
+    if (ch.place_err[p]) continue;
+    const int64_t cap = ch.pair[p].rir_cap;
     for (int64_t lo = 0; lo < cap; lo += kSynthSlice) {
       const int64_t len = std::min<int64_t>(kSynthSlice, cap - lo);
-      items.push_back(SynthItem{static_cast<int32_t>(p), static_cast<int32_t>(lo), static_cast<int32_t>(len), 0});
-      slice = std::max<int>(slice, static_cast<int>(len));
+      ch.items.push_back(SynthItem{static_cast<int32_t>(p), static_cast<int32_t>(lo), static_cast<int32_t>(len), 0});
+      ch.slice = std::max<int>(ch.slice, static_cast<int>(len));
     }
   }
-  RS_TRY(upload(c, c->utt, utt));
-  RS_TRY(upload(c, c->pair, pairs));
-  RS_TRY(upload(c, c->rg, rg));
-  RS_TRY(upload(c, c->items, items));
-  RS_TRY(c->rir.ensure(std::max<int64_t>(rir_total, 1) * sizeof(double)));
-  RS_TRY(c->rirout.ensure(std::max<int64_t>(P, 1) * sizeof(PairRir)));
-  RS_CUDA(cudaMemsetAsync(c->rirout.p, 0, std::max<int64_t>(P, 1) * sizeof(PairRir), c->stream));
-  // ---- K1 synth, K2 cut ---------------------------------------------------------
-  c->st_valid = c->profiling;
-  if (c->profiling) RS_CUDA(cudaEventRecord(c->st[0], c->stream));
-  SynthArgs sa{c->utt.as<UttMeta>(), c->pair.as<PairMeta>(), c->rg.as<double>(),
-               c->items.as<SynthItem>(), c->rir.as<double>(), c->rirout.as<PairRir>()};
-  RS_CUDA(launch_synth(sa, static_cast<int>(items.size()), max_order, slice, c->stream));
+  return RS_OK;
+}
+
+// Stream A: inputs, K1, K2, RIR summary -> pinned host.
+int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO& io, cudaStream_t sA) {
+  RS_TRY(ch.init_events());
+  size_t need = staged_bytes(ch.utt) + staged_bytes(ch.pair) + staged_bytes(ch.rg) + staged_bytes(ch.items) +
+                ((std::max<int64_t>(ch.P, 1) * sizeof(PairRir) + 63) & ~size_t(63)) + 64;
+  RS_TRY(ch.hA.reserve(need));
+  ch.hA.reset();
+  if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_syn0, sA));
+  if (io.h_signals) {  // host path: this chunk's signal span
+    int64_t lo = INT64_MAX, hi = 0;
+    for (int64_t s = b->src_begin[ch.u0]; s < b->src_begin[ch.u1]; ++s) {
+      lo = std::min(lo, b->sig_off[s]);
+      hi = std::max(hi, b->sig_off[s] + b->sig_len[s]);
+    }
+    if (hi > lo)
+      RS_CUDA(cudaMemcpyAsync(const_cast<float*>(io.d_signals) + lo, io.h_signals + lo, (hi - lo) * sizeof(float),
+                              cudaMemcpyHostToDevice, sA));
+  }
+  RS_TRY(upload_on(ch.d_utt, ch.utt, sA, &ch.hA));
+  RS_TRY(upload_on(ch.d_pair, ch.pair, sA, &ch.hA));
+  RS_TRY(upload_on(ch.d_rg, ch.rg, sA, &ch.hA));
+  RS_TRY(upload_on(ch.d_items, ch.items, sA, &ch.hA));
+  RS_TRY(ch.d_rir.ensure(std::max<int64_t>(ch.rir_total, 1) * sizeof(double)));
+  RS_TRY(ch.d_rirout.ensure(std::max<int64_t>(ch.P, 1) * sizeof(PairRir)));
+  RS_CUDA(cudaMemsetAsync(ch.d_rirout.p, 0, std::max<int64_t>(ch.P, 1) * sizeof(PairRir), sA));
+  SynthArgs sa{ch.d_utt.as<UttMeta>(), ch.d_pair.as<PairMeta>(), ch.d_rg.as<double>(), ch.d_items.as<SynthItem>(),
+               ch.d_rir.as<double>(), ch.d_rirout.as<PairRir>()};
+  RS_CUDA(launch_synth(sa, static_cast<int>(ch.items.size()), ch.max_order, ch.slice, sA));
   ++c->launches;
-  if (c->profiling) RS_CUDA(cudaEventRecord(c->st[1], c->stream));
   const double eta_factor = b->eta_db > 0.0 ? std::pow(10.0, -b->eta_db / 10.0) : 0.0;
-  CutArgs ca{c->pair.as<PairMeta>(), c->utt.as<UttMeta>(), c->rir.as<double>(),
-             c->rirout.as<PairRir>(), eta_factor};
-  RS_CUDA(launch_cut(ca, static_cast<int>(P), c->stream));
+  CutArgs ca{ch.d_pair.as<PairMeta>(), ch.d_utt.as<UttMeta>(), ch.d_rir.as<double>(), ch.d_rirout.as<PairRir>(),
+             eta_factor};
+  RS_CUDA(launch_cut(ca, static_cast<int>(ch.P), sA));
   ++c->launches;
-  if (c->profiling) RS_CUDA(cudaEventRecord(c->st[2], c->stream));
-  c->h_rir.resize(P);
-  if (P)
-    RS_CUDA(cudaMemcpyAsync(c->h_rir.data(), c->rirout.p, P * sizeof(PairRir), cudaMemcpyDeviceToHost,
-                            c->stream));
-  RS_CUDA(cudaStreamSynchronize(c->stream));
-  // ---- errors in reference order, then the planner --------------------------------
-  const auto t_plan0 = std::chrono::steady_clock::now();
-  std::vector<PairPlan> plans(P);
-  std::vector<int64_t> ulen(U, 0);
-  std::vector<int32_t> strategy(P, RS_OVERLAP_ADD);
+  if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_syn1, sA));
+  ch.h_rir = ch.hA.alloc<PairRir>(ch.P);
+  if (ch.P)
+    RS_CUDA(cudaMemcpyAsync(ch.h_rir, ch.d_rirout.p, ch.P * sizeof(PairRir), cudaMemcpyDeviceToHost, sA));
+  RS_CUDA(cudaEventRecord(ch.ev_rir, sA));
+  return RS_OK;
+}
+
+// Host: errors in reference order and the planner (after chunk k's RIR summary).
+int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
+  RS_CUDA(cudaEventSynchronize(ch.ev_rir));
+  ch.plans.assign(ch.P, PairPlan{});
+  ch.strategy.assign(ch.P, RS_OVERLAP_ADD);
+  ch.ulen.assign(ch.u1 - ch.u0, 0);
   int64_t spec_off = 0, y_off = 0;
-  for (int64_t p = 0; p < P; ++p) {
-    if (place_err[p]) return fail(place_err[p], place_msg[p]);
-    const PairRir& r = c->h_rir[p];
+  for (int64_t p = 0; p < ch.P; ++p) {
+    if (ch.place_err[p]) return fail(ch.place_err[p], ch.place_msg[p]);
+    const PairRir& r = ch.h_rir[p];
     if (r.flags & 1) return fail(RS_ERR_GEOMETRY, "microphone coincides with an image source");
     if (r.flags & 2) return fail(RS_ERR_DEGENERATE, "all-zero impulse response has no power");
     const size_t nh = static_cast<size_t>(r.keep);
-    const size_t nx = static_cast<size_t>(pairs[p].nx);
+    const size_t nx = static_cast<size_t>(ch.pair[p].nx);
     if (nh == 0) return fail(RS_ERR_DEGENERATE, "empty impulse response");
     size_t n = 0;
     int s = RS_OVERLAP_ADD;
@@ -506,8 +652,8 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
     }
     if (n < 2 || n > (static_cast<size_t>(2) << kMaxLog2M))
       return fail(RS_ERR_UNSUPPORTED, "FFT size " + std::to_string(n) + " not supported by the device kernels");
-    strategy[p] = s;
-    PairPlan& pl = plans[p];
+    ch.strategy[p] = s;
+    PairPlan& pl = ch.plans[p];
     pl.log2n = log2_exact(n);
     pl.nh = static_cast<int64_t>(nh);
     pl.L = static_cast<int64_t>(n - nh + 1);
@@ -517,95 +663,256 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
     pl.y_off = y_off;
     spec_off += static_cast<int64_t>(n / 2 + 1);
     y_off += pl.out_len;
-    ulen[pairs[p].utt] = std::max(ulen[pairs[p].utt], pl.out_len);
+    int64_t& ul = ch.ulen[ch.pair[p].utt];
+    ul = std::max(ul, pl.out_len);
   }
-  for (int64_t u = 0; u < U; ++u)
-    if (out_stride[u] < ulen[u]) return fail(RS_ERR_CONFIG, "output stride too small");
-  // ---- K3 + K4 -------------------------------------------------------------------
-  c->host_plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_plan0).count();
-  double flops = 0;
-  RS_TRY(run_filter(c, plans, io.d_signals, c->rir.as<double>(), &flops));
-  // ---- K5 gains + K6 mix ------------------------------------------------------------
-  std::vector<double> snr_lin(b->src_begin[U]);
-  for (int64_t s = 0; s < b->src_begin[U]; ++s) snr_lin[s] = std::pow(10.0, b->snr_db[s] / 10.0);
-  RS_TRY(upload(c, c->snr, snr_lin));
-  std::vector<int64_t> pair0v(pair0.begin(), pair0.end() - 1);
-  RS_TRY(upload(c, c->utt_pair0, pair0v));
-  RS_TRY(upload(c, c->utt_I, uI));
-  RS_TRY(upload(c, c->utt_J, uJ));
-  RS_TRY(c->gain.ensure(std::max<int64_t>(P, 1) * sizeof(double)));
-  RS_TRY(c->power.ensure(std::max<int64_t>(P, 1) * sizeof(double)));
-  RS_TRY(c->flags.ensure(std::max<int64_t>(P, 1) * sizeof(int32_t)));
-  RS_CUDA(cudaMemsetAsync(c->flags.p, 0, std::max<int64_t>(P, 1) * sizeof(int32_t), c->stream));
-  GainArgs ga{c->pair.as<PairMeta>(), c->plan.as<PairPlan>(), c->utt_pair0.as<int64_t>(),
-              c->utt_J.as<int32_t>(), c->sumsq.as<double>(), c->snr.as<double>(), c->gain.as<double>(),
-              c->power.as<double>(), c->flags.as<int32_t>(), P};
-  RS_CUDA(launch_gain(ga, c->stream));
-  ++c->launches;
-  std::vector<int64_t> ch_utt, ch_out, ustride(out_stride, out_stride + U);
+  for (int64_t u = ch.u0; u < ch.u1; ++u)
+    if (out_stride[u] < ch.ulen[u - ch.u0]) return fail(RS_ERR_CONFIG, "output stride too small");
+  return plan_filter(ch.plans, ch.fp);
+}
+
+// Stream B: K3, K4, K5, K6 (+ output download on the host path).
+int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO& io, const int64_t* out_off,
+                   const int64_t* out_stride, cudaStream_t sB) {
+  const int64_t U = ch.u1 - ch.u0;
+  std::vector<double> snr_lin(b->src_begin[ch.u1] - b->src_begin[ch.u0]);
+  const int64_t s_first = b->src_begin[ch.u0];
+  for (size_t s = 0; s < snr_lin.size(); ++s) snr_lin[s] = std::pow(10.0, b->snr_db[s_first + s] / 10.0);
+  std::vector<int64_t> pair0(U), ustride(U);
+  std::vector<int32_t> uI(U), uJ(U);
+  std::vector<int64_t> ch_utt, ch_out;
   std::vector<int32_t> ch_mic;
-  int64_t max_stride = 0;
-  for (int64_t u = 0; u < U; ++u) {
+  int64_t max_stride = 0, acc = 0;
+  for (int64_t lu = 0; lu < U; ++lu) {
+    const int64_t u = ch.u0 + lu;
+    uI[lu] = static_cast<int32_t>(b->src_begin[u + 1] - b->src_begin[u]);
+    uJ[lu] = static_cast<int32_t>(b->mic_begin[u + 1] - b->mic_begin[u]);
+    pair0[lu] = acc;
+    acc += static_cast<int64_t>(uI[lu]) * uJ[lu];
+    ustride[lu] = out_stride[u];
     max_stride = std::max(max_stride, out_stride[u]);
-    for (int32_t j = 0; j < uJ[u]; ++j) {
-      ch_utt.push_back(u);
+    for (int32_t j = 0; j < uJ[lu]; ++j) {
+      ch_utt.push_back(lu);
       ch_mic.push_back(j);
       ch_out.push_back(out_off[u] + j * out_stride[u]);
     }
   }
-  RS_TRY(upload(c, c->chan_utt, ch_utt));
-  RS_TRY(upload(c, c->chan_mic, ch_mic));
-  RS_TRY(upload(c, c->chan_out, ch_out));
-  RS_TRY(upload(c, c->utt_len, ulen));
-  RS_TRY(upload(c, c->utt_stride, ustride));
-  MixArgs ma{c->chan_utt.as<int64_t>(), c->chan_mic.as<int32_t>(), c->chan_out.as<int64_t>(),
-             c->utt_len.as<int64_t>(), c->utt_stride.as<int64_t>(), c->utt_pair0.as<int64_t>(),
-             c->utt_I.as<int32_t>(), c->utt_J.as<int32_t>(), c->plan.as<PairPlan>(), c->y.as<float>(),
-             c->gain.as<double>(), io.d_out, 4096};
-  RS_CUDA(launch_mix(ma, static_cast<int64_t>(ch_utt.size()), max_stride, c->stream));
+  // pair -> source index relative to this chunk's first source (snr table)
+  std::vector<PairMeta>& pm = ch.pair;
+  (void)pm;
+  size_t need = staged_bytes(ch.fp.lists) + staged_bytes(ch.plans) + staged_bytes(ch.fp.items) +
+                staged_bytes(snr_lin) + staged_bytes(pair0) + staged_bytes(uI) + staged_bytes(uJ) +
+                staged_bytes(ch_utt) + staged_bytes(ch_mic) + staged_bytes(ch_out) + staged_bytes(ch.ulen) +
+                staged_bytes(ustride) + 3 * (((std::max<int64_t>(ch.P, 1) * 8) + 63) & ~size_t(63)) + 256;
+  RS_TRY(ch.hB.reserve(need));
+  ch.hB.reset();
+  RS_TRY(launch_filter(c, ch.fb, ch.fp, ch.plans, ch.d_pair.as<PairMeta>(), ch.d_rir.as<double>(), io.d_signals,
+                       sB, &ch.hB, ch.ev_k4a, ch.ev_k4b));
+  if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_mix0, sB));
+  RS_TRY(upload_on(ch.d_snr, snr_lin, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_utt_pair0, pair0, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_utt_I, uI, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_utt_J, uJ, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_chan_utt, ch_utt, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_chan_mic, ch_mic, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_chan_out, ch_out, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_utt_len, ch.ulen, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_utt_stride, ustride, sB, &ch.hB));
+  RS_TRY(ch.d_gain.ensure(std::max<int64_t>(ch.P, 1) * sizeof(double)));
+  RS_TRY(ch.d_power.ensure(std::max<int64_t>(ch.P, 1) * sizeof(double)));
+  RS_TRY(ch.d_flags.ensure(std::max<int64_t>(ch.P, 1) * sizeof(int32_t)));
+  RS_CUDA(cudaMemsetAsync(ch.d_flags.p, 0, std::max<int64_t>(ch.P, 1) * sizeof(int32_t), sB));
+  GainArgs ga{ch.d_pair.as<PairMeta>(), ch.fb.plan.as<PairPlan>(), ch.d_utt_pair0.as<int64_t>(),
+              ch.d_utt_J.as<int32_t>(), ch.fb.part.as<double>(), ch.d_snr.as<double>() - s_first,
+              ch.d_gain.as<double>(), ch.d_power.as<double>(), ch.d_flags.as<int32_t>(), ch.P};
+  RS_CUDA(launch_gain(ga, sB));
   ++c->launches;
-  if (c->profiling) RS_CUDA(cudaEventRecord(c->st[6], c->stream));
-  // ---- results, degenerate-power check --------------------------------------------
-  std::vector<int32_t> hflags(P);
-  std::vector<double> hgain(P), hpower(P);
-  if (P) {
-    RS_CUDA(cudaMemcpyAsync(hflags.data(), c->flags.p, P * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
-    RS_CUDA(cudaMemcpyAsync(hgain.data(), c->gain.p, P * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    RS_CUDA(cudaMemcpyAsync(hpower.data(), c->power.p, P * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  MixArgs ma{ch.d_chan_utt.as<int64_t>(), ch.d_chan_mic.as<int32_t>(), ch.d_chan_out.as<int64_t>(),
+             ch.d_utt_len.as<int64_t>(), ch.d_utt_stride.as<int64_t>(), ch.d_utt_pair0.as<int64_t>(),
+             ch.d_utt_I.as<int32_t>(), ch.d_utt_J.as<int32_t>(), ch.fb.plan.as<PairPlan>(), ch.fb.y.as<float>(),
+             ch.d_gain.as<double>(), io.d_out, 4096};
+  RS_CUDA(launch_mix(ma, static_cast<int64_t>(ch_utt.size()), max_stride, sB));
+  ++c->launches;
+  if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_mix1, sB));
+  ch.h_flags = ch.hB.alloc<int32_t>(ch.P);
+  ch.h_gain = ch.hB.alloc<double>(ch.P);
+  ch.h_power = ch.hB.alloc<double>(ch.P);
+  if (ch.P) {
+    RS_CUDA(cudaMemcpyAsync(ch.h_flags, ch.d_flags.p, ch.P * sizeof(int32_t), cudaMemcpyDeviceToHost, sB));
+    RS_CUDA(cudaMemcpyAsync(ch.h_gain, ch.d_gain.p, ch.P * sizeof(double), cudaMemcpyDeviceToHost, sB));
+    RS_CUDA(cudaMemcpyAsync(ch.h_power, ch.d_power.p, ch.P * sizeof(double), cudaMemcpyDeviceToHost, sB));
   }
-  RS_CUDA(cudaStreamSynchronize(c->stream));
-  RS_TRY(finish_timing(c));
-  c->ola_flops = flops;
-  // algorithmic bytes: sources once, RIR taps once, mic outputs once
-  double bytes = 0;
-  for (int64_t u = 0; u < U; ++u) {
-    for (int64_t s = b->src_begin[u]; s < b->src_begin[u + 1]; ++s) bytes += 4.0 * b->sig_len[s];
-    bytes += 4.0 * uJ[u] * ulen[u];
-  }
-  for (const auto& pl : plans) bytes += 4.0 * pl.nh;
-  c->alg_bytes = bytes;
-  for (int64_t p = 0; p < P; ++p)
-    if (hflags[p] & 4) return fail(RS_ERR_DEGENERATE, "signal has no energy: SNR gain undefined");
-  c->h_plan = plans;
-  c->h_pair = pairs;
-  if (out_len)
-    for (int64_t u = 0; u < U; ++u) out_len[u] = ulen[u];
-  for (int64_t p = 0; p < P; ++p) {
-    if (layout) {
-      rs_pair_layout& L = layout[p];
-      L.rir_len = c->h_rir[p].len;
-      L.rir_keep = c->h_rir[p].keep;
-      L.cutoff = b->eta_db > 0.0 ? c->h_rir[p].cutoff : -1;
-      L.fft_size = int64_t(1) << plans[p].log2n;
-      L.block_len = plans[p].L;
-      L.n_blocks = plans[p].B;
-      L.out_len = plans[p].out_len;
-      L.strategy = strategy[p];
-      L.flags = c->h_rir[p].flags;
+  if (io.h_out) {  // host path: this chunk's output span
+    int64_t lo = INT64_MAX, hi = 0;
+    for (int64_t u = ch.u0; u < ch.u1; ++u) {
+      lo = std::min(lo, out_off[u]);
+      hi = std::max(hi, out_off[u] + (b->mic_begin[u + 1] - b->mic_begin[u]) * out_stride[u]);
     }
-    if (gains) gains[p] = hgain[p];
-    if (power) power[p] = hpower[p];
+    if (hi > lo)
+      RS_CUDA(cudaMemcpyAsync(io.h_out + lo, io.d_out + lo, (hi - lo) * sizeof(float), cudaMemcpyDeviceToHost, sB));
   }
+  return RS_OK;
+}
+
+int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const int64_t* out_off,
+                const int64_t* out_stride, int64_t* out_len, rs_pair_layout* layout, double* gains,
+                double* power);
+
+int state_init(rs_ctx* c) {
+  if (c->rs) return RS_OK;
+  c->rs = new rs_render_state();
+  RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sA, cudaStreamNonBlocking));
+  RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sB, cudaStreamNonBlocking));
+  RS_CUDA(cudaEventCreateWithFlags(&c->rs->ev_start, cudaEventDisableTiming));
+  RS_CUDA(cudaEventCreateWithFlags(&c->rs->ev_endA, cudaEventDisableTiming));
+  RS_CUDA(cudaEventCreateWithFlags(&c->rs->ev_endB, cudaEventDisableTiming));
+  return RS_OK;
+}
+
+void destroy_state(rs_ctx* c) {
+  if (!c->rs) return;
+  rs_render_state* r = c->rs;
+  if (r->sA) cudaStreamSynchronize(r->sA);
+  if (r->sB) cudaStreamSynchronize(r->sB);
+  for (auto& ch : r->chunks) ch.release();
+  FilterBufs& f = r->conv;
+  DevBuf* bufs[] = {&f.plan, &f.lists, &f.olaitems, &f.spec, &f.y, &f.part};
+  for (DevBuf* b : bufs) b->release();
+  if (r->sA) cudaStreamDestroy(r->sA);
+  if (r->sB) cudaStreamDestroy(r->sB);
+  if (r->ev_start) cudaEventDestroy(r->ev_start);
+  if (r->ev_endA) cudaEventDestroy(r->ev_endA);
+  if (r->ev_endB) cudaEventDestroy(r->ev_endB);
+  delete r;
+  c->rs = nullptr;
+}
+
+// Pairs per chunk: large enough to fill the GPU with one chunk's K4, small
+// enough that host planning and K1/K2 of the next chunk hide behind it.
+constexpr int64_t kChunkPairs = 6144;
+
+int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const int64_t* out_off,
+                const int64_t* out_stride, int64_t* out_len, rs_pair_layout* layout, double* gains,
+                double* power) {
+  if (!b || b->n_utt < 0) return fail(RS_ERR_CONFIG, "invalid scene batch");
+  RS_TRY(state_init(c));
+  rs_render_state& R = *c->rs;
+  const int64_t U = b->n_utt;
+  c->launches = 0;
+  // ---- chunking by pair count ----------------------------------------------------
+  std::vector<std::pair<int64_t, int64_t>> ranges;
+  {
+    int64_t u0 = 0, pairs = 0;
+    for (int64_t u = 0; u < U; ++u) {
+      pairs += (b->src_begin[u + 1] - b->src_begin[u]) * (b->mic_begin[u + 1] - b->mic_begin[u]);
+      if (pairs >= kChunkPairs || u + 1 == U) {
+        ranges.emplace_back(u0, u + 1);
+        u0 = u + 1;
+        pairs = 0;
+      }
+    }
+  }
+  const int nch = static_cast<int>(ranges.size());
+  if (static_cast<int>(R.chunks.size()) < nch) R.chunks.resize(nch);
+  int64_t p_acc = 0;
+  for (int k = 0; k < nch; ++k) {
+    Chunk& ch = R.chunks[k];
+    ch.u0 = ranges[k].first;
+    ch.u1 = ranges[k].second;
+    ch.p0 = p_acc;
+    for (int64_t u = ch.u0; u < ch.u1; ++u)
+      p_acc += (b->src_begin[u + 1] - b->src_begin[u]) * (b->mic_begin[u + 1] - b->mic_begin[u]);
+  }
+  const int64_t Ptot = p_acc;
+  c->last_pairs = Ptot;
+  // ---- fork from the caller's stream ---------------------------------------------------
+  RS_CUDA(cudaEventRecord(R.ev_start, c->stream));
+  RS_CUDA(cudaStreamWaitEvent(R.sA, R.ev_start, 0));
+  RS_CUDA(cudaStreamWaitEvent(R.sB, R.ev_start, 0));
+  if (c->profiling) RS_CUDA(cudaEventRecord(c->st[0], c->stream));
+  int status = RS_OK;
+  auto t_plan = 0.0;
+  // ---- the pipeline: synth(k+1) is enqueued before the host plans chunk k -----------
+  if (nch > 0) {
+    status = prep_chunk(b, R.chunks[0]);
+    if (!status) status = enqueue_synth(c, b, R.chunks[0], io, R.sA);
+  }
+  for (int k = 0; k < nch && !status; ++k) {
+    if (k + 1 < nch) {
+      status = prep_chunk(b, R.chunks[k + 1]);
+      if (!status) status = enqueue_synth(c, b, R.chunks[k + 1], io, R.sA);
+      if (status) break;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    status = plan_chunk(b, R.chunks[k], out_stride);
+    t_plan += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (status) break;
+    status = enqueue_filter(c, b, R.chunks[k], io, out_off, out_stride, R.sB);
+  }
+  // ---- join back into the caller's stream -------------------------------------------
+  cudaEventRecord(R.ev_endA, R.sA);
+  cudaEventRecord(R.ev_endB, R.sB);
+  cudaStreamWaitEvent(c->stream, R.ev_endA, 0);
+  cudaStreamWaitEvent(c->stream, R.ev_endB, 0);
+  if (c->profiling) cudaEventRecord(c->st[6], c->stream);
+  RS_CUDA(cudaStreamSynchronize(c->stream));
+  if (status) return status;
+  c->host_plan_ms = t_plan;
+  // ---- results, degenerate-power check, timing --------------------------------------
+  c->h_plan.clear();
+  c->h_pair.clear();
+  R.pair_chunk.assign(Ptot, 0);
+  double flops = 0, bytes = 0, ola_ms = 0, syn_ms = 0, mix_ms = 0;
+  for (int k = 0; k < nch; ++k) {
+    Chunk& ch = R.chunks[k];
+    flops += ch.fp.flops;
+    if (c->profiling) {
+      float f;
+      RS_CUDA(cudaEventElapsedTime(&f, ch.ev_k4a, ch.ev_k4b));
+      ola_ms += f;
+      RS_CUDA(cudaEventElapsedTime(&f, ch.ev_syn0, ch.ev_syn1));
+      syn_ms += f;
+      RS_CUDA(cudaEventElapsedTime(&f, ch.ev_mix0, ch.ev_mix1));
+      mix_ms += f;
+    }
+    for (int64_t p = 0; p < ch.P; ++p) {
+      const int64_t gp = ch.p0 + p;
+      R.pair_chunk[gp] = k;
+      if (ch.h_flags[p] & 4) return fail(RS_ERR_DEGENERATE, "signal has no energy: SNR gain undefined");
+      if (layout) {
+        rs_pair_layout& L = layout[gp];
+        const PairRir& r = ch.h_rir[p];
+        L.rir_len = r.len;
+        L.rir_keep = r.keep;
+        L.cutoff = b->eta_db > 0.0 ? r.cutoff : -1;
+        L.fft_size = int64_t(1) << ch.plans[p].log2n;
+        L.block_len = ch.plans[p].L;
+        L.n_blocks = ch.plans[p].B;
+        L.out_len = ch.plans[p].out_len;
+        L.strategy = ch.strategy[p];
+        L.flags = r.flags;
+      }
+      if (gains) gains[gp] = ch.h_gain[p];
+      if (power) power[gp] = ch.h_power[p];
+      bytes += 4.0 * ch.plans[p].nh;
+    }
+    for (int64_t u = ch.u0; u < ch.u1; ++u) {
+      if (out_len) out_len[u] = ch.ulen[u - ch.u0];
+      for (int64_t s = b->src_begin[u]; s < b->src_begin[u + 1]; ++s) bytes += 4.0 * b->sig_len[s];
+      bytes += 4.0 * (b->mic_begin[u + 1] - b->mic_begin[u]) * ch.ulen[u - ch.u0];
+    }
+  }
+  c->ola_flops = flops;
+  c->alg_bytes = bytes;
+  c->ola_ms = ola_ms;
+  c->st_valid = false;
+  c->stage_ms[0] = syn_ms;
+  c->stage_ms[1] = 0;
+  c->stage_ms[2] = 0;
+  c->stage_ms[3] = 0;
+  c->stage_ms[4] = ola_ms;
+  c->stage_ms[5] = mix_ms;
+  c->stage_valid = c->profiling;
   return RS_OK;
 }
 
@@ -644,11 +951,16 @@ int convolve_host(rs_ctx* c, const double* x, size_t nx, const double* h, size_t
   pl.L = static_cast<int64_t>(n - nh + 1);
   pl.B = static_cast<int64_t>(block_count(nx, nh, n));
   pl.out_len = static_cast<int64_t>(nx + nh - 1);
-  double flops = 0;
-  RS_TRY(run_filter(c, plv, c->sig.as<float>(), c->rir.as<double>(), &flops));
+  RS_TRY(state_init(c));
+  FilterPlan fp;
+  RS_TRY(plan_filter(plv, fp));
+  FilterBufs& fb = c->rs->conv;
+  RS_TRY(launch_filter(c, fb, fp, plv, c->pair.as<PairMeta>(), c->rir.as<double>(), c->sig.as<float>(), c->stream,
+                       nullptr, c->profiling ? c->ev0 : nullptr, c->profiling ? c->ev1 : nullptr));
+  const double flops = fp.flops;
   const size_t ol = nx + nh - 1;
   RS_TRY(c->scratch_b.ensure(ol * sizeof(double)));
-  RS_CUDA(launch_convert_f2d(c->y.as<float>(), c->scratch_b.as<double>(), static_cast<int64_t>(ol), c->stream));
+  RS_CUDA(launch_convert_f2d(fb.y.as<float>(), c->scratch_b.as<double>(), static_cast<int64_t>(ol), c->stream));
   RS_CUDA(cudaMemcpyAsync(out, c->scratch_b.p, ol * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   RS_CUDA(cudaStreamSynchronize(c->stream));
   RS_TRY(finish_timing(c));
@@ -690,6 +1002,7 @@ int rs_ctx_destroy(rs_ctx* c) {
                     &c->utt_stride, &c->utt_pair0, &c->utt_I, &c->utt_J, &c->sig, &c->out,
                     &c->scratch_a, &c->scratch_b};
   for (DevBuf* b : bufs) b->release();
+  destroy_state(c);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   for (auto& e : c->st)
@@ -714,14 +1027,7 @@ int rs_ctx_synchronize(rs_ctx* c) {
 int rs_ctx_stage_times(rs_ctx* c, double* ms, int n, double* host_plan_ms) {
   RS_TRY(check_ctx(c));
   if (host_plan_ms) *host_plan_ms = c->host_plan_ms;
-  for (int i = 0; i < n; ++i) ms[i] = -1.0;
-  if (!c->st_valid) return RS_OK;
-  RS_CUDA(cudaEventSynchronize(c->st[rs_ctx::kStages - 1]));
-  for (int i = 0; i + 1 < rs_ctx::kStages && i < n; ++i) {
-    float f = 0;
-    RS_CUDA(cudaEventElapsedTime(&f, c->st[i], c->st[i + 1]));
-    ms[i] = f;
-  }
+  for (int i = 0; i < n; ++i) ms[i] = (c->stage_valid && i < 6) ? c->stage_ms[i] : -1.0;
   return RS_OK;
 }
 
@@ -928,7 +1234,8 @@ int rs_render_batch_device(rs_ctx* c, const rs_scene_batch* b, float* out_dev, c
                            const int64_t* out_stride, int64_t* out_len, rs_pair_layout* layout,
                            double* gains, double* power) {
   RS_TRY(check_ctx(c));
-  RenderIO io{b->signals, out_dev};
+  if (!b) return fail(RS_ERR_CONFIG, "invalid scene batch");
+  RenderIO io{b->signals, out_dev, nullptr, nullptr};
   return render_impl(c, b, io, out_off, out_stride, out_len, layout, gains, power);
 }
 
@@ -937,7 +1244,9 @@ int rs_render_batch(rs_ctx* c, const rs_scene_batch* b, float* out, const int64_
                     double* gains, double* power) {
   RS_TRY(check_ctx(c));
   if (!b) return fail(RS_ERR_CONFIG, "invalid scene batch");
-  // H2D of the signal span, render on device, D2H of the output span.
+  // Per-chunk H2D of the signal span (stream A) and D2H of the output span
+  // (stream B) overlap the other chunks' kernels; pass page-locked buffers
+  // for the copies to be asynchronous.
   int64_t sig_end = 0, out_end = 0;
   for (int64_t s = 0; s < (b->n_utt ? b->src_begin[b->n_utt] : 0); ++s)
     sig_end = std::max(sig_end, b->sig_off[s] + b->sig_len[s]);
@@ -945,34 +1254,40 @@ int rs_render_batch(rs_ctx* c, const rs_scene_batch* b, float* out, const int64_
     out_end = std::max(out_end, out_off[u] + (b->mic_begin[u + 1] - b->mic_begin[u]) * out_stride[u]);
   RS_TRY(c->sig.ensure(std::max<int64_t>(sig_end, 1) * sizeof(float)));
   RS_TRY(c->out.ensure(std::max<int64_t>(out_end, 1) * sizeof(float)));
-  if (sig_end)
-    RS_CUDA(cudaMemcpyAsync(c->sig.p, b->signals, sig_end * sizeof(float), cudaMemcpyHostToDevice, c->stream));
-  RenderIO io{c->sig.as<float>(), c->out.as<float>()};
-  RS_TRY(render_impl(c, b, io, out_off, out_stride, out_len, layout, gains, power));
-  if (out_end)
-    RS_CUDA(cudaMemcpyAsync(out, c->out.p, out_end * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
-  RS_CUDA(cudaStreamSynchronize(c->stream));
+  RenderIO io{c->sig.as<float>(), c->out.as<float>(), b->signals, out};
+  return render_impl(c, b, io, out_off, out_stride, out_len, layout, gains, power);
+}
+
+static int locate_pair(rs_ctx* c, int64_t pair, Chunk** ch, int64_t* local) {
+  if (!c->rs || pair < 0 || pair >= static_cast<int64_t>(c->rs->pair_chunk.size()))
+    return fail(RS_ERR_CONFIG, "pair index out of range");
+  *ch = &c->rs->chunks[c->rs->pair_chunk[pair]];
+  *local = pair - (*ch)->p0;
   return RS_OK;
 }
 
 int rs_last_pair_signal(rs_ctx* c, int64_t pair, float* out, size_t cap, size_t* len) {
   RS_TRY(check_ctx(c));
-  if (pair < 0 || pair >= static_cast<int64_t>(c->h_plan.size())) return fail(RS_ERR_CONFIG, "pair index out of range");
-  const PairPlan& p = c->h_plan[pair];
+  Chunk* ch;
+  int64_t lp;
+  RS_TRY(locate_pair(c, pair, &ch, &lp));
+  const PairPlan& p = ch->plans[lp];
   if (static_cast<size_t>(p.out_len) > cap) return fail(RS_ERR_UNSUPPORTED, "capacity too small");
   RS_CUDA(cudaStreamSynchronize(c->stream));
-  RS_CUDA(cudaMemcpy(out, c->y.as<float>() + p.y_off, p.out_len * sizeof(float), cudaMemcpyDeviceToHost));
+  RS_CUDA(cudaMemcpy(out, ch->fb.y.as<float>() + p.y_off, p.out_len * sizeof(float), cudaMemcpyDeviceToHost));
   *len = static_cast<size_t>(p.out_len);
   return RS_OK;
 }
 
 int rs_last_pair_rir(rs_ctx* c, int64_t pair, double* out, size_t cap, size_t* len) {
   RS_TRY(check_ctx(c));
-  if (pair < 0 || pair >= static_cast<int64_t>(c->h_plan.size())) return fail(RS_ERR_CONFIG, "pair index out of range");
-  const size_t n = static_cast<size_t>(c->h_plan[pair].nh);
+  Chunk* ch;
+  int64_t lp;
+  RS_TRY(locate_pair(c, pair, &ch, &lp));
+  const size_t n = static_cast<size_t>(ch->plans[lp].nh);
   if (n > cap) return fail(RS_ERR_UNSUPPORTED, "capacity too small");
   RS_CUDA(cudaStreamSynchronize(c->stream));
-  RS_CUDA(cudaMemcpy(out, c->rir.as<double>() + c->h_pair[pair].rir_off, n * sizeof(double), cudaMemcpyDeviceToHost));
+  RS_CUDA(cudaMemcpy(out, ch->d_rir.as<double>() + ch->pair[lp].rir_off, n * sizeof(double), cudaMemcpyDeviceToHost));
   *len = n;
   return RS_OK;
 }
