@@ -12,6 +12,7 @@
 #include <limits>
 #include <numeric>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/roomsim_gpu.h"
@@ -448,6 +449,7 @@ struct Chunk {
   std::vector<double> rg;
   std::vector<PairMeta> pair;
   std::vector<SynthItem> items;
+  std::vector<std::tuple<int64_t, int64_t, int>> synth_class;  // (offset, count, slice cap)
   std::vector<int> place_err;
   std::vector<std::string> place_msg;
   std::vector<PairPlan> plans;
@@ -567,14 +569,24 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
       }
   }
   ch.P = static_cast<int64_t>(ch.pair.size());
+  static const int kClass[3] = {2048, 6144, kSynthSlice};
+  std::vector<SynthItem> cls[3];
   for (int64_t p = 0; p < ch.P; ++p) {
     if (ch.place_err[p]) continue;
     const int64_t cap = ch.pair[p].rir_cap;
     for (int64_t lo = 0; lo < cap; lo += kSynthSlice) {
       const int64_t len = std::min<int64_t>(kSynthSlice, cap - lo);
-      ch.items.push_back(SynthItem{static_cast<int32_t>(p), static_cast<int32_t>(lo), static_cast<int32_t>(len), 0});
-      ch.slice = std::max<int>(ch.slice, static_cast<int>(len));
+      const int k = len <= kClass[0] ? 0 : (len <= kClass[1] ? 1 : 2);
+      cls[k].push_back(SynthItem{static_cast<int32_t>(p), static_cast<int32_t>(lo), static_cast<int32_t>(len), 0});
     }
+  }
+  ch.synth_class.clear();
+  for (int k = 2; k >= 0; --k) {  // largest slices first
+    int cap = 1;
+    for (const auto& itm : cls[k]) cap = std::max(cap, itm.slice_len);
+    ch.synth_class.emplace_back(static_cast<int64_t>(ch.items.size()), static_cast<int64_t>(cls[k].size()), cap);
+    ch.items.insert(ch.items.end(), cls[k].begin(), cls[k].end());
+    ch.slice = std::max(ch.slice, cap);
   }
   return RS_OK;
 }
@@ -604,10 +616,15 @@ int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO&
   RS_TRY(ch.d_rir.ensure(std::max<int64_t>(ch.rir_total, 1) * sizeof(double)));
   RS_TRY(ch.d_rirout.ensure(std::max<int64_t>(ch.P, 1) * sizeof(PairRir)));
   RS_CUDA(cudaMemsetAsync(ch.d_rirout.p, 0, std::max<int64_t>(ch.P, 1) * sizeof(PairRir), sA));
-  SynthArgs sa{ch.d_utt.as<UttMeta>(), ch.d_pair.as<PairMeta>(), ch.d_rg.as<double>(), ch.d_items.as<SynthItem>(),
-               ch.d_rir.as<double>(), ch.d_rirout.as<PairRir>()};
-  RS_CUDA(launch_synth(sa, static_cast<int>(ch.items.size()), ch.max_order, ch.slice, sA));
-  ++c->launches;
+  // one K1 launch per slice-size class, so short RIRs get more CTAs per SM
+  for (size_t k = 0; k < ch.synth_class.size(); ++k) {
+    const auto& [off, n, cap] = ch.synth_class[k];
+    if (n == 0) continue;
+    SynthArgs sa{ch.d_utt.as<UttMeta>(), ch.d_pair.as<PairMeta>(), ch.d_rg.as<double>(),
+                 ch.d_items.as<SynthItem>() + off, ch.d_rir.as<double>(), ch.d_rirout.as<PairRir>()};
+    RS_CUDA(launch_synth(sa, static_cast<int>(n), ch.max_order, cap, sA));
+    ++c->launches;
+  }
   const double eta_factor = b->eta_db > 0.0 ? std::pow(10.0, -b->eta_db / 10.0) : 0.0;
   CutArgs ca{ch.d_pair.as<PairMeta>(), ch.d_utt.as<UttMeta>(), ch.d_rir.as<double>(), ch.d_rirout.as<PairRir>(),
              eta_factor};

@@ -37,23 +37,40 @@ namespace rsg {
 // fold the group in lane order.  All arithmetic uses _rn intrinsics so no
 // FMA contraction can change a bit; r^g comes from the host's std::pow.
 // ============================================================================
+// 0-indexed position of the k-th set bit of m (k < popc(m)).
+__device__ __forceinline__ int nth_set_bit(unsigned m, int k) {
+  int pos = 0;
+#pragma unroll
+  for (int w = 16; w > 0; w >>= 1) {
+    const int c = __popc(m & ((1u << w) - 1u));
+    if (k >= c) {
+      k -= c;
+      m >>= w;
+      pos += w;
+    }
+  }
+  return pos;
+}
+
 __global__ void __launch_bounds__(kSynthThreads) rir_synth_kernel(SynthArgs a, int slice_cap) {
   extern __shared__ __align__(16) unsigned char sm[];
+  constexpr int NT = kSynthThreads, NW = NT / 32;
+  static_assert(NW == 16, "16 owner warps x 16 compute warps");
   const SynthItem it = a.items[blockIdx.x];
   const PairMeta& pm = a.pair[it.pair];
   const UttMeta& um = a.utt[pm.utt];
   const int K = um.order, W = 2 * K + 1;
   double* bins = reinterpret_cast<double*>(sm);
-  double* ax = bins + slice_cap;      // [3][W] squared per-axis offsets
-  double* rg = ax + 3 * W;            // [3K+1]
-  double* ent_a = rg + (3 * K + 1);   // [512]
-  int* ent_d = reinterpret_cast<int*>(ent_a + kSynthThreads);  // [512]
-  unsigned* mask = reinterpret_cast<unsigned*>(ent_d + kSynthThreads);  // [16][16]
+  double* ax = bins + slice_cap;                 // [3][W] squared per-axis offsets
+  double* rg = ax + 3 * W;                       // [3K+1]
+  double* ent_a = rg + (3 * K + 1);              // [2][NT]
+  int* ent_d = reinterpret_cast<int*>(ent_a + 2 * NT);          // [2][NT]
+  unsigned* mask = reinterpret_cast<unsigned*>(ent_d + 2 * NT);  // [2][NW compute][NW owner]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lo = it.slice_lo, len = it.slice_len;
 
-  for (int l = tid; l < len; l += kSynthThreads) bins[l] = 0.0;
-  for (int idx = tid; idx < 3 * W; idx += kSynthThreads) {
+  for (int l = tid; l < len; l += NT) bins[l] = 0.0;
+  for (int idx = tid; idx < 3 * W; idx += NT) {
     const int axis = idx / W, n = idx - axis * W - K;
     const double L = um.dims[axis], s = pm.src[axis];
     // room_model.hpp:126-127: mirrored = n even ? s : L - s; pos = n*L + mirrored
@@ -62,68 +79,106 @@ __global__ void __launch_bounds__(kSynthThreads) rir_synth_kernel(SynthArgs a, i
     const double diff = __dsub_rn(pos, pm.mic[axis]);  // room_model.hpp:37 (a - b)
     ax[idx] = __dmul_rn(diff, diff);                    // :43 v.x * v.x
   }
-  for (int g = tid; g <= 3 * K; g += kSynthThreads) rg[g] = a.rg[um.rg_off + g];
+  for (int g = tid; g <= 3 * K; g += NT) rg[g] = a.rg[um.rg_off + g];
+  for (int i = tid; i < 2 * NW * NW; i += NT) mask[i] = 0u;
   __syncthreads();
 
   const long long V = static_cast<long long>(W) * W * W;
-  const unsigned WW = static_cast<unsigned>(W);
+  // image index i = (ix W + iy) W + iz, advanced incrementally by NT per chunk
+  int ix, iy, iz;
+  {
+    const int t0 = tid;  // < NT <= W^3 not required: carries handle small lattices
+    iz = t0 % W;
+    const int q = t0 / W;
+    iy = q % W;
+    ix = q / W;
+  }
+  const int step_z = NT % W, step_q = NT / W;
+  const int step_y = step_q % W, step_x = step_q / W;
   unsigned long long max_d = 0;
   int geo = 0;
-  for (long long base = 0; base < V; base += kSynthThreads) {
+  int buf = 0;
+  for (long long base = 0; base < V; base += NT, buf ^= 1) {
     const long long i = base + tid;
     int rel_bin = -1;
     double amp = 0.0;
     if (i < V) {
-      const unsigned ui = static_cast<unsigned>(i);
-      const unsigned iz = ui % WW, t2 = ui / WW;
-      const unsigned iy = t2 % WW, ix = t2 / WW;
       // norm: sqrt((x*x + y*y) + z*z), room_model.hpp:43
       const double d2 = __dadd_rn(__dadd_rn(ax[ix], ax[W + iy]), ax[2 * W + iz]);
       const double d = __dsqrt_rn(d2);
-      if (d <= 0.0) geo = 1;  // :157-158
+      if (d <= 0.0) geo = 1;                         // :157-158
       const double dl = ceil(__dmul_rn(d, um.spm));  // :159-160
       const unsigned long long D = static_cast<unsigned long long>(dl);
       max_d = D > max_d ? D : max_d;
       const long long rel = static_cast<long long>(D) - lo;
       if (rel >= 0 && rel < len) {
-        const int g = abs(static_cast<int>(ix) - K) + abs(static_cast<int>(iy) - K) +
-                      abs(static_cast<int>(iz) - K);
+        const int g = abs(ix - K) + abs(iy - K) + abs(iz - K);
         amp = __ddiv_rn(rg[g], d);  // :161-162 pow(r, g) / d
         rel_bin = static_cast<int>(rel);
       }
     }
-    ent_d[tid] = rel_bin;
-    ent_a[tid] = amp;
-    const int owner = rel_bin >= 0 ? (rel_bin & 15) : -1;
-#pragma unroll
-    for (int o = 0; o < 16; ++o) {
-      const unsigned m = __ballot_sync(0xffffffffu, owner == o);
-      if (lane == o) mask[warp * 16 + o] = m;
-    }
+    // advance (ix, iy, iz) by NT images
+    iz += step_z;
+    int cy = step_y;
+    if (iz >= W) { iz -= W; ++cy; }
+    iy += cy;
+    int cx = step_x;
+    while (iy >= W) { iy -= W; ++cx; }
+    ix += cx;
+    // publish this chunk's entries; owner of a bin: bin & 15
+    int* ed = ent_d + buf * NT;
+    double* ea = ent_a + buf * NT;
+    unsigned* mk = mask + buf * NW * NW;
+    ed[tid] = rel_bin;
+    ea[tid] = amp;
+    const int owner = rel_bin >= 0 ? (rel_bin & 15) : 16;
+    const unsigned same = __match_any_sync(0xffffffffu, owner);
+    if (owner < 16 && lane == __ffs(same) - 1) mk[warp * NW + owner] = same;
     __syncthreads();
-    // Ordered scatter: owner warp `warp` walks compute warps 0..15 in order.
-    for (int cw = 0; cw < kSynthThreads / 32; ++cw) {
-      const unsigned m = mask[cw * 16 + warp];
-      if (m == 0u) continue;
-      if ((m >> lane) & 1u) {
-        const int b = ent_d[cw * 32 + lane];
-        const unsigned grp = __match_any_sync(m, b);
-        if (lane == __ffs(grp) - 1) {
-          double acc = bins[b];
-          unsigned gg = grp;
-          while (gg) {
-            const int src = __ffs(gg) - 1;
-            gg &= gg - 1;
-            acc = __dadd_rn(acc, ent_a[cw * 32 + src]);
-          }
-          bins[b] = acc;
+    // Ordered scatter by owner warp `warp`: its entries from the 16 compute
+    // warps, concatenated in compute-warp order (= enumeration order), are
+    // compacted onto the 32 lanes; equal-delay groups fold in lane order.
+    {
+      const unsigned m = lane < NW ? mk[lane * NW + warp] : 0u;
+      const int cnt = __popc(m);
+      int incl = cnt;  // inclusive prefix over compute warps (lanes 0..15)
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, NW - 1);
+      for (int r0 = 0; r0 < total; r0 += 32) {
+        const int l = r0 + lane;  // this lane's entry rank
+        int cw = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) cw += (__shfl_sync(0xffffffffu, incl, w) <= l) ? 1 : 0;
+        const bool valid = l < total;
+        const int cws = cw < NW ? cw : NW - 1;
+        const unsigned mm = __shfl_sync(0xffffffffu, m, cws);
+        const int excl = __shfl_sync(0xffffffffu, incl, cws) - __popc(mm);
+        const int e = cws * 32 + (valid ? nth_set_bit(mm, l - excl) : 0);
+        const int bn = valid ? ed[e] : -1 - lane;  // distinct dummy keys for idle lanes
+        const double av = valid ? ea[e] : 0.0;
+        const unsigned grp = __match_any_sync(0xffffffffu, bn);
+        const int gsz = __popc(grp);
+        const bool leader = valid && lane == __ffs(grp) - 1;
+        double acc = leader ? bins[bn] : 0.0;
+        const int maxg = __reduce_max_sync(0xffffffffu, valid ? gsz : 0);
+        for (int k = 0; k < maxg; ++k) {  // fold each group in lane (= enumeration) order
+          const int src = k < gsz ? nth_set_bit(grp, k) : lane;
+          const double v = __shfl_sync(0xffffffffu, av, src);
+          if (leader && k < gsz) acc = __dadd_rn(acc, v);
         }
+        if (leader) bins[bn] = acc;
+        __syncwarp();
       }
     }
-    __syncthreads();
+    if (lane < NW) mk[lane * NW + warp] = 0u;  // owner clears its column for reuse
   }
+  __syncthreads();
   double* out = a.rir + pm.rir_off + lo;
-  for (int l = tid; l < len; l += kSynthThreads) out[l] = bins[l];
+  for (int l = tid; l < len; l += NT) out[l] = bins[l];
   // max delay / geometry flag over the CTA
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long other = __shfl_xor_sync(0xffffffffu, max_d, o);
@@ -138,8 +193,8 @@ __global__ void __launch_bounds__(kSynthThreads) rir_synth_kernel(SynthArgs a, i
 
 size_t synth_smem_bytes(int max_order, int slice) {
   const int W = 2 * max_order + 1;
-  return sizeof(double) * (static_cast<size_t>(slice) + 3 * W + 3 * max_order + 1 + kSynthThreads) +
-         sizeof(int) * kSynthThreads + sizeof(unsigned) * 256;
+  return sizeof(double) * (static_cast<size_t>(slice) + 3 * W + 3 * max_order + 1 + 2 * kSynthThreads) +
+         sizeof(int) * 2 * kSynthThreads + sizeof(unsigned) * 2 * 256;
 }
 
 cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice,
