@@ -359,6 +359,9 @@ __device__ __forceinline__ void inverse_but_last(float2* s, int t, const float2*
 // Last inverse pass: reads smem, twiddles, DFT, then a barrier (smem may be
 // reused) and hands every output element to `emit(q, r, c, v)` in registers,
 // c = complex index in natural order (c = j + r*M/R).
+#ifndef EMIT_BATCH
+#define EMIT_BATCH 4
+#endif
 template <int M, class Bar, class Emit, bool TWS = false, bool SYNC = true>
 __device__ __forceinline__ void stockham_emit_pass(float2* s, int t, const float2* __restrict__ tw,
                                                    bool active, Bar bar, Emit emit) {
@@ -391,7 +394,11 @@ __device__ __forceinline__ void stockham_emit_pass(float2* s, int t, const float
 #pragma unroll
     for (int q = 0; q < NB; ++q)
 #pragma unroll
-      for (int r = 0; r < R; ++r) emit(q, r, t + q * T + r * STRIDE, v[q][r]);
+      for (int r = 0; r < R; ++r) {
+        emit(q, r, t + q * T + r * STRIDE, v[q][r]);
+        // keep the emit's loads from being hoisted all at once (register pressure)
+        if ((r & (EMIT_BATCH - 1)) == EMIT_BATCH - 1) asm volatile("" ::: "memory");
+      }
   }
 }
 

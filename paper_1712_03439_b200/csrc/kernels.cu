@@ -420,12 +420,15 @@ int ola_groups(int log2m) {
 constexpr int kSmallMaxLog2M = 12;
 
 template <int M>
-struct SmallLayout {  // float2 offsets inside one group's region
+struct SmallLayout {  // float2 offsets inside one group's region, all even (16-byte aligned)
+  static constexpr int ev(int v) { return (v + 1) & ~1; }
   static constexpr int FFT = 0;
-  static constexpr int GS = Plan<M>::PADDED;
-  static constexpr int CARRY = GS + M + 2;        // 2 x N floats (double-buffered)
-  static constexpr int STAGE = CARRY + 2 * M;     // N floats
-  static constexpr int TOTAL = STAGE + M;
+  static constexpr int GS = ev(Plan<M>::PADDED);
+  static constexpr int CARRY = ev(GS + M + 1);     // 2 x N floats (double-buffered)
+  static constexpr int STAGE = ev(CARRY + 2 * M);  // N + 8 floats (bulk-copy window slack)
+  static constexpr int MBAR = ev(STAGE + M + 4);   // one 8-byte mbarrier
+  static constexpr int TOTAL = ev(MBAR + 1);
+  static_assert(STAGE % 2 == 0 && TOTAL % 2 == 0, "16-byte alignment of the bulk-copy window");
 };
 
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
@@ -435,6 +438,25 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+// One thread: arm the barrier with `bytes` and start a 1-D TMA bulk copy.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
@@ -457,7 +479,7 @@ ola_small_kernel(OlaArgs a) {
   const PairPlan& pl = a.plan[it.pair];
   const PairMeta& pm = a.pair[it.pair];
   const float* __restrict__ x = a.signals + pm.sig_off;
-  const long long nx = pm.nx;
+  const int nx = static_cast<int>(pm.nx);
   float* __restrict__ y = a.y + pl.y_off;
   const int L = static_cast<int>(pl.L);
   const int B = static_cast<int>(pl.B);
@@ -476,14 +498,30 @@ ola_small_kernel(OlaArgs a) {
   const int own_hi = it.b_end == B ? out_len : it.b_end * L;
   // block b's samples -> stage[0, take) (4-byte cp.async: any alignment); fixed
   // trip count N/T = 2E, predicated
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(base + LY::MBAR);
+  // Block b's samples land in stage[d, d + take) with d = (address mod 16)/4: one
+  // 1-D TMA bulk copy (cp.async.bulk, a 16-byte aligned window) issued by one
+  // thread, or — near the end of the signal, where the window would read past
+  // it — per-thread 4-byte cp.async.
+  auto window = [&](int b, int& d, int& take, bool& bulk) {
+    const int st = b * L;
+    take = nx - st < L ? nx - st : L;
+    d = static_cast<int>((reinterpret_cast<uintptr_t>(x + st) & 15u) >> 2);
+    bulk = st + take + 4 <= nx;
+  };
   auto prefetch = [&](int b) {
-    const long long st = static_cast<long long>(b) * L;
-    const int take = static_cast<int>(nx - st < L ? nx - st : L);
-    const float* src = x + st;
+    int d, take;
+    bool bulk;
+    window(b, d, take, bulk);
+    const float* src = x + b * L;
+    if (bulk) {
+      if (t == 0) bulk_g2s(stage, src - d, static_cast<unsigned>(((d + take) * 4 + 15) & ~15), mbar);
+    } else {
 #pragma unroll
-    for (int m = 0; m < N / T; ++m) {
-      const int i = t + m * T;
-      if (i < take) cp_async4(stage + i, src + i);
+      for (int m = 0; m < N / T; ++m) {
+        const int i = t + m * T;
+        if (i < take) cp_async4(stage + d + i, src + i);
+      }
     }
   };
   for (int i = threadIdx.x; i < PL::TW_TOTAL; i += CTA) cp_async8(tws + i, a.tw + i);
@@ -492,35 +530,47 @@ ola_small_kernel(OlaArgs a) {
     const float2* Gsrc = a.spec + pl.spec_off;
     for (int k = t; k <= M; k += T) cp_async8(gs + k, Gsrc + k);
     for (int i = t; i < 2 * N; i += T) carry0[i] = 0.f;
-    for (int i = L + t; i < N; i += T) stage[i] = 0.f;  // zero padding of every block
-    prefetch(it.b_begin);
+    if (t == 0) {
+      mbar_init(mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
   }
   cp_async_wait_all();
-  __syncthreads();  // per-CTA twiddles, G, carry and padding in place (all threads)
-  double pw4[4] = {0.0, 0.0, 0.0, 0.0};
+  __syncthreads();  // per-CTA twiddles, G, carry and barriers in place (all threads)
+  if (has) prefetch(it.b_begin);
+  unsigned phase = 0;
+  double pw2[2] = {0.0, 0.0};
   constexpr int R = PL::radix(PL::NP - 1);
   constexpr int NB = PL::E / R;
 #pragma unroll 1
   for (int k = 0; k < trips; ++k) {
     const int b = it.b_begin + k;
     const bool active = has && b < it.b_end;
-    const long long start = static_cast<long long>(b) * L;
-    const int take = active ? static_cast<int>(nx - start < L ? nx - start : L) : L;
-    cp_async_wait_all();
-    if (take < L)  // the signal ends inside this block: clear stale samples
-      for (int i = take + t; i < L; i += T) stage[i] = 0.f;
+    const int start = b * L;
+    int d = 0, take = 0;
+    bool bulk = false;
+    if (active) {
+      window(b, d, take, bulk);
+      if (bulk) {
+        mbar_wait(mbar, phase);
+        phase ^= 1u;
+      } else {
+        cp_async_wait_all();
+      }
+    }
     bar();
-    first_pass<M, float, GroupBar<T>, true>(s, t, active, stage, N, bar);
+    first_pass<M, float, GroupBar<T>, false>(s, t, active, stage + d, take, bar);
+#ifndef RSG_NO_PREFETCH
     if (active && b + 1 < it.b_end) prefetch(b + 1);  // lands while this block is transformed
+#endif
     forward_rest<M, 1, GroupBar<T>, true>(s, t, tws, active, bar);
     spectral_multiply<M, GroupBar<T>, true, true>(s, t, gs, W, active, bar);
     inverse_but_last<M, 0, GroupBar<T>, true>(s, t, tws, active, bar);
     // emit: e < L -> final output (carry + v), e >= L -> carry for block b+1
     float* yb = y + start;
-    const int lo = own_lo - static_cast<int>(start);
-    const int hi = own_hi - static_cast<int>(start);
+    const int lo = own_lo - start;
+    const int hi = own_hi - start;
     const bool last = b == B - 1;
-    const bool fast = lo <= 0 && hi >= L && !last;  // interior block of the owned range
     // carry of this block (read) and of the next (written): double-buffered, so
     // the emit needs no barrier and nothing stays live across one
     const float* cin = carry0 + (k & 1) * N;
@@ -529,22 +579,7 @@ ola_small_kernel(OlaArgs a) {
       const int e0 = 2 * c;
       const float2 ci = *reinterpret_cast<const float2*>(cin + e0);
       const float2 acc = make_float2(ci.x + v.x, ci.y + v.y);
-      double& p = pw4[(q * R + r) & 3];  // 4 independent FP64 chains
-      if (fast) {
-        if (e0 < L) {
-          yb[e0] = acc.x;
-          p = fma(static_cast<double>(acc.x), static_cast<double>(acc.x), p);
-        } else {
-          carry[e0 - L] = acc.x;
-        }
-        if (e0 + 1 < L) {
-          yb[e0 + 1] = acc.y;
-          p = fma(static_cast<double>(acc.y), static_cast<double>(acc.y), p);
-        } else {
-          carry[e0 + 1 - L] = acc.y;
-        }
-        return;
-      }
+      double& p = pw2[(q * R + r) & 1];  // 2 independent FP64 chains
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int e = e0 + h;
@@ -564,7 +599,7 @@ ola_small_kernel(OlaArgs a) {
     // old carry at e in [L, N_h - 1) comes from the other buffer.)
   }
   // Σ y^2 of the group (fixed order: deterministic) -> part[item]
-  double pw = (pw4[0] + pw4[1]) + (pw4[2] + pw4[3]);
+  double pw = pw2[0] + pw2[1];
   if constexpr (T >= 32) {
     __shared__ double red[CTA / 32];
     for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
@@ -738,7 +773,8 @@ rfft_inverse_kernel(const float2* in, float* out, int count, const float2* tw) {
 size_t k4_smem_bytes(int log2m) {
   if (log2m > kSmallMaxLog2M) return ola_smem_bytes(log2m);
   const int M = 1 << log2m;
-  const int per_group = (M + M / 16) + (M + 2) + 2 * M + M;  // SmallLayout<M>::TOTAL
+  auto ev = [](int v) { return (v + 1) & ~1; };
+  const int per_group = ev(ev(ev(ev(ev(M + M / 16) + M + 1) + 2 * M) + M + 4) + 1);  // SmallLayout<M>::TOTAL
   const int twn = (tw_total(log2m) + 1) & ~1;            // per-CTA twiddle tables
   return (static_cast<size_t>(ola_groups(log2m)) * per_group + twn) * sizeof(float2);
 }
@@ -749,7 +785,6 @@ static cudaError_t set_attrs() {
   cudaError_t e;
   const int carve = cudaSharedmemCarveoutMaxShared;
   if constexpr (Plan<M>::LOG <= kSmallMaxLog2M) {
-    static_assert(SmallLayout<M>::TOTAL == (M + M / 16) + (M + 2) + 2 * M + M, "layout");
     if ((e = cudaFuncSetAttribute(ola_small_kernel<M>, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
     if ((e = cudaFuncSetAttribute(ola_small_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(k4_smem_bytes(Plan<M>::LOG))))) return e;
