@@ -333,8 +333,8 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
       const int64_t n = int64_t(1) << plans[p].log2n;
       max_pre = std::max<int64_t>(max_pre, (n - plans[p].L + plans[p].L - 1) / plans[p].L);
     }
-    const int64_t slots = 148LL * 2 * ola_groups(l);
-    const int64_t run = std::max<int64_t>((total_blocks + 4 * slots - 1) / (4 * slots), 16 * max_pre);
+    const int64_t slots = 148LL * ola_resident_groups(l);
+    const int64_t run = std::max<int64_t>((total_blocks + 6 * slots - 1) / (6 * slots), 16 * max_pre);
     Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
             static_cast<int64_t>(fp.items.size()), 0};
     for (int32_t p : v) {

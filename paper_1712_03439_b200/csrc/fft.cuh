@@ -142,9 +142,14 @@ struct Plan {
   // complex elements per thread: whole transform for M < 16, else 16 (32 for
   // the two largest sizes so that T <= 512 threads keeps 128 registers).
 #ifndef RSG_E
-#define RSG_E 16  // complex elements (max radix) per thread; measured best on B200
+#define RSG_E 16  // complex elements (max radix) per thread for M >= 1024
 #endif
-  static constexpr int E = M < RSG_E ? M : (M >= 8192 ? 32 : RSG_E);
+#ifndef RSG_E_SMALL
+#define RSG_E_SMALL 8  // ... for M <= 512
+#endif
+  // complex elements (= max radix) per thread, per size (measured on B200):
+  // 8 up to M = 512, 16 above, 32 for the two largest (T <= 512 threads)
+  static constexpr int E = M < RSG_E_SMALL ? M : (M >= 8192 ? 32 : (M <= 512 ? RSG_E_SMALL : RSG_E));
   static constexpr int T = M / E;                          // threads per transform
   static constexpr int LE = ilog2(E < 16 ? E : 16);         // log2 of the max radix
   static constexpr int NP = LOG == 0 ? 1 : (LOG + LE - 1) / LE;  // Stockham passes

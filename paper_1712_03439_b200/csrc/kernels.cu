@@ -15,7 +15,10 @@
 #include "kernels.cuh"
 
 #ifndef RSG_E
-#define RSG_E 16  // complex elements (max radix) per thread; measured best on B200
+#define RSG_E 16
+#endif
+#ifndef RSG_E_SMALL
+#define RSG_E_SMALL 8
 #endif
 
 #ifndef RSG_OLA_MINB
@@ -270,11 +273,13 @@ cudaError_t launch_cut(const CutArgs& a, int n_pairs, cudaStream_t s) {
 // ============================================================================
 // FFT sizing helpers
 // ============================================================================
+__host__ __device__ constexpr int e_of(int log2m) {  // == Plan<1 << log2m>::E
+  return (1 << log2m) < RSG_E_SMALL ? (1 << log2m)
+                                    : (log2m >= 13 ? 32 : ((1 << log2m) <= 512 ? RSG_E_SMALL : RSG_E));
+}
 __host__ __device__ constexpr int cta_threads_of(int log2m) {
   // T = M / E threads per transform (E = 16, or 32 for M >= 8192); >= 256 per CTA.
-  return log2m <= ilog2(RSG_E) ? 256
-                               : (log2m >= 13 ? (1 << log2m) / 32
-                                              : ((1 << log2m) / RSG_E > 256 ? (1 << log2m) / RSG_E : 256));
+  return (1 << log2m) / e_of(log2m) > 256 ? (1 << log2m) / e_of(log2m) : 256;
 }
 int cta_threads(int log2m) { return cta_threads_of(log2m); }
 
@@ -285,7 +290,7 @@ __host__ __device__ constexpr int groups_of() {
 
 size_t ola_smem_bytes(int log2m) {
   const int M = 1 << log2m;
-  const int E = M < RSG_E ? M : (M >= 8192 ? 32 : RSG_E);
+  const int E = e_of(log2m);
   const int T = M / E;
   const int G = cta_threads_of(log2m) / T;
   return static_cast<size_t>(G) * (M + M / 16) * sizeof(float2);
@@ -405,11 +410,6 @@ struct GroupBar {
   }
 };
 
-int ola_groups(int log2m) {
-  const int M = 1 << log2m;
-  const int E = M < RSG_E ? M : (M >= 8192 ? 32 : RSG_E);
-  return cta_threads_of(log2m) / (M / E);
-}
 
 // ---- small/medium transforms (M <= 4096): everything a block needs is in
 // shared memory.  Per group: the transform buffer, the pair's filter spectrum
@@ -417,7 +417,36 @@ int ola_groups(int log2m) {
 // previous block (so the output is written once, final, never re-read), and
 // the next block's input, prefetched with cp.async while the current block is
 // transformed.
+
 constexpr int kSmallMaxLog2M = 12;
+
+#ifndef RSG_K4_WARPS
+#define RSG_K4_WARPS 8  // target resident warps / SM for the radix-16 K4 sizes
+#endif
+// K4 (small M) CTA: a single group when T >= 64, else 64 threads of groups.
+__host__ __device__ constexpr int k4_cta_of(int log2m) {
+  return (1 << log2m) / e_of(log2m) > 64 ? (1 << log2m) / e_of(log2m) : 64;
+}
+// resident-warp target per SM: 16 for the radix-8 sizes, 8 for radix-16 (measured)
+__host__ __device__ constexpr int k4_warps_of(int log2m) { return (1 << log2m) <= 512 ? 16 : RSG_K4_WARPS; }
+__host__ __device__ constexpr int k4_minb_of(int log2m) {
+  return k4_warps_of(log2m) / (k4_cta_of(log2m) / 32) > 0 ? k4_warps_of(log2m) / (k4_cta_of(log2m) / 32) : 1;
+}
+
+int ola_groups(int log2m) {
+  const int M = 1 << log2m;
+  const int E = e_of(log2m);
+  const int cta = log2m <= kSmallMaxLog2M ? k4_cta_of(log2m) : cta_threads_of(log2m);
+  return cta / (M / E);
+}
+
+// K4 work-item groups resident per SM (for sizing work items).
+int ola_resident_groups(int log2m) {
+  if (log2m > kSmallMaxLog2M) return ola_groups(log2m);
+  const int cta = k4_cta_of(log2m);
+  return k4_minb_of(log2m) * ola_groups(log2m) > 0 ? k4_minb_of(log2m) * ola_groups(log2m) : 1;
+  (void)cta;
+}
 
 template <int M>
 struct SmallLayout {  // float2 offsets inside one group's region, all even (16-byte aligned)
@@ -425,10 +454,11 @@ struct SmallLayout {  // float2 offsets inside one group's region, all even (16-
   static constexpr int FFT = 0;
   static constexpr int GS = ev(Plan<M>::PADDED);
   static constexpr int CARRY = ev(GS + M + 1);     // 2 x N floats (double-buffered)
-  static constexpr int STAGE = ev(CARRY + 2 * M);  // N + 8 floats (bulk-copy window slack)
-  static constexpr int MBAR = ev(STAGE + M + 4);   // one 8-byte mbarrier
-  static constexpr int TOTAL = ev(MBAR + 1);
-  static_assert(STAGE % 2 == 0 && TOTAL % 2 == 0, "16-byte alignment of the bulk-copy window");
+  static constexpr int STAGE = ev(CARRY + 2 * M);  // 2 x (N + 8) floats: two blocks in flight
+  static constexpr int STAGE_STRIDE = ev(M + 4);   // float2 per stage buffer (even: 16-B aligned)
+  static constexpr int MBAR = ev(STAGE + 2 * STAGE_STRIDE);  // two 8-byte mbarriers
+  static constexpr int TOTAL = ev(MBAR + 2);
+  static_assert(STAGE % 2 == 0 && STAGE_STRIDE % 2 == 0 && TOTAL % 2 == 0, "16-byte alignment of the bulk-copy windows");
 };
 
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
@@ -463,15 +493,15 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 template <int M>
-__global__ void __launch_bounds__(cta_threads_of(Plan<M>::LOG), (Plan<M>::T > 256 ? 1 : RSG_OLA_MINB))
+__global__ void __launch_bounds__(k4_cta_of(Plan<M>::LOG), k4_minb_of(Plan<M>::LOG))
 ola_small_kernel(OlaArgs a) {
   using PL = Plan<M>;
   using LY = SmallLayout<M>;
   extern __shared__ __align__(16) float2 smem[];
   constexpr int T = PL::T;
-  constexpr int G = groups_of<M>();
+  constexpr int CTA = k4_cta_of(PL::LOG);
+  constexpr int G = CTA / T;
   constexpr int N = 2 * M;
-  constexpr int CTA = cta_threads_of(PL::LOG);
   const int g = threadIdx.x / T, t = threadIdx.x % T;
   const int item = blockIdx.x * G + g;
   const bool has = item < a.count;
@@ -490,7 +520,7 @@ ola_small_kernel(OlaArgs a) {
   float2* s = base + LY::FFT;
   float2* gs = base + LY::GS;
   float* carry0 = reinterpret_cast<float*>(base + LY::CARRY);  // 2 x N floats, zero beyond N_h - 1
-  float* stage = reinterpret_cast<float*>(base + LY::STAGE);  // N floats, zero beyond the block
+  float* stage0 = reinterpret_cast<float*>(base + LY::STAGE);  // 2 buffers of N + 8 floats
   const GroupBar<T> bar{1 + g};
   int trips = has ? it.b_end - it.b_begin : 0;
   if constexpr (T < 32) trips = __reduce_max_sync(0xffffffffu, trips);
@@ -498,31 +528,26 @@ ola_small_kernel(OlaArgs a) {
   const int own_hi = it.b_end == B ? out_len : it.b_end * L;
   // block b's samples -> stage[0, take) (4-byte cp.async: any alignment); fixed
   // trip count N/T = 2E, predicated
-  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(base + LY::MBAR);
-  // Block b's samples land in stage[d, d + take) with d = (address mod 16)/4: one
-  // 1-D TMA bulk copy (cp.async.bulk, a 16-byte aligned window) issued by one
-  // thread, or — near the end of the signal, where the window would read past
-  // it — per-thread 4-byte cp.async.
+  unsigned long long* mbar0 = reinterpret_cast<unsigned long long*>(base + LY::MBAR);
+  // Block b's samples land in stage(b)[d, d + take) with d = (address mod 16)/4:
+  // one 1-D TMA bulk copy (cp.async.bulk, a 16-byte aligned window) issued by
+  // one thread two blocks ahead (double-buffered), or — near the end of the
+  // signal, where the window would read past it — per-thread 4-byte cp.async
+  // at consumption time.
   auto window = [&](int b, int& d, int& take, bool& bulk) {
     const int st = b * L;
     take = nx - st < L ? nx - st : L;
     d = static_cast<int>((reinterpret_cast<uintptr_t>(x + st) & 15u) >> 2);
     bulk = st + take + 4 <= nx;
   };
-  auto prefetch = [&](int b) {
+  auto stage_of = [&](int k) { return stage0 + (k & 1) * (2 * LY::STAGE_STRIDE); };
+  auto prefetch = [&](int k) {  // k: index of the block within this item
+    const int b = it.b_begin + k;
     int d, take;
     bool bulk;
     window(b, d, take, bulk);
-    const float* src = x + b * L;
-    if (bulk) {
-      if (t == 0) bulk_g2s(stage, src - d, static_cast<unsigned>(((d + take) * 4 + 15) & ~15), mbar);
-    } else {
-#pragma unroll
-      for (int m = 0; m < N / T; ++m) {
-        const int i = t + m * T;
-        if (i < take) cp_async4(stage + d + i, src + i);
-      }
-    }
+    if (bulk && t == 0)
+      bulk_g2s(stage_of(k), x + b * L - d, static_cast<unsigned>(((d + take) * 4 + 15) & ~15), mbar0 + (k & 1));
   };
   for (int i = threadIdx.x; i < PL::TW_TOTAL; i += CTA) cp_async8(tws + i, a.tw + i);
   const float2* W = tws + PL::TW_PASS;
@@ -531,15 +556,20 @@ ola_small_kernel(OlaArgs a) {
     for (int k = t; k <= M; k += T) cp_async8(gs + k, Gsrc + k);
     for (int i = t; i < 2 * N; i += T) carry0[i] = 0.f;
     if (t == 0) {
-      mbar_init(mbar, 1);
+      mbar_init(mbar0, 1);
+      mbar_init(mbar0 + 1, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
   }
   cp_async_wait_all();
   __syncthreads();  // per-CTA twiddles, G, carry and barriers in place (all threads)
-  if (has) prefetch(it.b_begin);
-  unsigned phase = 0;
-  double pw2[2] = {0.0, 0.0};
+#ifndef RSG_X_NOLOAD
+  if (has) {
+    prefetch(0);
+    if (it.b_begin + 1 < it.b_end) prefetch(1);
+  }
+#endif
+  double pw = 0.0;
   constexpr int R = PL::radix(PL::NP - 1);
   constexpr int NB = PL::E / R;
 #pragma unroll 1
@@ -549,19 +579,27 @@ ola_small_kernel(OlaArgs a) {
     const int start = b * L;
     int d = 0, take = 0;
     bool bulk = false;
+    float* stage = stage_of(k);
     if (active) {
       window(b, d, take, bulk);
+#ifndef RSG_X_NOLOAD
       if (bulk) {
-        mbar_wait(mbar, phase);
-        phase ^= 1u;
+        mbar_wait(mbar0 + (k & 1), (k >> 1) & 1);
       } else {
+        const float* src = x + start;
+#pragma unroll
+        for (int m = 0; m < N / T; ++m) {
+          const int i = t + m * T;
+          if (i < take) cp_async4(stage + d + i, src + i);
+        }
         cp_async_wait_all();
       }
+#endif
     }
     bar();
     first_pass<M, float, GroupBar<T>, false>(s, t, active, stage + d, take, bar);
-#ifndef RSG_NO_PREFETCH
-    if (active && b + 1 < it.b_end) prefetch(b + 1);  // lands while this block is transformed
+#if !defined(RSG_NO_PREFETCH) && !defined(RSG_X_NOLOAD)
+    if (active && b + 2 < it.b_end) prefetch(k + 2);  // lands while blocks b, b+1 are transformed
 #endif
     forward_rest<M, 1, GroupBar<T>, true>(s, t, tws, active, bar);
     spectral_multiply<M, GroupBar<T>, true, true>(s, t, gs, W, active, bar);
@@ -575,19 +613,23 @@ ola_small_kernel(OlaArgs a) {
     // the emit needs no barrier and nothing stays live across one
     const float* cin = carry0 + (k & 1) * N;
     float* carry = carry0 + ((k + 1) & 1) * N;
+    float pb = 0.f;  // this block's power partial (FP32, <= 2E terms), folded into FP64 below
     auto emit_fn = [&](int q, int r, int c, float2 v) {
       const int e0 = 2 * c;
       const float2 ci = *reinterpret_cast<const float2*>(cin + e0);
       const float2 acc = make_float2(ci.x + v.x, ci.y + v.y);
-      double& p = pw2[(q * R + r) & 1];  // 2 independent FP64 chains
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int e = e0 + h;
         const float val = h ? acc.y : acc.x;
         if (e < L || last) {  // final sample
           if (e >= lo && e < hi) {
+#ifndef RSG_X_NOSTORE
             yb[e] = val;
-            p = fma(static_cast<double>(val), static_cast<double>(val), p);
+#endif
+#ifndef RSG_X_NOPOWER
+            pb = fmaf(val, val, pb);
+#endif
           }
         } else {
           carry[e - L] = val;  // partial sum for the next block
@@ -595,11 +637,11 @@ ola_small_kernel(OlaArgs a) {
       }
     };
     stockham_emit_pass<M, GroupBar<T>, decltype(emit_fn), true, false>(s, t, tws, active, bar, emit_fn);
+    pw += static_cast<double>(pb);
     // (N_h - 1 > L, three or more overlapping blocks, needs no extra step: the
     // old carry at e in [L, N_h - 1) comes from the other buffer.)
   }
   // Σ y^2 of the group (fixed order: deterministic) -> part[item]
-  double pw = pw2[0] + pw2[1];
   if constexpr (T >= 32) {
     __shared__ double red[CTA / 32];
     for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
@@ -774,7 +816,7 @@ size_t k4_smem_bytes(int log2m) {
   if (log2m > kSmallMaxLog2M) return ola_smem_bytes(log2m);
   const int M = 1 << log2m;
   auto ev = [](int v) { return (v + 1) & ~1; };
-  const int per_group = ev(ev(ev(ev(ev(M + M / 16) + M + 1) + 2 * M) + M + 4) + 1);  // SmallLayout<M>::TOTAL
+  const int per_group = ev(ev(ev(ev(ev(M + M / 16) + M + 1) + 2 * M) + 2 * ev(M + 4)) + 2);  // SmallLayout<M>::TOTAL
   const int twn = (tw_total(log2m) + 1) & ~1;            // per-CTA twiddle tables
   return (static_cast<size_t>(ola_groups(log2m)) * per_group + twn) * sizeof(float2);
 }
@@ -819,12 +861,13 @@ static cudaError_t spectrum_t(const SpecArgs& a, cudaStream_t s) {
 
 template <int M>
 static cudaError_t ola_t(const OlaArgs& a, cudaStream_t s) {
-  constexpr int G = groups_of<M>();
-  const int grid = (a.count + G - 1) / G;
-  if constexpr (Plan<M>::LOG <= kSmallMaxLog2M)
-    ola_small_kernel<M><<<grid, cta_threads_of(Plan<M>::LOG), k4_smem_bytes(Plan<M>::LOG), s>>>(a);
-  else
-    ola_kernel<M><<<grid, cta_threads_of(Plan<M>::LOG), k4_smem_bytes(Plan<M>::LOG), s>>>(a);
+  if constexpr (Plan<M>::LOG <= kSmallMaxLog2M) {
+    constexpr int CTA = k4_cta_of(Plan<M>::LOG), G = CTA / Plan<M>::T;
+    ola_small_kernel<M><<<(a.count + G - 1) / G, CTA, k4_smem_bytes(Plan<M>::LOG), s>>>(a);
+  } else {
+    constexpr int G = groups_of<M>();
+    ola_kernel<M><<<(a.count + G - 1) / G, cta_threads_of(Plan<M>::LOG), k4_smem_bytes(Plan<M>::LOG), s>>>(a);
+  }
   return cudaGetLastError();
 }
 

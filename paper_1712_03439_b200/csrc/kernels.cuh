@@ -145,6 +145,7 @@ struct GainArgs {
 constexpr int kMaxLog2M = 14;  // M <= 16384  (N <= 32768) in one CTA
 int cta_threads(int log2m);
 int ola_groups(int log2m);     // K4 work items per CTA
+int ola_resident_groups(int log2m);  // K4 work items resident per SM
 size_t ola_smem_bytes(int log2m);
 int tw_total(int log2m);       // float2 entries of the twiddle table of 2^log2m
 void fill_twiddles(int log2m, float2* host);  // host, FP64 -> FP32
