@@ -7,7 +7,10 @@ SRC := paper_1712_03439_b200/csrc
 OUT := paper_1712_03439_b200/_lib
 OBJS := $(OUT)/kernels.o $(OUT)/api.o
 
-all: $(OUT)/libroomsim_gpu.so oracle
+REF_INC ?= /root/reference/proj/include
+ADAPTER := tests/cpp/_build/adapter_test
+
+all: $(OUT)/libroomsim_gpu.so oracle adapter
 
 $(OUT)/kernels.o: $(SRC)/kernels.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh
 	@mkdir -p $(OUT)
@@ -23,8 +26,17 @@ $(OUT)/libroomsim_gpu.so: $(OBJS)
 oracle:
 	$(MAKE) -s -C oracle
 
+# C++ drop-in test against the reference headers (only where they exist; the
+# binary travels to the GPU box like the .so files).
+adapter: $(OUT)/libroomsim_gpu.so
+	@if [ -d "$(REF_INC)/roomsim" ]; then \
+	  mkdir -p tests/cpp/_build && \
+	  g++ -O2 -std=c++20 -I$(REF_INC) -Iinclude -I/usr/local/cuda/include tests/cpp/adapter_test.cpp \
+	    -L$(OUT) -lroomsim_gpu -Wl,-rpath,'$$ORIGIN/../../../$(OUT)' -o $(ADAPTER); \
+	else echo "reference headers not present; keeping prebuilt $(ADAPTER) (if any)"; fi
+
 clean:
 	rm -rf $(OUT)
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle adapter clean

@@ -1,0 +1,90 @@
+"""Multi-process host logic on CPU (gloo, world_size 2).
+
+The path shards by utterance with no data-path collective:
+each rank renders its LPT shard; the union of the shards must equal the
+single-process render byte for byte (outputs do not depend on the parallelism
+degree).  The per-rank compute here is the CPU oracle standing in
+for the device (there is no GPU in this container); the sharding, timing
+reduction and gather logic are the ones bench.py uses.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_1712_03439_b200 import scenes, shard
+
+    full = scenes.config3(n_utt=6, seed=77)
+    sub, ids = shard.shard_batch(full, rank, world)
+    out, out_len, layout, gains, power = oracle.port().render_batch(sub)
+    per_utt = {}
+    for k, u in enumerate(ids):
+        J = int(np.diff(sub.mic_begin)[k])
+        per_utt[int(u)] = [sub.channel(out, k, j, out_len[k]).copy() for j in range(J)]
+    gathered = [None] * world
+    dist.all_gather_object(gathered, per_utt)
+    # bench.py's timing reduction: max over ranks
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        merged = {}
+        for d in gathered:
+            assert not set(d) & set(merged), "an utterance was rendered twice"
+            merged.update(d)
+        q.put((merged, float(t[0])))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_lpt_partition_properties():
+    from paper_1712_03439_b200 import scenes, shard
+
+    b = scenes.config4(n_utt=64, signals=False)
+    w = shard.predicted_work(b)
+    for world in (1, 2, 4, 8):
+        parts = shard.lpt_partition(w, world)
+        allids = np.sort(np.concatenate(parts))
+        assert (allids == np.arange(b.n_utt)).all()
+        loads = np.array([w[p].sum() for p in parts])
+        assert loads.max() <= loads.mean() + w.max()  # LPT bound
+
+
+def test_gloo_two_ranks_match_single_process():
+    import oracle
+    from paper_1712_03439_b200 import scenes
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    merged, tmax = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert tmax == 2.0
+    full = scenes.config3(n_utt=6, seed=77)
+    out, out_len, *_ = oracle.port().render_batch(full)
+    assert sorted(merged) == list(range(full.n_utt))
+    for u in range(full.n_utt):
+        for j, ch in enumerate(merged[u]):
+            want = full.channel(out, u, j, out_len[u])
+            assert (ch.view(np.uint64) == want.view(np.uint64)).all()
