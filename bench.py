@@ -143,7 +143,8 @@ def reference_arm(args, rank, world):
 
     n_utt = args.utterances or DEFAULT_UTTS[args.config]
     threads = os.cpu_count() or 1
-    want = args.cpu_sample_utts or max(16, 6 * threads)
+    # each step ~3-5 s of the host's cores: the whole K+W run stays within minutes
+    want = args.cpu_sample_utts or max(16, 24 * threads)
     fn = lambda signals=False: scenes.CONFIGS[args.config](n_utt=n_utt, seed=args.seed, signals=signals)  # noqa: E731
     sub, k = cpu_sample(fn, n_utt, want)
     for _ in range(args.warmup):
@@ -290,7 +291,7 @@ def ours(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        want = args.cpu_sample_utts or max(16, 6 * threads)
+        want = args.cpu_sample_utts or max(32, 64 * threads)  # ~10 s of the host's cores
         fn = lambda signals=False: scenes.CONFIGS[args.config](n_utt=n_cfg, seed=args.seed, signals=signals)  # noqa: E731
         sub, k = cpu_sample(fn, n_cfg, want)
         v, dt, kind = run_cpu_reference(sub, threads)
