@@ -199,6 +199,26 @@ int choose_plan_impl(double I, double J, size_t nx, size_t nh, int* s, size_t* n
   return RS_OK;
 }
 
+// Exact max over the image lattice of ceil(|image - mic| * fs/c0): the squared
+// distance is a sum of per-axis terms and every rounded operation on the way
+// (fl(x*x), fl(a+b), sqrt, fl(d*spm), ceil) is monotone, so the maximum is the
+// one of the per-axis maxima (room_model.hpp:126-127, :42-44, :159-160).
+uint64_t lattice_max_delay(const double* L, const double* s, const double* m, int K, double spm) {
+  double mx[3];
+  for (int a = 0; a < 3; ++a) {
+    double best = 0.0;
+    for (int n = -K; n <= K; ++n) {
+      const double mirrored = (n % 2 == 0) ? s[a] : L[a] - s[a];
+      const double pos = static_cast<double>(n) * L[a] + mirrored;
+      const double diff = pos - m[a];
+      const double sq = diff * diff;
+      best = sq > best ? sq : best;
+    }
+    mx[a] = best;
+  }
+  return static_cast<uint64_t>(std::ceil(std::sqrt(mx[0] + mx[1] + mx[2]) * spm));
+}
+
 // RoomConfig::validate, room_model.hpp:57-65
 int room_validate(const double* L, double r, double fs, double c0, int order) {
   if (L[0] <= 0.0 || L[1] <= 0.0 || L[2] <= 0.0) return fail(RS_ERR_CONFIG, "room dimensions must be positive");
@@ -449,7 +469,7 @@ struct Chunk {
   std::vector<double> rg;
   std::vector<PairMeta> pair;
   std::vector<SynthItem> items;
-  std::vector<std::tuple<int64_t, int64_t, int>> synth_class;  // (offset, count, slice cap)
+  std::vector<std::tuple<int64_t, int64_t, int, int>> synth_class;  // (offset, count, slice cap, threads)
   std::vector<int> place_err;
   std::vector<std::string> place_msg;
   std::vector<PairPlan> plans;
@@ -548,9 +568,15 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
         pm.src_local = static_cast<int32_t>(i);
         pm.sig_off = b->sig_off[s0 + i];
         pm.nx = b->sig_len[s0 + i];
+        // RIR length = min(max_delay + 1, horizon), known exactly before the synth
+        int64_t pcap = cap;
+        if (strictly_inside(L, sp) && strictly_inside(L, mp)) {
+          const int64_t md = static_cast<int64_t>(lattice_max_delay(L, sp, mp, K, um.spm)) + 1;
+          pcap = um.max_taps > 0 ? std::min<int64_t>(md, um.max_taps) : md;
+        }
         pm.rir_off = ch.rir_total;
-        pm.rir_cap = cap;
-        ch.rir_total += cap;
+        pm.rir_cap = pcap;
+        ch.rir_total += pcap;
         int err = RS_OK;
         std::string msg;
         if (!strictly_inside(L, sp)) {  // room_model.hpp:144-145
@@ -569,25 +595,31 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
       }
   }
   ch.P = static_cast<int64_t>(ch.pair.size());
+  // K1 launch classes: (threads, slice size).  Small lattices (K <= 7) use
+  // 128-thread CTAs; slices are grouped so the dynamic smem fits the class.
   static const int kClass[3] = {2048, 6144, kSynthSlice};
-  std::vector<SynthItem> cls[3];
+  std::vector<SynthItem> cls[2][3];
   for (int64_t p = 0; p < ch.P; ++p) {
     if (ch.place_err[p]) continue;
     const int64_t cap = ch.pair[p].rir_cap;
+    const int K = ch.utt[ch.pair[p].utt].order;
+    const int small = K <= 7 ? 1 : 0;
     for (int64_t lo = 0; lo < cap; lo += kSynthSlice) {
       const int64_t len = std::min<int64_t>(kSynthSlice, cap - lo);
       const int k = len <= kClass[0] ? 0 : (len <= kClass[1] ? 1 : 2);
-      cls[k].push_back(SynthItem{static_cast<int32_t>(p), static_cast<int32_t>(lo), static_cast<int32_t>(len), 0});
+      cls[small][k].push_back(SynthItem{static_cast<int32_t>(p), static_cast<int32_t>(lo), static_cast<int32_t>(len), 0});
     }
   }
   ch.synth_class.clear();
-  for (int k = 2; k >= 0; --k) {  // largest slices first
-    int cap = 1;
-    for (const auto& itm : cls[k]) cap = std::max(cap, itm.slice_len);
-    ch.synth_class.emplace_back(static_cast<int64_t>(ch.items.size()), static_cast<int64_t>(cls[k].size()), cap);
-    ch.items.insert(ch.items.end(), cls[k].begin(), cls[k].end());
-    ch.slice = std::max(ch.slice, cap);
-  }
+  for (int small = 0; small < 2; ++small)
+    for (int k = 2; k >= 0; --k) {  // large lattices and slices first
+      int cap = 1;
+      for (const auto& itm : cls[small][k]) cap = std::max(cap, itm.slice_len);
+      ch.synth_class.emplace_back(static_cast<int64_t>(ch.items.size()), static_cast<int64_t>(cls[small][k].size()),
+                                  cap, small ? 128 : 512);
+      ch.items.insert(ch.items.end(), cls[small][k].begin(), cls[small][k].end());
+      ch.slice = std::max(ch.slice, cap);
+    }
   return RS_OK;
 }
 
@@ -618,11 +650,11 @@ int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO&
   RS_CUDA(cudaMemsetAsync(ch.d_rirout.p, 0, std::max<int64_t>(ch.P, 1) * sizeof(PairRir), sA));
   // one K1 launch per slice-size class, so short RIRs get more CTAs per SM
   for (size_t k = 0; k < ch.synth_class.size(); ++k) {
-    const auto& [off, n, cap] = ch.synth_class[k];
+    const auto& [off, n, cap, nt] = ch.synth_class[k];
     if (n == 0) continue;
     SynthArgs sa{ch.d_utt.as<UttMeta>(), ch.d_pair.as<PairMeta>(), ch.d_rg.as<double>(),
                  ch.d_items.as<SynthItem>() + off, ch.d_rir.as<double>(), ch.d_rirout.as<PairRir>()};
-    RS_CUDA(launch_synth(sa, static_cast<int>(n), ch.max_order, cap, sA));
+    RS_CUDA(launch_synth(sa, static_cast<int>(n), ch.max_order, cap, sA, nt));
     ++c->launches;
   }
   const double eta_factor = b->eta_db > 0.0 ? std::pow(10.0, -b->eta_db / 10.0) : 0.0;
@@ -649,6 +681,7 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
     if (ch.place_err[p]) return fail(ch.place_err[p], ch.place_msg[p]);
     const PairRir& r = ch.h_rir[p];
     if (r.flags & 1) return fail(RS_ERR_GEOMETRY, "microphone coincides with an image source");
+    if (r.flags & 8) return fail(RS_ERR_CUDA, "internal: device RIR length exceeds the host bound");
     if (r.flags & 2) return fail(RS_ERR_DEGENERATE, "all-zero impulse response has no power");
     const size_t nh = static_cast<size_t>(r.keep);
     const size_t nx = static_cast<size_t>(ch.pair[p].nx);
@@ -1137,15 +1170,8 @@ int rs_synthesize_rir(rs_ctx* c, const double room_dims[3], double reflection, d
   um.max_taps = mt;
   std::vector<double> rg;
   for (int g = 0; g <= 3 * K; ++g) rg.push_back(std::pow(r, static_cast<double>(g)));
-  int64_t capd = mt;
-  if (capd <= 0) {
-    double d2 = 0;
-    for (int a = 0; a < 3; ++a) {
-      const double e = (K + 2.0) * room_dims[a];
-      d2 += e * e;
-    }
-    capd = static_cast<int64_t>(std::ceil(std::sqrt(d2) * um.spm)) + 2;
-  }
+  const int64_t md = static_cast<int64_t>(lattice_max_delay(room_dims, src, mic, K, um.spm)) + 1;
+  const int64_t capd = mt > 0 ? std::min<int64_t>(md, mt) : md;
   PairMeta pm{};
   for (int a = 0; a < 3; ++a) {
     pm.src[a] = src[a];
@@ -1203,6 +1229,7 @@ int rs_truncate_rir(rs_ctx* c, const double* h, size_t n, double eta_db, size_t*
   PairRir hr{};
   RS_CUDA(cudaMemcpyAsync(&hr, c->rirout.p, sizeof(PairRir), cudaMemcpyDeviceToHost, c->stream));
   RS_CUDA(cudaStreamSynchronize(c->stream));
+  if (hr.flags & 8) return fail(RS_ERR_CUDA, "internal: device RIR length exceeds the host bound");
   if (hr.flags & 2) return fail(RS_ERR_DEGENERATE, "all-zero impulse response has no power");
   if (keep) *keep = static_cast<size_t>(hr.keep);
   if (cutoff_index) *cutoff_index = static_cast<size_t>(hr.cutoff);

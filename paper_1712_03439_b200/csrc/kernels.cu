@@ -55,10 +55,11 @@ __device__ __forceinline__ int nth_set_bit(unsigned m, int k) {
   return pos;
 }
 
-__global__ void __launch_bounds__(kSynthThreads) rir_synth_kernel(SynthArgs a, int slice_cap) {
+template <int NT>
+__global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_cap) {
   extern __shared__ __align__(16) unsigned char sm[];
-  constexpr int NT = kSynthThreads, NW = NT / 32;
-  static_assert(NW == 16, "16 owner warps x 16 compute warps");
+  constexpr int NW = NT / 32;  // compute warps per chunk = owner warps
+  static_assert(NW >= 2 && NW <= 32 && (NW & (NW - 1)) == 0, "power-of-two warp count");
   const SynthItem it = a.items[blockIdx.x];
   const PairMeta& pm = a.pair[it.pair];
   const UttMeta& um = a.utt[pm.utt];
@@ -88,11 +89,9 @@ __global__ void __launch_bounds__(kSynthThreads) rir_synth_kernel(SynthArgs a, i
 
   const long long V = static_cast<long long>(W) * W * W;
   // image index i = (ix W + iy) W + iz, advanced incrementally by NT per chunk
-  int ix, iy, iz;
+  int iz = tid % W, iy, ix;
   {
-    const int t0 = tid;  // < NT <= W^3 not required: carries handle small lattices
-    iz = t0 % W;
-    const int q = t0 / W;
+    const int q = tid / W;
     iy = q % W;
     ix = q / W;
   }
@@ -128,55 +127,63 @@ __global__ void __launch_bounds__(kSynthThreads) rir_synth_kernel(SynthArgs a, i
     int cx = step_x;
     while (iy >= W) { iy -= W; ++cx; }
     ix += cx;
-    // publish this chunk's entries; owner of a bin: bin & 15
+    // publish this chunk's entries; owner of a bin: bin mod NW
     int* ed = ent_d + buf * NT;
     double* ea = ent_a + buf * NT;
     unsigned* mk = mask + buf * NW * NW;
     ed[tid] = rel_bin;
     ea[tid] = amp;
-    const int owner = rel_bin >= 0 ? (rel_bin & 15) : 16;
+    const int owner = rel_bin >= 0 ? (rel_bin & (NW - 1)) : NW;
     const unsigned same = __match_any_sync(0xffffffffu, owner);
-    if (owner < 16 && lane == __ffs(same) - 1) mk[warp * NW + owner] = same;
+    if (owner < NW && lane == __ffs(same) - 1) mk[warp * NW + owner] = same;
     __syncthreads();
-    // Ordered scatter by owner warp `warp`: its entries from the 16 compute
+#ifndef RSG_X_NOSCATTER
+    // Ordered scatter by owner warp `warp`: its entries from the NW compute
     // warps, concatenated in compute-warp order (= enumeration order), are
     // compacted onto the 32 lanes; equal-delay groups fold in lane order.
     {
       const unsigned m = lane < NW ? mk[lane * NW + warp] : 0u;
-      const int cnt = __popc(m);
-      int incl = cnt;  // inclusive prefix over compute warps (lanes 0..15)
+      int incl = __popc(m);  // inclusive prefix over compute warps (lanes 0..NW-1)
 #pragma unroll
-      for (int o = 1; o < 16; o <<= 1) {
+      for (int o = 1; o < NW; o <<= 1) {
         const int v = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += v;
       }
       const int total = __shfl_sync(0xffffffffu, incl, NW - 1);
       for (int r0 = 0; r0 < total; r0 += 32) {
         const int l = r0 + lane;  // this lane's entry rank
+        // compute warp holding rank l: first w with incl[w] > l (binary search, incl monotone)
         int cw = 0;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) cw += (__shfl_sync(0xffffffffu, incl, w) <= l) ? 1 : 0;
+        for (int step = NW / 2; step > 0; step >>= 1) {
+          const int probe = __shfl_sync(0xffffffffu, incl, cw + step - 1);
+          if (probe <= l) cw += step;
+        }
         const bool valid = l < total;
-        const int cws = cw < NW ? cw : NW - 1;
-        const unsigned mm = __shfl_sync(0xffffffffu, m, cws);
-        const int excl = __shfl_sync(0xffffffffu, incl, cws) - __popc(mm);
-        const int e = cws * 32 + (valid ? nth_set_bit(mm, l - excl) : 0);
+        const unsigned mm = __shfl_sync(0xffffffffu, m, cw);
+        const int excl = __shfl_sync(0xffffffffu, incl, cw) - __popc(mm);
+        const int e = cw * 32 + (valid ? nth_set_bit(mm, l - excl) : 0);
         const int bn = valid ? ed[e] : -1 - lane;  // distinct dummy keys for idle lanes
         const double av = valid ? ea[e] : 0.0;
         const unsigned grp = __match_any_sync(0xffffffffu, bn);
         const int gsz = __popc(grp);
         const bool leader = valid && lane == __ffs(grp) - 1;
-        double acc = leader ? bins[bn] : 0.0;
         const int maxg = __reduce_max_sync(0xffffffffu, valid ? gsz : 0);
-        for (int k = 0; k < maxg; ++k) {  // fold each group in lane (= enumeration) order
-          const int src = k < gsz ? nth_set_bit(grp, k) : lane;
-          const double v = __shfl_sync(0xffffffffu, av, src);
-          if (leader && k < gsz) acc = __dadd_rn(acc, v);
+        if (maxg == 1) {  // common case: no repeated delay among these entries
+          if (valid) bins[bn] = __dadd_rn(bins[bn], av);
+        } else {
+          double acc = leader ? bins[bn] : 0.0;
+          for (int k = 0; k < maxg; ++k) {  // fold each group in lane (= enumeration) order
+            const int src = k < gsz ? nth_set_bit(grp, k) : lane;
+            const double v = __shfl_sync(0xffffffffu, av, src);
+            if (leader && k < gsz) acc = __dadd_rn(acc, v);
+          }
+          if (leader) bins[bn] = acc;
         }
-        if (leader) bins[bn] = acc;
         __syncwarp();
       }
     }
+#endif
     if (lane < NW) mk[lane * NW + warp] = 0u;  // owner clears its column for reuse
   }
   __syncthreads();
@@ -194,20 +201,26 @@ __global__ void __launch_bounds__(kSynthThreads) rir_synth_kernel(SynthArgs a, i
   }
 }
 
-size_t synth_smem_bytes(int max_order, int slice) {
-  const int W = 2 * max_order + 1;
-  return sizeof(double) * (static_cast<size_t>(slice) + 3 * W + 3 * max_order + 1 + 2 * kSynthThreads) +
-         sizeof(int) * 2 * kSynthThreads + sizeof(unsigned) * 2 * 256;
+size_t synth_smem_bytes(int max_order, int slice, int nt) {
+  const int W = 2 * max_order + 1, nw = nt / 32;
+  return sizeof(double) * (static_cast<size_t>(slice) + 3 * W + 3 * max_order + 1 + 2 * nt) +
+         sizeof(int) * 2 * nt + sizeof(unsigned) * 2 * nw * nw;
 }
 
-cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice,
-                         cudaStream_t s) {
+cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice, cudaStream_t s,
+                         int nt) {
   if (n_items == 0) return cudaSuccess;
-  const size_t smem = synth_smem_bytes(max_order, slice);
-  cudaError_t e = cudaFuncSetAttribute(rir_synth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  rir_synth_kernel<<<n_items, kSynthThreads, smem, s>>>(a, slice);
+  const size_t smem = synth_smem_bytes(max_order, slice, nt);
+  cudaError_t e;
+  if (nt == 128) {
+    e = cudaFuncSetAttribute(rir_synth_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    rir_synth_kernel<128><<<n_items, 128, smem, s>>>(a, slice);
+  } else {
+    e = cudaFuncSetAttribute(rir_synth_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    rir_synth_kernel<512><<<n_items, 512, smem, s>>>(a, slice);
+  }
   return cudaGetLastError();
 }
 
@@ -226,6 +239,10 @@ __global__ void __launch_bounds__(256) rir_cut_kernel(CutArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   long long len = static_cast<long long>(r.max_delay) + 1;
   if (um.max_taps > 0 && um.max_taps < len) len = um.max_taps;
+  if (len > pm.rir_cap) {  // cannot happen: the host computes the same maximum exactly
+    if (threadIdx.x == 0) r.flags |= 8;
+    len = pm.rir_cap;
+  }
   if (r.flags & 1) len = 0;
   const double* h = a.rir + pm.rir_off;
   if (a.eta_factor <= 0.0 || len == 0) {

@@ -153,10 +153,11 @@ cudaError_t kernels_init();    // smem attributes
 
 constexpr int kSynthThreads = 512;
 constexpr int kSynthSlice = 12288;  // FP64 bins per K1 CTA (96 KB)
-size_t synth_smem_bytes(int max_order, int slice);
+size_t synth_smem_bytes(int max_order, int slice, int nt);
 
+// nt = 512 (16 warps) or 128 (4 warps, small lattices)
 cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice,
-                         cudaStream_t s);
+                         cudaStream_t s, int nt = 512);
 cudaError_t launch_cut(const CutArgs& a, int n_pairs, cudaStream_t s);
 cudaError_t launch_spectrum(int log2m, const SpecArgs& a, cudaStream_t s);
 cudaError_t launch_ola(int log2m, const OlaArgs& a, cudaStream_t s);
