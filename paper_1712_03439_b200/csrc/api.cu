@@ -8,6 +8,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <numeric>
@@ -79,6 +80,7 @@ struct DevBuf {
 // Page-locked host staging (bump allocator) so H2D/D2H copies are truly async.
 struct PinnedArena {
   char* p = nullptr;
+  char* dp = nullptr;
   size_t cap = 0, used = 0;
   int reserve(size_t bytes) {  // only call while no copy from this arena is pending
     if (bytes <= cap) return RS_OK;
@@ -86,15 +88,20 @@ struct PinnedArena {
     p = nullptr;
     cap = 0;
     const size_t want = bytes + bytes / 4 + 4096;
-    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p), want, cudaHostAllocDefault);
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p), want, cudaHostAllocMapped);
     if (e != cudaSuccess) {
       p = nullptr;
       return fail(RS_ERR_OOM, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
     }
     cap = want;
+    e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), p, 0);
+    if (e != cudaSuccess) return fail(RS_ERR_CUDA, std::string("cudaHostGetDevicePointer: ") + cudaGetErrorString(e));
     return RS_OK;
   }
   void reset() { used = 0; }
+  // device-side alias of a pointer into this arena (mapped pinned memory)
+  template <class T>
+  T* dev(T* h) const { return reinterpret_cast<T*>(dp + (reinterpret_cast<char*>(h) - p)); }
   template <class T>
   T* alloc(size_t n) {
     used = (used + 63) & ~size_t(63);
@@ -387,6 +394,25 @@ struct FilterBufs {
   DevBuf plan, lists, olaitems, spec, y, part;
 };
 
+thread_local int64_t g_copy_launches = 0;  // pcie_copy_kernel launches of the current render
+// Host-buffer renders move metadata with pcie_copy_kernel (the copy engines are busy
+// with signal/output transfers and serve copies in FIFO order); device-buffer renders
+// keep the copy engines, which are otherwise idle.
+thread_local bool g_kernel_copies = false;
+
+// Small pinned-host <-> device copy on `st` by the path chosen above.
+int small_copy(void* dst, void* dst_mapped, const void* src, const void* src_mapped, size_t bytes,
+               cudaMemcpyKind kind, cudaStream_t st) {
+  if (bytes == 0) return RS_OK;
+  if (g_kernel_copies) {
+    RS_CUDA(launch_pcie_copy(dst_mapped, src_mapped, bytes, st));
+    ++g_copy_launches;
+  } else {
+    RS_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, st));
+  }
+  return RS_OK;
+}
+
 // Async H2D of a host vector through a pinned arena (or synchronously staged
 // pageable memory when `arena` is null).
 template <class T>
@@ -398,7 +424,7 @@ int upload_on(DevBuf& b, const std::vector<T>& v, cudaStream_t st, PinnedArena* 
     T* h = arena->alloc<T>(v.size());
     if (!h) return fail(RS_ERR_OOM, "pinned staging arena exhausted");
     std::memcpy(h, v.data(), v.size() * sizeof(T));
-    src = h;
+    return small_copy(b.p, b.p, h, arena->dev(h), v.size() * sizeof(T), cudaMemcpyHostToDevice, st);
   }
   RS_CUDA(cudaMemcpyAsync(b.p, src, v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
   return RS_OK;
@@ -487,11 +513,14 @@ struct Chunk {
   double* h_gain = nullptr;
   double* h_power = nullptr;
   cudaEvent_t ev_rir = nullptr, ev_syn0 = nullptr, ev_syn1 = nullptr, ev_k4a = nullptr, ev_k4b = nullptr,
-              ev_mix0 = nullptr, ev_mix1 = nullptr;
+              ev_mix0 = nullptr, ev_mix1 = nullptr, ev_sig = nullptr, ev_out = nullptr;
   int init_events() {
     cudaEvent_t* evs[] = {&ev_rir, &ev_syn0, &ev_syn1, &ev_k4a, &ev_k4b, &ev_mix0, &ev_mix1};
     for (auto* e : evs)
       if (!*e) RS_CUDA(cudaEventCreate(e));
+    cudaEvent_t* sync_only[] = {&ev_sig, &ev_out};
+    for (auto* e : sync_only)
+      if (!*e) RS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     return RS_OK;
   }
   void release() {
@@ -502,7 +531,7 @@ struct Chunk {
     for (DevBuf* b : bufs) b->release();
     hA.release();
     hB.release();
-    cudaEvent_t evs[] = {ev_rir, ev_syn0, ev_syn1, ev_k4a, ev_k4b, ev_mix0, ev_mix1};
+    cudaEvent_t evs[] = {ev_rir, ev_syn0, ev_syn1, ev_k4a, ev_k4b, ev_mix0, ev_mix1, ev_sig, ev_out};
     for (auto e : evs)
       if (e) cudaEventDestroy(e);
   }
@@ -514,8 +543,40 @@ struct rs_render_state {
   FilterBufs conv;                  // single-pair convolve path
   std::vector<Chunk> chunks;
   std::vector<int64_t> pair_chunk;  // global pair -> chunk
-  cudaStream_t sA = nullptr, sB = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_endA = nullptr, ev_endB = nullptr;
+  // sA: K1/K2 and RIR summaries; sB: K3-K6; sH/sD: host<->device copies of the
+  // signals and outputs, so the PCIe transfers run back to back under the kernels.
+  cudaStream_t sA = nullptr, sB = nullptr, sH = nullptr, sD = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_endA = nullptr, ev_endB = nullptr, ev_endH = nullptr, ev_endD = nullptr;
+  // RSG_TRACE=1: per-chunk timeline of the pipeline (device events + host marks) on stderr
+  bool tracing = false;
+  cudaEvent_t tr0 = nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> trace_ev;
+  std::vector<std::pair<std::string, double>> trace_host;
+  std::chrono::steady_clock::time_point trace_t0;
+  void mark(cudaStream_t st, const std::string& label) {
+    if (!tracing) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    trace_ev.emplace_back(label, e);
+  }
+  void hmark(const std::string& label) {
+    if (tracing)
+      trace_host.emplace_back(
+          label, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - trace_t0).count());
+  }
+  void dump() {
+    if (!tracing) return;
+    for (auto& [l, e] : trace_ev) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, tr0, e);
+      std::fprintf(stderr, "[trace] dev %8.2f %s\n", ms, l.c_str());
+      cudaEventDestroy(e);
+    }
+    for (auto& [l, t] : trace_host) std::fprintf(stderr, "[trace] host %8.2f %s\n", t, l.c_str());
+    trace_ev.clear();
+    trace_host.clear();
+  }
 };
 
 namespace {
@@ -624,23 +685,13 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
 }
 
 // Stream A: inputs, K1, K2, RIR summary -> pinned host.
-int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO& io, cudaStream_t sA) {
+int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, cudaStream_t sA) {
   RS_TRY(ch.init_events());
   size_t need = staged_bytes(ch.utt) + staged_bytes(ch.pair) + staged_bytes(ch.rg) + staged_bytes(ch.items) +
                 ((std::max<int64_t>(ch.P, 1) * sizeof(PairRir) + 63) & ~size_t(63)) + 64;
   RS_TRY(ch.hA.reserve(need));
   ch.hA.reset();
   if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_syn0, sA));
-  if (io.h_signals) {  // host path: this chunk's signal span
-    int64_t lo = INT64_MAX, hi = 0;
-    for (int64_t s = b->src_begin[ch.u0]; s < b->src_begin[ch.u1]; ++s) {
-      lo = std::min(lo, b->sig_off[s]);
-      hi = std::max(hi, b->sig_off[s] + b->sig_len[s]);
-    }
-    if (hi > lo)
-      RS_CUDA(cudaMemcpyAsync(const_cast<float*>(io.d_signals) + lo, io.h_signals + lo, (hi - lo) * sizeof(float),
-                              cudaMemcpyHostToDevice, sA));
-  }
   RS_TRY(upload_on(ch.d_utt, ch.utt, sA, &ch.hA));
   RS_TRY(upload_on(ch.d_pair, ch.pair, sA, &ch.hA));
   RS_TRY(upload_on(ch.d_rg, ch.rg, sA, &ch.hA));
@@ -664,8 +715,8 @@ int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO&
   ++c->launches;
   if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_syn1, sA));
   ch.h_rir = ch.hA.alloc<PairRir>(ch.P);
-  if (ch.P)
-    RS_CUDA(cudaMemcpyAsync(ch.h_rir, ch.d_rirout.p, ch.P * sizeof(PairRir), cudaMemcpyDeviceToHost, sA));
+  RS_TRY(small_copy(ch.h_rir, ch.hA.dev(ch.h_rir), ch.d_rirout.p, ch.d_rirout.p, ch.P * sizeof(PairRir),
+                    cudaMemcpyDeviceToHost, sA));
   RS_CUDA(cudaEventRecord(ch.ev_rir, sA));
   return RS_OK;
 }
@@ -723,7 +774,7 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
 
 // Stream B: K3, K4, K5, K6 (+ output download on the host path).
 int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO& io, const int64_t* out_off,
-                   const int64_t* out_stride, cudaStream_t sB) {
+                   const int64_t* out_stride, cudaStream_t sB, cudaStream_t sD) {
   const int64_t U = ch.u1 - ch.u0;
   std::vector<double> snr_lin(b->src_begin[ch.u1] - b->src_begin[ch.u0]);
   const int64_t s_first = b->src_begin[ch.u0];
@@ -756,6 +807,7 @@ int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO
                 staged_bytes(ustride) + 3 * (((std::max<int64_t>(ch.P, 1) * 8) + 63) & ~size_t(63)) + 256;
   RS_TRY(ch.hB.reserve(need));
   ch.hB.reset();
+  if (io.h_signals) RS_CUDA(cudaStreamWaitEvent(sB, ch.ev_sig, 0));
   RS_TRY(launch_filter(c, ch.fb, ch.fp, ch.plans, ch.d_pair.as<PairMeta>(), ch.d_rir.as<double>(), io.d_signals,
                        sB, &ch.hB, ch.ev_k4a, ch.ev_k4b));
   if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_mix0, sB));
@@ -788,18 +840,24 @@ int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO
   ch.h_gain = ch.hB.alloc<double>(ch.P);
   ch.h_power = ch.hB.alloc<double>(ch.P);
   if (ch.P) {
-    RS_CUDA(cudaMemcpyAsync(ch.h_flags, ch.d_flags.p, ch.P * sizeof(int32_t), cudaMemcpyDeviceToHost, sB));
-    RS_CUDA(cudaMemcpyAsync(ch.h_gain, ch.d_gain.p, ch.P * sizeof(double), cudaMemcpyDeviceToHost, sB));
-    RS_CUDA(cudaMemcpyAsync(ch.h_power, ch.d_power.p, ch.P * sizeof(double), cudaMemcpyDeviceToHost, sB));
+    RS_TRY(small_copy(ch.h_flags, ch.hB.dev(ch.h_flags), ch.d_flags.p, ch.d_flags.p, ch.P * sizeof(int32_t),
+                      cudaMemcpyDeviceToHost, sB));
+    RS_TRY(small_copy(ch.h_gain, ch.hB.dev(ch.h_gain), ch.d_gain.p, ch.d_gain.p, ch.P * sizeof(double),
+                      cudaMemcpyDeviceToHost, sB));
+    RS_TRY(small_copy(ch.h_power, ch.hB.dev(ch.h_power), ch.d_power.p, ch.d_power.p, ch.P * sizeof(double),
+                      cudaMemcpyDeviceToHost, sB));
   }
-  if (io.h_out) {  // host path: this chunk's output span
+  if (io.h_out) {  // host path: this chunk's output span, on the download stream
     int64_t lo = INT64_MAX, hi = 0;
     for (int64_t u = ch.u0; u < ch.u1; ++u) {
       lo = std::min(lo, out_off[u]);
       hi = std::max(hi, out_off[u] + (b->mic_begin[u + 1] - b->mic_begin[u]) * out_stride[u]);
     }
-    if (hi > lo)
-      RS_CUDA(cudaMemcpyAsync(io.h_out + lo, io.d_out + lo, (hi - lo) * sizeof(float), cudaMemcpyDeviceToHost, sB));
+    if (hi > lo) {
+      RS_CUDA(cudaEventRecord(ch.ev_out, sB));
+      RS_CUDA(cudaStreamWaitEvent(sD, ch.ev_out, 0));
+      RS_CUDA(cudaMemcpyAsync(io.h_out + lo, io.d_out + lo, (hi - lo) * sizeof(float), cudaMemcpyDeviceToHost, sD));
+    }
   }
   return RS_OK;
 }
@@ -813,26 +871,28 @@ int state_init(rs_ctx* c) {
   c->rs = new rs_render_state();
   RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sA, cudaStreamNonBlocking));
   RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sB, cudaStreamNonBlocking));
-  RS_CUDA(cudaEventCreateWithFlags(&c->rs->ev_start, cudaEventDisableTiming));
-  RS_CUDA(cudaEventCreateWithFlags(&c->rs->ev_endA, cudaEventDisableTiming));
-  RS_CUDA(cudaEventCreateWithFlags(&c->rs->ev_endB, cudaEventDisableTiming));
+  RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sH, cudaStreamNonBlocking));
+  RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sD, cudaStreamNonBlocking));
+  cudaEvent_t* evs[] = {&c->rs->ev_start, &c->rs->ev_endA, &c->rs->ev_endB, &c->rs->ev_endH, &c->rs->ev_endD};
+  for (auto* e : evs) RS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   return RS_OK;
 }
 
 void destroy_state(rs_ctx* c) {
   if (!c->rs) return;
   rs_render_state* r = c->rs;
-  if (r->sA) cudaStreamSynchronize(r->sA);
-  if (r->sB) cudaStreamSynchronize(r->sB);
+  cudaStream_t ss[] = {r->sA, r->sB, r->sH, r->sD};
+  for (auto st : ss)
+    if (st) cudaStreamSynchronize(st);
   for (auto& ch : r->chunks) ch.release();
   FilterBufs& f = r->conv;
   DevBuf* bufs[] = {&f.plan, &f.lists, &f.olaitems, &f.spec, &f.y, &f.part};
   for (DevBuf* b : bufs) b->release();
-  if (r->sA) cudaStreamDestroy(r->sA);
-  if (r->sB) cudaStreamDestroy(r->sB);
-  if (r->ev_start) cudaEventDestroy(r->ev_start);
-  if (r->ev_endA) cudaEventDestroy(r->ev_endA);
-  if (r->ev_endB) cudaEventDestroy(r->ev_endB);
+  for (auto st : ss)
+    if (st) cudaStreamDestroy(st);
+  cudaEvent_t evs[] = {r->ev_start, r->ev_endA, r->ev_endB, r->ev_endH, r->ev_endD};
+  for (auto e : evs)
+    if (e) cudaEventDestroy(e);
   delete r;
   c->rs = nullptr;
 }
@@ -849,16 +909,37 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
   rs_render_state& R = *c->rs;
   const int64_t U = b->n_utt;
   c->launches = 0;
+  g_copy_launches = 0;
+  const bool host_io = io.h_signals || io.h_out;
+  g_kernel_copies = host_io;
   // ---- chunking by pair count ----------------------------------------------------
+  static const int64_t chunk_pairs = [] {
+    const char* e = std::getenv("RSG_CHUNK_PAIRS");  // tuning override
+    return e ? std::max<int64_t>(1, std::atoll(e)) : kChunkPairs;
+  }();
+  // Host path: the last chunk_pairs are split C/2, C/4, C/4 so the pipeline drains
+  // quickly (only the final chunk's filter and download follow the last upload).
   std::vector<std::pair<int64_t, int64_t>> ranges;
   {
-    int64_t u0 = 0, pairs = 0;
+    int64_t total = 0;
+    for (int64_t u = 0; u < U; ++u)
+      total += (b->src_begin[u + 1] - b->src_begin[u]) * (b->mic_begin[u + 1] - b->mic_begin[u]);
+    int64_t u0 = 0, pairs = 0, done = 0;
+    auto target = [&] {
+      const int64_t rem = total - done;
+      if (!host_io) return chunk_pairs;
+      if (rem > chunk_pairs) return std::min(chunk_pairs, rem - chunk_pairs);
+      return rem > chunk_pairs / 4 ? std::max<int64_t>(rem / 2, chunk_pairs / 4) : rem;
+    };
+    int64_t want = target();
     for (int64_t u = 0; u < U; ++u) {
       pairs += (b->src_begin[u + 1] - b->src_begin[u]) * (b->mic_begin[u + 1] - b->mic_begin[u]);
-      if (pairs >= kChunkPairs || u + 1 == U) {
+      if (pairs >= want || u + 1 == U) {
         ranges.emplace_back(u0, u + 1);
         u0 = u + 1;
+        done += pairs;
         pairs = 0;
+        want = target();
       }
     }
   }
@@ -877,35 +958,79 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
   c->last_pairs = Ptot;
   // ---- fork from the caller's stream ---------------------------------------------------
   RS_CUDA(cudaEventRecord(R.ev_start, c->stream));
+  R.tracing = std::getenv("RSG_TRACE") != nullptr;
+  if (R.tracing) {
+    if (!R.tr0) cudaEventCreate(&R.tr0);
+    cudaEventRecord(R.tr0, c->stream);
+    R.trace_t0 = std::chrono::steady_clock::now();
+  }
   RS_CUDA(cudaStreamWaitEvent(R.sA, R.ev_start, 0));
   RS_CUDA(cudaStreamWaitEvent(R.sB, R.ev_start, 0));
+  RS_CUDA(cudaStreamWaitEvent(R.sH, R.ev_start, 0));
+  RS_CUDA(cudaStreamWaitEvent(R.sD, R.ev_start, 0));
   if (c->profiling) RS_CUDA(cudaEventRecord(c->st[0], c->stream));
+  // Host path: chunk k's signal span goes up on sH, kSigAhead chunks ahead of the
+  // filter.  Not all at once: the copy engine serves H2D copies in FIFO order, so the
+  // small per-chunk metadata uploads on sA/sB would otherwise queue behind every
+  // chunk's signals.
+  constexpr int kSigAhead = 2;
+  auto enqueue_sig = [&](int k) -> int {
+    if (!io.h_signals || k >= nch) return RS_OK;
+    Chunk& ch = R.chunks[k];
+    RS_TRY(ch.init_events());
+    int64_t lo = INT64_MAX, hi = 0;
+    for (int64_t s = b->src_begin[ch.u0]; s < b->src_begin[ch.u1]; ++s) {
+      lo = std::min(lo, b->sig_off[s]);
+      hi = std::max(hi, b->sig_off[s] + b->sig_len[s]);
+    }
+    if (hi > lo)
+      RS_CUDA(cudaMemcpyAsync(const_cast<float*>(io.d_signals) + lo, io.h_signals + lo, (hi - lo) * sizeof(float),
+                              cudaMemcpyHostToDevice, R.sH));
+    RS_CUDA(cudaEventRecord(ch.ev_sig, R.sH));
+    R.mark(R.sH, "sig done " + std::to_string(k));
+    return RS_OK;
+  };
   int status = RS_OK;
   auto t_plan = 0.0;
   // ---- the pipeline: synth(k+1) is enqueued before the host plans chunk k -----------
   if (nch > 0) {
     status = prep_chunk(b, R.chunks[0]);
-    if (!status) status = enqueue_synth(c, b, R.chunks[0], io, R.sA);
+    if (!status) status = enqueue_synth(c, b, R.chunks[0], R.sA);
   }
+  for (int k = 0; k < kSigAhead && !status; ++k) status = enqueue_sig(k);
   for (int k = 0; k < nch && !status; ++k) {
     if (k + 1 < nch) {
       status = prep_chunk(b, R.chunks[k + 1]);
-      if (!status) status = enqueue_synth(c, b, R.chunks[k + 1], io, R.sA);
+      if (!status) status = enqueue_synth(c, b, R.chunks[k + 1], R.sA);
       if (status) break;
     }
+    R.hmark("plan wait " + std::to_string(k));
     const auto t0 = std::chrono::steady_clock::now();
     status = plan_chunk(b, R.chunks[k], out_stride);
+    R.hmark("plan done " + std::to_string(k));
     t_plan += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (status) break;
-    status = enqueue_filter(c, b, R.chunks[k], io, out_off, out_stride, R.sB);
+    status = enqueue_filter(c, b, R.chunks[k], io, out_off, out_stride, R.sB, R.sD);
+    R.mark(R.sB, "filter+mix enq-end " + std::to_string(k));
+    R.mark(R.sD, "d2h done " + std::to_string(k));
+    R.mark(R.sA, "sA at " + std::to_string(k));
+    if (!status) status = enqueue_sig(k + kSigAhead);
   }
   // ---- join back into the caller's stream -------------------------------------------
   cudaEventRecord(R.ev_endA, R.sA);
   cudaEventRecord(R.ev_endB, R.sB);
+  cudaEventRecord(R.ev_endH, R.sH);
+  cudaEventRecord(R.ev_endD, R.sD);
   cudaStreamWaitEvent(c->stream, R.ev_endA, 0);
   cudaStreamWaitEvent(c->stream, R.ev_endB, 0);
+  cudaStreamWaitEvent(c->stream, R.ev_endH, 0);
+  cudaStreamWaitEvent(c->stream, R.ev_endD, 0);
   if (c->profiling) cudaEventRecord(c->st[6], c->stream);
   RS_CUDA(cudaStreamSynchronize(c->stream));
+  R.hmark("sync done");
+  c->launches += g_copy_launches;
+  g_kernel_copies = false;
+  R.dump();
   if (status) return status;
   c->host_plan_ms = t_plan;
   // ---- results, degenerate-power check, timing --------------------------------------

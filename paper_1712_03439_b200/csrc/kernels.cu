@@ -1013,6 +1013,30 @@ cudaError_t launch_mix(const MixArgs& a, int64_t n_chan, int64_t max_len, cudaSt
   return cudaGetLastError();
 }
 
+// ---- small host<->device copies through the SMs ----------------------------------
+// Per-chunk metadata and summaries move through mapped pinned memory with a kernel
+// instead of the copy engines: the engines serve copies in FIFO order, and these
+// small transfers must not queue behind a chunk's signal or output transfer.
+__global__ void pcie_copy_kernel(char* __restrict__ dst, const char* __restrict__ src, size_t n) {
+  const size_t n16 = n / 16;
+  uint4* d16 = reinterpret_cast<uint4*>(dst);
+  const uint4* s16 = reinterpret_cast<const uint4*>(src);
+  const size_t tid = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = tid; i < n16; i += stride) d16[i] = s16[i];
+  const size_t t = n16 * 16 + tid;
+  if (t < n) dst[t] = src[t];
+}
+
+cudaError_t launch_pcie_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return cudaSuccess;
+  if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) return cudaErrorMisalignedAddress;
+  const size_t n16 = bytes / 16 + 1;
+  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((n16 + 255) / 256, 148 * 4));
+  pcie_copy_kernel<<<blocks, 256, 0, s>>>(static_cast<char*>(dst), static_cast<const char*>(src), bytes);
+  return cudaGetLastError();
+}
+
 // ---- conversions -------------------------------------------------------------
 __global__ void d2f_kernel(const double* in, float* out, int64_t n) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;

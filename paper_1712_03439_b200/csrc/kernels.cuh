@@ -163,6 +163,8 @@ cudaError_t launch_spectrum(int log2m, const SpecArgs& a, cudaStream_t s);
 cudaError_t launch_ola(int log2m, const OlaArgs& a, cudaStream_t s);
 cudaError_t launch_gain(const GainArgs& a, cudaStream_t s);
 cudaError_t launch_mix(const MixArgs& a, int64_t n_chan, int64_t max_len, cudaStream_t s);
+// dst/src: device or mapped-pinned-host pointers, 16-byte aligned
+cudaError_t launch_pcie_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
 // Seam kernels (RealFftEngine): count transforms of size 2^(log2m+1).
 cudaError_t launch_rfft(int log2m, bool inverse, const float* in_real, const float2* in_spec,
                         float* out_real, float2* out_spec, int count, const float2* tw,
