@@ -763,7 +763,7 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
     pl.spec_off = spec_off;
     pl.y_off = y_off;
     spec_off += static_cast<int64_t>(n / 2 + 1);
-    y_off += pl.out_len;
+    y_off += (pl.out_len + 3) & ~int64_t(3);  // 16-byte aligned rows: K6 reads float4
     int64_t& ul = ch.ulen[ch.pair[p].utt];
     ul = std::max(ul, pl.out_len);
   }

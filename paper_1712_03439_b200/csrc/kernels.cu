@@ -993,16 +993,43 @@ __global__ void __launch_bounds__(256) mix_kernel(MixArgs a) {
   const int I = a.utt_I[u], J = a.utt_J[u];
   const long long pair0 = a.utt_pair0[u];
   float* out = a.out + a.chan_out[ch];
-  for (long long n = n0 + threadIdx.x; n < n1; n += blockDim.x) {
-    double acc = 0.0;
+  const bool out16 = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+  // four consecutive samples per thread: float4 loads of every source's row (rows are
+  // 16-byte aligned, y_off % 4 == 0), FP64 sums in source order, one float4 store
+  for (long long n = n0 + 4 * threadIdx.x; n < n1; n += 4 * blockDim.x) {
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
     if (n < len) {
       for (int i = 0; i < I; ++i) {
         const long long p = pair0 + static_cast<long long>(i) * J + j;
-        const PairPlan& pl = a.plan[p];
-        if (n < pl.out_len) acc = fma(a.gain[p], static_cast<double>(__ldg(a.y + pl.y_off + n)), acc);
+        const long long ol = a.plan[p].out_len;
+        if (n >= ol) continue;
+        const double g = a.gain[p];
+        const float* yr = a.y + a.plan[p].y_off;
+        if (n + 3 < ol) {
+          const float4 v = __ldcs(reinterpret_cast<const float4*>(yr + n));
+          acc0 = fma(g, static_cast<double>(v.x), acc0);
+          acc1 = fma(g, static_cast<double>(v.y), acc1);
+          acc2 = fma(g, static_cast<double>(v.z), acc2);
+          acc3 = fma(g, static_cast<double>(v.w), acc3);
+        } else {  // the row ends inside this quad
+          acc0 = fma(g, static_cast<double>(yr[n]), acc0);
+          if (n + 1 < ol) acc1 = fma(g, static_cast<double>(yr[n + 1]), acc1);
+          if (n + 2 < ol) acc2 = fma(g, static_cast<double>(yr[n + 2]), acc2);
+        }
       }
     }
-    out[n] = static_cast<float>(acc);
+    // samples in [len, stride) are the zero-filled tail (acc stays 0 there)
+    const float4 o = make_float4(static_cast<float>(acc0), n + 1 < len ? static_cast<float>(acc1) : 0.f,
+                                 n + 2 < len ? static_cast<float>(acc2) : 0.f,
+                                 n + 3 < len ? static_cast<float>(acc3) : 0.f);
+    if (out16 && n + 3 < n1) {
+      __stcs(reinterpret_cast<float4*>(out + n), o);
+    } else {
+      out[n] = o.x;
+      if (n + 1 < n1) out[n + 1] = o.y;
+      if (n + 2 < n1) out[n + 2] = o.z;
+      if (n + 3 < n1) out[n + 3] = o.w;
+    }
   }
 }
 
