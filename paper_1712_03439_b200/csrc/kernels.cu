@@ -32,27 +32,22 @@ namespace rsg {
 //
 // One CTA per (pair, slice of delay bins).  The RIR slice lives in shared
 // memory as FP64.  Images are processed in enumeration order (nx -> ny -> nz,
-// room_model.hpp:118-120) in chunks of 512; every bin must receive its
-// contributions sequentially in that order (rir[delay] += amp, :170), so the
-// chunk is resolved by "owner" warps: warp o owns the bins with
-// (bin & 15) == o, walks the 16 compute warps' entries in order, and per
-// compute warp lets the first lane of each equal-delay group (match_any)
-// fold the group in lane order.  All arithmetic uses _rn intrinsics so no
-// FMA contraction can change a bit; r^g comes from the host's std::pow.
+// room_model.hpp:118-120) in chunks of NT, one per thread; every bin must
+// receive its contributions sequentially in that order (rir[delay] += amp,
+// :170).  Each chunk is resolved by "owner" warps: warp o owns the bins with
+// (bin mod NW) == o.  After the chunk's images are computed, each warp
+// publishes one ballot-built lane mask per owner; the entries are then
+// counting-sorted into owner-major lists (stable: compute-warp order, then
+// lane order = enumeration order), and each owner folds its list into the bins
+// in rounds — round r applies the r-th entry of every equal-delay group, so
+// no two lanes touch one bin at once and each bin sees its entries in order.
+// All arithmetic uses _rn intrinsics so no FMA contraction can change a bit;
+// r^g comes from the host's std::pow.
 // ============================================================================
-// 0-indexed position of the k-th set bit of m (k < popc(m)).
-__device__ __forceinline__ int nth_set_bit(unsigned m, int k) {
-  int pos = 0;
-#pragma unroll
-  for (int w = 16; w > 0; w >>= 1) {
-    const int c = __popc(m & ((1u << w) - 1u));
-    if (k >= c) {
-      k -= c;
-      m >>= w;
-      pos += w;
-    }
-  }
-  return pos;
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
 }
 
 template <int NT>
@@ -60,19 +55,20 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   extern __shared__ __align__(16) unsigned char sm[];
   constexpr int NW = NT / 32;  // compute warps per chunk = owner warps
   static_assert(NW >= 2 && NW <= 32 && (NW & (NW - 1)) == 0, "power-of-two warp count");
+  constexpr int OB = NW == 2 ? 1 : NW == 4 ? 2 : NW == 8 ? 3 : NW == 16 ? 4 : 5;  // owner bits
   const SynthItem it = a.items[blockIdx.x];
   const PairMeta& pm = a.pair[it.pair];
   const UttMeta& um = a.utt[pm.utt];
   const int K = um.order, W = 2 * K + 1;
+  const double spm = um.spm;
   double* bins = reinterpret_cast<double*>(sm);
   double* ax = bins + slice_cap;                 // [3][W] squared per-axis offsets
   double* rg = ax + 3 * W;                       // [3K+1]
-  double* ent_a = rg + (3 * K + 1);              // [2][NT]
-  int* ent_d = reinterpret_cast<int*>(ent_a + 2 * NT);          // [2][NT]
-  unsigned* mask = reinterpret_cast<unsigned*>(ent_d + 2 * NT);  // [2][NW compute][NW owner]
+  double* ent_a = rg + (3 * K + 1);              // [NT] owner-major sorted amplitudes
+  int* ent_d = reinterpret_cast<int*>(ent_a + NT);           // [NT] their bins
+  unsigned* mask = reinterpret_cast<unsigned*>(ent_d + NT);  // [NW compute][NW owner]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lo = it.slice_lo, len = it.slice_len;
-
   for (int l = tid; l < len; l += NT) bins[l] = 0.0;
   for (int idx = tid; idx < 3 * W; idx += NT) {
     const int axis = idx / W, n = idx - axis * W - K;
@@ -84,7 +80,6 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
     ax[idx] = __dmul_rn(diff, diff);                    // :43 v.x * v.x
   }
   for (int g = tid; g <= 3 * K; g += NT) rg[g] = a.rg[um.rg_off + g];
-  for (int i = tid; i < 2 * NW * NW; i += NT) mask[i] = 0u;
   __syncthreads();
 
   const long long V = static_cast<long long>(W) * W * W;
@@ -97,10 +92,10 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   }
   const int step_z = NT % W, step_q = NT / W;
   const int step_y = step_q % W, step_x = step_q / W;
+  const unsigned lt = lanemask_lt();
   unsigned long long max_d = 0;
   int geo = 0;
-  int buf = 0;
-  for (long long base = 0; base < V; base += NT, buf ^= 1) {
+  for (long long base = 0; base < V; base += NT) {
     const long long i = base + tid;
     int rel_bin = -1;
     double amp = 0.0;
@@ -108,8 +103,8 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
       // norm: sqrt((x*x + y*y) + z*z), room_model.hpp:43
       const double d2 = __dadd_rn(__dadd_rn(ax[ix], ax[W + iy]), ax[2 * W + iz]);
       const double d = __dsqrt_rn(d2);
-      if (d <= 0.0) geo = 1;                         // :157-158
-      const double dl = ceil(__dmul_rn(d, um.spm));  // :159-160
+      if (d <= 0.0) geo = 1;                     // :157-158
+      const double dl = ceil(__dmul_rn(d, spm));  // :159-160
       const unsigned long long D = static_cast<unsigned long long>(dl);
       max_d = D > max_d ? D : max_d;
       const long long rel = static_cast<long long>(D) - lo;
@@ -127,64 +122,64 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
     int cx = step_x;
     while (iy >= W) { iy -= W; ++cx; }
     ix += cx;
-    // publish this chunk's entries; owner of a bin: bin mod NW
-    int* ed = ent_d + buf * NT;
-    double* ea = ent_a + buf * NT;
-    unsigned* mk = mask + buf * NW * NW;
-    ed[tid] = rel_bin;
-    ea[tid] = amp;
-    const int owner = rel_bin >= 0 ? (rel_bin & (NW - 1)) : NW;
-    const unsigned same = __match_any_sync(0xffffffffu, owner);
-    if (owner < NW && lane == __ffs(same) - 1) mk[warp * NW + owner] = same;
-    __syncthreads();
 #ifndef RSG_X_NOSCATTER
-    // Ordered scatter by owner warp `warp`: its entries from the NW compute
-    // warps, concatenated in compute-warp order (= enumeration order), are
-    // compacted onto the 32 lanes; equal-delay groups fold in lane order.
-    {
-      const unsigned m = lane < NW ? mk[lane * NW + warp] : 0u;
-      int incl = __popc(m);  // inclusive prefix over compute warps (lanes 0..NW-1)
+    // ---- publish: lane masks per owner from OB + 1 ballots ----
+    const int owner = rel_bin & (NW - 1);
+    unsigned mine = __ballot_sync(0xffffffffu, rel_bin >= 0);  // lanes sharing my owner
+    unsigned row = mine;                                        // lane o < NW: lanes owned by o
 #pragma unroll
-      for (int o = 1; o < NW; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, NW - 1);
-      for (int r0 = 0; r0 < total; r0 += 32) {
-        const int l = r0 + lane;  // this lane's entry rank
-        // compute warp holding rank l: first w with incl[w] > l (binary search, incl monotone)
-        int cw = 0;
-#pragma unroll
-        for (int step = NW / 2; step > 0; step >>= 1) {
-          const int probe = __shfl_sync(0xffffffffu, incl, cw + step - 1);
-          if (probe <= l) cw += step;
-        }
-        const bool valid = l < total;
-        const unsigned mm = __shfl_sync(0xffffffffu, m, cw);
-        const int excl = __shfl_sync(0xffffffffu, incl, cw) - __popc(mm);
-        const int e = cw * 32 + (valid ? nth_set_bit(mm, l - excl) : 0);
-        const int bn = valid ? ed[e] : -1 - lane;  // distinct dummy keys for idle lanes
-        const double av = valid ? ea[e] : 0.0;
-        const unsigned grp = __match_any_sync(0xffffffffu, bn);
-        const int gsz = __popc(grp);
-        const bool leader = valid && lane == __ffs(grp) - 1;
-        const int maxg = __reduce_max_sync(0xffffffffu, valid ? gsz : 0);
-        if (maxg == 1) {  // common case: no repeated delay among these entries
-          if (valid) bins[bn] = __dadd_rn(bins[bn], av);
-        } else {
-          double acc = leader ? bins[bn] : 0.0;
-          for (int k = 0; k < maxg; ++k) {  // fold each group in lane (= enumeration) order
-            const int src = k < gsz ? nth_set_bit(grp, k) : lane;
-            const double v = __shfl_sync(0xffffffffu, av, src);
-            if (leader && k < gsz) acc = __dadd_rn(acc, v);
-          }
-          if (leader) bins[bn] = acc;
-        }
-        __syncwarp();
+    for (int k = 0; k < OB; ++k) {
+      const unsigned bk = __ballot_sync(0xffffffffu, (owner >> k) & 1);
+      mine &= ((owner >> k) & 1) ? bk : ~bk;
+      row &= ((lane >> k) & 1) ? bk : ~bk;
+    }
+    if (lane < NW) mask[warp * NW + lane] = row;
+    __syncthreads();
+    // ---- stable counting sort into owner-major lists ----
+    // lane o < NW: entries of owner o in warps < this one (`before`) and in all (`total`)
+    int before = 0, total = 0;
+    if (lane < NW) {
+#pragma unroll 4
+      for (int w2 = 0; w2 < NW; ++w2) {
+        const int c = __popc(mask[w2 * NW + lane]);
+        total += c;
+        before += w2 < warp ? c : 0;
       }
     }
+    int incl = total;  // inclusive scan of the owner totals over lanes 0..NW-1
+#pragma unroll
+    for (int o = 1; o < NW; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int obase = incl - total;  // list start of owner `lane`
+    const int seg = __shfl_sync(0xffffffffu, obase + before, rel_bin >= 0 ? owner : 0);
+    if (rel_bin >= 0) {
+      const int pos = seg + __popc(mine & lt);
+      ent_d[pos] = rel_bin;
+      ent_a[pos] = amp;
+    }
+    const int my_base = __shfl_sync(0xffffffffu, obase, warp);
+    const int my_total = __shfl_sync(0xffffffffu, total, warp);
+    __syncthreads();
+    // ---- owner `warp` folds its list: round r applies the r-th entry of each
+    // equal-delay group (lane order = enumeration order) ----
+    for (int r0 = 0; r0 < my_total; r0 += 32) {
+      const int l = r0 + lane;
+      const bool valid = l < my_total;
+      const int bn = valid ? ent_d[my_base + l] : -1 - lane;  // distinct dummy keys for idle lanes
+      const double av = valid ? ent_a[my_base + l] : 0.0;
+      const unsigned grp = __match_any_sync(0xffffffffu, bn);
+      const int rank = __popc(grp & lt);
+      const int rounds = __reduce_max_sync(0xffffffffu, valid ? __popc(grp) : 0);
+      if (valid && rank == 0) bins[bn] = __dadd_rn(bins[bn], av);
+      for (int r = 1; r < rounds; ++r) {
+        __syncwarp();
+        if (valid && rank == r) bins[bn] = __dadd_rn(bins[bn], av);
+      }
+      __syncwarp();
+    }
 #endif
-    if (lane < NW) mk[lane * NW + warp] = 0u;  // owner clears its column for reuse
   }
   __syncthreads();
   double* out = a.rir + pm.rir_off + lo;
@@ -203,8 +198,8 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
 
 size_t synth_smem_bytes(int max_order, int slice, int nt) {
   const int W = 2 * max_order + 1, nw = nt / 32;
-  return sizeof(double) * (static_cast<size_t>(slice) + 3 * W + 3 * max_order + 1 + 2 * nt) +
-         sizeof(int) * 2 * nt + sizeof(unsigned) * 2 * nw * nw;
+  return sizeof(double) * (static_cast<size_t>(slice) + 3 * W + 3 * max_order + 1 + nt) + sizeof(int) * nt +
+         sizeof(unsigned) * nw * nw;
 }
 
 cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice, cudaStream_t s,
