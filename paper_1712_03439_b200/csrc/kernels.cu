@@ -66,7 +66,8 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   double* rg = ax + 3 * W;                       // [3K+1]
   double* ent_a = rg + (3 * K + 1);              // [NT] owner-major sorted amplitudes
   int* ent_d = reinterpret_cast<int*>(ent_a + NT);           // [NT] their bins
-  unsigned* mask = reinterpret_cast<unsigned*>(ent_d + NT);  // [NW compute][NW owner]
+  // [NW owner][NW compute] entry counts, one byte each (<= 32), 16-byte aligned rows
+  unsigned char* cnt8 = reinterpret_cast<unsigned char*>(ent_d + NT);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lo = it.slice_lo, len = it.slice_len;
   for (int l = tid; l < len; l += NT) bins[l] = 0.0;
@@ -93,6 +94,14 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   const int step_z = NT % W, step_q = NT / W;
   const int step_y = step_q % W, step_x = step_q / W;
   const unsigned lt = lanemask_lt();
+  // byte masks selecting the counts of compute warps < `warp` in each 4-byte word
+  constexpr int NQ = (NW + 3) / 4;
+  unsigned below[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int nb = warp - 4 * q;  // bytes of word q that belong to earlier warps
+    below[q] = nb <= 0 ? 0u : nb >= 4 ? 0xffffffffu : (1u << (8 * nb)) - 1u;
+  }
   unsigned long long max_d = 0;
   int geo = 0;
   for (long long base = 0; base < V; base += NT) {
@@ -133,19 +142,22 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
       mine &= ((owner >> k) & 1) ? bk : ~bk;
       row &= ((lane >> k) & 1) ? bk : ~bk;
     }
-    if (lane < NW) mask[warp * NW + lane] = row;
+    if (lane < NW) cnt8[lane * (4 * NQ) + warp] = static_cast<unsigned char>(__popc(row));
     __syncthreads();
     // ---- stable counting sort into owner-major lists ----
-    // lane o < NW: entries of owner o in warps < this one (`before`) and in all (`total`)
-    int before = 0, total = 0;
+    // lane o < NW: entries of owner o in warps < this one (`before`) and in all (`total`),
+    // byte sums of the owner's count row by dp4a
+    unsigned ubefore = 0u, utotal = 0u;
     if (lane < NW) {
-#pragma unroll 4
-      for (int w2 = 0; w2 < NW; ++w2) {
-        const int c = __popc(mask[w2 * NW + lane]);
-        total += c;
-        before += w2 < warp ? c : 0;
+      const unsigned* rowp = reinterpret_cast<const unsigned*>(cnt8 + lane * (4 * NQ));
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const unsigned wq = NW >= 4 ? rowp[q] : (rowp[0] & ((1u << (8 * NW)) - 1u));
+        utotal = __dp4a(wq, 0x01010101u, utotal);
+        ubefore = __dp4a(wq & below[q], 0x01010101u, ubefore);
       }
     }
+    const int before = static_cast<int>(ubefore), total = static_cast<int>(utotal);
     int incl = total;  // inclusive scan of the owner totals over lanes 0..NW-1
 #pragma unroll
     for (int o = 1; o < NW; o <<= 1) {
@@ -199,7 +211,7 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
 size_t synth_smem_bytes(int max_order, int slice, int nt) {
   const int W = 2 * max_order + 1, nw = nt / 32;
   return sizeof(double) * (static_cast<size_t>(slice) + 3 * W + 3 * max_order + 1 + nt) + sizeof(int) * nt +
-         sizeof(unsigned) * nw * nw;
+         static_cast<size_t>(nw) * 4 * ((nw + 3) / 4);
 }
 
 cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice, cudaStream_t s,
