@@ -153,7 +153,17 @@ struct Plan {
   static constexpr int T = M / E;                          // threads per transform
   static constexpr int LE = ilog2(E < 16 ? E : 16);         // log2 of the max radix
   static constexpr int NP = LOG == 0 ? 1 : (LOG + LE - 1) / LE;  // Stockham passes
-  static constexpr int PADDED = M + M / 16;                // smem float2 slots per transform
+  // Layout of the array between passes: PAD(i) = i + i/16 by default.  The output
+  // of a radix-8 pass with NS = 8 (E = 8 sizes, M >= 128) is written in the
+  // Q layout i + 8*(i/64) instead: its butterfly outputs land at 64a + k + 8r,
+  // which PAD maps onto the same banks for the two 8-thread groups a, a+1 of a
+  // half-warp (2-way conflicts on every 64-bit store); Q moves them 8 banks apart
+  // and still reads conflict-free in the next pass.
+  __host__ __device__ static constexpr bool q_out(int p) {
+    return E == 8 && p >= 1 && p < NP - 1 && ns(p) == 8;
+  }
+  __host__ __device__ static constexpr bool q_in(int p) { return p >= 1 && q_out(p - 1); }
+  static constexpr int PADDED = (E == 8 && NP >= 3) ? M + M / 8 : M + M / 16;  // smem float2 slots
   __host__ __device__ static constexpr int radix(int p) {
     return p < NP - 1 ? (1 << LE) : (1 << (LOG - LE * (NP - 1)));
   }
@@ -169,6 +179,14 @@ struct Plan {
 };
 
 __host__ __device__ __forceinline__ constexpr int PAD(int i) { return i + (i >> 4); }
+
+// Q-layout slot of element t + c (t < T <= 64, c a compile-time offset whose
+// low six bits plus T stay within 64, so no carry reaches bit 6): one base
+// register plus a compile-time offset.
+template <int T>
+__device__ __forceinline__ int q_slot(int t, int c) {
+  return t + c + 8 * (c >> 6);
+}
 
 // smem slot of element base + r*STEP.  When STEP is a multiple of 16 the
 // padding distributes over the sum, so every r is a compile-time offset from
@@ -255,7 +273,9 @@ __device__ __forceinline__ void stockham_pass(float2* s, int t, const float2* __
     for (int q = 0; q < NB; ++q) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        if constexpr (STRIDE % 16 == 0 && LIN)
+        if constexpr (PL::q_in(P))
+          v[q][r] = s[q_slot<T>(t, q * T + r * STRIDE)];
+        else if constexpr (STRIDE % 16 == 0 && LIN)
           v[q][r] = sr[q * PAD(T) + r * PAD(STRIDE)];
         else
           v[q][r] = s[PAD(t + q * T + r * STRIDE)];
@@ -273,6 +293,14 @@ __device__ __forceinline__ void stockham_pass(float2* s, int t, const float2* __
       float2* sw = s + 17 * t;  // PAD(16 t + r) = 17 t + r
 #pragma unroll
       for (int r = 0; r < R; ++r) sw[r] = v[0][r];
+    } else if constexpr (PL::q_out(P)) {
+      // i = 64a + k + 8r + q*T*R with t = 8a + k: Q(i) = i + 8a + q*T*R/8
+      static_assert(R == 8 && NS == 8 && T % 8 == 0 && (T * R) % 64 == 0, "Q-layout pass shape");
+      float2* sw = s + (t - kt) * R + kt + (t >> 3) * 8;
+#pragma unroll
+      for (int q = 0; q < NB; ++q)
+#pragma unroll
+        for (int r = 0; r < R; ++r) sw[q * (T * R + T) + r * NS] = v[q][r];
     } else {
       // base of q = 0; for q > 0 the base moves by q*T*R (same k) or q*T (k = j)
       const int base0 = SAME_K ? (t - kt) * R + kt : t;
@@ -382,7 +410,9 @@ __device__ __forceinline__ void stockham_emit_pass(float2* s, int t, const float
     for (int q = 0; q < NB; ++q) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        if constexpr (STRIDE % 16 == 0 && LIN)
+        if constexpr (PL::q_in(P))
+          v[q][r] = s[q_slot<T>(t, q * T + r * STRIDE)];
+        else if constexpr (STRIDE % 16 == 0 && LIN)
           v[q][r] = sr[q * PAD(T) + r * PAD(STRIDE)];
         else
           v[q][r] = s[PAD(t + q * T + r * STRIDE)];
@@ -424,9 +454,10 @@ __device__ __forceinline__ void spectral_multiply(float2* s, int t, const float2
   constexpr int T = Plan<M>::T;
   if (active) {
 #pragma unroll 2
-    for (int k = 1 + t; k < M / 2; k += T) {  // k in [1, M/2)
+    for (int k = t; k < (M + 1) / 2; k += T) {  // k in [0, M/2) (k = 0 for M = 1); bin 0 pairs with itself
+      const int km = (M - k) & (M - 1);
       const float2 a = s[PAD(k)];
-      const float2 b = c_conj(s[PAD(M - k)]);
+      const float2 b = c_conj(s[PAD(km)]);
       const float2 w = ldw(W + k);
       const float2 S = c_add(a, b);
       const float2 D = c_rot<false>(c_sub(a, b));
@@ -437,18 +468,9 @@ __device__ __forceinline__ void spectral_multiply(float2* s, int t, const float2
       const float2 U = c_add(P, Q);
       const float2 V = c_mulc(c_sub(P, Q), w);
       s[PAD(k)] = make_float2(U.x - V.y, U.y + V.x);
-      s[PAD(M - k)] = make_float2(U.x + V.y, V.x - U.y);
+      if (k != 0) s[PAD(km)] = make_float2(U.x + V.y, V.x - U.y);
     }
     if (t == 0) {
-      {  // k = 0 (partner bin M of G)
-        const float2 a = s[0];
-        const float2 S = make_float2(2.f * a.x, 0.f), D = make_float2(2.f * a.y, 0.f);
-        const float2 X2 = c_add(S, D), X2m = c_sub(S, D);
-        const float2 P = c_mul(X2, ldg(G + 0));
-        const float2 Q = c_mulc(X2m, ldg(G + M));
-        const float2 U = c_add(P, Q), V = c_sub(P, Q);
-        s[0] = make_float2(U.x - V.y, U.y + V.x);
-      }
       if (M >= 2) {  // k = M/2, its own partner
         const int k = M / 2;
         const float2 a = s[PAD(k)];

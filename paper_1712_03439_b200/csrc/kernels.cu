@@ -301,11 +301,21 @@ __host__ __device__ constexpr int e_of(int log2m) {  // == Plan<1 << log2m>::E
   return (1 << log2m) < RSG_E_SMALL ? (1 << log2m)
                                     : (log2m >= 13 ? 32 : ((1 << log2m) <= 512 ? RSG_E_SMALL : RSG_E));
 }
+// smem float2 slots of one transform (== Plan<1 << log2m>::PADDED)
+__host__ __device__ constexpr int padded_of(int log2m) {
+  return (e_of(log2m) == 8 && (log2m + 2) / 3 >= 3) ? (1 << log2m) + (1 << log2m) / 8
+                                                    : (1 << log2m) + (1 << log2m) / 16;
+}
 __host__ __device__ constexpr int cta_threads_of(int log2m) {
   // T = M / E threads per transform (E = 16, or 32 for M >= 8192); >= 256 per CTA.
   return (1 << log2m) / e_of(log2m) > 256 ? (1 << log2m) / e_of(log2m) : 256;
 }
 int cta_threads(int log2m) { return cta_threads_of(log2m); }
+
+static_assert(padded_of(3) == Plan<8>::PADDED && padded_of(6) == Plan<64>::PADDED &&
+                  padded_of(7) == Plan<128>::PADDED && padded_of(9) == Plan<512>::PADDED &&
+                  padded_of(10) == Plan<1024>::PADDED && padded_of(14) == Plan<16384>::PADDED,
+              "host smem sizing matches the device plan");
 
 template <int M>
 __host__ __device__ constexpr int groups_of() {
@@ -317,7 +327,7 @@ size_t ola_smem_bytes(int log2m) {
   const int E = e_of(log2m);
   const int T = M / E;
   const int G = cta_threads_of(log2m) / T;
-  return static_cast<size_t>(G) * (M + M / 16) * sizeof(float2);
+  return static_cast<size_t>(G) * padded_of(log2m) * sizeof(float2);
 }
 
 template <int M>
@@ -840,7 +850,7 @@ size_t k4_smem_bytes(int log2m) {
   if (log2m > kSmallMaxLog2M) return ola_smem_bytes(log2m);
   const int M = 1 << log2m;
   auto ev = [](int v) { return (v + 1) & ~1; };
-  const int per_group = ev(ev(ev(ev(ev(M + M / 16) + M + 1) + 2 * M) + 2 * ev(M + 4)) + 2);  // SmallLayout<M>::TOTAL
+  const int per_group = ev(ev(ev(ev(ev(padded_of(log2m)) + M + 1) + 2 * M) + 2 * ev(M + 4)) + 2);  // SmallLayout<M>::TOTAL
   const int twn = (tw_total(log2m) + 1) & ~1;            // per-CTA twiddle tables
   return (static_cast<size_t>(ola_groups(log2m)) * per_group + twn) * sizeof(float2);
 }
