@@ -318,40 +318,98 @@ double pair_flops(const PairPlan& p) {
 // Pairs are bucketed by transform size; buckets run largest work first.  Each
 // pair's blocks are split into runs (K4 work items) long enough that the
 // recomputed overlap blocks cost <= ~6%, short enough to fill the GPU.
-struct Span { int l; int64_t list_off, list_n, item_off, item_n; };
+struct Span { int l; int64_t list_off, list_n, item_off, item_n; bool large; };
+
+// A batch of one large span (four-step path): pairs [pair_lo, pair_hi) of the
+// span's list, their (pair, block) units [unit_lo, unit_hi) and stage-D items
+// [item_lo, item_hi) (global indices); the batch's units share one scratch.
+struct LargeBatch { int span; int64_t pair_lo, pair_hi, unit_lo, unit_hi, item_lo, item_hi; };
 
 struct FilterPlan {
   std::vector<int32_t> lists;
   std::vector<OlaItem> items;
   std::vector<Span> spans;
+  std::vector<int2> units;          // large spans: (pair, block)
+  std::vector<LargeBatch> batches;
+  int64_t max_scratch = 0;          // complex elements of the largest batch's scratch
   int64_t spec_total = 0, y_total = 0;
   double flops = 0;
 };
 
+// Sizes that take the four-step path: measured faster than the one-CTA kernel at
+// M = 8192 and for every M > 16384 (tuning override: RSG_LARGE_MIN = smallest log2 M).
+bool use_large(int l) {
+  static const int v = [] {
+    const char* e = std::getenv("RSG_LARGE_MIN");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (l > kMaxLog2M) return true;
+  return v >= 0 ? l >= v : l == 13;
+}
+constexpr int64_t kLargeScratchBytes = int64_t(1) << 31;  // per batch (16 M bytes per unit)
+
 int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
   const int64_t n_pairs = static_cast<int64_t>(plans.size());
-  std::vector<std::vector<int32_t>> bucket(kMaxLog2M + 1);
+  std::vector<std::vector<int32_t>> bucket(kLargeMaxLog2M + 1);
   std::vector<double> work(n_pairs);
   fp.flops = 0;
   for (int64_t p = 0; p < n_pairs; ++p) {
     const int l = plans[p].log2n - 1;
-    if (l < 0 || l > kMaxLog2M) return fail(RS_ERR_UNSUPPORTED, "FFT size outside the supported range");
+    if (l < 0 || l > kLargeMaxLog2M) return fail(RS_ERR_UNSUPPORTED, "FFT size outside the supported range");
     bucket[l].push_back(static_cast<int32_t>(p));
     work[p] = pair_flops(plans[p]);
     fp.flops += work[p];
   }
-  std::vector<int> order(kMaxLog2M + 1);
+  std::vector<int> order(kLargeMaxLog2M + 1);
   std::iota(order.begin(), order.end(), 0);
-  std::vector<double> bucket_work(kMaxLog2M + 1, 0.0);
-  for (int l = 0; l <= kMaxLog2M; ++l)
+  std::vector<double> bucket_work(kLargeMaxLog2M + 1, 0.0);
+  for (int l = 0; l <= kLargeMaxLog2M; ++l)
     for (int32_t p : bucket[l]) bucket_work[l] += work[p];
   std::sort(order.begin(), order.end(), [&](int a, int b) { return bucket_work[a] > bucket_work[b]; });
   fp.lists.clear();
   fp.items.clear();
   fp.spans.clear();
+  fp.units.clear();
+  fp.batches.clear();
+  fp.max_scratch = 0;
   for (int l : order) {
     auto& v = bucket[l];
     if (v.empty()) continue;
+    if (use_large(l)) {  // four-step path, batched by scratch size
+      Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
+              static_cast<int64_t>(fp.items.size()), 0, true};
+      const int64_t m = int64_t(1) << l;
+      const int64_t per_batch = std::max<int64_t>(1, kLargeScratchBytes / (16 * m));
+      LargeBatch bt{static_cast<int>(fp.spans.size()), 0, 0, static_cast<int64_t>(fp.units.size()), 0,
+                    static_cast<int64_t>(fp.items.size()), 0};
+      auto close = [&](int64_t i) {
+        bt.pair_hi = i;
+        bt.unit_hi = static_cast<int64_t>(fp.units.size());
+        bt.item_hi = static_cast<int64_t>(fp.items.size());
+        if (bt.pair_hi > bt.pair_lo) {
+          fp.batches.push_back(bt);
+          fp.max_scratch = std::max(fp.max_scratch, (bt.unit_hi - bt.unit_lo) * m);
+        }
+        bt.pair_lo = i;
+        bt.unit_lo = bt.unit_hi;
+        bt.item_lo = bt.item_hi;
+      };
+      for (int64_t i = 0; i < static_cast<int64_t>(v.size()); ++i) {
+        PairPlan& pl = plans[v[i]];
+        if (static_cast<int64_t>(fp.units.size()) - bt.unit_lo + pl.B > per_batch) close(i);
+        const int64_t unit0 = static_cast<int64_t>(fp.units.size()) - bt.unit_lo;
+        for (int64_t b = 0; b < pl.B; ++b) fp.units.push_back(make_int2(v[i], static_cast<int>(b)));
+        pl.item0 = static_cast<int64_t>(fp.items.size());
+        pl.nitems = (pl.out_len + large_tile() - 1) / large_tile();
+        for (int64_t tl = 0; tl < pl.nitems; ++tl)
+          fp.items.push_back(OlaItem{v[i], static_cast<int32_t>(tl), static_cast<int32_t>(unit0), 0});
+      }
+      close(static_cast<int64_t>(v.size()));
+      sp.item_n = static_cast<int64_t>(fp.items.size()) - sp.item_off;
+      fp.spans.push_back(sp);
+      fp.lists.insert(fp.lists.end(), v.begin(), v.end());
+      continue;
+    }
     // largest pairs first (LPT) so the tail of the launch is short
     std::stable_sort(v.begin(), v.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
     int64_t total_blocks = 0, max_pre = 1;
@@ -363,7 +421,7 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
     const int64_t slots = 148LL * ola_resident_groups(l);
     const int64_t run = std::max<int64_t>((total_blocks + 6 * slots - 1) / (6 * slots), 16 * max_pre);
     Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
-            static_cast<int64_t>(fp.items.size()), 0};
+            static_cast<int64_t>(fp.items.size()), 0, false};
     for (int32_t p : v) {
       PairPlan& pl = plans[p];
       const int64_t n = int64_t(1) << pl.log2n;
@@ -391,7 +449,7 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
 
 // Device buffers of one filter stage (K3 + K4 + K5 + K6 of a chunk).
 struct FilterBufs {
-  DevBuf plan, lists, olaitems, spec, y, part;
+  DevBuf plan, lists, olaitems, spec, y, part, units, scratch, yblk;
 };
 
 thread_local int64_t g_copy_launches = 0;  // pcie_copy_kernel launches of the current render
@@ -447,15 +505,37 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
   RS_TRY(fb.spec.ensure(std::max<int64_t>(fp.spec_total, 1) * sizeof(float2)));
   RS_TRY(fb.y.ensure(std::max<int64_t>(fp.y_total, 1) * sizeof(float)));
   RS_TRY(fb.part.ensure(std::max<size_t>(fp.items.size(), 1) * sizeof(double)));
+  if (!fp.batches.empty()) {
+    RS_TRY(upload_on(fb.units, fp.units, st, arena));
+    RS_TRY(fb.scratch.ensure(fp.max_scratch * sizeof(float2)));
+    RS_TRY(fb.yblk.ensure(fp.max_scratch * 2 * sizeof(float)));
+  }
   const int32_t* d_lists = fb.lists.as<int32_t>();
   for (const Span& sp : fp.spans) {
+    if (sp.large) continue;  // spectrum inside the four-step batches
     SpecArgs a{d_lists + sp.list_off, static_cast<int32_t>(sp.list_n), d_pair, fb.plan.as<PairPlan>(),
                d_rir, fb.spec.as<float2>(), c->tw[sp.l]};
     RS_CUDA(launch_spectrum(sp.l, a, st));
     ++c->launches;
   }
   if (ev_k4a) RS_CUDA(cudaEventRecord(ev_k4a, st));
+  for (const LargeBatch& bt : fp.batches) {
+    const Span& sp = fp.spans[bt.span];
+    int l1, l2;
+    large_split(sp.l, &l1, &l2);
+    LargeArgs a{fb.units.as<int2>() + bt.unit_lo, d_lists + sp.list_off + bt.pair_lo,
+                static_cast<int32_t>(bt.unit_hi - bt.unit_lo), static_cast<int32_t>(bt.pair_hi - bt.pair_lo),
+                d_pair, fb.plan.as<PairPlan>(), d_signals, d_rir, fb.spec.as<float2>(), fb.scratch.as<float2>(),
+                fb.yblk.as<float>(), fb.y.as<float>(), fb.part.as<double>() + bt.item_lo,
+                fb.olaitems.as<OlaItem>() + bt.item_lo, static_cast<int32_t>(bt.item_hi - bt.item_lo),
+                c->tw[l1], c->tw[l2]};
+    for (int stage = 0; stage < 6; ++stage) {
+      RS_CUDA(launch_large(sp.l, a, stage, st));
+      ++c->launches;
+    }
+  }
   for (const Span& sp : fp.spans) {
+    if (sp.large) continue;
     OlaArgs a{fb.olaitems.as<OlaItem>() + sp.item_off, static_cast<int32_t>(sp.item_n), d_pair,
               fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(),
               fb.part.as<double>() + sp.item_off, c->tw[sp.l]};
@@ -527,7 +607,7 @@ struct Chunk {
     DevBuf* bufs[] = {&d_utt, &d_pair, &d_rg, &d_items, &d_rir, &d_rirout, &d_gain, &d_power, &d_flags,
                       &d_snr, &d_chan_utt, &d_chan_mic, &d_chan_out, &d_utt_len, &d_utt_stride,
                       &d_utt_pair0, &d_utt_I, &d_utt_J, &fb.plan, &fb.lists, &fb.olaitems, &fb.spec,
-                      &fb.y, &fb.part};
+                      &fb.y, &fb.part, &fb.units, &fb.scratch, &fb.yblk};
     for (DevBuf* b : bufs) b->release();
     hA.release();
     hB.release();
@@ -751,7 +831,7 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
     } else {
       return fail(RS_ERR_CONFIG, "unknown plan rule");
     }
-    if (n < 2 || n > (static_cast<size_t>(2) << kMaxLog2M))
+    if (n < 2 || n > (static_cast<size_t>(2) << kLargeMaxLog2M))
       return fail(RS_ERR_UNSUPPORTED, "FFT size " + std::to_string(n) + " not supported by the device kernels");
     ch.strategy[p] = s;
     PairPlan& pl = ch.plans[p];
@@ -886,7 +966,7 @@ void destroy_state(rs_ctx* c) {
     if (st) cudaStreamSynchronize(st);
   for (auto& ch : r->chunks) ch.release();
   FilterBufs& f = r->conv;
-  DevBuf* bufs[] = {&f.plan, &f.lists, &f.olaitems, &f.spec, &f.y, &f.part};
+  DevBuf* bufs[] = {&f.plan, &f.lists, &f.olaitems, &f.spec, &f.y, &f.part, &f.units, &f.scratch, &f.yblk};
   for (DevBuf* b : bufs) b->release();
   for (auto st : ss)
     if (st) cudaStreamDestroy(st);
@@ -1103,7 +1183,7 @@ int convolve_host(rs_ctx* c, const double* x, size_t nx, const double* h, size_t
   if (nx == 0) return fail(RS_ERR_DEGENERATE, "convolution input must be non-empty mono audio");
   if (nh == 0) return fail(RS_ERR_DEGENERATE, "empty impulse response");
   RS_TRY(checked_fft_size(n, nh, "overlap-add"));
-  if (n > (static_cast<size_t>(2) << kMaxLog2M))
+  if (n > (static_cast<size_t>(2) << kLargeMaxLog2M))
     return fail(RS_ERR_UNSUPPORTED, "FFT size " + std::to_string(n) + " not supported by the device kernels");
   c->launches = 0;
   RS_TRY(c->scratch_a.ensure(std::max(nx, nh) * sizeof(double)));

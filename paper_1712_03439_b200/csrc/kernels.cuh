@@ -141,6 +141,32 @@ struct GainArgs {
   int64_t n_pairs;
 };
 
+// Large transforms (large.cu): four-step FFT through global scratch.
+struct LargeArgs {
+  const int2* units;         // (pair, block) per unit of this batch
+  const int32_t* spec_pairs; // pairs of this batch (spectrum stages)
+  int32_t n_units;
+  int32_t n_spec;
+  const PairMeta* pair;
+  const PairPlan* plan;
+  const float* signals;
+  const double* rir;
+  float2* spec;              // per pair: G(k1 + M1 k2) at [k1*M2 + k2], G(M) at [M]
+  float2* scratch;           // per unit: M complex
+  float* yblk;               // per unit: N = 2M block output samples
+  float* y;
+  double* part;              // per stage-D item (indexed like `items`)
+  const OlaItem* items;      // stage-D tiles: {pair, tile, unit of block 0, 0}
+  int32_t n_items;
+  const float2* tw1;         // Plan<M1> twiddle tables
+  const float2* tw2;         // Plan<M2> twiddle tables
+};
+constexpr int kLargeMaxLog2M = 22;  // M <= 2^22 (N <= 2^23) through the four-step path
+void large_split(int log2m, int* l1, int* l2);
+int large_tile();
+// stage: 0/1 spectrum (cols, rows), 2 cols fwd, 3 rows, 4 cols inv, 5 overlap-add
+cudaError_t launch_large(int log2m, const LargeArgs& a, int stage, cudaStream_t s);
+
 // ---- launchers (kernels.cu) --------------------------------------------------
 constexpr int kMaxLog2M = 14;  // M <= 16384  (N <= 32768) in one CTA
 int cta_threads(int log2m);

@@ -130,12 +130,47 @@ def test_ola_block_boundaries(rs, ctx, port):
     assert rel_err(rs.convolve_ola(x, h, 64, ctx=ctx), port.convolve_ola(x, h, 64)) <= WAVE_TOL  # L=1
 
 
-@pytest.mark.parametrize("n", [2 ** k for k in range(1, 16)])
+@pytest.mark.parametrize("n", [2 ** k for k in range(1, 21)])
 def test_every_fft_size(rs, ctx, port, n):
+    # N <= 32768: one CTA per transform (K4); N >= 65536: the four-step path (large.cu)
     rng = np.random.default_rng(100 + n)
     nh = max(1, n // 2 - 3) if n > 2 else 1
-    x, h = rng.standard_normal(5 * n + 7), rng.standard_normal(nh)
+    nx = 5 * n + 7 if n <= 65536 else 2 * n + 7
+    x, h = rng.standard_normal(nx), rng.standard_normal(nh)
     assert rel_err(rs.convolve_ola(x, h, n, ctx=ctx), port.convolve_ola(x, h, n)) <= WAVE_TOL
+
+
+def test_full_fft_long_signal(rs, ctx, port):
+    # one-block filtering of a 20 s signal: N = 2^19 through the four-step path
+    rng = np.random.default_rng(14)
+    x, h = rng.standard_normal(320000), rng.standard_normal(9000) * np.exp(-np.arange(9000) / 2000)
+    got = rs.convolve_full_fft(x, h, ctx=ctx)
+    assert rel_err(got, port.convolve_full_fft(x, h)) <= WAVE_TOL
+
+
+def test_four_step_path_small_sizes(tmp_path):
+    """Route every size >= 2^7 through the four-step path (RSG_LARGE_MIN) in a fresh
+    process and check it against the oracle at sizes where K4 normally runs."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import numpy as np, oracle\n"
+        "from paper_1712_03439_b200 import roomsim as rs\n"
+        "ctx = rs.Context(0); port = oracle.port(); rng = np.random.default_rng(7); worst = 0.0\n"
+        "for k in range(7, 17):\n"
+        "    n = 2 ** k\n"
+        "    for nh in (1, n // 4 + 1, n // 2 - 3, n - 5):\n"
+        "        x, h = rng.standard_normal(3 * n + 11), rng.standard_normal(max(nh, 1))\n"
+        "        want = port.convolve_ola(x, h, n); got = rs.convolve_ola(x, h, n, ctx=ctx)\n"
+        "        worst = max(worst, float(np.abs(got - want).max() / np.abs(want).max()))\n"
+        "print(worst)\n")
+    env = dict(os.environ, RSG_LARGE_MIN="6")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= WAVE_TOL
 
 
 def test_config1(rs, ctx, port):
@@ -196,6 +231,17 @@ def test_render_config2_subset(rs, ctx, port):
 
     b = scenes.config2(n_utt=4, seed=23)
     g, o = _render_both(rs, ctx, port, b)
+    _check_render(b, g, o)
+
+
+def test_render_forced_65536(rs, ctx, port):
+    # the batched render through the four-step path (N = 65536, M = 32768)
+    from paper_1712_03439_b200 import scenes
+
+    b = scenes.config3(n_utt=2, seed=25)
+    b.plan_rule, b.forced_fft_size = scenes.PLAN_FORCED, 65536
+    g, o = _render_both(rs, ctx, port, b)
+    assert (g.layout["fft_size"] == 65536).all()
     _check_render(b, g, o)
 
 
