@@ -5,20 +5,24 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC,-O2,-ffp-contract=off
 SRC := paper_1712_03439_b200/csrc
 OUT := paper_1712_03439_b200/_lib
-OBJS := $(OUT)/kernels.o $(OUT)/large.o $(OUT)/api.o
+OBJS := $(OUT)/kernels.o $(OUT)/large.o $(OUT)/ola2.o $(OUT)/api.o
 
 REF_INC ?= /root/reference/proj/include
 ADAPTER := tests/cpp/_build/adapter_test
 
 all: $(OUT)/libroomsim_gpu.so oracle adapter
 
-$(OUT)/kernels.o: $(SRC)/kernels.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh
+$(OUT)/kernels.o: $(SRC)/kernels.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh $(SRC)/async.cuh
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/kernels.ptxas.log || (cat $(OUT)/kernels.ptxas.log; false)
 
-$(OUT)/large.o: $(SRC)/large.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh
+$(OUT)/large.o: $(SRC)/large.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh $(SRC)/async.cuh
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/large.ptxas.log || (cat $(OUT)/large.ptxas.log; false)
+
+$(OUT)/ola2.o: $(SRC)/ola2.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh $(SRC)/fft2.cuh $(SRC)/async.cuh
+	@mkdir -p $(OUT)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/ola2.ptxas.log || (cat $(OUT)/ola2.ptxas.log; false)
 
 $(OUT)/api.o: $(SRC)/api.cu $(SRC)/kernels.cuh include/roomsim_gpu.h
 	@mkdir -p $(OUT)

@@ -260,6 +260,8 @@ struct rs_ctx {
   double stage_ms[6] = {};
   bool stage_valid = false;
   float2* tw[kMaxLog2M + 1] = {};
+  float2* tw2f[kOla2MaxLog2N + 1] = {};  // two-stream K4: forward / reversed pass tables
+  float2* tw2i[kOla2MaxLog2N + 1] = {};
   DevBuf tw_all;
   // arena
   DevBuf utt, pair, rg, items, olaitems, rir, rirout, plan, lists, spec, y, sumsq, gain, power, flags,
@@ -287,16 +289,27 @@ int ctx_init(rs_ctx* c) {
   for (auto& e : c->st) RS_CUDA(cudaEventCreate(&e));
   RS_CUDA(kernels_init());
   size_t total = 0;
-  size_t off[kMaxLog2M + 1];
+  size_t off[kMaxLog2M + 1], off2[kOla2MaxLog2N + 1][2] = {};
   for (int l = 0; l <= kMaxLog2M; ++l) {
     off[l] = total;
-    total += static_cast<size_t>(tw_total(l));
+    total += (static_cast<size_t>(tw_total(l)) + 1) & ~size_t(1);
   }
+  for (int l = kOla2MinLog2N; l <= kOla2MaxLog2N; ++l)
+    for (int r = 0; r < 2; ++r) {
+      off2[l][r] = total;
+      total += (static_cast<size_t>(ola2_tw_total(l, r == 1)) + 1) & ~size_t(1);
+    }
   std::vector<float2> h(total);
   for (int l = 0; l <= kMaxLog2M; ++l) fill_twiddles(l, h.data() + off[l]);
+  for (int l = kOla2MinLog2N; l <= kOla2MaxLog2N; ++l)
+    for (int r = 0; r < 2; ++r) ola2_fill_twiddles(l, r == 1, h.data() + off2[l][r]);
   RS_TRY(c->tw_all.ensure(total * sizeof(float2)));
   RS_CUDA(cudaMemcpy(c->tw_all.p, h.data(), total * sizeof(float2), cudaMemcpyHostToDevice));
   for (int l = 0; l <= kMaxLog2M; ++l) c->tw[l] = c->tw_all.as<float2>() + off[l];
+  for (int l = kOla2MinLog2N; l <= kOla2MaxLog2N; ++l) {
+    c->tw2f[l] = c->tw_all.as<float2>() + off2[l][0];
+    c->tw2i[l] = c->tw_all.as<float2>() + off2[l][1];
+  }
   return RS_OK;
 }
 
@@ -318,7 +331,12 @@ double pair_flops(const PairPlan& p) {
 // Pairs are bucketed by transform size; buckets run largest work first.  Each
 // pair's blocks are split into runs (K4 work items) long enough that the
 // recomputed overlap blocks cost <= ~6%, short enough to fill the GPU.
-struct Span { int l; int64_t list_off, list_n, item_off, item_n; bool large; };
+struct Span {
+  int l;
+  int64_t list_off, list_n, item_off, item_n;
+  bool large;  // four-step path (large.cu)
+  bool two;    // two-stream K4 (ola2.cu): items in FilterPlan::items2
+};
 
 // A batch of one large span (four-step path): pairs [pair_lo, pair_hi) of the
 // span's list, their (pair, block) units [unit_lo, unit_hi) and stage-D items
@@ -329,6 +347,7 @@ struct FilterPlan {
   std::vector<int32_t> lists;
   std::vector<OlaItem> items;
   std::vector<Span> spans;
+  std::vector<OlaItem2> items2;     // two-stream spans (part index = items.size() + i)
   std::vector<int2> units;          // large spans: (pair, block)
   std::vector<LargeBatch> batches;
   int64_t max_scratch = 0;          // complex elements of the largest batch's scratch
@@ -346,6 +365,22 @@ bool use_large(int l) {
   if (l > kMaxLog2M) return true;
   return v >= 0 ? l >= v : l == 13;
 }
+// Real FFT sizes (log2 N) that run the two-stream K4 (tuning override RSG_OLA2="lo,hi";
+// "0,0" disables it).
+bool use_ola2(int log2n) {
+  static const std::pair<int, int> r = [] {
+    const char* e = std::getenv("RSG_OLA2");
+    int lo = -1, hi = -1;
+    if (e) std::sscanf(e, "%d,%d", &lo, &hi);
+    return std::make_pair(lo, hi);
+  }();
+  if (!ola2_supported(log2n)) return false;
+  if (r.first >= 0) return log2n >= r.first && log2n <= r.second;
+  // default: the size where it measured faster than K4 inside the config-4 render
+  // (ncu launch list, B200); elsewhere K4 is as fast or faster
+  return log2n == 8;
+}
+
 constexpr int64_t kLargeScratchBytes = int64_t(1) << 31;  // per batch (16 M bytes per unit)
 
 int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
@@ -370,6 +405,7 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
   fp.items.clear();
   fp.spans.clear();
   fp.units.clear();
+  fp.items2.clear();
   fp.batches.clear();
   fp.max_scratch = 0;
   for (int l : order) {
@@ -377,7 +413,7 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
     if (v.empty()) continue;
     if (use_large(l)) {  // four-step path, batched by scratch size
       Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
-              static_cast<int64_t>(fp.items.size()), 0, true};
+              static_cast<int64_t>(fp.items.size()), 0, true, false};
       const int64_t m = int64_t(1) << l;
       const int64_t per_batch = std::max<int64_t>(1, kLargeScratchBytes / (16 * m));
       LargeBatch bt{static_cast<int>(fp.spans.size()), 0, 0, static_cast<int64_t>(fp.units.size()), 0,
@@ -412,6 +448,48 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
     }
     // largest pairs first (LPT) so the tail of the launch is short
     std::stable_sort(v.begin(), v.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
+    if (use_ola2(l + 1)) {  // two-stream K4: items are pairs of runs of one pair
+      int64_t total_blocks = 0, max_pre = 1;
+      for (int32_t p : v) {
+        total_blocks += plans[p].B;
+        const int64_t n = int64_t(1) << plans[p].log2n;
+        max_pre = std::max<int64_t>(max_pre, (n - plans[p].L + plans[p].L - 1) / plans[p].L);
+      }
+      const int64_t slots = 148LL * ola2_resident_items(l + 1);
+      const int64_t run = std::max<int64_t>((total_blocks + 12 * slots - 1) / (12 * slots), 16 * max_pre);
+      Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
+              static_cast<int64_t>(fp.items2.size()), 0, false, true};
+      for (int32_t p : v) {
+        PairPlan& pl = plans[p];
+        const int64_t n = int64_t(1) << pl.log2n;
+        const int64_t pre = (n - pl.L + pl.L - 1) / pl.L;
+        int64_t nr = (pl.B + run - 1) / run;
+        if (nr > 1 && (nr & 1)) ++nr;  // an even number of runs: two per item
+        const int64_t len = (pl.B + nr - 1) / nr;
+        pl.item0 = -1 - static_cast<int64_t>(fp.items2.size());  // fixed up below
+        pl.nitems = 0;
+        for (int64_t r = 0; r < nr; r += 2) {
+          OlaItem2 it{p, 0, 0, 0, static_cast<int32_t>(pl.B), static_cast<int32_t>(pl.B),
+                      static_cast<int32_t>(pl.B), 0};
+          for (int h = 0; h < 2 && r + h < nr; ++h) {
+            const int64_t r0 = std::min<int64_t>(pl.B, (r + h) * len), r1 = std::min<int64_t>(pl.B, r0 + len);
+            if (r0 >= r1) continue;  // empty run: stays (B, B, B), no trips, owns nothing
+            const int32_t b0 = static_cast<int32_t>(r0 == 0 ? 0 : std::max<int64_t>(0, r0 - pre));
+            if (h == 0) {
+              it.a_begin = b0; it.a_own = static_cast<int32_t>(r0); it.a_end = static_cast<int32_t>(r1);
+            } else {
+              it.b_begin = b0; it.b_own = static_cast<int32_t>(r0); it.b_end = static_cast<int32_t>(r1);
+            }
+          }
+          fp.items2.push_back(it);
+          ++pl.nitems;
+        }
+      }
+      sp.item_n = static_cast<int64_t>(fp.items2.size()) - sp.item_off;
+      fp.spans.push_back(sp);
+      fp.lists.insert(fp.lists.end(), v.begin(), v.end());
+      continue;
+    }
     int64_t total_blocks = 0, max_pre = 1;
     for (int32_t p : v) {
       total_blocks += plans[p].B;
@@ -421,7 +499,7 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
     const int64_t slots = 148LL * ola_resident_groups(l);
     const int64_t run = std::max<int64_t>((total_blocks + 6 * slots - 1) / (6 * slots), 16 * max_pre);
     Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
-            static_cast<int64_t>(fp.items.size()), 0, false};
+            static_cast<int64_t>(fp.items.size()), 0, false, false};
     for (int32_t p : v) {
       PairPlan& pl = plans[p];
       const int64_t n = int64_t(1) << pl.log2n;
@@ -439,6 +517,8 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
     fp.spans.push_back(sp);
     fp.lists.insert(fp.lists.end(), v.begin(), v.end());
   }
+  for (auto& q : plans)  // two-stream items: part indices after the K4 / stage-D items
+    if (q.item0 < 0) q.item0 = static_cast<int64_t>(fp.items.size()) + (-1 - q.item0);
   fp.spec_total = fp.y_total = 0;
   for (const auto& q : plans) {
     fp.spec_total = std::max<int64_t>(fp.spec_total, q.spec_off + (int64_t(1) << (q.log2n - 1)) + 1);
@@ -449,7 +529,7 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
 
 // Device buffers of one filter stage (K3 + K4 + K5 + K6 of a chunk).
 struct FilterBufs {
-  DevBuf plan, lists, olaitems, spec, y, part, units, scratch, yblk;
+  DevBuf plan, lists, olaitems, spec, y, part, units, scratch, yblk, olaitems2;
 };
 
 thread_local int64_t g_copy_launches = 0;  // pcie_copy_kernel launches of the current render
@@ -504,7 +584,8 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
   RS_TRY(upload_on(fb.olaitems, fp.items, st, arena));
   RS_TRY(fb.spec.ensure(std::max<int64_t>(fp.spec_total, 1) * sizeof(float2)));
   RS_TRY(fb.y.ensure(std::max<int64_t>(fp.y_total, 1) * sizeof(float)));
-  RS_TRY(fb.part.ensure(std::max<size_t>(fp.items.size(), 1) * sizeof(double)));
+  RS_TRY(fb.part.ensure(std::max<size_t>(fp.items.size() + fp.items2.size(), 1) * sizeof(double)));
+  if (!fp.items2.empty()) RS_TRY(upload_on(fb.olaitems2, fp.items2, st, arena));
   if (!fp.batches.empty()) {
     RS_TRY(upload_on(fb.units, fp.units, st, arena));
     RS_TRY(fb.scratch.ensure(fp.max_scratch * sizeof(float2)));
@@ -535,7 +616,23 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
     }
   }
   for (const Span& sp : fp.spans) {
-    if (sp.large) continue;
+    if (!sp.two) continue;
+    int64_t max_nh = 1, max_l = 1;
+    for (int64_t i = 0; i < sp.list_n; ++i) {
+      const PairPlan& q = plans[fp.lists[sp.list_off + i]];
+      max_nh = std::max<int64_t>(max_nh, q.nh);
+      max_l = std::max<int64_t>(max_l, q.L);
+    }
+    Ola2Args a{fb.olaitems2.as<OlaItem2>() + sp.item_off, static_cast<int32_t>(sp.item_n), d_pair,
+               fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(),
+               fb.part.as<double>() + fp.items.size() + sp.item_off, c->tw2f[sp.l + 1], c->tw2i[sp.l + 1],
+               static_cast<int32_t>((std::max<int64_t>(max_nh - 1, 1) + 3) & ~int64_t(3)),
+               static_cast<int32_t>((max_l + 8 + 3) & ~int64_t(3))};
+    RS_CUDA(launch_ola2(sp.l + 1, a, st));
+    ++c->launches;
+  }
+  for (const Span& sp : fp.spans) {
+    if (sp.large || sp.two) continue;
     OlaArgs a{fb.olaitems.as<OlaItem>() + sp.item_off, static_cast<int32_t>(sp.item_n), d_pair,
               fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(),
               fb.part.as<double>() + sp.item_off, c->tw[sp.l]};
@@ -607,7 +704,7 @@ struct Chunk {
     DevBuf* bufs[] = {&d_utt, &d_pair, &d_rg, &d_items, &d_rir, &d_rirout, &d_gain, &d_power, &d_flags,
                       &d_snr, &d_chan_utt, &d_chan_mic, &d_chan_out, &d_utt_len, &d_utt_stride,
                       &d_utt_pair0, &d_utt_I, &d_utt_J, &fb.plan, &fb.lists, &fb.olaitems, &fb.spec,
-                      &fb.y, &fb.part, &fb.units, &fb.scratch, &fb.yblk};
+                      &fb.y, &fb.part, &fb.units, &fb.scratch, &fb.yblk, &fb.olaitems2};
     for (DevBuf* b : bufs) b->release();
     hA.release();
     hB.release();
@@ -882,6 +979,7 @@ int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO
   std::vector<PairMeta>& pm = ch.pair;
   (void)pm;
   size_t need = staged_bytes(ch.fp.lists) + staged_bytes(ch.plans) + staged_bytes(ch.fp.items) +
+                staged_bytes(ch.fp.items2) + staged_bytes(ch.fp.units) +
                 staged_bytes(snr_lin) + staged_bytes(pair0) + staged_bytes(uI) + staged_bytes(uJ) +
                 staged_bytes(ch_utt) + staged_bytes(ch_mic) + staged_bytes(ch_out) + staged_bytes(ch.ulen) +
                 staged_bytes(ustride) + 3 * (((std::max<int64_t>(ch.P, 1) * 8) + 63) & ~size_t(63)) + 256;
@@ -966,7 +1064,8 @@ void destroy_state(rs_ctx* c) {
     if (st) cudaStreamSynchronize(st);
   for (auto& ch : r->chunks) ch.release();
   FilterBufs& f = r->conv;
-  DevBuf* bufs[] = {&f.plan, &f.lists, &f.olaitems, &f.spec, &f.y, &f.part, &f.units, &f.scratch, &f.yblk};
+  DevBuf* bufs[] = {&f.plan, &f.lists, &f.olaitems, &f.spec, &f.y, &f.part, &f.units, &f.scratch, &f.yblk,
+                    &f.olaitems2};
   for (DevBuf* b : bufs) b->release();
   for (auto st : ss)
     if (st) cudaStreamDestroy(st);

@@ -141,6 +141,36 @@ struct GainArgs {
   int64_t n_pairs;
 };
 
+// K4 two-stream variant (ola2.cu): runs A and B of one pair share each complex
+// transform.  Owned ranges as OlaItem.
+struct OlaItem2 {
+  int32_t pair;
+  int32_t a_begin, a_own, a_end;
+  int32_t b_begin, b_own, b_end;
+  int32_t pad;
+};
+
+struct Ola2Args {
+  const OlaItem2* items;
+  int32_t count;
+  const PairMeta* pair;
+  const PairPlan* plan;
+  const float* signals;
+  const float2* spec;   // K3's G = H / (2N), k in [0, N/2]
+  float* y;
+  double* part;         // per item: Σ y^2 over both runs' owned samples
+  const float2* twf;    // PlanC<N, false> pass tables
+  const float2* twi;    // PlanC<N, true> pass tables
+  int32_t ccap;         // floats per carry buffer: >= max N_h - 1 of the launch, multiple of 4
+  int32_t scap;         // floats per input window: >= max L + 8 of the launch, multiple of 4
+};
+constexpr int kOla2MinLog2N = 5, kOla2MaxLog2N = 12;
+bool ola2_supported(int log2n);
+int ola2_resident_items(int log2n);
+int ola2_tw_total(int log2n, bool rev);
+void ola2_fill_twiddles(int log2n, bool rev, float2* host);
+cudaError_t launch_ola2(int log2n, const Ola2Args& a, cudaStream_t s);
+
 // Large transforms (large.cu): four-step FFT through global scratch.
 struct LargeArgs {
   const int2* units;         // (pair, block) per unit of this batch
