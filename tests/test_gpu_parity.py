@@ -148,6 +148,39 @@ def test_full_fft_long_signal(rs, ctx, port):
     assert rel_err(got, port.convolve_full_fft(x, h)) <= WAVE_TOL
 
 
+def test_two_stream_k4_all_sizes():
+    """Run the two-stream K4 (ola2.cu) at every size it supports (RSG_OLA2) in a fresh
+    process: single pairs long enough for several runs per item, and a render."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import numpy as np, oracle\n"
+        "from paper_1712_03439_b200 import roomsim as rs, scenes\n"
+        "ctx = rs.Context(0); port = oracle.port(); rng = np.random.default_rng(8); worst = 0.0\n"
+        "for k in range(5, 13):\n"
+        "    n = 2 ** k\n"
+        "    for nh in (1, n // 4 + 1, n // 2, n - 3):\n"
+        "        x, h = rng.standard_normal(40 * n + 13), rng.standard_normal(max(nh, 1))\n"
+        "        want = port.convolve_ola(x, h, n); got = rs.convolve_ola(x, h, n, ctx=ctx)\n"
+        "        worst = max(worst, float(np.abs(got - want).max() / np.abs(want).max()))\n"
+        "b = scenes.config4(n_utt=3, seed=31)\n"
+        "g = rs.render_batch(b, ctx=ctx); o = port.render_batch(b, threads=8)\n"
+        "assert np.allclose(g.gains, o[3], rtol=1e-5), (g.gains, o[3])\n"
+        "assert np.allclose(g.power, o[4], rtol=1e-5), (g.power, o[4])\n"
+        "for u in range(b.n_utt):\n"
+        "    for j in range(int(b.mic_begin[u + 1] - b.mic_begin[u])):\n"
+        "        a_ = b.channel(g.out, u, j, g.out_len[u]); w_ = b.channel(o[0], u, j, o[1][u])\n"
+        "        worst = max(worst, float(np.abs(a_ - w_).max() / np.abs(w_).max()))\n"
+        "print(worst)\n")
+    env = dict(os.environ, RSG_OLA2="5,12")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= WAVE_TOL
+
+
 def test_four_step_path_small_sizes(tmp_path):
     """Route every size >= 2^7 through the four-step path (RSG_LARGE_MIN) in a fresh
     process and check it against the oracle at sizes where K4 normally runs."""
