@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   double* ent_a = rg + (3 * K + 1);              // [NT] owner-major sorted amplitudes
   int* ent_d = reinterpret_cast<int*>(ent_a + NT);           // [NT] their bins
   // [NW owner][NW compute] entry counts, one byte each (<= 32), 16-byte aligned rows
-  unsigned char* cnt8 = reinterpret_cast<unsigned char*>(ent_d + NT);
+  unsigned char* cnt8 = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(ent_d + NT) + 15) & ~uintptr_t(15));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lo = it.slice_lo, len = it.slice_len;
   for (int l = tid; l < len; l += NT) bins[l] = 0.0;
@@ -134,7 +134,10 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
     ix += cx;
 #ifndef RSG_X_NOSCATTER
     // ---- publish: lane masks per owner from OB + 1 ballots ----
-    const int owner = rel_bin & (NW - 1);
+    // owner of a bin: any function of the bin keeps each bin's entries in order; mixing
+    // in bin/16 spreads one owner's FP64 bins over all smem banks (bin mod NW alone
+    // puts them all in one bank pair)
+    const int owner = (rel_bin ^ (rel_bin >> 4)) & (NW - 1);
     unsigned mine = __ballot_sync(0xffffffffu, rel_bin >= 0);  // lanes sharing my owner
     unsigned row = mine;                                        // lane o < NW: lanes owned by o
 #pragma unroll
@@ -150,10 +153,17 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
     // byte sums of the owner's count row by dp4a
     unsigned ubefore = 0u, utotal = 0u;
     if (lane < NW) {
-      const unsigned* rowp = reinterpret_cast<const unsigned*>(cnt8 + lane * (4 * NQ));
+      unsigned rowv[NQ];
+      if constexpr (NQ == 4) {  // one 16-byte load per lane (a strided 4-byte loop is 4-way conflicted)
+        const uint4 r4 = *reinterpret_cast<const uint4*>(cnt8 + lane * 16);
+        rowv[0] = r4.x; rowv[1] = r4.y; rowv[2] = r4.z; rowv[3] = r4.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) rowv[q] = reinterpret_cast<const unsigned*>(cnt8 + lane * (4 * NQ))[q];
+      }
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        const unsigned wq = NW >= 4 ? rowp[q] : (rowp[0] & ((1u << (8 * NW)) - 1u));
+        const unsigned wq = NW >= 4 ? rowv[q] : (rowv[0] & ((1u << (8 * NW)) - 1u));
         utotal = __dp4a(wq, 0x01010101u, utotal);
         ubefore = __dp4a(wq & below[q], 0x01010101u, ubefore);
       }
@@ -212,7 +222,7 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
 size_t synth_smem_bytes(int max_order, int slice, int nt) {
   const int W = 2 * max_order + 1, nw = nt / 32;
   return sizeof(double) * (static_cast<size_t>(slice) + 3 * W + 3 * max_order + 1 + nt) + sizeof(int) * nt +
-         static_cast<size_t>(nw) * 4 * ((nw + 3) / 4);
+         static_cast<size_t>(nw) * 4 * ((nw + 3) / 4) + 16;
 }
 
 cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice, cudaStream_t s,
