@@ -276,9 +276,18 @@ def ours(args, rank, world, local_rank):
     per_step_flops = flops / args.steps
     achieved = per_step_flops / (ola_ms / args.steps / 1e3) / 1e12 if ola_ms > 0 else None
     hbm = float(peaks.get("hbm_gbs") or 6543.1)
+    traffic, traffic_src = None, None
+    if args.config == "config4" and n_cfg == DEFAULT_UTTS["config4"]:
+        try:  # K4 DRAM bytes per render, from the committed ncu launch list of this workload
+            with open(os.path.join(ROOT, "profiles", "r01_k4_traffic.json")) as f:
+                tj = json.load(f)
+            traffic, traffic_src = tj["dram_bytes_per_render"], tj["source"] + "; " + tj["note"]
+        except Exception:
+            pass
     roofline = {
         "bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-        "frac": achieved / fp32_peak if achieved else None, "traffic": None,
+        "frac": achieved / fp32_peak if achieved else None, "traffic": traffic,
+        "traffic_unit": "DRAM bytes per step (all K4 launches)", "traffic_source": traffic_src,
         "kernel": "ola_kernel<M> (K4), all FFT sizes of one render",
         "ola_ms_per_step": ola_ms / args.steps,
         "alg_flops_per_step": per_step_flops,
