@@ -257,7 +257,11 @@ struct CtaBar {
   __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
 
-template <int M, int P, bool INV, class Bar = CtaBar, bool TWS = false>
+// L2 layout: PAD(i) + 8*(i/128), the output layout of the fused pairing pass
+// (fused_pair_512) — conflict-free for its butterfly -> thread map.
+__host__ __device__ __forceinline__ constexpr int L2S(int i) { return i + (i >> 4) + 8 * (i >> 7); }
+
+template <int M, int P, bool INV, class Bar = CtaBar, bool TWS = false, bool L2IN = false>
 __device__ __forceinline__ void stockham_pass(float2* s, int t, const float2* __restrict__ tw,
                                               bool active, Bar bar = Bar()) {
   using PL = Plan<M>;
@@ -273,7 +277,10 @@ __device__ __forceinline__ void stockham_pass(float2* s, int t, const float2* __
     for (int q = 0; q < NB; ++q) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        if constexpr (PL::q_in(P))
+        if constexpr (L2IN) {
+          static_assert(NB == 1 && STRIDE == 64 && T == 64, "L2 input: the pass after fused_pair_512");
+          v[q][r] = s[PAD(t) + 68 * r + 8 * (r >> 1)];  // L2S(t + 64 r), t < 64
+        } else if constexpr (PL::q_in(P))
           v[q][r] = s[q_slot<T>(t, q * T + r * STRIDE)];
         else if constexpr (STRIDE % 16 == 0 && LIN)
           v[q][r] = sr[q * PAD(T) + r * PAD(STRIDE)];
@@ -488,6 +495,90 @@ __device__ __forceinline__ void spectral_multiply(float2* s, int t, const float2
         s[PAD(k)] = make_float2(U.x - V.y, U.y + V.x);
       }
     }
+  }
+  bar();
+}
+
+// ---- M = 512: last forward pass + untangle x G x repack + first inverse pass in
+// registers.  Thread t runs butterfly j = sigma(t) of both passes, chosen so that j and
+// its partner 64 - j (which holds Z[M - k] for every k = j + 64 r of j) sit in lanes
+// l and l ^ 16 of one warp:  warp 0: lanes 0-15 -> j = 0-15, lane 16 -> 32,
+// lanes 17-31 -> 80 - l;  warp 1: lanes 0-15 -> 16-31, lanes 16-31 -> 64 - l.
+// Each lane computes the pairs (k, M-k) for its r = 0..3 from the partner's raw
+// Z[j' + 64 r'], r' = 4..7 (shuffled in) and returns the partner's outputs (shuffled
+// back); j = 0 and j = 32 pair with themselves.  Formulas as spectral_multiply.
+// Reads the Q layout (output of the NS = 8 pass), writes the L2 layout.
+template <class Bar>
+__device__ __forceinline__ void fused_pair_512(float2* s, int t, const float2* tws, const float2* G,
+                                               const float2* W, bool active, Bar bar) {
+  using PL = Plan<512>;
+  constexpr int M = 512;
+  static_assert(PL::T == 64 && PL::NP == 3 && PL::radix(2) == 8 && PL::ns(2) == 64, "plan shape");
+  const int w = t >> 5, l = t & 31;
+  const int j = w == 0 ? (l < 16 ? l : (l == 16 ? 32 : 80 - l)) : (l < 16 ? 16 + l : 64 - l);
+  float2 v[8];
+  if (active) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = s[j + 72 * r];  // q_slot(j + 64 r), j < 64
+    apply_twiddles<8, false>(v, tws[PL::tw_off(2) + j]);
+    Dft<8, false>::run(v);  // v[r] = Z[j + 64 r]
+  }
+  // partner's raw Z[j' + 64 r'], r' = 4..7 (all lanes shuffle; inactive lanes carry junk)
+  float2 pv[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    pv[r].x = __shfl_xor_sync(0xffffffffu, v[4 + r].x, 16);
+    pv[r].y = __shfl_xor_sync(0xffffffffu, v[4 + r].y, 16);
+  }
+  // one pair (k, M - k): a = Z[k], b = conj(Z[M - k]) -> (Z'[k], Z'[M - k])
+  auto pair = [&](int k, float2 a, float2 b, float2& zk, float2& zm) {
+    const float2 wk = W[k];
+    const float2 S = c_add(a, b);
+    const float2 D = c_rot<false>(c_sub(a, b));
+    const float2 wD = c_mul(wk, D);
+    const float2 X2 = c_add(S, wD), X2m = c_sub(S, wD);
+    const float2 P = c_mul(X2, G[k]);
+    const float2 Q = c_mulc(X2m, G[M - k]);
+    const float2 U = c_add(P, Q);
+    const float2 V = c_mulc(c_sub(P, Q), wk);
+    zk = make_float2(U.x - V.y, U.y + V.x);
+    zm = make_float2(U.x + V.y, V.x - U.y);
+  };
+  float2 out[8];   // Z' of this butterfly
+  float2 back[4];  // Z' of the partner's r' = 4..7 (sent back)
+  // One code path for all lanes (no divergence): the partner element of r is
+  //   j = 0: r' = 8 - r in this lane (r = 0: Z[0] itself, G[M - 0] = G[M]);
+  //   j = 32: r' = 7 - r in this lane;  otherwise r' = 7 - r in the partner (pv[3 - r]).
+  const bool self0 = j == 0, self32 = j == 32;
+  if (active) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float2 bsrc = self0 ? v[(8 - r) & 7] : (self32 ? v[7 - r] : pv[3 - r]);
+      float2 zk, zm;
+      pair(j + 64 * r, v[r], c_conj(bsrc), zk, zm);
+      out[r] = zk;
+      back[3 - r] = zm;
+      if (self32) out[7 - r] = zm;
+      if (self0 && r > 0) out[8 - r] = zm;
+    }
+    if (self0) {  // k = M/2 pairs with itself (one lane)
+      float2 zm;
+      pair(M / 2, v[4], c_conj(v[4]), out[4], zm);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    float2 got;
+    got.x = __shfl_xor_sync(0xffffffffu, back[r].x, 16);
+    got.y = __shfl_xor_sync(0xffffffffu, back[r].y, 16);
+    if (!self0 && !self32) out[4 + r] = got;
+  }
+  if (active) Dft<8, true>::run(out);  // inverse pass 0 (NS = 1)
+  bar();                               // every thread's reads of s are done
+  if (active) {
+    float2* sw = s + L2S(8 * j);       // L2S(8 j + r) = L2S(8 j) + r
+#pragma unroll
+    for (int r = 0; r < 8; ++r) sw[r] = out[r];
   }
   bar();
 }

@@ -616,9 +616,18 @@ ola_small_kernel(OlaArgs a) {
 #if !defined(RSG_NO_PREFETCH) && !defined(RSG_X_NOLOAD)
     if (active && b + 2 < it.b_end) prefetch(k + 2);  // lands while blocks b, b+1 are transformed
 #endif
-    forward_rest<M, 1, GroupBar<T>, true>(s, t, tws, active, bar);
-    spectral_multiply<M, GroupBar<T>, true, true>(s, t, gs, W, active, bar);
-    inverse_but_last<M, 0, GroupBar<T>, true>(s, t, tws, active, bar);
+#ifndef RSG_NO_FUSED_PAIR
+    if constexpr (M == 512) {  // last forward pass + pairing + first inverse pass in registers
+      stockham_pass<M, 1, false, GroupBar<T>, true>(s, t, tws, active, bar);
+      fused_pair_512(s, t, tws, gs, W, active, bar);
+      stockham_pass<M, 1, true, GroupBar<T>, true, true>(s, t, tws, active, bar);
+    } else
+#endif
+    {
+      forward_rest<M, 1, GroupBar<T>, true>(s, t, tws, active, bar);
+      spectral_multiply<M, GroupBar<T>, true, true>(s, t, gs, W, active, bar);
+      inverse_but_last<M, 0, GroupBar<T>, true>(s, t, tws, active, bar);
+    }
     // emit: e < L -> final output (carry + v), e >= L -> carry for block b+1
     float* yb = y + start;
     const int lo = own_lo - start;
