@@ -186,6 +186,60 @@ int rs_last_pair_signal(rs_ctx* ctx, int64_t pair, float* out, size_t cap, size_
 /* Copy the synthesized (and truncated) RIR of pair `pair` of the last render. */
 int rs_last_pair_rir(rs_ctx* ctx, int64_t pair, double* out, size_t cap, size_t* len);
 
+/* ---- scene sampler and signal generator (SPEC.md:141-192 config_sampler; SURVEY.md
+ * §8f row 1).  The reference specifies the sampler contract but ships no code.  Every
+ * scene is a pure function of (seed, utterance, epoch) (Philox4x32-10 counter streams
+ * keyed by a hash of the three); the host functions are the fixture generator and
+ * produce the same bits as the device functions (one shared source, IEEE basic ops
+ * only).  Noise count: categorical over 0..n_weights-1 when n_weights > 0 (SPEC
+ * default weights 0.15/0.35/0.30/0.20, mean 1.55), else num_noises.              */
+typedef struct rs_sampler_spec {
+  double dim_lo[3], dim_hi[3];   /* room dimension ranges, metres */
+  double refl_lo, refl_hi;       /* reflection coefficient range (t60_hi <= 0) */
+  double t60_max;                /* resample while Eyring T60 > t60_max (t60_hi <= 0) */
+  double t60_lo, t60_hi;         /* t60_hi > 0: sample T60, r = exp(-0.0805 V / (S T60)) */
+  double snr_lo, snr_hi;         /* SNR range, dB (noise sources) */
+  double mic_spacing;            /* line array (mic_radius <= 0): 1 or 2 mics */
+  double mic_radius;             /* > 0: circular array of mic_count mics */
+  double clearance;              /* minimum distance of every placement to the walls */
+  double sec_lo, sec_hi;         /* utterance duration range, seconds */
+  double fs, c0;                 /* sample rate, speed of sound */
+  double signal_std;             /* synthetic signals: N(0, signal_std^2) */
+  int32_t num_noises;            /* fixed noise count when n_weights == 0 */
+  int32_t mic_count;
+  int32_t n_weights;             /* 0..8 */
+  int32_t pad_;
+  double weights[8];
+} rs_sampler_spec;
+
+/* Sources per utterance (1 + noise count) of utterances first_utt .. first_utt+n_utt-1. */
+int rs_sampler_counts(const rs_sampler_spec* spec, uint64_t seed, int64_t first_utt, int64_t n_utt,
+                      int64_t epoch, int32_t* n_src);
+/* Scenes into the rs_scene_batch arrays (host).  src_begin: CSR from rs_sampler_counts;
+ * mic_pos holds n_utt * mic_count rows; max_taps = ceil(T60 fs) (the T60 horizon);
+ * n_samples = N_x per utterance (shared by its sources). */
+int rs_sample_scenes(const rs_sampler_spec* spec, uint64_t seed, int64_t first_utt, int64_t n_utt,
+                     int64_t epoch, const int64_t* src_begin, double* room_dims, double* reflection,
+                     int32_t* image_order, int64_t* max_taps, double* src_pos, double* mic_pos,
+                     double* snr_db, int64_t* n_samples);
+/* The same on the device (all pointers device memory; `stream` a cudaStream_t or NULL). */
+int rs_sampler_counts_device(const rs_sampler_spec* spec, uint64_t seed, int64_t first_utt,
+                             int64_t n_utt, int64_t epoch, int32_t* n_src_dev, void* stream);
+int rs_sample_scenes_device(const rs_sampler_spec* spec, uint64_t seed, int64_t first_utt,
+                            int64_t n_utt, int64_t epoch, const int64_t* src_begin_dev,
+                            double* room_dims, double* reflection, int32_t* image_order,
+                            int64_t* max_taps, double* src_pos, double* mic_pos, double* snr_db,
+                            int64_t* n_samples, void* stream);
+/* Synthetic source signals, N(0, signal_std^2) (Box-Muller on Philox), keyed by
+ * (seed, utterance, epoch) and the source's index within its utterance; written at
+ * out + sig_off[s] for sig_len[s] samples.  Metadata arrays are host arrays. */
+int rs_generate_signals_host(const rs_sampler_spec* spec, uint64_t seed, int64_t epoch, int64_t n_src,
+                             const int64_t* utt_of_src, const int32_t* src_local,
+                             const int64_t* sig_off, const int64_t* sig_len, float* out);
+int rs_generate_signals(const rs_sampler_spec* spec, uint64_t seed, int64_t epoch, int64_t n_src,
+                        const int64_t* utt_of_src, const int32_t* src_local, const int64_t* sig_off,
+                        const int64_t* sig_len, float* out_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

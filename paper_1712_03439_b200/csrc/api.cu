@@ -30,6 +30,15 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+}  // namespace
+
+// error reporting shared with the other translation units (sampler.cu)
+namespace rsg {
+int report_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace rsg
+
+namespace {
+
 #define RS_CUDA(call)                                                                  \
   do {                                                                                 \
     cudaError_t e_ = (call);                                                           \

@@ -637,7 +637,9 @@ ola_small_kernel(OlaArgs a) {
     // the emit needs no barrier and nothing stays live across one
     const float* cin = carry0 + (k & 1) * N;
     float* carry = carry0 + ((k + 1) & 1) * N;
-    float pb = 0.f;  // this block's power partial (FP32, <= 2E terms), folded into FP64 below
+    // this block's power partials (FP32, <= 2E terms over four independent chains so the
+    // FMAs do not serialise), folded into FP64 below in a fixed order
+    float pb[4] = {0.f, 0.f, 0.f, 0.f};
     auto emit_fn = [&](int q, int r, int c, float2 v) {
       const int e0 = 2 * c;
       const float2 ci = *reinterpret_cast<const float2*>(cin + e0);
@@ -652,7 +654,7 @@ ola_small_kernel(OlaArgs a) {
             yb[e] = val;
 #endif
 #ifndef RSG_X_NOPOWER
-            pb = fmaf(val, val, pb);
+            pb[2 * (r & 1) + h] = fmaf(val, val, pb[2 * (r & 1) + h]);
 #endif
           }
         } else {
@@ -661,7 +663,7 @@ ola_small_kernel(OlaArgs a) {
       }
     };
     stockham_emit_pass<M, GroupBar<T>, decltype(emit_fn), true, false>(s, t, tws, active, bar, emit_fn);
-    pw += static_cast<double>(pb);
+    pw += static_cast<double>((pb[0] + pb[1]) + (pb[2] + pb[3]));
     // (N_h - 1 > L, three or more overlapping blocks, needs no extra step: the
     // old carry at e in [L, N_h - 1) comes from the other buffer.)
   }

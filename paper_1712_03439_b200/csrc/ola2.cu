@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(ola2_cta(ilog2(N)), ola2_minb(ilog2(N))) ola2_
     fused_mid<PF, PI>(s, t, twf, hs, active, bar);
     middle_passes<PI, 1, true>(s, t, twi, active, bar);
     // emit: element e of run r's block: e < L (or its last block) final, else carry
-    float pb = 0.f;
+    float pb[2] = {0.f, 0.f};  // one chain per run
     const float* cin[2];
     float* cout[2];
     int lo[2], hi[2], start[2];
@@ -201,14 +201,14 @@ __global__ void __launch_bounds__(ola2_cta(ilog2(N)), ola2_minb(ilog2(N))) ola2_
         if (e < L || last[r]) {
           if (e >= lo[r] && e < hi[r]) {
             y[start[r] + e] = val;
-            pb = fmaf(val, val, pb);
+            pb[r] = fmaf(val, val, pb[r]);
           }
         } else {
           cout[r][e - L] = val;
         }
       }
     });
-    pw += static_cast<double>(pb);
+    pw += static_cast<double>(pb[0] + pb[1]);
   }
   // Σ y^2 of both runs' owned samples (fixed order) -> part[item]
   if constexpr (T >= 32) {

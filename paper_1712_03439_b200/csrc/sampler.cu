@@ -1,0 +1,198 @@
+// sampler.cu — the scene sampler and signal generator (sampler.cuh) on the host (the
+// fixture generator) and on the device, behind the C-ABI.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/roomsim_gpu.h"
+#include "sampler.cuh"
+
+namespace rsg {
+int report_error(int code, const std::string& msg);  // api.cu: sets rs_last_error()
+static_assert(sizeof(SamplerSpecD) == sizeof(rs_sampler_spec), "rs_sampler_spec layout");
+
+namespace {
+
+const SamplerSpecD& spec_of(const rs_sampler_spec* s) { return *reinterpret_cast<const SamplerSpecD*>(s); }
+
+__global__ void counts_kernel(SamplerSpecD sp, uint64_t seed, int64_t first, int64_t n, int64_t epoch,
+                              int32_t* n_src) {
+  const int64_t u = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (u < n) n_src[u] = 1 + sampler_num_noises(sp, seed, static_cast<uint64_t>(first + u), epoch);
+}
+
+__global__ void scenes_kernel(SamplerSpecD sp, uint64_t seed, int64_t first, int64_t n, int64_t epoch,
+                              const int64_t* src_begin, double* room, double* refl, int32_t* order,
+                              int64_t* horizon, double* src_pos, double* mic_pos, double* snr, int64_t* nsamp) {
+  const int64_t u = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (u >= n) return;
+  const int64_t s0 = src_begin[u];
+  const int I = static_cast<int>(src_begin[u + 1] - s0);
+  const SceneOut o = sampler_scene(sp, seed, static_cast<uint64_t>(first + u), epoch, I, src_pos + 3 * s0,
+                                   mic_pos + 3 * u * sp.mic_count, snr + s0);
+  for (int a = 0; a < 3; ++a) room[3 * u + a] = o.room[a];
+  refl[u] = o.refl;
+  order[u] = o.order;
+  horizon[u] = o.horizon;
+  nsamp[u] = o.n_samples;
+}
+
+struct SrcInfo {
+  int64_t utt, off, len;
+  int32_t local, pad;
+};
+
+// grid.y = source, grid.x = tiles of 4 * blockDim.x sample pairs
+__global__ void __launch_bounds__(256) signals_kernel(SamplerSpecD sp, uint64_t seed, int64_t epoch,
+                                                      const SrcInfo* src, float* out) {
+  const SrcInfo si = src[blockIdx.y];
+  const Stream g(seed ^ 0x5EED5EED5EEDull, static_cast<uint64_t>(si.utt), static_cast<uint64_t>(epoch),
+                 kTagSignal + static_cast<uint32_t>(si.local));
+  const int64_t npairs = (si.len + 1) / 2;
+  float* o = out + si.off;
+  for (int k = 0; k < 4; ++k) {
+    const int64_t p = (static_cast<int64_t>(blockIdx.x) * 4 + k) * blockDim.x + threadIdx.x;
+    if (p >= npairs) return;
+    float z0, z1;
+    signal_pair(sp, g, static_cast<uint64_t>(p), &z0, &z1);
+    o[2 * p] = z0;
+    if (2 * p + 1 < si.len) o[2 * p + 1] = z1;
+  }
+}
+
+int sfail(int code, const std::string& m) { return report_error(code, m); }
+
+int check_spec(const rs_sampler_spec* s) {
+  if (!s) return sfail(RS_ERR_CONFIG, "null sampler spec");
+  for (int a = 0; a < 3; ++a)
+    if (!(s->dim_lo[a] > 0.0) || s->dim_hi[a] < s->dim_lo[a] ||
+        s->dim_lo[a] - 2.0 * s->clearance <= 0.0)
+      return sfail(RS_ERR_CONFIG, "room ranges incompatible with the wall clearance");
+  if (s->n_weights < 0 || s->n_weights > 8) return sfail(RS_ERR_CONFIG, "at most 8 noise-count weights");
+  double tot = 0.0;
+  for (int i = 0; i < s->n_weights; ++i) {
+    if (s->weights[i] < 0.0) return sfail(RS_ERR_CONFIG, "noise-count weights must be non-negative");
+    tot += s->weights[i];
+  }
+  if (s->n_weights > 0 && !(tot > 0.0)) return sfail(RS_ERR_CONFIG, "noise-count weights all zero");
+  if (s->mic_count < 1 || (s->mic_radius <= 0.0 && s->mic_count > 2))
+    return sfail(RS_ERR_CONFIG, "line arrays hold 1 or 2 mics; use mic_radius > 0 for more");
+  if (!(s->fs > 0.0) || !(s->c0 > 0.0)) return sfail(RS_ERR_CONFIG, "sample rate and speed of sound must be positive");
+  return RS_OK;
+}
+
+}  // namespace
+}  // namespace rsg
+
+using namespace rsg;
+
+extern "C" {
+
+int rs_sampler_counts(const rs_sampler_spec* spec, uint64_t seed, int64_t first_utt, int64_t n_utt,
+                      int64_t epoch, int32_t* n_src) {
+  if (int st = check_spec(spec)) return st;
+  for (int64_t u = 0; u < n_utt; ++u)
+    n_src[u] = 1 + sampler_num_noises(spec_of(spec), seed, static_cast<uint64_t>(first_utt + u), epoch);
+  return RS_OK;
+}
+
+int rs_sample_scenes(const rs_sampler_spec* spec, uint64_t seed, int64_t first_utt, int64_t n_utt, int64_t epoch,
+                     const int64_t* src_begin, double* room_dims, double* reflection, int32_t* image_order,
+                     int64_t* max_taps, double* src_pos, double* mic_pos, double* snr_db, int64_t* n_samples) {
+  if (int st = check_spec(spec)) return st;
+  const SamplerSpecD& sp = spec_of(spec);
+  for (int64_t u = 0; u < n_utt; ++u) {
+    const int64_t s0 = src_begin[u];
+    const SceneOut o = sampler_scene(sp, seed, static_cast<uint64_t>(first_utt + u), epoch,
+                                     static_cast<int>(src_begin[u + 1] - s0), src_pos + 3 * s0,
+                                     mic_pos + 3 * u * sp.mic_count, snr_db + s0);
+    for (int a = 0; a < 3; ++a) room_dims[3 * u + a] = o.room[a];
+    reflection[u] = o.refl;
+    image_order[u] = o.order;
+    max_taps[u] = o.horizon;
+    n_samples[u] = o.n_samples;
+  }
+  return RS_OK;
+}
+
+int rs_sampler_counts_device(const rs_sampler_spec* spec, uint64_t seed, int64_t first_utt, int64_t n_utt,
+                             int64_t epoch, int32_t* n_src_dev, void* stream) {
+  if (int st = check_spec(spec)) return st;
+  if (n_utt <= 0) return RS_OK;
+  counts_kernel<<<static_cast<unsigned>((n_utt + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      spec_of(spec), seed, first_utt, n_utt, epoch, n_src_dev);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? RS_OK : sfail(RS_ERR_CUDA, cudaGetErrorString(e));
+}
+
+int rs_sample_scenes_device(const rs_sampler_spec* spec, uint64_t seed, int64_t first_utt, int64_t n_utt,
+                            int64_t epoch, const int64_t* src_begin_dev, double* room_dims, double* reflection,
+                            int32_t* image_order, int64_t* max_taps, double* src_pos, double* mic_pos,
+                            double* snr_db, int64_t* n_samples, void* stream) {
+  if (int st = check_spec(spec)) return st;
+  if (n_utt <= 0) return RS_OK;
+  scenes_kernel<<<static_cast<unsigned>((n_utt + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      spec_of(spec), seed, first_utt, n_utt, epoch, src_begin_dev, room_dims, reflection, image_order, max_taps,
+      src_pos, mic_pos, snr_db, n_samples);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? RS_OK : sfail(RS_ERR_CUDA, cudaGetErrorString(e));
+}
+
+int rs_generate_signals_host(const rs_sampler_spec* spec, uint64_t seed, int64_t epoch, int64_t n_src,
+                             const int64_t* utt_of_src, const int32_t* src_local, const int64_t* sig_off,
+                             const int64_t* sig_len, float* out) {
+  if (int st = check_spec(spec)) return st;
+  const SamplerSpecD& sp = spec_of(spec);
+  for (int64_t s = 0; s < n_src; ++s) {
+    const Stream g(seed ^ 0x5EED5EED5EEDull, static_cast<uint64_t>(utt_of_src[s]), static_cast<uint64_t>(epoch),
+                   kTagSignal + static_cast<uint32_t>(src_local[s]));
+    float* o = out + sig_off[s];
+    const int64_t len = sig_len[s];
+    for (int64_t p = 0; 2 * p < len; ++p) {
+      float z0, z1;
+      signal_pair(sp, g, static_cast<uint64_t>(p), &z0, &z1);
+      o[2 * p] = z0;
+      if (2 * p + 1 < len) o[2 * p + 1] = z1;
+    }
+  }
+  return RS_OK;
+}
+
+int rs_generate_signals(const rs_sampler_spec* spec, uint64_t seed, int64_t epoch, int64_t n_src,
+                        const int64_t* utt_of_src, const int32_t* src_local, const int64_t* sig_off,
+                        const int64_t* sig_len, float* out_dev, void* stream) {
+  if (int st = check_spec(spec)) return st;
+  if (n_src <= 0) return RS_OK;
+  if (n_src > 65535) {  // grid.y limit: split
+    for (int64_t s0 = 0; s0 < n_src; s0 += 65535) {
+      const int64_t m = std::min<int64_t>(65535, n_src - s0);
+      if (int st = rs_generate_signals(spec, seed, epoch, m, utt_of_src + s0, src_local + s0, sig_off + s0,
+                                       sig_len + s0, out_dev, stream))
+        return st;
+    }
+    return RS_OK;
+  }
+  std::vector<SrcInfo> info(n_src);
+  int64_t max_pairs = 1;
+  for (int64_t s = 0; s < n_src; ++s) {
+    info[s] = SrcInfo{utt_of_src[s], sig_off[s], sig_len[s], src_local[s], 0};
+    max_pairs = std::max<int64_t>(max_pairs, (sig_len[s] + 1) / 2);
+  }
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SrcInfo* d = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), info.size() * sizeof(SrcInfo), st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d, info.data(), info.size() * sizeof(SrcInfo), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    const dim3 grid(static_cast<unsigned>((max_pairs + 1023) / 1024), static_cast<unsigned>(n_src));
+    signals_kernel<<<grid, 256, 0, st>>>(spec_of(spec), seed, epoch, d, out_dev);
+    e = cudaGetLastError();
+  }
+  if (d) cudaFreeAsync(d, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the host table must outlive the copy
+  return e == cudaSuccess ? RS_OK : sfail(RS_ERR_CUDA, cudaGetErrorString(e));
+}
+
+}  // extern "C"

@@ -1,0 +1,308 @@
+// sampler.cuh — the scene sampler (SPEC.md:141-192 config_sampler contract) and the
+// synthetic-signal generator as ONE host/device source, so the host fixture generator
+// and the on-device generator agree bit for bit.
+//
+// Randomness: Philox4x32-10 (Salmon, Moraes, Dror & Shaw, SC'11), keyed by a
+// splitmix64 hash of (seed, utterance, epoch) — every scene is a pure function of
+// (seed, utterance_id, epoch) and batch order never matters.
+// Arithmetic: integer ops, and FP64 +, -, *, /, sqrt with round-to-nearest and no
+// contraction (device: __d*_rn intrinsics; host: compiled with -ffp-contract=off);
+// log / exp / sin / cos are polynomial restatements built only from those ops, so
+// both sides execute the identical IEEE operation sequence.
+#pragma once
+
+#include <stdint.h>
+#include <string.h>
+
+#include <cmath>
+
+namespace rsg {
+
+#ifdef __CUDA_ARCH__
+#define RSH __host__ __device__ __forceinline__
+#define RS_ADD(a, b) __dadd_rn((a), (b))
+#define RS_SUB(a, b) __dsub_rn((a), (b))
+#define RS_MUL(a, b) __dmul_rn((a), (b))
+#define RS_DIV(a, b) __ddiv_rn((a), (b))
+#define RS_SQRT(a) __dsqrt_rn(a)
+#define RS_FLOOR(a) floor(a)
+#define RS_CEIL(a) ceil(a)
+#else
+#define RSH __host__ __device__ inline
+#define RS_ADD(a, b) ((a) + (b))
+#define RS_SUB(a, b) ((a) - (b))
+#define RS_MUL(a, b) ((a) * (b))
+#define RS_DIV(a, b) ((a) / (b))
+#define RS_SQRT(a) std::sqrt(a)
+#define RS_FLOOR(a) std::floor(a)
+#define RS_CEIL(a) std::ceil(a)
+#endif
+
+// ---- Philox4x32-10 -----------------------------------------------------------------
+struct U4 {
+  uint32_t x, y, z, w;
+};
+
+RSH uint32_t mulhilo32(uint32_t a, uint32_t b, uint32_t* hi) {
+  const uint64_t p = static_cast<uint64_t>(a) * b;
+  *hi = static_cast<uint32_t>(p >> 32);
+  return static_cast<uint32_t>(p);
+}
+
+RSH U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    uint32_t hi0, hi1;
+    const uint32_t lo0 = mulhilo32(0xD2511F53u, c.x, &hi0);
+    const uint32_t lo1 = mulhilo32(0xCD9E8D57u, c.z, &hi1);
+    c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+RSH uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Stream of uniforms keyed by (seed, a, b) (a = utterance, b = epoch).
+struct Stream {
+  uint32_t k0, k1;
+  uint32_t tag;   // stream purpose / sub-stream
+  uint64_t ctr;   // draws taken
+  RSH Stream(uint64_t seed, uint64_t a, uint64_t b, uint32_t t) : tag(t), ctr(0) {
+    const uint64_t k = splitmix64(splitmix64(seed) ^ splitmix64(a * 0x9E3779B97F4A7C15ull + b));
+    k0 = static_cast<uint32_t>(k);
+    k1 = static_cast<uint32_t>(k >> 32);
+  }
+  // two 53-bit uniforms in [0, 1) from counter `i`
+  RSH void pair_at(uint64_t i, double* u0, double* u1) const {
+    const U4 r = philox4x32_10(U4{static_cast<uint32_t>(i), static_cast<uint32_t>(i >> 32), tag, 0x5CE4Eu}, k0, k1);
+    const uint64_t a = (static_cast<uint64_t>(r.x) << 32 | r.y) >> 11;
+    const uint64_t b = (static_cast<uint64_t>(r.z) << 32 | r.w) >> 11;
+    *u0 = static_cast<double>(a) * 0x1.0p-53;  // exact
+    *u1 = static_cast<double>(b) * 0x1.0p-53;
+  }
+  RSH double next() {
+    double u0, u1;
+    pair_at(ctr++, &u0, &u1);
+    return u0;
+  }
+  RSH double uniform(double lo, double hi) { return RS_ADD(lo, RS_MUL(RS_SUB(hi, lo), next())); }
+};
+
+// ---- portable elementary functions (basic IEEE ops only) -------------------------
+RSH double bits_to_double(uint64_t b) {
+  double d;
+  memcpy(&d, &b, 8);
+  return d;
+}
+RSH uint64_t double_to_bits(double d) {
+  uint64_t b;
+  memcpy(&b, &d, 8);
+  return b;
+}
+
+constexpr double kLn2 = 0.6931471805599453094;
+constexpr double kLn2Hi = 0x1.62e42fefa3800p-1;  // trailing zeros: k * kLn2Hi exact for |k| < 2^11
+constexpr double kLn2Lo = 0x1.ef35793c76730p-45;
+constexpr double kPi = 3.141592653589793116;
+constexpr double kPio2Hi = 0x1.921fb54400000p0;  // trailing zeros
+constexpr double kPio2Lo = 0x1.0b4611a626331p-34;
+
+// natural log, x > 0 normal: x = m 2^e, m in [sqrt(1/2), sqrt(2)), atanh series
+RSH double plog(double x) {
+  uint64_t b = double_to_bits(x);
+  int e = static_cast<int>((b >> 52) & 0x7ff) - 1023;
+  b = (b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull;
+  double m = bits_to_double(b);
+  if (m > 1.4142135623730951) {
+    m = RS_MUL(m, 0.5);
+    e += 1;
+  }
+  const double s = RS_DIV(RS_SUB(m, 1.0), RS_ADD(m, 1.0));
+  const double s2 = RS_MUL(s, s);
+  double p = 1.0 / 23.0;
+  p = RS_ADD(1.0 / 21.0, RS_MUL(s2, p));
+  p = RS_ADD(1.0 / 19.0, RS_MUL(s2, p));
+  p = RS_ADD(1.0 / 17.0, RS_MUL(s2, p));
+  p = RS_ADD(1.0 / 15.0, RS_MUL(s2, p));
+  p = RS_ADD(1.0 / 13.0, RS_MUL(s2, p));
+  p = RS_ADD(1.0 / 11.0, RS_MUL(s2, p));
+  p = RS_ADD(1.0 / 9.0, RS_MUL(s2, p));
+  p = RS_ADD(1.0 / 7.0, RS_MUL(s2, p));
+  p = RS_ADD(1.0 / 5.0, RS_MUL(s2, p));
+  p = RS_ADD(1.0 / 3.0, RS_MUL(s2, p));
+  p = RS_ADD(1.0, RS_MUL(s2, p));
+  const double lm = RS_MUL(RS_MUL(2.0, s), p);
+  const double ed = static_cast<double>(e);
+  return RS_ADD(RS_MUL(ed, kLn2Hi), RS_ADD(RS_MUL(ed, kLn2Lo), lm));
+}
+
+// exp(x), |x| < 700: x = k ln2 + r, Taylor to degree 13, scale by 2^k via the exponent
+RSH double pexp(double x) {
+  const double k = RS_FLOOR(RS_ADD(RS_MUL(x, 1.0 / kLn2), 0.5));
+  const double r = RS_SUB(RS_SUB(x, RS_MUL(k, kLn2Hi)), RS_MUL(k, kLn2Lo));
+  double p = 1.0 / 6227020800.0;  // 1/13!
+  p = RS_ADD(1.0 / 479001600.0, RS_MUL(r, p));
+  p = RS_ADD(1.0 / 39916800.0, RS_MUL(r, p));
+  p = RS_ADD(1.0 / 3628800.0, RS_MUL(r, p));
+  p = RS_ADD(1.0 / 362880.0, RS_MUL(r, p));
+  p = RS_ADD(1.0 / 40320.0, RS_MUL(r, p));
+  p = RS_ADD(1.0 / 5040.0, RS_MUL(r, p));
+  p = RS_ADD(1.0 / 720.0, RS_MUL(r, p));
+  p = RS_ADD(1.0 / 120.0, RS_MUL(r, p));
+  p = RS_ADD(1.0 / 24.0, RS_MUL(r, p));
+  p = RS_ADD(1.0 / 6.0, RS_MUL(r, p));
+  p = RS_ADD(0.5, RS_MUL(r, p));
+  p = RS_ADD(1.0, RS_MUL(r, p));
+  p = RS_ADD(1.0, RS_MUL(r, p));
+  const int ki = static_cast<int>(k);
+  return bits_to_double(double_to_bits(p) + (static_cast<uint64_t>(static_cast<int64_t>(ki)) << 52));
+}
+
+// sin and cos of x, |x| < 64: quadrant reduction by pi/2 (Cody-Waite), Taylor polynomials
+RSH void psincos(double x, double* sn, double* cs) {
+  const double k = RS_FLOOR(RS_ADD(RS_MUL(x, 2.0 / kPi), 0.5));
+  const double r = RS_SUB(RS_SUB(x, RS_MUL(k, kPio2Hi)), RS_MUL(k, kPio2Lo));
+  const double r2 = RS_MUL(r, r);
+  double s = -1.0 / 1307674368000.0;  // -1/15!
+  s = RS_ADD(1.0 / 6227020800.0, RS_MUL(r2, s));
+  s = RS_ADD(-1.0 / 39916800.0, RS_MUL(r2, s));
+  s = RS_ADD(1.0 / 362880.0, RS_MUL(r2, s));
+  s = RS_ADD(-1.0 / 5040.0, RS_MUL(r2, s));
+  s = RS_ADD(1.0 / 120.0, RS_MUL(r2, s));
+  s = RS_ADD(-1.0 / 6.0, RS_MUL(r2, s));
+  s = RS_ADD(r, RS_MUL(RS_MUL(r, r2), s));
+  double c = 1.0 / 20922789888000.0;  // 1/16!
+  c = RS_ADD(-1.0 / 87178291200.0, RS_MUL(r2, c));
+  c = RS_ADD(1.0 / 479001600.0, RS_MUL(r2, c));
+  c = RS_ADD(-1.0 / 3628800.0, RS_MUL(r2, c));
+  c = RS_ADD(1.0 / 40320.0, RS_MUL(r2, c));
+  c = RS_ADD(-1.0 / 720.0, RS_MUL(r2, c));
+  c = RS_ADD(1.0 / 24.0, RS_MUL(r2, c));
+  c = RS_ADD(-0.5, RS_MUL(r2, c));
+  c = RS_ADD(1.0, RS_MUL(r2, c));
+  const int q = static_cast<int>(static_cast<int64_t>(k) & 3);
+  const double sv = q == 0 ? s : (q == 1 ? c : (q == 2 ? -s : -c));
+  const double cv = q == 0 ? c : (q == 1 ? -s : (q == 2 ? -c : s));
+  *sn = sv;
+  *cs = cv;
+}
+
+// ---- the sampler ------------------------------------------------------------------
+struct SamplerSpecD {  // mirrors rs_sampler_spec (include/roomsim_gpu.h)
+  double dim_lo[3], dim_hi[3];
+  double refl_lo, refl_hi, t60_max;
+  double t60_lo, t60_hi;
+  double snr_lo, snr_hi;
+  double mic_spacing, mic_radius, clearance;
+  double sec_lo, sec_hi;
+  double fs, c0, signal_std;
+  int32_t num_noises, mic_count, n_weights, pad;
+  double weights[8];
+};
+
+constexpr uint32_t kTagScene = 0x5CE7Eu, kTagSignal = 0x516Au;
+
+// noise count for utterance `utt` (the first draws of its stream)
+RSH int sampler_num_noises(const SamplerSpecD& sp, uint64_t seed, uint64_t utt, uint64_t epoch) {
+  if (sp.n_weights <= 0) return sp.num_noises;
+  Stream g(seed, utt, epoch, kTagScene + 1);
+  double tot = 0.0;
+  for (int i = 0; i < sp.n_weights; ++i) tot = RS_ADD(tot, sp.weights[i]);
+  const double u = RS_MUL(g.next(), tot);
+  double cum = 0.0;
+  for (int i = 0; i < sp.n_weights; ++i) {
+    cum = RS_ADD(cum, sp.weights[i]);
+    if (u < cum) return i;
+  }
+  return sp.n_weights - 1;
+}
+
+struct SceneOut {
+  double room[3], refl;
+  int32_t order;
+  int64_t horizon, n_samples;
+};
+
+// One utterance: room, reflection, T60 -> K and horizon, I sources (row 0 target),
+// J mics, SNRs, N_x.  `src`/`mic`/`snr` have room for I / J / I entries.
+RSH SceneOut sampler_scene(const SamplerSpecD& sp, uint64_t seed, uint64_t utt, uint64_t epoch, int n_src,
+                           double* src, double* mic, double* snr) {
+  Stream g(seed, utt, epoch, kTagScene);
+  SceneOut o{};
+  double t60 = 0.0;
+  for (int attempt = 0;; ++attempt) {  // rejection: T60 inside the spec
+    for (int a = 0; a < 3; ++a) o.room[a] = g.uniform(sp.dim_lo[a], sp.dim_hi[a]);
+    const double V = RS_MUL(RS_MUL(o.room[0], o.room[1]), o.room[2]);
+    const double S = RS_MUL(2.0, RS_ADD(RS_ADD(RS_MUL(o.room[0], o.room[1]), RS_MUL(o.room[0], o.room[2])),
+                                        RS_MUL(o.room[1], o.room[2])));
+    if (sp.t60_hi > 0.0) {  // sample T60, solve r from Eyring: r = exp(-0.0805 V / (S T60))
+      t60 = g.uniform(sp.t60_lo, sp.t60_hi);
+      o.refl = pexp(RS_DIV(RS_MUL(-0.0805, V), RS_MUL(S, t60)));
+      if (o.refl > 0.0 && o.refl < 1.0) break;
+    } else {  // sample r, Eyring T60 = 0.161 V / (-S ln r^2)
+      o.refl = g.uniform(sp.refl_lo, sp.refl_hi);
+      t60 = RS_DIV(RS_MUL(0.161, V), RS_MUL(-S, plog(RS_MUL(o.refl, o.refl))));
+      if (t60 <= sp.t60_max) break;
+    }
+    if (attempt > 10000) break;  // spec error guard (ranges incompatible)
+  }
+  const double nrm = RS_SQRT(RS_ADD(RS_ADD(RS_MUL(o.room[0], o.room[0]), RS_MUL(o.room[1], o.room[1])),
+                                    RS_MUL(o.room[2], o.room[2])));
+  o.order = static_cast<int32_t>(RS_CEIL(RS_DIV(RS_MUL(sp.c0, t60), nrm)));
+  o.horizon = static_cast<int64_t>(RS_CEIL(RS_MUL(t60, sp.fs)));
+  const double c = sp.clearance;
+  for (int i = 0; i < n_src; ++i)
+    for (int a = 0; a < 3; ++a) src[3 * i + a] = g.uniform(c, RS_SUB(o.room[a], c));
+  const double ext = sp.mic_radius > 0.0 ? sp.mic_radius : RS_MUL(sp.mic_spacing, 0.5);
+  double centre[3];
+  centre[0] = g.uniform(RS_ADD(c, ext), RS_SUB(RS_SUB(o.room[0], c), ext));
+  centre[1] = g.uniform(RS_ADD(c, ext), RS_SUB(RS_SUB(o.room[1], c), ext));
+  centre[2] = g.uniform(c, RS_SUB(o.room[2], c));
+  const double phi = RS_MUL(RS_MUL(2.0, kPi), g.next());
+  const int J = sp.mic_count;
+  if (sp.mic_radius > 0.0) {
+    for (int m = 0; m < J; ++m) {
+      const double ang = RS_ADD(phi, RS_DIV(RS_MUL(RS_MUL(2.0, kPi), static_cast<double>(m)), static_cast<double>(J)));
+      double sn, cs;
+      psincos(ang, &sn, &cs);
+      mic[3 * m + 0] = RS_ADD(centre[0], RS_MUL(sp.mic_radius, cs));
+      mic[3 * m + 1] = RS_ADD(centre[1], RS_MUL(sp.mic_radius, sn));
+      mic[3 * m + 2] = centre[2];
+    }
+  } else {
+    double sn, cs;
+    psincos(phi, &sn, &cs);
+    const double h = RS_MUL(sp.mic_spacing, 0.5);
+    for (int m = 0; m < J && m < 2; ++m) {
+      const double sg = m == 0 ? -1.0 : 1.0;
+      mic[3 * m + 0] = RS_ADD(centre[0], RS_MUL(sg, RS_MUL(cs, h)));
+      mic[3 * m + 1] = RS_ADD(centre[1], RS_MUL(sg, RS_MUL(sn, h)));
+      mic[3 * m + 2] = centre[2];
+    }
+  }
+  snr[0] = 0.0;
+  for (int i = 1; i < n_src; ++i) snr[i] = g.uniform(sp.snr_lo, sp.snr_hi);
+  const double secs = g.uniform(sp.sec_lo, sp.sec_hi);
+  o.n_samples = static_cast<int64_t>(RS_FLOOR(RS_ADD(RS_MUL(secs, sp.fs), 0.5)));
+  return o;
+}
+
+// Samples 2p, 2p+1 of source `src_local` of utterance `utt`: N(0, std) by Box-Muller.
+RSH void signal_pair(const SamplerSpecD& sp, const Stream& g, uint64_t p, float* z0, float* z1) {
+  double u0, u1;
+  g.pair_at(p, &u0, &u1);
+  const double r = RS_SQRT(RS_MUL(-2.0, plog(RS_SUB(1.0, u0))));  // 1 - u0 in (0, 1]
+  double sn, cs;
+  psincos(RS_MUL(RS_MUL(2.0, kPi), u1), &sn, &cs);
+  *z0 = static_cast<float>(RS_MUL(sp.signal_std, RS_MUL(r, cs)));
+  *z1 = static_cast<float>(RS_MUL(sp.signal_std, RS_MUL(r, sn)));
+}
+
+}  // namespace rsg

@@ -98,7 +98,21 @@ ABI_SYMBOLS = [
     "rs_rfft_forward", "rs_rfft_inverse", "rs_synthesize_rir", "rs_truncate_rir",
     "rs_convolve_ola", "rs_convolve_full_fft", "rs_convolve", "rs_batch_num_pairs",
     "rs_render_batch", "rs_render_batch_device", "rs_last_pair_signal", "rs_last_pair_rir",
+    "rs_sampler_counts", "rs_sample_scenes", "rs_sampler_counts_device", "rs_sample_scenes_device",
+    "rs_generate_signals_host", "rs_generate_signals",
 ]
+
+
+class RsSamplerSpec(C.Structure):
+    _fields_ = [
+        ("dim_lo", C.c_double * 3), ("dim_hi", C.c_double * 3), ("refl_lo", C.c_double),
+        ("refl_hi", C.c_double), ("t60_max", C.c_double), ("t60_lo", C.c_double), ("t60_hi", C.c_double),
+        ("snr_lo", C.c_double), ("snr_hi", C.c_double), ("mic_spacing", C.c_double),
+        ("mic_radius", C.c_double), ("clearance", C.c_double), ("sec_lo", C.c_double),
+        ("sec_hi", C.c_double), ("fs", C.c_double), ("c0", C.c_double), ("signal_std", C.c_double),
+        ("num_noises", C.c_int32), ("mic_count", C.c_int32), ("n_weights", C.c_int32), ("pad_", C.c_int32),
+        ("weights", C.c_double * 8),
+    ]
 
 _lib = None
 
@@ -142,6 +156,12 @@ def load_library() -> C.CDLL:
         "rs_render_batch_device": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
         "rs_last_pair_signal": (C.c_int, [vp, i64, vp, sz, szp]),
         "rs_last_pair_rir": (C.c_int, [vp, i64, vp, sz, szp]),
+        "rs_sampler_counts": (C.c_int, [vp, C.c_uint64, i64, i64, i64, vp]),
+        "rs_sample_scenes": (C.c_int, [vp, C.c_uint64, i64, i64, i64] + [vp] * 9),
+        "rs_sampler_counts_device": (C.c_int, [vp, C.c_uint64, i64, i64, i64, vp, vp]),
+        "rs_sample_scenes_device": (C.c_int, [vp, C.c_uint64, i64, i64, i64] + [vp] * 10),
+        "rs_generate_signals_host": (C.c_int, [vp, C.c_uint64, i64, i64, vp, vp, vp, vp, vp]),
+        "rs_generate_signals": (C.c_int, [vp, C.c_uint64, i64, i64, vp, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -418,3 +438,75 @@ def last_pair_rir(pair: int, cap: int, ctx: Optional[Context] = None) -> np.ndar
     n = C.c_size_t()
     _check(load_library().rs_last_pair_rir(ctx.h, int(pair), _ptr(out), cap, C.byref(n)))
     return out[: n.value]
+
+
+# ---- scene sampler and signal generator ----------
+def sampler_spec(spec, *, weights=None, signal_std: float = 0.1, fs: float = 16000.0,
+                 c0: float = 343.0) -> RsSamplerSpec:
+    """An rs_sampler_spec from a ``scenes.SamplerSpec`` (``weights``: categorical
+    noise-count weights over 0..len-1 noises; None keeps ``spec.num_noises`` fixed)."""
+    s = RsSamplerSpec()
+    s.dim_lo[:] = list(spec.dim_lo)
+    s.dim_hi[:] = list(spec.dim_hi)
+    s.refl_lo, s.refl_hi = spec.refl_range
+    s.t60_max = spec.t60_max
+    s.t60_lo, s.t60_hi = spec.t60_range if spec.t60_range is not None else (0.0, 0.0)
+    s.snr_lo, s.snr_hi = spec.snr_range_db
+    s.mic_spacing, s.mic_radius, s.clearance = spec.mic_spacing, spec.mic_radius, spec.min_wall_clearance
+    s.sec_lo, s.sec_hi = spec.seconds_range
+    s.fs, s.c0, s.signal_std = fs, c0, signal_std
+    s.num_noises, s.mic_count = spec.num_noises, spec.mic_count
+    w = list(weights or [])
+    s.n_weights = len(w)
+    s.weights[: len(w)] = w
+    return s
+
+
+def sample_batch(spec: RsSamplerSpec, n_utt: int, *, seed: int, first_utt: int = 0, epoch: int = 0,
+                 eta_db: float = 0.0, plan_rule: int = 0, forced_fft_size: int = 0):
+    """Scenes of utterances first_utt.. from the library's host sampler (the fixture
+    generator) as a ``scenes.SceneBatch`` without signals."""
+    from . import scenes as sc
+
+    L = load_library()
+    I = np.zeros(n_utt, np.int32)
+    _check(L.rs_sampler_counts(C.byref(spec), seed, first_utt, n_utt, epoch, _ptr(I)))
+    src_begin = np.concatenate([[0], np.cumsum(I)]).astype(np.int64)
+    n_src, J = int(src_begin[-1]), int(spec.mic_count)
+    room = np.zeros((n_utt, 3)); refl = np.zeros(n_utt); order = np.zeros(n_utt, np.int32)
+    taps = np.zeros(n_utt, np.int64); src = np.zeros((n_src, 3)); mic = np.zeros((n_utt * J, 3))
+    snr = np.zeros(n_src); nx = np.zeros(n_utt, np.int64)
+    _check(L.rs_sample_scenes(C.byref(spec), seed, first_utt, n_utt, epoch, _ptr(src_begin), _ptr(room),
+                              _ptr(refl), _ptr(order), _ptr(taps), _ptr(src), _ptr(mic), _ptr(snr), _ptr(nx)))
+    sig_len = np.repeat(nx, I).astype(np.int64)
+    return sc.SceneBatch(
+        src_begin=src_begin, mic_begin=(np.arange(n_utt + 1) * J).astype(np.int64), room_dims=room,
+        reflection=refl, sample_rate=np.full(n_utt, spec.fs), speed_of_sound=np.full(n_utt, spec.c0),
+        image_order=order, max_taps=taps, src_pos=src, mic_pos=mic, snr_db=snr,
+        sig_off=np.concatenate([[0], np.cumsum(sig_len)[:-1]]).astype(np.int64), sig_len=sig_len,
+        signals=None, eta_db=eta_db, plan_rule=plan_rule, forced_fft_size=forced_fft_size, seed=seed)
+
+
+def _signal_meta(batch, first_utt: int):
+    I = np.diff(batch.src_begin)
+    utt = (np.repeat(np.arange(batch.n_utt), I) + first_utt).astype(np.int64)
+    local = (np.arange(batch.n_src) - np.repeat(batch.src_begin[:-1], I)).astype(np.int32)
+    return utt, local
+
+
+def generate_signals(spec: RsSamplerSpec, batch, *, seed: int, first_utt: int = 0, epoch: int = 0,
+                     device_ptr: Optional[int] = None, stream: int = 0) -> Optional[np.ndarray]:
+    """Synthetic N(0, std^2) source signals of ``batch``: on the host (returns the array)
+    or straight into device memory at ``device_ptr`` (returns None)."""
+    L = load_library()
+    utt, local = _signal_meta(batch, first_utt)
+    off = np.ascontiguousarray(batch.sig_off, np.int64)
+    ln = np.ascontiguousarray(batch.sig_len, np.int64)
+    if device_ptr is None:
+        out = np.zeros(max(batch.total_samples, 1), np.float32)
+        _check(L.rs_generate_signals_host(C.byref(spec), seed, epoch, batch.n_src, _ptr(utt), _ptr(local),
+                                          _ptr(off), _ptr(ln), _ptr(out)))
+        return out
+    _check(L.rs_generate_signals(C.byref(spec), seed, epoch, batch.n_src, _ptr(utt), _ptr(local), _ptr(off),
+                                 _ptr(ln), device_ptr, stream or None))
+    return None
