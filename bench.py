@@ -263,6 +263,39 @@ def ours(args, rank, world, local_rank):
                "ms_per_step": float(te[0])}
         batch.signals = None
 
+    # ---- epoch loop: source signals generated in HBM (rs_generate_signals, SURVEY.md §8f
+    # row 1) + the render, per step; no host staging of the 12.6 GB of inputs ----------------
+    epoch_loop = None
+    if not args.no_e2e and args.config != "config1":
+        spec = roomsim.sampler_spec(getattr(scenes, "spec_" + args.config)(args.seed))
+        gen_ms = 0.0
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        def epoch_step(ep):
+            g0.record(stream)
+            roomsim.generate_signals(spec, batch, seed=args.seed, epoch=ep, first_utt=rank * n_cfg,
+                                     device_ptr=signals.data_ptr(), stream=stream.cuda_stream)
+            g1.record(stream)
+            return step()
+        epoch_step(0)
+        barrier()
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for k in range(args.steps):
+            epoch_step(k + 1)
+            torch.cuda.synchronize(dev)
+            gen_ms += g0.elapsed_time(g1)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms_ep = e0.elapsed_time(e1) / args.steps
+        te = torch.tensor([ms_ep], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        epoch_loop = {"value": total_audio / (float(te[0]) / 1e3), "unit": UNIT, "ms_per_step": float(te[0]),
+                      "signal_gen_ms": gen_ms / args.steps,
+                      "what": "per step: N(0, 0.1) source signals generated in HBM by rs_generate_signals "
+                              "(Philox, bit-exact with the host fixture generator) + rs_render_batch_device; "
+                              "scene metadata from the host sampler; no host<->device staging of samples"}
+
     # ---- roofline of the OLA filter kernels (K4) -------------------------------------
     props = torch.cuda.get_device_properties(dev)
     peaks = {}
@@ -320,7 +353,7 @@ def ours(args, rank, world, local_rank):
                        "eta_db": batch.eta_db, "fft_rule": {0: "choose_plan", 1: f"forced {batch.forced_fft_size}",
                                                              2: "bit_ceil(2*N_h)"}[batch.plan_rule],
                        "l2": "inputs (%.1f GB/GPU) >> L2 (126 MB): no flush needed" % (4 * batch.total_samples / 1e9)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "epoch_loop": epoch_loop,
             "gpu_launches": launches, "clocks": clocks,
             "stage_ms": {k: round(v, 3) for k, v in stages.items()},
         }

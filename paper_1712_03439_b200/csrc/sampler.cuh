@@ -27,6 +27,12 @@ namespace rsg {
 #define RS_SQRT(a) __dsqrt_rn(a)
 #define RS_FLOOR(a) floor(a)
 #define RS_CEIL(a) ceil(a)
+#define RF_ADD(a, b) __fadd_rn((a), (b))
+#define RF_SUB(a, b) __fsub_rn((a), (b))
+#define RF_MUL(a, b) __fmul_rn((a), (b))
+#define RF_DIV(a, b) __fdiv_rn((a), (b))
+#define RF_SQRT(a) __fsqrt_rn(a)
+#define RF_FLOOR(a) floorf(a)
 #else
 #define RSH __host__ __device__ inline
 #define RS_ADD(a, b) ((a) + (b))
@@ -36,6 +42,12 @@ namespace rsg {
 #define RS_SQRT(a) std::sqrt(a)
 #define RS_FLOOR(a) std::floor(a)
 #define RS_CEIL(a) std::ceil(a)
+#define RF_ADD(a, b) ((a) + (b))
+#define RF_SUB(a, b) ((a) - (b))
+#define RF_MUL(a, b) ((a) * (b))
+#define RF_DIV(a, b) ((a) / (b))
+#define RF_SQRT(a) std::sqrt(a)
+#define RF_FLOOR(a) std::floor(a)
 #endif
 
 // ---- Philox4x32-10 -----------------------------------------------------------------
@@ -294,15 +306,63 @@ RSH SceneOut sampler_scene(const SamplerSpecD& sp, uint64_t seed, uint64_t utt, 
   return o;
 }
 
-// Samples 2p, 2p+1 of source `src_local` of utterance `utt`: N(0, std) by Box-Muller.
+// ---- FP32 restatements for the signal generator (same construction, fewer terms) ----
+RSH float plogf_(float x) {  // x in (0, 1]
+  uint32_t b;
+  memcpy(&b, &x, 4);
+  int e = static_cast<int>((b >> 23) & 0xff) - 127;
+  b = (b & 0x007FFFFFu) | 0x3F800000u;
+  float m;
+  memcpy(&m, &b, 4);
+  if (m > 1.41421356f) {
+    m = RF_MUL(m, 0.5f);
+    e += 1;
+  }
+  const float s = RF_DIV(RF_SUB(m, 1.0f), RF_ADD(m, 1.0f));
+  const float s2 = RF_MUL(s, s);
+  float p = 1.0f / 11.0f;
+  p = RF_ADD(1.0f / 9.0f, RF_MUL(s2, p));
+  p = RF_ADD(1.0f / 7.0f, RF_MUL(s2, p));
+  p = RF_ADD(1.0f / 5.0f, RF_MUL(s2, p));
+  p = RF_ADD(1.0f / 3.0f, RF_MUL(s2, p));
+  p = RF_ADD(1.0f, RF_MUL(s2, p));
+  const float ed = static_cast<float>(e);
+  return RF_ADD(RF_MUL(ed, 0.693147182f), RF_MUL(RF_MUL(2.0f, s), p));
+}
+
+RSH void psincosf_(float x, float* sn, float* cs) {  // x in [0, 2 pi)
+  const float k = RF_FLOOR(RF_ADD(RF_MUL(x, 0.636619772f), 0.5f));
+  const float r = RF_SUB(RF_SUB(x, RF_MUL(k, 1.5703125f)), RF_MUL(k, 4.83826794e-4f));  // pi/2 = hi + lo
+  const float r2 = RF_MUL(r, r);
+  float s = 1.0f / 362880.0f;
+  s = RF_ADD(-1.0f / 5040.0f, RF_MUL(r2, s));
+  s = RF_ADD(1.0f / 120.0f, RF_MUL(r2, s));
+  s = RF_ADD(-1.0f / 6.0f, RF_MUL(r2, s));
+  s = RF_ADD(r, RF_MUL(RF_MUL(r, r2), s));
+  float c = 1.0f / 3628800.0f;
+  c = RF_ADD(-1.0f / 40320.0f, RF_MUL(r2, c));
+  c = RF_ADD(1.0f / 720.0f, RF_MUL(r2, c));
+  c = RF_ADD(-1.0f / 24.0f, RF_MUL(r2, c));
+  c = RF_ADD(0.5f, RF_MUL(r2, c));  // 1/2 - r^2 (1/24 - ...)
+  c = RF_SUB(1.0f, RF_MUL(r2, c));
+  const int q = static_cast<int>(k) & 3;
+  *sn = q == 0 ? s : (q == 1 ? c : (q == 2 ? -s : -c));
+  *cs = q == 0 ? c : (q == 1 ? -s : (q == 2 ? -c : s));
+}
+
+// Samples 2p, 2p+1 of a source stream: N(0, std) by Box-Muller in FP32 from two 24-bit
+// uniforms (counter p of the stream's Philox sequence).
 RSH void signal_pair(const SamplerSpecD& sp, const Stream& g, uint64_t p, float* z0, float* z1) {
-  double u0, u1;
-  g.pair_at(p, &u0, &u1);
-  const double r = RS_SQRT(RS_MUL(-2.0, plog(RS_SUB(1.0, u0))));  // 1 - u0 in (0, 1]
-  double sn, cs;
-  psincos(RS_MUL(RS_MUL(2.0, kPi), u1), &sn, &cs);
-  *z0 = static_cast<float>(RS_MUL(sp.signal_std, RS_MUL(r, cs)));
-  *z1 = static_cast<float>(RS_MUL(sp.signal_std, RS_MUL(r, sn)));
+  const U4 w = philox4x32_10(U4{static_cast<uint32_t>(p), static_cast<uint32_t>(p >> 32), g.tag, 0x51A1u},
+                             g.k0, g.k1);
+  const float u0 = static_cast<float>(w.x >> 8) * 0x1.0p-24f;  // exact, [0, 1)
+  const float u1 = static_cast<float>(w.y >> 8) * 0x1.0p-24f;
+  const float r = RF_SQRT(RF_MUL(-2.0f, plogf_(RF_SUB(1.0f, u0))));  // 1 - u0 in (0, 1]
+  float sn, cs;
+  psincosf_(RF_MUL(6.28318548f, u1), &sn, &cs);
+  const float sd = static_cast<float>(sp.signal_std);
+  *z0 = RF_MUL(sd, RF_MUL(r, cs));
+  *z1 = RF_MUL(sd, RF_MUL(r, sn));
 }
 
 }  // namespace rsg

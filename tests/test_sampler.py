@@ -100,6 +100,10 @@ def test_signals_moments_and_determinism():
     k = float(((x.astype(np.float64) / x.std()) ** 4).mean())
     assert abs(k - 3.0) < 0.05  # Gaussian kurtosis
     assert np.array_equal(x, rs.generate_signals(sp, b, seed=4))
+    from scipy import stats
+
+    ks = stats.kstest(x[:1_000_000].astype(np.float64) / 0.1, "norm")
+    assert ks.statistic < 1.95 / math.sqrt(1_000_000)  # KS at the 0.1% level
     # one source's samples do not depend on the batch it is generated in
     c = b.subset([3])
     y = rs.generate_signals(sp, c, seed=4, first_utt=3)
