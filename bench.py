@@ -296,6 +296,28 @@ def ours(args, rank, world, local_rank):
                               "(Philox, bit-exact with the host fixture generator) + rs_render_batch_device; "
                               "scene metadata from the host sampler; no host<->device staging of samples"}
 
+    # ---- log-Mel front end on the rendered channels -----------------
+    logmel = None
+    if not args.no_e2e:
+        res = step()
+        J = np.diff(batch.mic_begin)
+        ch_off = np.concatenate([batch.out_off[u] + np.arange(J[u]) * batch.out_stride[u] for u in range(batch.n_utt)])
+        ch_len = np.repeat(res.out_len, J)
+        S = np.array([roomsim.logmel_shape(int(n))[1] for n in ch_len], np.int64)
+        f_off = np.concatenate([[0], np.cumsum(S * 512)[:-1]]).astype(np.int64)
+        feat = torch.empty(max(int(S.sum()) * 512, 1), dtype=torch.float32, device=dev)
+        roomsim.logmel_device(out.data_ptr(), ch_off, ch_len, feat.data_ptr(), f_off, ctx=ctx)  # warm
+        lm_ms = 0.0
+        for _ in range(args.steps):
+            roomsim.logmel_device(out.data_ptr(), ch_off, ch_len, feat.data_ptr(), f_off, ctx=ctx)
+            lm_ms += ctx.last_timing()["ola_ms"]
+        frames = int(sum(3 * (s_ - 1) + 4 for s_ in S if s_ > 0))
+        logmel = {"ms_per_step": lm_ms / args.steps, "channels": int(ch_len.size), "frames": frames,
+                  "stacked_vectors": int(S.sum()),
+                  "frames_per_s": frames / (lm_ms / args.steps / 1e3) if lm_ms > 0 else None,
+                  "what": "128 log-Mel, 32 ms Hann / 10 ms hop, 125-7500 Hz, 4-frame stacks every 3rd "
+                          "(PAPER.md:452-460) of every rendered channel; device-timed kernel"}
+
     # ---- roofline of the OLA filter kernels (K4) -------------------------------------
     props = torch.cuda.get_device_properties(dev)
     peaks = {}
@@ -353,7 +375,7 @@ def ours(args, rank, world, local_rank):
                        "eta_db": batch.eta_db, "fft_rule": {0: "choose_plan", 1: f"forced {batch.forced_fft_size}",
                                                              2: "bit_ceil(2*N_h)"}[batch.plan_rule],
                        "l2": "inputs (%.1f GB/GPU) >> L2 (126 MB): no flush needed" % (4 * batch.total_samples / 1e9)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "epoch_loop": epoch_loop,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "epoch_loop": epoch_loop, "logmel": logmel,
             "gpu_launches": launches, "clocks": clocks,
             "stage_ms": {k: round(v, 3) for k, v in stages.items()},
         }

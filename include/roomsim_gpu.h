@@ -240,6 +240,17 @@ int rs_generate_signals(const rs_sampler_spec* spec, uint64_t seed, int64_t epoc
                         const int64_t* utt_of_src, const int32_t* src_local, const int64_t* sig_off,
                         const int64_t* sig_len, float* out_dev, void* stream);
 
+/* ---- log-Mel front end -------------------
+ * 128 log-Mel energies per 32 ms frame (512 samples, periodic Hann) every 10 ms (160
+ * samples), HTK-mel triangles 125-7500 Hz on |X|^2, ln(max(E, 1e-10)); 4 frames
+ * stacked into 512-element vectors, down-sampled by 3 (vector t = frames 3t..3t+3).
+ * For 16 kHz audio.  Channel ch: chan_len[ch] samples at wave_dev + chan_off[ch];
+ * its n_stacked vectors are written at feat_dev + feat_off[ch] (device pointers,
+ * host offset arrays). */
+int rs_logmel_shape(int64_t n_samples, int64_t* n_frames, int64_t* n_stacked);
+int rs_logmel_device(rs_ctx* ctx, const float* wave_dev, int64_t n_chan, const int64_t* chan_off,
+                     const int64_t* chan_len, float* feat_dev, const int64_t* feat_off);
+
 #ifdef __cplusplus
 }
 #endif

@@ -285,6 +285,9 @@ struct rs_ctx {
   // timing of the last render
   double ola_ms = 0, ola_flops = 0, alg_bytes = 0;
   int64_t launches = 0;
+  // log-Mel front end tables (built on first use)
+  DevBuf lm_window, lm_ptr, lm_bin, lm_w, lm_tiles;
+  bool lm_ready = false;
 };
 
 namespace {
@@ -1646,6 +1649,75 @@ int rs_last_pair_rir(rs_ctx* c, int64_t pair, double* out, size_t cap, size_t* l
   RS_CUDA(cudaStreamSynchronize(c->stream));
   RS_CUDA(cudaMemcpy(out, ch->d_rir.as<double>() + ch->pair[lp].rir_off, n * sizeof(double), cudaMemcpyDeviceToHost));
   *len = n;
+  return RS_OK;
+}
+
+// ---- log-Mel front end ----------------------
+int rs_logmel_shape(int64_t n_samples, int64_t* n_frames, int64_t* n_stacked) {
+  const int64_t F = n_samples >= 512 ? 1 + (n_samples - 512) / 160 : 0;
+  if (n_frames) *n_frames = F;
+  if (n_stacked) *n_stacked = F >= 4 ? (F - 4) / 3 + 1 : 0;
+  return RS_OK;
+}
+
+int rs_logmel_device(rs_ctx* c, const float* wave_dev, int64_t n_chan, const int64_t* chan_off,
+                     const int64_t* chan_len, float* feat_dev, const int64_t* feat_off) {
+  RS_TRY(check_ctx(c));
+  if (!c->lm_ready) {  // periodic Hann window and the HTK-mel filterbank, FP64 on the host
+    const double pi = 3.14159265358979323846;
+    std::vector<float> win(512);
+    for (int n = 0; n < 512; ++n) win[n] = static_cast<float>(0.5 - 0.5 * std::cos(2.0 * pi * n / 512.0));
+    auto mel = [](double f) { return 2595.0 * std::log10(1.0 + f / 700.0); };
+    auto hz = [](double m) { return 700.0 * (std::pow(10.0, m / 2595.0) - 1.0); };
+    const double m_lo = mel(125.0), m_hi = mel(7500.0);
+    std::vector<double> edge(130);
+    for (int i = 0; i < 130; ++i) edge[i] = hz(m_lo + (m_hi - m_lo) * i / 129.0);
+    std::vector<int32_t> ptr(129, 0), bin;
+    std::vector<float> w;
+    for (int m = 0; m < 128; ++m) {
+      for (int k = 0; k <= 256; ++k) {
+        const double f = k * 16000.0 / 512.0;
+        double v = 0.0;
+        if (f > edge[m] && f <= edge[m + 1]) v = (f - edge[m]) / (edge[m + 1] - edge[m]);
+        else if (f > edge[m + 1] && f < edge[m + 2]) v = (edge[m + 2] - f) / (edge[m + 2] - edge[m + 1]);
+        if (v > 0.0) {
+          bin.push_back(k);
+          w.push_back(static_cast<float>(v));
+        }
+      }
+      ptr[m + 1] = static_cast<int32_t>(bin.size());
+    }
+    RS_TRY(upload(c, c->lm_window, win));
+    RS_TRY(upload(c, c->lm_ptr, ptr));
+    RS_TRY(upload(c, c->lm_bin, bin));
+    RS_TRY(upload(c, c->lm_w, w));
+    c->lm_ready = true;
+  }
+  std::vector<LogMelTile> tiles;
+  for (int64_t ch = 0; ch < n_chan; ++ch) {
+    int64_t F, S;
+    rs_logmel_shape(chan_len[ch], &F, &S);
+    const int64_t used = S > 0 ? 3 * (S - 1) + 4 : 0;  // frames that reach a stacked vector
+    for (int64_t f0 = 0; f0 < used; f0 += 8)
+      tiles.push_back(LogMelTile{chan_off[ch], feat_off[ch], static_cast<int32_t>(f0),
+                                 static_cast<int32_t>(std::min<int64_t>(8, used - f0)), static_cast<int32_t>(S), 0});
+  }
+  c->launches = 0;
+  if (tiles.empty()) return RS_OK;
+  RS_TRY(upload(c, c->lm_tiles, tiles));
+  LogMelArgs a{wave_dev, feat_dev, c->lm_tiles.as<LogMelTile>(), static_cast<int32_t>(tiles.size()),
+               c->lm_window.as<float>(), c->lm_ptr.as<int32_t>(), c->lm_bin.as<int32_t>(), c->lm_w.as<float>(),
+               c->tw[8], 1e-10f};
+  if (c->profiling) RS_CUDA(cudaEventRecord(c->ev0, c->stream));
+  RS_CUDA(launch_logmel(a, c->stream));
+  if (c->profiling) RS_CUDA(cudaEventRecord(c->ev1, c->stream));
+  c->launches = 1;
+  RS_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->profiling) {
+    float ms = 0;
+    RS_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    c->ola_ms = ms;
+  }
   return RS_OK;
 }
 

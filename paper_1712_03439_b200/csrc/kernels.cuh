@@ -171,6 +171,28 @@ int ola2_tw_total(int log2n, bool rev);
 void ola2_fill_twiddles(int log2n, bool rev, float2* host);
 cudaError_t launch_ola2(int log2n, const Ola2Args& a, cudaStream_t s);
 
+// log-Mel front end (features.cu).
+struct LogMelTile {
+  int64_t wave_off;  // channel start in `wave`
+  int64_t feat_off;  // channel start in `feat` (stacked vectors of 512 floats)
+  int32_t f0, nfr;   // first frame of the tile, frames in the tile (<= 8)
+  int32_t nstack;    // stacked vectors of the channel
+  int32_t pad;
+};
+struct LogMelArgs {
+  const float* wave;
+  float* feat;
+  const LogMelTile* tiles;
+  int32_t n_tiles;
+  const float* window;    // [512] periodic Hann
+  const int32_t* mel_ptr; // [129] CSR rows of the filterbank
+  const int32_t* mel_bin;
+  const float* mel_w;
+  const float2* tw;       // Plan<256> tables
+  float log_floor;
+};
+cudaError_t launch_logmel(const LogMelArgs& a, cudaStream_t s);
+
 // Large transforms (large.cu): four-step FFT through global scratch.
 struct LargeArgs {
   const int2* units;         // (pair, block) per unit of this batch

@@ -99,7 +99,7 @@ ABI_SYMBOLS = [
     "rs_convolve_ola", "rs_convolve_full_fft", "rs_convolve", "rs_batch_num_pairs",
     "rs_render_batch", "rs_render_batch_device", "rs_last_pair_signal", "rs_last_pair_rir",
     "rs_sampler_counts", "rs_sample_scenes", "rs_sampler_counts_device", "rs_sample_scenes_device",
-    "rs_generate_signals_host", "rs_generate_signals",
+    "rs_generate_signals_host", "rs_generate_signals", "rs_logmel_shape", "rs_logmel_device",
 ]
 
 
@@ -162,6 +162,8 @@ def load_library() -> C.CDLL:
         "rs_sample_scenes_device": (C.c_int, [vp, C.c_uint64, i64, i64, i64] + [vp] * 10),
         "rs_generate_signals_host": (C.c_int, [vp, C.c_uint64, i64, i64, vp, vp, vp, vp, vp]),
         "rs_generate_signals": (C.c_int, [vp, C.c_uint64, i64, i64, vp, vp, vp, vp, vp, vp]),
+        "rs_logmel_shape": (C.c_int, [i64, C.POINTER(i64), C.POINTER(i64)]),
+        "rs_logmel_device": (C.c_int, [vp, vp, i64, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -510,3 +512,21 @@ def generate_signals(spec: RsSamplerSpec, batch, *, seed: int, first_utt: int = 
     _check(L.rs_generate_signals(C.byref(spec), seed, epoch, batch.n_src, _ptr(utt), _ptr(local), _ptr(off),
                                  _ptr(ln), device_ptr, stream or None))
     return None
+
+
+# ---- log-Mel front end ---------------------------
+def logmel_shape(n_samples: int):
+    """(frames, stacked 512-element vectors) of an n-sample 16 kHz channel."""
+    F, S = C.c_int64(), C.c_int64()
+    _check(load_library().rs_logmel_shape(int(n_samples), C.byref(F), C.byref(S)))
+    return F.value, S.value
+
+
+def logmel_device(wave_ptr: int, chan_off, chan_len, feat_ptr: int, feat_off,
+                  ctx: Optional[Context] = None) -> None:
+    """Stacked log-Mel features of device channels into device memory (see roomsim_gpu.h)."""
+    ctx = ctx or default_context()
+    co = np.ascontiguousarray(chan_off, np.int64)
+    cl = np.ascontiguousarray(chan_len, np.int64)
+    fo = np.ascontiguousarray(feat_off, np.int64)
+    _check(load_library().rs_logmel_device(ctx.h, wave_ptr, co.size, _ptr(co), _ptr(cl), feat_ptr, _ptr(fo)))

@@ -1,0 +1,53 @@
+"""log-Mel front end (features.cu) against the numpy restatement oracle/logmel.py."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(rs, ctx, chans):
+    import torch
+
+    lens = np.array([c.size for c in chans], np.int64)
+    offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+    S = np.array([rs.logmel_shape(n)[1] for n in lens], np.int64)
+    foff = np.concatenate([[0], np.cumsum(S * 512)[:-1]]).astype(np.int64)
+    wave = torch.from_numpy(np.concatenate(chans).astype(np.float32)).cuda()
+    feat = torch.full((max(int(S.sum()) * 512, 1),), float("nan"), dtype=torch.float32, device="cuda")
+    rs.logmel_device(wave.data_ptr(), offs, lens, feat.data_ptr(), foff, ctx=ctx)
+    f = feat.cpu().numpy()
+    return [f[o:o + s * 512].reshape(s, 512) for o, s in zip(foff, S)]
+
+
+def _check(got, want):
+    assert got.shape == want.shape
+    if got.size == 0:
+        return
+    assert np.isfinite(got).all()
+    live = want > np.log(1e-6)  # filters with energy: log agreement
+    assert np.abs(got - want)[live].max() <= 2e-3
+    dead = want <= np.log(1e-8)  # empty filters sit on the floor
+    if dead.any():
+        assert np.abs(got - want)[dead].max() <= 1.0
+
+
+def test_logmel_random_channels(rs, ctx):
+    from oracle import logmel as L
+
+    rng = np.random.default_rng(3)
+    chans = [rng.standard_normal(n) * 0.1 for n in (512, 511, 1000, 16000, 48017, 160 * 9 + 512)]
+    chans.append(np.sin(2 * np.pi * 1000.0 * np.arange(16000) / 16000.0))  # a 1 kHz tone
+    for g, x in zip(_run(rs, ctx, chans), chans):
+        _check(g, L.logmel(x.astype(np.float32)))
+
+
+def test_logmel_of_a_render(rs, ctx, port):
+    from oracle import logmel as L
+    from paper_1712_03439_b200 import scenes
+
+    b = scenes.config3(n_utt=2, seed=41)
+    g = rs.render_batch(b, ctx=ctx)
+    chans = [b.channel(g.out, u, j, g.out_len[u]).copy() for u in range(b.n_utt) for j in range(2)]
+    for got, x in zip(_run(rs, ctx, chans), chans):
+        _check(got, L.logmel(x))
+    assert rs.logmel_shape(100)[1] == 0 and rs.logmel_shape(512 + 3 * 160)[1] == 1
