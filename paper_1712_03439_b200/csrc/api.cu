@@ -845,7 +845,7 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
       }
   }
   ch.P = static_cast<int64_t>(ch.pair.size());
-  // K1 launch classes: (threads, slice size).  Small lattices (K <= 7) use
+  // K1 launch classes: (threads, slice size).  Small lattices (K <= 12) use
   // 128-thread CTAs; slices are grouped so the dynamic smem fits the class.
   static const int kClass[3] = {2048, 6144, kSynthSlice};
   std::vector<SynthItem> cls[2][3];
@@ -853,7 +853,7 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
     if (ch.place_err[p]) continue;
     const int64_t cap = ch.pair[p].rir_cap;
     const int K = ch.utt[ch.pair[p].utt].order;
-    const int small = K <= 7 ? 1 : 0;
+    const int small = K <= 12 ? 1 : 0;  // measured crossover of the 128- and 512-thread K1
     for (int64_t lo = 0; lo < cap; lo += kSynthSlice) {
       const int64_t len = std::min<int64_t>(kSynthSlice, cap - lo);
       const int k = len <= kClass[0] ? 0 : (len <= kClass[1] ? 1 : 2);

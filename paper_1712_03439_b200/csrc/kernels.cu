@@ -51,12 +51,16 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
-template <int NT>
+// IPT = images per thread per chunk (4 measured best; 2 where 4 would cost occupancy)
+template <int NT, int IPT>
 __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_cap) {
   extern __shared__ __align__(16) unsigned char sm[];
-  constexpr int NW = NT / 32;  // compute warps per chunk = owner warps
+  constexpr int NW = NT / 32;  // warps = owner warps
+  constexpr int CH = IPT * NT;  // images per chunk: IPT x NW "virtual warps" of 32, in order
+  constexpr int NV = IPT * NW;  // virtual warps per chunk
   static_assert(NW >= 2 && NW <= 32 && (NW & (NW - 1)) == 0, "power-of-two warp count");
   constexpr int OB = NW == 2 ? 1 : NW == 4 ? 2 : NW == 8 ? 3 : NW == 16 ? 4 : 5;  // owner bits
+  constexpr int NQ = (NV + 3) / 4;  // 4-byte words per owner's count row
   const SynthItem it = a.items[blockIdx.x];
   const PairMeta& pm = a.pair[it.pair];
   const UttMeta& um = a.utt[pm.utt];
@@ -65,10 +69,10 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   double* bins = reinterpret_cast<double*>(sm);
   double* ax = bins + slice_cap;                 // [3][W] squared per-axis offsets
   double* rg = ax + 3 * W;                       // [3K+1]
-  double* ent_a = rg + (3 * K + 1);              // [NT] owner-major sorted amplitudes
-  int* ent_d = reinterpret_cast<int*>(ent_a + NT);           // [NT] their bins
-  // [NW owner][NW compute] entry counts, one byte each (<= 32), 16-byte aligned rows
-  unsigned char* cnt8 = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(ent_d + NT) + 15) & ~uintptr_t(15));
+  double* ent_a = rg + (3 * K + 1);              // [CH] owner-major sorted amplitudes
+  int* ent_d = reinterpret_cast<int*>(ent_a + CH);           // [CH] their bins
+  // [NW owner][NV virtual warp] entry counts, one byte each (<= 32), 16-byte aligned rows
+  unsigned char* cnt8 = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(ent_d + CH) + 15) & ~uintptr_t(15));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lo = it.slice_lo, len = it.slice_len;
   for (int l = tid; l < len; l += NT) bins[l] = 0.0;
@@ -85,7 +89,7 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   __syncthreads();
 
   const long long V = static_cast<long long>(W) * W * W;
-  // image index i = (ix W + iy) W + iz, advanced incrementally by NT per chunk
+  // image index i = (ix W + iy) W + iz, advanced incrementally by NT per image slot
   int iz = tid % W, iy, ix;
   {
     const int q = tid / W;
@@ -95,80 +99,95 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   const int step_z = NT % W, step_q = NT / W;
   const int step_y = step_q % W, step_x = step_q / W;
   const unsigned lt = lanemask_lt();
-  // byte masks selecting the counts of compute warps < `warp` in each 4-byte word
-  constexpr int NQ = (NW + 3) / 4;
-  unsigned below[NQ];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    const int nb = warp - 4 * q;  // bytes of word q that belong to earlier warps
-    below[q] = nb <= 0 ? 0u : nb >= 4 ? 0xffffffffu : (1u << (8 * nb)) - 1u;
-  }
   unsigned long long max_d = 0;
   int geo = 0;
-  for (long long base = 0; base < V; base += NT) {
-    const long long i = base + tid;
-    int rel_bin = -1;
-    double amp = 0.0;
-    if (i < V) {
-      // norm: sqrt((x*x + y*y) + z*z), room_model.hpp:43
-      const double d2 = __dadd_rn(__dadd_rn(ax[ix], ax[W + iy]), ax[2 * W + iz]);
-      const double d = __dsqrt_rn(d2);
-      if (d <= 0.0) geo = 1;                     // :157-158
-      const double dl = ceil(__dmul_rn(d, spm));  // :159-160
-      const unsigned long long D = static_cast<unsigned long long>(dl);
-      max_d = D > max_d ? D : max_d;
-      const long long rel = static_cast<long long>(D) - lo;
-      if (rel >= 0 && rel < len) {
-        const int g = abs(ix - K) + abs(iy - K) + abs(iz - K);
-        amp = __ddiv_rn(rg[g], d);  // :161-162 pow(r, g) / d
-        rel_bin = static_cast<int>(rel);
+  for (long long base = 0; base < V; base += CH) {
+    int rel_bin[IPT];
+    double amp[IPT];
+#pragma unroll
+    for (int h = 0; h < IPT; ++h) {  // image base + h NT + tid
+      const long long i = base + h * NT + tid;
+      rel_bin[h] = -1;
+      amp[h] = 0.0;
+      if (i < V) {
+        // norm: sqrt((x*x + y*y) + z*z), room_model.hpp:43
+        const double d2 = __dadd_rn(__dadd_rn(ax[ix], ax[W + iy]), ax[2 * W + iz]);
+        const double d = __dsqrt_rn(d2);
+        if (d <= 0.0) geo = 1;                     // :157-158
+        const double dl = ceil(__dmul_rn(d, spm));  // :159-160
+        const unsigned long long D = static_cast<unsigned long long>(dl);
+        max_d = D > max_d ? D : max_d;
+        const long long rel = static_cast<long long>(D) - lo;
+        if (rel >= 0 && rel < len) {
+          const int g = abs(ix - K) + abs(iy - K) + abs(iz - K);
+          amp[h] = __ddiv_rn(rg[g], d);  // :161-162 pow(r, g) / d
+          rel_bin[h] = static_cast<int>(rel);
+        }
       }
+      // advance (ix, iy, iz) by NT images
+      iz += step_z;
+      int cy = step_y;
+      if (iz >= W) { iz -= W; ++cy; }
+      iy += cy;
+      int cx = step_x;
+      while (iy >= W) { iy -= W; ++cx; }
+      ix += cx;
     }
-    // advance (ix, iy, iz) by NT images
-    iz += step_z;
-    int cy = step_y;
-    if (iz >= W) { iz -= W; ++cy; }
-    iy += cy;
-    int cx = step_x;
-    while (iy >= W) { iy -= W; ++cx; }
-    ix += cx;
 #ifndef RSG_X_NOSCATTER
-    // ---- publish: lane masks per owner from OB + 1 ballots ----
+    // ---- publish: per image slot, lane masks per owner from OB + 1 ballots ----
     // owner of a bin: any function of the bin keeps each bin's entries in order; mixing
     // in bin/16 spreads one owner's FP64 bins over all smem banks (bin mod NW alone
     // puts them all in one bank pair)
-    const int owner = (rel_bin ^ (rel_bin >> 4)) & (NW - 1);
-    unsigned mine = __ballot_sync(0xffffffffu, rel_bin >= 0);  // lanes sharing my owner
-    unsigned row = mine;                                        // lane o < NW: lanes owned by o
+    int owner[IPT];
+    unsigned mine[IPT];
 #pragma unroll
-    for (int k = 0; k < OB; ++k) {
-      const unsigned bk = __ballot_sync(0xffffffffu, (owner >> k) & 1);
-      mine &= ((owner >> k) & 1) ? bk : ~bk;
-      row &= ((lane >> k) & 1) ? bk : ~bk;
+    for (int h = 0; h < IPT; ++h) {
+      owner[h] = (rel_bin[h] ^ (rel_bin[h] >> 4)) & (NW - 1);
+      mine[h] = __ballot_sync(0xffffffffu, rel_bin[h] >= 0);  // lanes sharing my owner
+      unsigned row = mine[h];                                   // lane o < NW: lanes owned by o
+#pragma unroll
+      for (int k = 0; k < OB; ++k) {
+        const unsigned bk = __ballot_sync(0xffffffffu, (owner[h] >> k) & 1);
+        mine[h] &= ((owner[h] >> k) & 1) ? bk : ~bk;
+        row &= ((lane >> k) & 1) ? bk : ~bk;
+      }
+      if (lane < NW) cnt8[lane * (4 * NQ) + h * NW + warp] = static_cast<unsigned char>(__popc(row));
     }
-    if (lane < NW) cnt8[lane * (4 * NQ) + warp] = static_cast<unsigned char>(__popc(row));
     __syncthreads();
-    // ---- stable counting sort into owner-major lists ----
-    // lane o < NW: entries of owner o in warps < this one (`before`) and in all (`total`),
-    // byte sums of the owner's count row by dp4a
-    unsigned ubefore = 0u, utotal = 0u;
+    // ---- stable counting sort into owner-major lists (order: slot, warp, lane) ----
+    // lane o < NW: entries of owner o in virtual warps before slot h's (`before[h]`) and
+    // in all (`total`): byte sums of the owner's count row by dp4a
+    unsigned ub[IPT], utotal = 0u;
+#pragma unroll
+    for (int h = 0; h < IPT; ++h) ub[h] = 0u;
     if (lane < NW) {
-      unsigned rowv[NQ];
-      if constexpr (NQ == 4) {  // one 16-byte load per lane (a strided 4-byte loop is 4-way conflicted)
-        const uint4 r4 = *reinterpret_cast<const uint4*>(cnt8 + lane * 16);
-        rowv[0] = r4.x; rowv[1] = r4.y; rowv[2] = r4.z; rowv[3] = r4.w;
-      } else {
+      const unsigned* rowp = reinterpret_cast<const unsigned*>(cnt8 + lane * (4 * NQ));
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) rowv[q] = reinterpret_cast<const unsigned*>(cnt8 + lane * (4 * NQ))[q];
-      }
+      for (int q4 = 0; q4 < NQ; q4 += 4) {  // 16-byte loads (a strided 4-byte loop is conflicted)
+        unsigned rv[4];
+        if (q4 + 4 <= NQ) {
+          const uint4 r4 = *reinterpret_cast<const uint4*>(rowp + q4);
+          rv[0] = r4.x; rv[1] = r4.y; rv[2] = r4.z; rv[3] = r4.w;
+        } else {
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        const unsigned wq = NW >= 4 ? rowv[q] : (rowv[0] & ((1u << (8 * NW)) - 1u));
-        utotal = __dp4a(wq, 0x01010101u, utotal);
-        ubefore = __dp4a(wq & below[q], 0x01010101u, ubefore);
+          for (int u = 0; u < 4; ++u) rv[u] = q4 + u < NQ ? rowp[q4 + u] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int q = q4 + u;
+          if (q >= NQ) break;
+          const unsigned wq = 4 * q + 4 <= NV ? rv[u] : (rv[u] & ((1u << (8 * (NV - 4 * q))) - 1u));
+          utotal = __dp4a(wq, 0x01010101u, utotal);
+#pragma unroll
+          for (int h = 0; h < IPT; ++h) {
+            const int nb = h * NW + warp - 4 * q;  // bytes of word q before this slot's virtual warp
+            const unsigned m = nb <= 0 ? 0u : nb >= 4 ? 0xffffffffu : (1u << (8 * nb)) - 1u;
+            ub[h] = __dp4a(wq & m, 0x01010101u, ub[h]);
+          }
+        }
       }
     }
-    const int before = static_cast<int>(ubefore), total = static_cast<int>(utotal);
+    const int total = static_cast<int>(utotal);
     int incl = total;  // inclusive scan of the owner totals over lanes 0..NW-1
 #pragma unroll
     for (int o = 1; o < NW; o <<= 1) {
@@ -176,11 +195,14 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
       if (lane >= o) incl += v;
     }
     const int obase = incl - total;  // list start of owner `lane`
-    const int seg = __shfl_sync(0xffffffffu, obase + before, rel_bin >= 0 ? owner : 0);
-    if (rel_bin >= 0) {
-      const int pos = seg + __popc(mine & lt);
-      ent_d[pos] = rel_bin;
-      ent_a[pos] = amp;
+#pragma unroll
+    for (int h = 0; h < IPT; ++h) {
+      const int seg = __shfl_sync(0xffffffffu, obase + static_cast<int>(ub[h]), rel_bin[h] >= 0 ? owner[h] : 0);
+      if (rel_bin[h] >= 0) {
+        const int pos = seg + __popc(mine[h] & lt);
+        ent_d[pos] = rel_bin[h];
+        ent_a[pos] = amp[h];
+      }
     }
     const int my_base = __shfl_sync(0xffffffffu, obase, warp);
     const int my_total = __shfl_sync(0xffffffffu, total, warp);
@@ -219,27 +241,26 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   }
 }
 
-size_t synth_smem_bytes(int max_order, int slice, int nt) {
-  const int W = 2 * max_order + 1, nw = nt / 32;
-  return sizeof(double) * (static_cast<size_t>(slice) + 3 * W + 3 * max_order + 1 + nt) + sizeof(int) * nt +
-         static_cast<size_t>(nw) * 4 * ((nw + 3) / 4) + 16;
+size_t synth_smem_bytes(int max_order, int slice, int nt, int ipt) {
+  const int W = 2 * max_order + 1, nw = nt / 32, ch = ipt * nt, nv = ipt * nw;
+  return sizeof(double) * (static_cast<size_t>(slice) + 3 * W + 3 * max_order + 1 + ch) + sizeof(int) * ch +
+         static_cast<size_t>(nw) * 4 * ((nv + 3) / 4) + 16 + 16;
 }
 
 cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice, cudaStream_t s,
                          int nt) {
   if (n_items == 0) return cudaSuccess;
-  const size_t smem = synth_smem_bytes(max_order, slice, nt);
-  cudaError_t e;
-  if (nt == 128) {
-    e = cudaFuncSetAttribute(rir_synth_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  // 4 images per thread unless that would drop a 512-thread CTA below 2 per SM
+  const int ipt = (nt == 512 && 2 * synth_smem_bytes(max_order, slice, nt, 4) > 227 * 1024) ? 2 : 4;
+  const size_t smem = synth_smem_bytes(max_order, slice, nt, ipt);
+  auto go = [&](auto kern, int threads) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    rir_synth_kernel<128><<<n_items, 128, smem, s>>>(a, slice);
-  } else {
-    e = cudaFuncSetAttribute(rir_synth_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    rir_synth_kernel<512><<<n_items, 512, smem, s>>>(a, slice);
-  }
-  return cudaGetLastError();
+    kern<<<n_items, threads, smem, s>>>(a, slice);
+    return cudaGetLastError();
+  };
+  if (nt == 128) return go(rir_synth_kernel<128, 4>, 128);
+  return ipt == 4 ? go(rir_synth_kernel<512, 4>, 512) : go(rir_synth_kernel<512, 2>, 512);
 }
 
 // ============================================================================

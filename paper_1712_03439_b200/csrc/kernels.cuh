@@ -231,7 +231,7 @@ cudaError_t kernels_init();    // smem attributes
 
 constexpr int kSynthThreads = 512;
 constexpr int kSynthSlice = 12288;  // FP64 bins per K1 CTA (96 KB)
-size_t synth_smem_bytes(int max_order, int slice, int nt);
+size_t synth_smem_bytes(int max_order, int slice, int nt, int ipt);
 
 // nt = 512 (16 warps) or 128 (4 warps, small lattices)
 cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice,
