@@ -285,6 +285,11 @@ struct rs_ctx {
   // timing of the last render
   double ola_ms = 0, ola_flops = 0, alg_bytes = 0;
   int64_t launches = 0;
+  // side streams: the per-size K4 launches of a chunk run concurrently (fills each
+  // launch's tail with another size's CTAs)
+  static constexpr int kSide = 4;
+  cudaStream_t side[kSide] = {};
+  cudaEvent_t side_fork = nullptr, side_join[kSide] = {};
   // log-Mel front end tables (built on first use)
   DevBuf lm_window, lm_ptr, lm_bin, lm_w, lm_tiles;
   bool lm_ready = false;
@@ -299,6 +304,11 @@ int ctx_init(rs_ctx* c) {
   RS_CUDA(cudaEventCreate(&c->ev0));
   RS_CUDA(cudaEventCreate(&c->ev1));
   for (auto& e : c->st) RS_CUDA(cudaEventCreate(&e));
+  for (int i = 0; i < rs_ctx::kSide; ++i) {
+    RS_CUDA(cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking));
+    RS_CUDA(cudaEventCreateWithFlags(&c->side_join[i], cudaEventDisableTiming));
+  }
+  RS_CUDA(cudaEventCreateWithFlags(&c->side_fork, cudaEventDisableTiming));
   RS_CUDA(kernels_init());
   size_t total = 0;
   size_t off[kMaxLog2M + 1], off2[kOla2MaxLog2N + 1][2] = {};
@@ -612,6 +622,21 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
     ++c->launches;
   }
   if (ev_k4a) RS_CUDA(cudaEventRecord(ev_k4a, st));
+  // fork: each size's K4 launch on its own side stream (the four-step batches share one
+  // scratch, so they stay in order on one stream), joined back into `st` below
+  RS_CUDA(cudaEventRecord(c->side_fork, st));
+  bool used[rs_ctx::kSide] = {};
+  int next_side = 0;
+  auto side_for = [&](bool fresh) -> cudaStream_t {
+    static_cast<void>(fresh);
+    const int i = next_side++ % rs_ctx::kSide;
+    if (!used[i]) {
+      cudaStreamWaitEvent(c->side[i], c->side_fork, 0);
+      used[i] = true;
+    }
+    return c->side[i];
+  };
+  cudaStream_t large_st = fp.batches.empty() ? st : side_for(true);
   for (const LargeBatch& bt : fp.batches) {
     const Span& sp = fp.spans[bt.span];
     int l1, l2;
@@ -623,7 +648,7 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
                 fb.olaitems.as<OlaItem>() + bt.item_lo, static_cast<int32_t>(bt.item_hi - bt.item_lo),
                 c->tw[l1], c->tw[l2]};
     for (int stage = 0; stage < 6; ++stage) {
-      RS_CUDA(launch_large(sp.l, a, stage, st));
+      RS_CUDA(launch_large(sp.l, a, stage, large_st));
       ++c->launches;
     }
   }
@@ -640,7 +665,7 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
                fb.part.as<double>() + fp.items.size() + sp.item_off, c->tw2f[sp.l + 1], c->tw2i[sp.l + 1],
                static_cast<int32_t>((std::max<int64_t>(max_nh - 1, 1) + 3) & ~int64_t(3)),
                static_cast<int32_t>((max_l + 8 + 3) & ~int64_t(3))};
-    RS_CUDA(launch_ola2(sp.l + 1, a, st));
+    RS_CUDA(launch_ola2(sp.l + 1, a, side_for(false)));
     ++c->launches;
   }
   for (const Span& sp : fp.spans) {
@@ -648,9 +673,14 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
     OlaArgs a{fb.olaitems.as<OlaItem>() + sp.item_off, static_cast<int32_t>(sp.item_n), d_pair,
               fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(),
               fb.part.as<double>() + sp.item_off, c->tw[sp.l]};
-    RS_CUDA(launch_ola(sp.l, a, st));
+    RS_CUDA(launch_ola(sp.l, a, side_for(false)));
     ++c->launches;
   }
+  for (int i = 0; i < rs_ctx::kSide; ++i)  // join
+    if (used[i]) {
+      RS_CUDA(cudaEventRecord(c->side_join[i], c->side[i]));
+      RS_CUDA(cudaStreamWaitEvent(st, c->side_join[i], 0));
+    }
   if (ev_k4b) RS_CUDA(cudaEventRecord(ev_k4b, st));
   return RS_OK;
 }
@@ -1369,6 +1399,11 @@ int rs_ctx_destroy(rs_ctx* c) {
                     &c->scratch_a, &c->scratch_b};
   for (DevBuf* b : bufs) b->release();
   destroy_state(c);
+  for (int i = 0; i < rs_ctx::kSide; ++i) {
+    if (c->side[i]) cudaStreamDestroy(c->side[i]);
+    if (c->side_join[i]) cudaEventDestroy(c->side_join[i]);
+  }
+  if (c->side_fork) cudaEventDestroy(c->side_fork);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   for (auto& e : c->st)
