@@ -230,7 +230,7 @@ void fill_twiddles(int log2m, float2* host);  // host, FP64 -> FP32
 cudaError_t kernels_init();    // smem attributes
 
 constexpr int kSynthThreads = 512;
-constexpr int kSynthSlice = 12288;  // FP64 bins per K1 CTA (96 KB)
+constexpr int kSynthSlice = 10240;  // FP64 bins per K1 CTA (80 KB: two 512-thread CTAs per SM with 4 images/thread)
 size_t synth_smem_bytes(int max_order, int slice, int nt, int ipt);
 
 // nt = 512 (16 warps) or 128 (4 warps, small lattices)
