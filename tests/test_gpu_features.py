@@ -51,3 +51,17 @@ def test_logmel_of_a_render(rs, ctx, port):
     for got, x in zip(_run(rs, ctx, chans), chans):
         _check(got, L.logmel(x))
     assert rs.logmel_shape(100)[1] == 0 and rs.logmel_shape(512 + 3 * 160)[1] == 1
+
+
+def test_render_to_wav_roundtrip(rs, ctx, tmp_path):
+    from paper_1712_03439_b200 import audio_io as aio
+    from paper_1712_03439_b200 import scenes
+
+    b = scenes.config3(n_utt=2, seed=43)
+    g = rs.render_batch(b, ctx=ctx)
+    paths = aio.write_render(b, g, str(tmp_path / "utt"), "float32")
+    for u, p in enumerate(paths):
+        x, fs = aio.read_wav(p, expect_rate=16000)
+        assert x.shape == (2, g.out_len[u])
+        for j in range(2):
+            assert np.array_equal(x[j].astype(np.float32), b.channel(g.out, u, j, g.out_len[u]))
