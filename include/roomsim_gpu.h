@@ -90,7 +90,8 @@ int rs_choose_plan(double num_sources, double num_mics, size_t nx, size_t nh,
                    int* strategy_out, size_t* fft_size_out, double* cost_out);
 
 /* ---- RealFftEngine seam (fft.hpp:38-49, RadixTwoRealFft fft.hpp:57-169) ---
- * Batch of `count` transforms of size n (power of two, 2 <= n <= 32768).
+ * Batch of `count` transforms of size n (power of two, 2 <= n <= 2^23; n > 32768 runs
+ * through the four-step stages).
  * forward: in [count][n] reals -> out [count][n/2+1] complex (re,im
  * interleaved), unnormalized.  inverse: includes 1/N (fft.hpp:33-36).
  * Host pointers; FP32 arithmetic on the device.                             */

@@ -1471,10 +1471,11 @@ int rs_choose_plan(double I, double J, size_t nx, size_t nh, int* s, size_t* n, 
 static int rfft_common(rs_ctx* c, size_t n, size_t count, const double* in, double* out, bool inverse) {
   RS_TRY(check_ctx(c));
   if (n < 2 || !has_single_bit(n)) return fail(RS_ERR_PLAN, "FFT size must be a power of two >= 2");
-  if (n > (static_cast<size_t>(2) << kMaxLog2M))
+  if (n > (static_cast<size_t>(2) << kLargeMaxLog2M))
     return fail(RS_ERR_UNSUPPORTED, "FFT size " + std::to_string(n) + " not supported by the device kernels");
   if (count == 0) return RS_OK;
   const int l = log2_exact(n) - 1;
+  const bool large = l > kMaxLog2M;  // four-step stages (large.cu)
   const size_t M = n / 2;
   const size_t nin = count * (inverse ? 2 * (M + 1) : n);
   const size_t nout = count * (inverse ? n : 2 * (M + 1));
@@ -1483,7 +1484,16 @@ static int rfft_common(rs_ctx* c, size_t n, size_t count, const double* in, doub
   RS_TRY(c->sig.ensure(nout * sizeof(float)));
   RS_CUDA(cudaMemcpyAsync(c->scratch_a.p, in, nin * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   RS_CUDA(launch_convert_d2f(c->scratch_a.as<double>(), c->scratch_b.as<float>(), static_cast<int64_t>(nin), c->stream));
-  if (inverse)
+  if (large) {
+    int l1, l2;
+    large_split(l, &l1, &l2);
+    RS_TRY(state_init(c));
+    FilterBufs& fb = c->rs->conv;
+    RS_TRY(fb.scratch.ensure(count * M * sizeof(float2)));
+    RS_CUDA(launch_large_rfft(l, inverse, c->scratch_b.as<float>(), reinterpret_cast<const float2*>(c->scratch_b.p),
+                              c->sig.as<float>(), reinterpret_cast<float2*>(c->sig.p), static_cast<int>(count),
+                              fb.scratch.as<float2>(), c->tw[l1], c->tw[l2], c->stream));
+  } else if (inverse)
     RS_CUDA(launch_rfft(l, true, nullptr, reinterpret_cast<const float2*>(c->scratch_b.p), c->sig.as<float>(),
                         nullptr, static_cast<int>(count), c->tw[l], c->stream));
   else

@@ -218,6 +218,11 @@ void large_split(int log2m, int* l1, int* l2);
 int large_tile();
 // stage: 0/1 spectrum (cols, rows), 2 cols fwd, 3 rows, 4 cols inv, 5 overlap-add
 cudaError_t launch_large(int log2m, const LargeArgs& a, int stage, cudaStream_t s);
+// RealFftEngine seam for M = N/2 >= 8192: natural-order spectra through the same four-step
+// stages; `scratch` holds count * M complex
+cudaError_t launch_large_rfft(int log2m, bool inverse, const float* in_real, const float2* in_spec,
+                              float* out_real, float2* out_spec, int count, float2* scratch,
+                              const float2* tw1, const float2* tw2, cudaStream_t s);
 
 // ---- launchers (kernels.cu) --------------------------------------------------
 constexpr int kMaxLog2M = 14;  // M <= 16384  (N <= 32768) in one CTA

@@ -280,6 +280,165 @@ cudaError_t large_launch(const LargeArgs& a, int stage, cudaStream_t s) {
 
 }  // namespace
 
+// ---- the RealFftEngine seam (fft.hpp:38-49) for large N: natural-order spectra ------
+namespace {
+
+// forward stage A: column FFTs of the packed real input (no zero padding)
+template <int M1, int M2>
+__global__ void __launch_bounds__(col_tile<M1, M2>() * Plan<M1>::T)
+rfft_cols_fwd(const float* in, float2* scratch, const float2* tw1) {
+  using P1 = Plan<M1>;
+  constexpr int CT = col_tile<M1, M2>(), NT = CT * P1::T, TILES = M2 / CT;
+  constexpr int LOGM = P1::LOG + Plan<M2>::LOG;
+  constexpr long long M = static_cast<long long>(M1) * M2;
+  extern __shared__ __align__(16) float2 smem[];
+  const int item = blockIdx.x / TILES, c0 = (blockIdx.x % TILES) * CT;
+  const float2* z = reinterpret_cast<const float2*>(in + item * 2 * M);
+  for (int idx = threadIdx.x; idx < M1 * CT; idx += NT) {
+    const int n1 = idx / CT, c = idx - n1 * CT;
+    smem[c * P1::PADDED + PAD(n1)] = z[static_cast<long long>(n1) * M2 + c0 + c];
+  }
+  __syncthreads();
+  forward_rest<M1, 0>(smem + (threadIdx.x / P1::T) * P1::PADDED, threadIdx.x % P1::T, tw1, true);
+  float2* dst = scratch + item * M;
+  for (int idx = threadIdx.x; idx < M1 * CT; idx += NT) {
+    const int k1 = idx / CT, cc = idx - k1 * CT;
+    dst[static_cast<long long>(k1) * M2 + c0 + cc] = c_mul(smem[cc * P1::PADDED + PAD(k1)], twiddle_m((c0 + cc) * k1, LOGM));
+  }
+}
+
+// forward stage B: row FFTs of rows k1, M1 - k1, untangle into X[k] (natural order, N/2 + 1)
+template <int M1, int M2>
+__global__ void __launch_bounds__(2 * Plan<M2>::T) rfft_rows_fwd(const float2* scratch, float2* out, const float2* tw2) {
+  using P2 = Plan<M2>;
+  constexpr int T = P2::T, JOBS = M1 / 2 + 1;
+  constexpr int LOGM = Plan<M1>::LOG + P2::LOG;
+  constexpr long long M = static_cast<long long>(M1) * M2;
+  extern __shared__ __align__(16) float2 smem[];
+  const int item = blockIdx.x / JOBS, job = blockIdx.x % JOBS;
+  const bool self = job == 0 || job == M1 / 2;
+  const int row0 = job, row1 = (M1 - job) & (M1 - 1);
+  const int g = threadIdx.x / T, t = threadIdx.x % T;
+  const bool active = g == 0 || !self;
+  float2* s = smem + g * P2::PADDED;
+  const float2* src = scratch + item * M + static_cast<long long>(g ? row1 : row0) * M2;
+  if (active)
+    for (int n2 = t; n2 < M2; n2 += T) s[PAD(n2)] = src[n2];
+  __syncthreads();
+  forward_rest<M2, 0>(s, t, tw2, active);
+  float2* s0 = smem;
+  float2* s1 = self ? smem : smem + P2::PADDED;
+  auto partner = [&](int k2) { return job == 0 ? ((M2 - k2) & (M2 - 1)) : (M2 - 1 - k2); };
+  float2* o = out + item * (M + 1);
+  for (int e = threadIdx.x; e < 2 * M2; e += 2 * T) {
+    const int gg = e / M2, k2 = e - gg * M2;
+    if (gg == 1 && self) continue;
+    const int rk = gg ? row1 : row0;
+    const int k = rk + M1 * k2;
+    const float2 za = (gg ? s1 : s0)[PAD(k2)];
+    const float2 zb = c_conj((gg ? s0 : s1)[PAD(partner(k2))]);
+    const float2 S = c_add(za, zb);
+    const float2 D = c_rot<false>(c_sub(za, zb));
+    o[k] = c_scale(c_add(S, c_mul(twiddle_n(k, LOGM), D)), 0.5f);
+    if (k == 0) o[M] = c_scale(c_sub(S, D), 0.5f);  // W^M = -1
+  }
+}
+
+// inverse stage B: repack row k1 of the spectrum (fft.hpp:104-110), inverse row FFT,
+// conj twiddles -> scratch
+template <int M1, int M2>
+__global__ void __launch_bounds__(Plan<M2>::T) rfft_rows_inv(const float2* in, float2* scratch, const float2* tw2) {
+  using P2 = Plan<M2>;
+  constexpr int T = P2::T;
+  constexpr int LOGM = Plan<M1>::LOG + P2::LOG;
+  constexpr long long M = static_cast<long long>(M1) * M2;
+  extern __shared__ __align__(16) float2 smem[];
+  const int item = blockIdx.x / M1, row = blockIdx.x % M1;
+  const int t = threadIdx.x;
+  const float2* X = in + item * (M + 1);
+  for (int k2 = t; k2 < M2; k2 += T) {
+    const long long k = row + static_cast<long long>(M1) * k2;
+    const float2 xa = X[k], xb = c_conj(X[M - k]);
+    const float2 e = c_scale(c_add(xa, xb), 0.5f);
+    const float2 o = c_mulc(c_scale(c_sub(xa, xb), 0.5f), twiddle_n(static_cast<int>(k), LOGM));
+    smem[PAD(k2)] = make_float2(e.x - o.y, e.y + o.x);
+  }
+  __syncthreads();
+  inverse_all<M2>(smem, t, tw2, true);
+  float2* dst = scratch + item * M + static_cast<long long>(row) * M2;
+  for (int n2 = t; n2 < M2; n2 += T) dst[n2] = c_mulc(smem[PAD(n2)], twiddle_m(n2 * row, LOGM));
+}
+
+// inverse stage C: inverse column FFTs -> N real samples, scaled by 1/M (fft.hpp:112-116)
+template <int M1, int M2>
+__global__ void __launch_bounds__(col_tile<M1, M2>() * Plan<M1>::T)
+rfft_cols_inv(const float2* scratch, float* out, const float2* tw1) {
+  using P1 = Plan<M1>;
+  constexpr int CT = col_tile<M1, M2>(), NT = CT * P1::T, TILES = M2 / CT;
+  constexpr long long M = static_cast<long long>(M1) * M2;
+  extern __shared__ __align__(16) float2 smem[];
+  const int item = blockIdx.x / TILES, c0 = (blockIdx.x % TILES) * CT;
+  const float2* src = scratch + item * M;
+  for (int idx = threadIdx.x; idx < M1 * CT; idx += NT) {
+    const int k1 = idx / CT, c = idx - k1 * CT;
+    smem[c * P1::PADDED + PAD(k1)] = src[static_cast<long long>(k1) * M2 + c0 + c];
+  }
+  __syncthreads();
+  inverse_all<M1>(smem + (threadIdx.x / P1::T) * P1::PADDED, threadIdx.x % P1::T, tw1, true);
+  float2* o = reinterpret_cast<float2*>(out + item * 2 * M);
+  const float sc = 1.0f / static_cast<float>(M);
+  for (int idx = threadIdx.x; idx < M1 * CT; idx += NT) {
+    const int n1 = idx / CT, cc = idx - n1 * CT;
+    o[static_cast<long long>(n1) * M2 + c0 + cc] = c_scale(smem[cc * P1::PADDED + PAD(n1)], sc);
+  }
+}
+
+template <int M1, int M2>
+cudaError_t rfft_large_t(bool inverse, const float* in_real, const float2* in_spec, float* out_real,
+                         float2* out_spec, int count, float2* scratch, const float2* tw1, const float2* tw2,
+                         cudaStream_t s) {
+  using P1 = Plan<M1>;
+  using P2 = Plan<M2>;
+  constexpr int CT = col_tile<M1, M2>(), TILES = M2 / CT;
+  const int smem_cols = CT * P1::PADDED * static_cast<int>(sizeof(float2));
+  cudaError_t e;
+  if (!inverse) {
+    if ((e = cudaFuncSetAttribute(rfft_cols_fwd<M1, M2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cols)))
+      return e;
+    rfft_cols_fwd<M1, M2><<<count * TILES, CT * P1::T, smem_cols, s>>>(in_real, scratch, tw1);
+    const int smem_rows = 2 * P2::PADDED * static_cast<int>(sizeof(float2));
+    if ((e = cudaFuncSetAttribute(rfft_rows_fwd<M1, M2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_rows)))
+      return e;
+    rfft_rows_fwd<M1, M2><<<count * (M1 / 2 + 1), 2 * P2::T, smem_rows, s>>>(scratch, out_spec, tw2);
+  } else {
+    const int smem_row = P2::PADDED * static_cast<int>(sizeof(float2));
+    if ((e = cudaFuncSetAttribute(rfft_rows_inv<M1, M2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_row)))
+      return e;
+    rfft_rows_inv<M1, M2><<<count * M1, P2::T, smem_row, s>>>(in_spec, scratch, tw2);
+    if ((e = cudaFuncSetAttribute(rfft_cols_inv<M1, M2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cols)))
+      return e;
+    rfft_cols_inv<M1, M2><<<count * TILES, CT * P1::T, smem_cols, s>>>(scratch, out_real, tw1);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_large_rfft(int log2m, bool inverse, const float* in_real, const float2* in_spec,
+                              float* out_real, float2* out_spec, int count, float2* scratch,
+                              const float2* tw1, const float2* tw2, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  switch (log2m) {
+#define RSG_RF(L, A, B) \
+  case L: return rfft_large_t<A, B>(inverse, in_real, in_spec, out_real, out_spec, count, scratch, tw1, tw2, s);
+    RSG_RF(13, 64, 128) RSG_RF(14, 128, 128) RSG_RF(15, 128, 256) RSG_RF(16, 256, 256) RSG_RF(17, 256, 512)
+    RSG_RF(18, 512, 512) RSG_RF(19, 512, 1024) RSG_RF(20, 1024, 1024) RSG_RF(21, 1024, 2048)
+    RSG_RF(22, 2048, 2048)
+#undef RSG_RF
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 // log2 M -> (log2 M1, log2 M2): M1 = 2^floor(l/2) columns of M2 = 2^ceil(l/2)
 void large_split(int log2m, int* l1, int* l2) {
   *l1 = log2m / 2;

@@ -80,7 +80,7 @@ def test_errors(rs, ctx):
 
 
 # ---- FFT seam ---------------------------------------------------------------------
-@pytest.mark.parametrize("n", [2 ** k for k in range(1, 16)])
+@pytest.mark.parametrize("n", [2 ** k for k in range(1, 16)] + [2 ** 16, 2 ** 18, 2 ** 20])
 def test_rfft_engine(rs, ctx, port, n):
     rng = np.random.default_rng(n)
     eng = rs.CudaRealFft(n, ctx=ctx)
