@@ -20,6 +20,60 @@
 namespace rsg {
 
 // ---- complex helpers ---------------------------------------------------------
+// sm_100a has packed FP32x2 instructions (FADD2 / FMUL2 / FFMA2): one issue slot
+// for both halves of a complex value, with per-half swizzle / negate / scalar
+// broadcast operand modifiers, so a complex add is one instruction and a complex
+// multiply two.  The FFT kernels are issue-bound, so this roughly halves their FP32
+// instruction count (IEEE round-to-nearest per half, same as the scalar forms).
+// RSG_NO_F32X2 selects the scalar forms (A/B measurement).
+#ifndef RSG_NO_F32X2
+__device__ __forceinline__ unsigned long long f2_u(float2 a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ float2 u_f2(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ float2 f2_add(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_u(a)), "l"(f2_u(b)));
+  return u_f2(d);
+}
+__device__ __forceinline__ float2 f2_sub(float2 a, float2 b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_u(a)), "l"(f2_u(b)));
+  return u_f2(d);
+}
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_u(a)), "l"(f2_u(b)));
+  return u_f2(d);
+}
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_u(a)), "l"(f2_u(b)), "l"(f2_u(c)));
+  return u_f2(d);
+}
+__device__ __forceinline__ float2 c_add(float2 a, float2 b) { return f2_add(a, b); }
+__device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return f2_sub(a, b); }
+// Half-negated swizzles (i b, conj b) as one FMUL2 by a (+-1, +-1) pair: ptxas folds
+// the swap and the one-half negate into operand modifiers (MOV + FADD otherwise).
+__device__ __forceinline__ float2 f2_ib(float2 b) { return f2_mul(make_float2(b.y, b.x), make_float2(-1.f, 1.f)); }
+__device__ __forceinline__ float2 f2_conj(float2 b) { return f2_mul(b, make_float2(1.f, -1.f)); }
+// (a.x b.x - a.y b.y, a.x b.y + a.y b.x) = a.x (b.x, b.y) + a.y (-b.y, b.x): the
+// a.x / a.y factors are scalar-broadcast operands
+__device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
+  return f2_fma(make_float2(a.y, a.y), f2_ib(b), f2_mul(make_float2(a.x, a.x), b));
+}
+// a * conj(b) = a.x (b.x, -b.y) + a.y (b.y, b.x)
+__device__ __forceinline__ float2 c_mulc(float2 a, float2 b) {
+  return f2_fma(make_float2(a.y, a.y), make_float2(b.y, b.x), f2_mul(make_float2(a.x, a.x), f2_conj(b)));
+}
+__device__ __forceinline__ float2 c_scale(float2 a, float s) { return f2_mul(a, make_float2(s, s)); }
+#else
 __device__ __forceinline__ float2 c_add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
@@ -29,8 +83,9 @@ __device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
 __device__ __forceinline__ float2 c_mulc(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
 }
-__device__ __forceinline__ float2 c_conj(float2 a) { return make_float2(a.x, -a.y); }
 __device__ __forceinline__ float2 c_scale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+#endif
+__device__ __forceinline__ float2 c_conj(float2 a) { return make_float2(a.x, -a.y); }
 // multiply by -i (forward) or +i (inverse)
 template <bool INV>
 __device__ __forceinline__ float2 c_rot(float2 a) {
@@ -40,13 +95,23 @@ __device__ __forceinline__ float2 c_rot(float2 a) {
 template <bool INV>
 __device__ __forceinline__ float2 c_w8(float2 a) {
   const float c = 0.70710678118654752f;
+#ifndef RSG_NO_F32X2
+  // c (a + (a.y, -a.x)) forward, c (a + (-a.y, a.x)) inverse
+  return c_scale(c_add(a, c_rot<INV>(a)), c);
+#else
   return INV ? make_float2(c * (a.x - a.y), c * (a.x + a.y)) : make_float2(c * (a.x + a.y), c * (a.y - a.x));
+#endif
 }
 // multiply by exp(-+ 3 i pi/4)
 template <bool INV>
 __device__ __forceinline__ float2 c_w83(float2 a) {
   const float c = 0.70710678118654752f;
+#ifndef RSG_NO_F32X2
+  // forward c ((a.y, -a.x) - a), inverse c ((-a.y, a.x) - a)
+  return c_scale(c_sub(c_rot<INV>(a), a), c);
+#else
   return INV ? make_float2(-c * (a.x + a.y), c * (a.x - a.y)) : make_float2(c * (a.y - a.x), -c * (a.x + a.y));
+#endif
 }
 
 // ---- in-register DFTs, natural order in and out -----------------------------
@@ -129,6 +194,43 @@ struct Dft<16, INV> {
       Dft<4, INV>::run(z);
 #pragma unroll
       for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = z[k2];
+    }
+  }
+};
+
+template <bool INV>
+struct Dft<32, INV> {
+  // 32 = 16 (inner, over n1 with n = 2 n1 + n2) x 2 (outer): X[k] = E[k] + W32^k O[k],
+  // X[k + 16] = E[k] - W32^k O[k].
+  __device__ __forceinline__ static void run(float2* v) {
+    float2 e[16], o[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      e[i] = v[2 * i];
+      o[i] = v[2 * i + 1];
+    }
+    Dft<16, INV>::run(e);
+    Dft<16, INV>::run(o);
+    // W32^k = exp(-+ 2 pi i k / 32), k = 1..15 (k = 4, 8, 12 by the special forms)
+    constexpr float C[8] = {1.f, 0.98078528040323043f, 0.92387953251128674f, 0.83146961230254524f,
+                            0.70710678118654752f, 0.55557023301960218f, 0.38268343236508978f,
+                            0.19509032201612825f};
+#pragma unroll
+    for (int k = 1; k < 16; ++k) {
+      if (k == 4) o[k] = c_w8<INV>(o[k]);
+      else if (k == 8) o[k] = c_rot<INV>(o[k]);
+      else if (k == 12) o[k] = c_w83<INV>(o[k]);
+      else {
+        // cos(2 pi k/32), sin(2 pi k/32) from the first-octant table
+        const float c = k <= 8 ? C[k] : -C[16 - k];
+        const float sn = k <= 8 ? C[8 - k] : C[k - 8];
+        o[k] = c_mul(o[k], make_float2(c, INV ? sn : -sn));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      v[k] = c_add(e[k], o[k]);
+      v[k + 16] = c_sub(e[k], o[k]);
     }
   }
 };
@@ -250,6 +352,24 @@ __device__ __forceinline__ void apply_twiddles(float2* v, float2 w1) {
     const float2 w12 = c_mul(w8, w4);
     v[12] = mul(v[12], w12);
     v[13] = mul(v[13], c_mul(w12, w1)); v[14] = mul(v[14], c_mul(w12, w2)); v[15] = mul(v[15], c_mul(w12, w3));
+  } else if constexpr (R == 32) {
+    // w^r = w^(r & 3) w^(r & 12) w^(r & 16): three table levels, at most 6 roundings deep
+    float2 lo[4], mid[4];
+    lo[0] = make_float2(1.f, 0.f);
+    lo[1] = w1;
+    lo[2] = c_mul(w1, w1);
+    lo[3] = c_mul(lo[2], w1);
+    mid[0] = make_float2(1.f, 0.f);
+    mid[1] = c_mul(lo[2], lo[2]);      // w^4
+    mid[2] = c_mul(mid[1], mid[1]);    // w^8
+    mid[3] = c_mul(mid[2], mid[1]);    // w^12
+    const float2 w16 = c_mul(mid[2], mid[2]);
+#pragma unroll
+    for (int r = 1; r < 32; ++r) {
+      float2 p = (r & 3) == 0 ? mid[(r >> 2) & 3] : ((r & 12) == 0 ? lo[r & 3] : c_mul(mid[(r >> 2) & 3], lo[r & 3]));
+      if (r & 16) p = (r & 15) == 0 ? w16 : c_mul(w16, p);
+      v[r] = mul(v[r], p);
+    }
   }
 }
 
