@@ -5,7 +5,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC,-O2,-ffp-contract=off
 SRC := paper_1712_03439_b200/csrc
 OUT := paper_1712_03439_b200/_lib
-OBJS := $(OUT)/kernels.o $(OUT)/large.o $(OUT)/ola2.o $(OUT)/sampler.o $(OUT)/features.o $(OUT)/api.o
+OBJS := $(OUT)/kernels.o $(OUT)/big.o $(OUT)/large.o $(OUT)/ola2.o $(OUT)/sampler.o $(OUT)/features.o $(OUT)/api.o
 
 REF_INC ?= /root/reference/proj/include
 ADAPTER := tests/cpp/_build/adapter_test
@@ -19,6 +19,10 @@ $(OUT)/kernels.o: $(SRC)/kernels.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh $(SRC)/asy
 $(OUT)/large.o: $(SRC)/large.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh $(SRC)/async.cuh
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/large.ptxas.log || (cat $(OUT)/large.ptxas.log; false)
+
+$(OUT)/big.o: $(SRC)/big.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh
+	@mkdir -p $(OUT)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/big.ptxas.log || (cat $(OUT)/big.ptxas.log; false)
 
 $(OUT)/ola2.o: $(SRC)/ola2.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh $(SRC)/fft2.cuh $(SRC)/async.cuh
 	@mkdir -p $(OUT)

@@ -358,6 +358,8 @@ struct Span {
   int64_t list_off, list_n, item_off, item_n;
   bool large;  // four-step path (large.cu)
   bool two;    // two-stream K4 (ola2.cu): items in FilterPlan::items2
+  bool ip = false;     // in-place large-transform K4 (big.cu)
+  int64_t max_nh = 1;  // largest N_h of the span (in-place K4 carry size)
 };
 
 // A batch of one large span (four-step path): pairs [pair_lo, pair_hi) of the
@@ -386,6 +388,17 @@ bool use_large(int l) {
   }();
   if (l > kMaxLog2M) return true;
   return v >= 0 ? l >= v : l == 13;
+}
+// Sizes (log2 M) that take the in-place one-CTA K4 (big.cu) when its carry fits in
+// shared memory (tuning override RSG_IP="lo,hi"; "0,0" disables it).
+bool use_ip(int l, int64_t max_nh) {
+  static const std::pair<int, int> r = [] {
+    const char* e = std::getenv("RSG_IP");
+    int lo = 13, hi = 14;
+    if (e) std::sscanf(e, "%d,%d", &lo, &hi);
+    return std::make_pair(lo, hi);
+  }();
+  return l >= r.first && l <= r.second && ip_supported(l, max_nh);
 }
 // Real FFT sizes (log2 N) that run the two-stream K4 (tuning override RSG_OLA2="lo,hi";
 // "0,0" disables it).
@@ -433,7 +446,10 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
   for (int l : order) {
     auto& v = bucket[l];
     if (v.empty()) continue;
-    if (use_large(l)) {  // four-step path, batched by scratch size
+    int64_t bucket_nh = 1;
+    for (int32_t p : v) bucket_nh = std::max<int64_t>(bucket_nh, plans[p].nh);
+    const bool ip = use_ip(l, bucket_nh);
+    if (!ip && use_large(l)) {  // four-step path, batched by scratch size
       Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
               static_cast<int64_t>(fp.items.size()), 0, true, false};
       const int64_t m = int64_t(1) << l;
@@ -518,10 +534,12 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
       const int64_t n = int64_t(1) << plans[p].log2n;
       max_pre = std::max<int64_t>(max_pre, (n - plans[p].L + plans[p].L - 1) / plans[p].L);
     }
-    const int64_t slots = 148LL * ola_resident_groups(l);
+    const int64_t slots = 148LL * (ip ? ip_resident(l, bucket_nh) : ola_resident_groups(l));
     const int64_t run = std::max<int64_t>((total_blocks + 6 * slots - 1) / (6 * slots), 16 * max_pre);
     Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
             static_cast<int64_t>(fp.items.size()), 0, false, false};
+    sp.ip = ip;
+    sp.max_nh = bucket_nh;
     for (int32_t p : v) {
       PairPlan& pl = plans[p];
       const int64_t n = int64_t(1) << pl.log2n;
@@ -673,7 +691,10 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
     OlaArgs a{fb.olaitems.as<OlaItem>() + sp.item_off, static_cast<int32_t>(sp.item_n), d_pair,
               fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(),
               fb.part.as<double>() + sp.item_off, c->tw[sp.l]};
-    RS_CUDA(launch_ola(sp.l, a, side_for(false)));
+    if (sp.ip)
+      RS_CUDA(launch_ola_ip(sp.l, a, sp.max_nh, side_for(false)));
+    else
+      RS_CUDA(launch_ola(sp.l, a, side_for(false)));
     ++c->launches;
   }
   for (int i = 0; i < rs_ctx::kSide; ++i)  // join

@@ -1,0 +1,310 @@
+// big.cu — K4 for the large one-CTA transform sizes (M = N/2 = 8192, 16384): an
+// in-place mixed-radix FFT, one work item (a run of OLA blocks of one pair) per CTA.
+//
+// Reference: convolve_ola (convolution.hpp:219-255) with RadixTwoRealFft
+// (fft.hpp:57-169): per block, the real N-point transform of the zero-padded
+// L-sample block, times H, inverse, overlap-added at b*L; mean_power's Σy²
+// (audio_buffer.hpp:66-75) of the final samples.
+//
+// Why a separate kernel: the Stockham passes of ola_kernel<M> hold a thread's whole
+// E = 32-element share across the barrier between a pass's reads and writes; at one
+// 512-thread CTA per SM (the transform alone is 136 KB of smem) that leaves 128
+// registers and the kernel spills ~1 KB per thread (53 GB of local-memory traffic per
+// config-5 launch).  Here every pass is in place: a butterfly reads its R elements,
+// transforms them and writes them back to the same slots, so no value lives across a
+// barrier and a thread holds one butterfly (R <= 32 complex) at a time.
+//
+//   forward: decimation in frequency (natural order in, digit-reversed out), radices
+//            R_0 .. R_{P-1}, twiddles after each butterfly's DFT; pass 0 loads the
+//            packed block z[n] = x[2n] + i x[2n+1] straight from the signal;
+//   pairing: untangle x G x repack (the formulas of spectral_multiply, fft.cuh) on
+//            (k, M - k), both read from their digit-reversed slots, in place;
+//   inverse: decimation in time with the passes in reverse order (digit-reversed in,
+//            natural out), conj twiddles before each DFT; the last pass hands the
+//            outputs c = t + S_0 r to the emit in registers;
+//   emit:    overlap carry in smem (N_h - 1 floats, single buffer: all carry reads,
+//            barrier, carry writes), every owned output written once, FP32 per-block
+//            power partials folded into FP64 in a fixed order (deterministic).
+//
+// Slot of element i: i + i/16 + i/S_0.  With the radix orders below every access of
+// every pass (strides S_p, the S = 1 blocks, and the pairing's k -> digit-reversed
+// slot, which moves by S_0 per k) is bank-conflict free on 64-bit accesses.
+#include <cmath>
+
+#include "fft.cuh"
+#include "kernels.cuh"
+
+namespace rsg {
+namespace {
+
+template <int M>
+struct IpPlan;
+template <>
+struct IpPlan<16384> {
+  static constexpr int NP = 3, T = 512, MINB = 1, LS0 = 9;
+  __host__ __device__ static constexpr int radix(int p) { return p == 2 ? 16 : 32; }
+};
+template <>
+struct IpPlan<8192> {
+  static constexpr int NP = 3, T = 256, MINB = 2, LS0 = 8;
+  __host__ __device__ static constexpr int radix(int p) { return p == 0 ? 32 : 16; }
+};
+
+template <class PL, int M>
+struct IpShape {
+  // S_p = M / (R_0 ... R_p): the stride of pass p; W_p = R_0 ... R_{p-1}: the weight of
+  // digit p in the frequency index k = sum m_p W_p (its slot is sum m_p S_p)
+  __host__ __device__ static constexpr int stride(int p) { return p < 0 ? M : stride(p - 1) / PL::radix(p); }
+  __host__ __device__ static constexpr int weight(int p) { return p == 0 ? 1 : weight(p - 1) * PL::radix(p - 1); }
+  // twiddle-base table: pass p (p < NP - 1) holds S_p bases exp(-2 pi i j / (R_p S_p))
+  __host__ __device__ static constexpr int tw_off(int p) { return p == 0 ? 0 : tw_off(p - 1) + stride(p - 1); }
+  static constexpr int TWN = tw_off(PL::NP - 1);
+  static constexpr int SLOTS = M + M / 16 + (M >> PL::LS0);
+  static_assert(stride(0) == PL::T && stride(PL::NP - 1) == 1, "plan shape");
+};
+
+template <class PL>
+__device__ __forceinline__ int ipad(int i) { return i + (i >> 4) + (i >> PL::LS0); }
+
+// digit-reversed slot of frequency index k
+template <class PL, int M>
+__device__ __forceinline__ int ip_pos(int k) {
+  using SH = IpShape<PL, M>;
+  int pos = 0;
+#pragma unroll
+  for (int p = 0; p < PL::NP; ++p) pos += ((k / SH::weight(p)) % PL::radix(p)) * SH::stride(p);
+  return pos;
+}
+
+// In-place pass p of the forward (DIF) or inverse (DIT) transform.
+template <class PL, int M, int P, bool INV>
+__device__ __forceinline__ void ip_pass(float2* s, const float2* tws, int t) {
+  using SH = IpShape<PL, M>;
+  constexpr int R = PL::radix(P), S = SH::stride(P), NB = M / (R * PL::T);
+  static_assert(NB >= 1 && M % (R * PL::T) == 0, "pass shape");
+#pragma unroll
+  for (int q = 0; q < NB; ++q) {
+    const int u = t + q * PL::T;
+    const int j = u % S;
+    const int base = (u / S) * (R * S) + j;
+    float2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = s[ipad<PL>(base + r * S)];
+    if constexpr (!INV) {
+      Dft<R, false>::run(v);
+      if constexpr (S > 1) apply_twiddles<R, false>(v, tws[SH::tw_off(P) + j]);
+    } else {
+      if constexpr (S > 1) apply_twiddles<R, true>(v, tws[SH::tw_off(P) + j]);
+      Dft<R, true>::run(v);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[ipad<PL>(base + r * S)] = v[r];
+  }
+}
+
+template <class PL, int M, int P>
+__device__ __forceinline__ void ip_forward_rest(float2* s, const float2* tws, int t) {
+  if constexpr (P < PL::NP) {
+    ip_pass<PL, M, P, false>(s, tws, t);
+    __syncthreads();
+    ip_forward_rest<PL, M, P + 1>(s, tws, t);
+  }
+}
+// inverse passes NP-1 .. 1 (pass 0 is the emit pass)
+template <class PL, int M, int P>
+__device__ __forceinline__ void ip_inverse_rest(float2* s, const float2* tws, int t) {
+  if constexpr (P >= 1) {
+    ip_pass<PL, M, P, true>(s, tws, t);
+    __syncthreads();
+    ip_inverse_rest<PL, M, P - 1>(s, tws, t);
+  }
+}
+
+// One pair (k, M - k) of the spectral step (spectral_multiply, fft.cuh); k = M - k
+// pairs only with itself (k = 0: partner slot 0 and G[M]; k = M/2).
+template <class PL, int M>
+__device__ __forceinline__ void ip_pair(float2* s, int k, const float2* __restrict__ G,
+                                        const float2* __restrict__ W) {
+  const int km = (M - k) & (M - 1);
+  const int pa = ipad<PL>(ip_pos<PL, M>(k)), pb = ipad<PL>(ip_pos<PL, M>(km));
+  const float2 a = s[pa];
+  const float2 b = c_conj(s[pb]);
+  const float2 w = ld_tw(W + k);
+  const float2 S = c_add(a, b);
+  const float2 D = c_rot<false>(c_sub(a, b));
+  const float2 wD = c_mul(w, D);
+  const float2 X2 = c_add(S, wD), X2m = c_sub(S, wD);
+  const float2 P = c_mul(X2, ld_tw(G + k));
+  const float2 Q = c_mulc(X2m, ld_tw(G + (M - k)));
+  const float2 U = c_add(P, Q);
+  const float2 V = c_mulc(c_sub(P, Q), w);
+  s[pa] = make_float2(U.x - V.y, U.y + V.x);
+  if (k != 0 && km != k) s[pb] = make_float2(U.x + V.y, V.x - U.y);
+}
+
+template <int M>
+__global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(OlaArgs a, int ccap) {
+  using PL = IpPlan<M>;
+  using SH = IpShape<PL, M>;
+  constexpr int T = PL::T, N = 2 * M;
+  constexpr int R0 = PL::radix(0), S0 = SH::stride(0);
+  static_assert(S0 == T, "passes 0 (forward) and 0 (inverse): one butterfly per thread");
+  extern __shared__ __align__(16) float2 smem[];
+  float2* s = smem;
+  float2* tws = smem + SH::SLOTS;
+  float* carry = reinterpret_cast<float*>(tws + ((SH::TWN + 1) & ~1));
+  __shared__ double red[T / 32];
+  const int t = threadIdx.x;
+  const OlaItem it = a.items[blockIdx.x];
+  const PairPlan& pl = a.plan[it.pair];
+  const PairMeta& pm = a.pair[it.pair];
+  const float* __restrict__ x = a.signals + pm.sig_off;
+  const long long nx = pm.nx;
+  const float2* __restrict__ G = a.spec + pl.spec_off;
+  const float2* __restrict__ W = a.tw + Plan<M>::TW_PASS;  // pairing table W^k, k <= M/2
+  float* __restrict__ y = a.y + pl.y_off;
+  const int L = static_cast<int>(pl.L);
+  const int B = static_cast<int>(pl.B);
+  const int ovl = N - L;  // N_h - 1 <= ccap
+  const long long own_lo = static_cast<long long>(it.b_own) * L;
+  const long long own_hi = it.b_end == B ? pl.out_len : static_cast<long long>(it.b_end) * L;
+  // twiddle bases, FP64 sincospi rounded once
+  for (int i = t; i < SH::TWN; i += T) {
+    int p = 0;
+#pragma unroll
+    for (int q = 1; q < PL::NP - 1; ++q)
+      if (i >= SH::tw_off(q)) p = q;
+    const int j = i - SH::tw_off(p);
+    const int span = PL::radix(p) * SH::stride(p);
+    double sn, cs;
+    sincospi(-2.0 * j / span, &sn, &cs);
+    tws[i] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
+  }
+  for (int i = t; i < ovl; i += T) carry[i] = 0.f;
+  __syncthreads();
+  double pw = 0.0;
+#pragma unroll 1
+  for (int b = it.b_begin; b < it.b_end; ++b) {
+    const long long start = static_cast<long long>(b) * L;
+    const int take = static_cast<int>(nx - start < L ? nx - start : L);
+    const float* xb = x + start;
+    // forward pass 0 (S_0 = T): z[t + S_0 r] from the signal, zero past `take`
+    {
+      float2 v[R0];
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int n2 = 2 * (t + S0 * r);
+        v[r].x = n2 < take ? __ldg(xb + n2) : 0.f;
+        v[r].y = n2 + 1 < take ? __ldg(xb + n2 + 1) : 0.f;
+      }
+      Dft<R0, false>::run(v);
+      apply_twiddles<R0, false>(v, tws[t]);
+#pragma unroll
+      for (int r = 0; r < R0; ++r) s[ipad<PL>(t + S0 * r)] = v[r];
+    }
+    __syncthreads();
+    ip_forward_rest<PL, M, 1>(s, tws, t);
+    // pairs (k, M - k), k in [0, M/2]: consecutive k on consecutive threads
+#pragma unroll 2
+    for (int k = t; k < M / 2; k += T) ip_pair<PL, M>(s, k, G, W);
+    if (t == 0) ip_pair<PL, M>(s, M / 2, G, W);
+    __syncthreads();
+    ip_inverse_rest<PL, M, PL::NP - 1>(s, tws, t);
+    // inverse pass 0: outputs c = t + S_0 r in registers
+    float2 v[R0];
+#pragma unroll
+    for (int r = 0; r < R0; ++r) v[r] = s[ipad<PL>(t + S0 * r)];
+    apply_twiddles<R0, true>(v, tws[t]);
+    Dft<R0, true>::run(v);
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int e = 2 * (t + S0 * r);
+      if (e < ovl) v[r].x += carry[e];
+      if (e + 1 < ovl) v[r].y += carry[e + 1];
+    }
+    __syncthreads();  // carry reads and this block's smem reads are done
+    const int lo = static_cast<int>(max(own_lo - start, -1ll));
+    const int hi = static_cast<int>(min(own_hi - start, static_cast<long long>(N)));
+    const int fe = b == B - 1 ? N : L;  // e < fe: final after this block
+    float* yb = y + start;
+    float pb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = 2 * (t + S0 * r) + h;
+        const float val = h ? v[r].y : v[r].x;
+        if (e < fe) {
+          if (e >= lo && e < hi) {
+            yb[e] = val;
+            pb[(r & 1) * 2 + h] = fmaf(val, val, pb[(r & 1) * 2 + h]);
+          }
+        } else {
+          carry[e - L] = val;
+        }
+      }
+    }
+    pw += static_cast<double>((pb[0] + pb[1]) + (pb[2] + pb[3]));
+  }
+  for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
+  if ((t & 31) == 0) red[t >> 5] = pw;
+  __syncthreads();
+  if (t == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < T / 32; ++w) tot += red[w];
+    a.part[blockIdx.x] = tot;
+  }
+}
+
+template <int M>
+size_t ip_smem(int ccap) {
+  using SH = IpShape<IpPlan<M>, M>;
+  return (static_cast<size_t>(SH::SLOTS) + ((SH::TWN + 1) & ~1)) * sizeof(float2) +
+         static_cast<size_t>(ccap) * sizeof(float);
+}
+
+template <int M>
+cudaError_t ip_t(const OlaArgs& a, int ccap, cudaStream_t st) {
+  const size_t smem = ip_smem<M>(ccap);
+  cudaError_t e = cudaFuncSetAttribute(ola_ip_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  ola_ip_kernel<M><<<a.count, IpPlan<M>::T, smem, st>>>(a, ccap);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// Sizes (log2 M) with an in-place K4 and the largest N_h - 1 its carry can hold.
+bool ip_supported(int log2m, int64_t max_nh) {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int ccap = static_cast<int>((std::max<int64_t>(max_nh - 1, 1) + 3) & ~int64_t(3));
+  switch (log2m) {
+    case 13: return ip_smem<8192>(ccap) + 1024 <= static_cast<size_t>(optin);
+    case 14: return ip_smem<16384>(ccap) + 1024 <= static_cast<size_t>(optin);
+    default: return false;
+  }
+}
+
+int ip_resident(int log2m, int64_t max_nh) {
+  const int ccap = static_cast<int>((std::max<int64_t>(max_nh - 1, 1) + 3) & ~int64_t(3));
+  const size_t per_sm = 228 * 1024;
+  const size_t need = (log2m == 13 ? ip_smem<8192>(ccap) : ip_smem<16384>(ccap)) + 1024;
+  const int by_smem = static_cast<int>(per_sm / need);
+  const int by_threads = 2048 / (log2m == 13 ? IpPlan<8192>::T : IpPlan<16384>::T);
+  return std::max(1, std::min(by_smem, by_threads));
+}
+
+cudaError_t launch_ola_ip(int log2m, const OlaArgs& a, int64_t max_nh, cudaStream_t s) {
+  if (a.count == 0) return cudaSuccess;
+  const int ccap = static_cast<int>((std::max<int64_t>(max_nh - 1, 1) + 3) & ~int64_t(3));
+  switch (log2m) {
+    case 13: return ip_t<8192>(a, ccap, s);
+    case 14: return ip_t<16384>(a, ccap, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace rsg

@@ -253,7 +253,7 @@ struct Plan {
   // 8 up to M = 512, 16 above, 32 for the two largest (T <= 512 threads)
   static constexpr int E = M < RSG_E_SMALL ? M : (M >= 8192 ? 32 : (M <= 512 ? RSG_E_SMALL : RSG_E));
   static constexpr int T = M / E;                          // threads per transform
-  static constexpr int LE = ilog2(E < 16 ? E : 16);         // log2 of the max radix
+  static constexpr int LE = ilog2(E < 16 ? E : (E >= 32 ? 32 : 16));  // log2 of the max radix
   static constexpr int NP = LOG == 0 ? 1 : (LOG + LE - 1) / LE;  // Stockham passes
   // Layout of the array between passes: PAD(i) = i + i/16 by default.  The output
   // of a radix-8 pass with NS = 8 (E = 8 sizes, M >= 128) is written in the

@@ -713,7 +713,7 @@ ola_kernel(OlaArgs a) {
   constexpr int T = PL::T;
   constexpr int G = groups_of<M>();
   constexpr int N = 2 * M;
-  const int g = threadIdx.x / T, t = threadIdx.x % T;
+  const int g = threadIdx.x / T, t0 = threadIdx.x % T;
   const int item = blockIdx.x * G + g;
   const bool has = item < a.count;
   const OlaItem it = a.items[has ? item : 0];
@@ -742,6 +742,10 @@ ola_kernel(OlaArgs a) {
     const bool active = has && b < it.b_end;
     const long long start = static_cast<long long>(b) * L;
     const int take = active ? static_cast<int>(nx - start < L ? nx - start : L) : 0;
+    // the thread index laundered per block: keeps the compiler from hoisting every
+    // pass's loop-invariant smem addresses out of the block loop (which spills)
+    int t;
+    asm volatile("mov.b32 %0, %1;" : "=r"(t) : "r"(t0));
     first_pass<M>(s, t, active, x + start, take, bar);
 #ifndef RSG_NO_FWD
     forward_rest<M>(s, t, a.tw, active, bar);
@@ -783,14 +787,14 @@ ola_kernel(OlaArgs a) {
     for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pw;
     bar();
-    if (t == 0 && has) {
+    if (t0 == 0 && has) {
       double tot = 0.0;
       for (int w = 0; w < T / 32; ++w) tot += red[g * (T / 32) + w];
       a.part[item] = tot;
     }
   } else {
     for (int o = T / 2; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
-    if (t == 0 && has) a.part[item] = pw;
+    if (t0 == 0 && has) a.part[item] = pw;
   }
 }
 

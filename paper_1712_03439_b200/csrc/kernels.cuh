@@ -225,6 +225,12 @@ cudaError_t launch_large_rfft(int log2m, bool inverse, const float* in_real, con
                               const float2* tw1, const float2* tw2, cudaStream_t s);
 
 // ---- launchers (kernels.cu) --------------------------------------------------
+// In-place one-CTA K4 for M = 8192, 16384 (big.cu); the carry (N_h - 1 floats) must fit
+// next to the transform in shared memory.
+bool ip_supported(int log2m, int64_t max_nh);
+int ip_resident(int log2m, int64_t max_nh);  // CTAs (work items) resident per SM
+cudaError_t launch_ola_ip(int log2m, const OlaArgs& a, int64_t max_nh, cudaStream_t s);
+
 constexpr int kMaxLog2M = 14;  // M <= 16384  (N <= 32768) in one CTA
 int cta_threads(int log2m);
 int ola_groups(int log2m);     // K4 work items per CTA
