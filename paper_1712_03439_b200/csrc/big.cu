@@ -49,7 +49,11 @@ struct IpPlan<8192> {
   static constexpr int NP = 3, T = 256, MINB = 2, LS0 = 8;
   __host__ __device__ static constexpr int radix(int p) { return p == 0 ? 32 : 16; }
 };
-
+template <>
+struct IpPlan<4096> {
+  static constexpr int NP = 3, T = 256, MINB = 2, LS0 = 8;
+  __host__ __device__ static constexpr int radix(int p) { return 16; }
+};
 template <class PL, int M>
 struct IpShape {
   // S_p = M / (R_0 ... R_p): the stride of pass p; W_p = R_0 ... R_{p-1}: the weight of
@@ -66,14 +70,27 @@ struct IpShape {
 template <class PL>
 __device__ __forceinline__ int ipad(int i) { return i + (i >> 4) + (i >> PL::LS0); }
 
-// digit-reversed slot of frequency index k
-template <class PL, int M>
-__device__ __forceinline__ int ip_pos(int k) {
+// digit-reversed slot of frequency index k (compile-time powers of two: every digit is
+// a shift and a mask)
+template <class PL, int M, int P = 0>
+__device__ __forceinline__ int ip_pos(unsigned k) {
   using SH = IpShape<PL, M>;
-  int pos = 0;
-#pragma unroll
-  for (int p = 0; p < PL::NP; ++p) pos += ((k / SH::weight(p)) % PL::radix(p)) * SH::stride(p);
-  return pos;
+  if constexpr (P == PL::NP) {
+    return 0;
+  } else {
+    constexpr unsigned W = SH::weight(P), R = PL::radix(P), S = SH::stride(P);
+    return static_cast<int>(((k / W) % R) * S) + ip_pos<PL, M, P + 1>(k);
+  }
+}
+
+// Slot offset of element base + r*S from the slot of base, for a butterfly base
+// b*R*S + j (j < S): each padding term i/D (D = 16, S_0) either distributes over r*S
+// (D <= S) or is constant over the butterfly (D >= R*S, powers of two), so the
+// offsets are compile-time constants and a pass needs one slot computation per
+// butterfly.
+template <class PL, int R, int S>
+__host__ __device__ constexpr int ip_off(int r) {
+  return r * S + (16 <= S ? r * S / 16 : 0) + ((1 << PL::LS0) <= S ? (r * S) >> PL::LS0 : 0);
 }
 
 // In-place pass p of the forward (DIF) or inverse (DIT) transform.
@@ -82,14 +99,16 @@ __device__ __forceinline__ void ip_pass(float2* s, const float2* tws, int t) {
   using SH = IpShape<PL, M>;
   constexpr int R = PL::radix(P), S = SH::stride(P), NB = M / (R * PL::T);
   static_assert(NB >= 1 && M % (R * PL::T) == 0, "pass shape");
+  static_assert((16 <= S || 16 >= R * S) && ((1 << PL::LS0) <= S || (1 << PL::LS0) >= R * S),
+                "padding terms distribute over the butterfly");
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
-    const int u = t + q * PL::T;
-    const int j = u % S;
-    const int base = (u / S) * (R * S) + j;
+    const unsigned u = static_cast<unsigned>(t + q * PL::T);
+    const unsigned j = u % unsigned(S);
+    const int pb = ipad<PL>(static_cast<int>((u / unsigned(S)) * unsigned(R * S) + j));
     float2 v[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = s[ipad<PL>(base + r * S)];
+    for (int r = 0; r < R; ++r) v[r] = s[pb + ip_off<PL, R, S>(r)];
     if constexpr (!INV) {
       Dft<R, false>::run(v);
       if constexpr (S > 1) apply_twiddles<R, false>(v, tws[SH::tw_off(P) + j]);
@@ -98,7 +117,7 @@ __device__ __forceinline__ void ip_pass(float2* s, const float2* tws, int t) {
       Dft<R, true>::run(v);
     }
 #pragma unroll
-    for (int r = 0; r < R; ++r) s[ipad<PL>(base + r * S)] = v[r];
+    for (int r = 0; r < R; ++r) s[pb + ip_off<PL, R, S>(r)] = v[r];
   }
 }
 
@@ -126,7 +145,8 @@ template <class PL, int M>
 __device__ __forceinline__ void ip_pair(float2* s, int k, const float2* __restrict__ G,
                                         const float2* __restrict__ W) {
   const int km = (M - k) & (M - 1);
-  const int pa = ipad<PL>(ip_pos<PL, M>(k)), pb = ipad<PL>(ip_pos<PL, M>(km));
+  const int pa = ipad<PL>(ip_pos<PL, M>(static_cast<unsigned>(k)));
+  const int pb = ipad<PL>(ip_pos<PL, M>(static_cast<unsigned>(km)));
   const float2 a = s[pa];
   const float2 b = c_conj(s[pb]);
   const float2 w = ld_tw(W + k);
@@ -140,6 +160,17 @@ __device__ __forceinline__ void ip_pair(float2* s, int k, const float2* __restri
   const float2 V = c_mulc(c_sub(P, Q), w);
   s[pa] = make_float2(U.x - V.y, U.y + V.x);
   if (k != 0 && km != k) s[pb] = make_float2(U.x + V.y, V.x - U.y);
+}
+
+// One thread: pull [p, p + bytes) into L2 ahead of use (1-D bulk prefetch; the window
+// is widened to 16-byte alignment).
+__device__ __forceinline__ void prefetch_l2(const void* p, long long bytes) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + static_cast<uintptr_t>(bytes) + 15) & ~uintptr_t(15);
+  for (uintptr_t a = a0; a < a1; a += (1u << 20)) {
+    const unsigned n = static_cast<unsigned>(a1 - a < (1u << 20) ? a1 - a : (1u << 20));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+  }
 }
 
 template <int M>
@@ -181,6 +212,11 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
     tws[i] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
   }
   for (int i = t; i < ovl; i += T) carry[i] = 0.f;
+  if (t == 0) {  // the pair's filter and the run's first block
+    prefetch_l2(G, (M + 1) * sizeof(float2));
+    const long long s0 = static_cast<long long>(it.b_begin) * L;
+    prefetch_l2(x + s0, 4 * (nx - s0 < L ? nx - s0 : L));
+  }
   __syncthreads();
   double pw = 0.0;
 #pragma unroll 1
@@ -188,19 +224,28 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
     const long long start = static_cast<long long>(b) * L;
     const int take = static_cast<int>(nx - start < L ? nx - start : L);
     const float* xb = x + start;
+    if (t == 0 && b + 1 < it.b_end) {  // next block's samples land in L2 during this one
+      const long long s1 = start + L;
+      prefetch_l2(x + s1, 4 * (nx - s1 < L ? nx - s1 : L));
+    }
     // forward pass 0 (S_0 = T): z[t + S_0 r] from the signal, zero past `take`
     {
       float2 v[R0];
 #pragma unroll
       for (int r = 0; r < R0; ++r) {
-        const int n2 = 2 * (t + S0 * r);
-        v[r].x = n2 < take ? __ldg(xb + n2) : 0.f;
-        v[r].y = n2 + 1 < take ? __ldg(xb + n2 + 1) : 0.f;
+        const int n2 = 2 * (t + S0 * r), w0 = 2 * ((t & ~31) + S0 * r);
+        if (w0 + 64 <= take) {  // the warp's 64 samples are all in the block (uniform)
+          v[r].x = __ldg(xb + n2);
+          v[r].y = __ldg(xb + n2 + 1);
+        } else {
+          v[r].x = n2 < take ? __ldg(xb + n2) : 0.f;
+          v[r].y = n2 + 1 < take ? __ldg(xb + n2 + 1) : 0.f;
+        }
       }
       Dft<R0, false>::run(v);
       apply_twiddles<R0, false>(v, tws[t]);
 #pragma unroll
-      for (int r = 0; r < R0; ++r) s[ipad<PL>(t + S0 * r)] = v[r];
+      for (int r = 0; r < R0; ++r) s[ipad<PL>(t) + ip_off<PL, R0, S0>(r)] = v[r];
     }
     __syncthreads();
     ip_forward_rest<PL, M, 1>(s, tws, t);
@@ -213,14 +258,22 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
     // inverse pass 0: outputs c = t + S_0 r in registers
     float2 v[R0];
 #pragma unroll
-    for (int r = 0; r < R0; ++r) v[r] = s[ipad<PL>(t + S0 * r)];
+    for (int r = 0; r < R0; ++r) v[r] = s[ipad<PL>(t) + ip_off<PL, R0, S0>(r)];
     apply_twiddles<R0, true>(v, tws[t]);
     Dft<R0, true>::run(v);
+    // Warp-uniform classification per r: the warp's 64 samples e in [w0, w0 + 64)
+    // are contiguous, so all but the few r that straddle ovl, L, lo or hi take a
+    // branch-free path (float2 carry loads, plain stores).
+    const int wt = t & ~31;
 #pragma unroll
     for (int r = 0; r < R0; ++r) {
-      const int e = 2 * (t + S0 * r);
-      if (e < ovl) v[r].x += carry[e];
-      if (e + 1 < ovl) v[r].y += carry[e + 1];
+      const int e = 2 * (t + S0 * r), w0 = 2 * (wt + S0 * r);
+      if (w0 + 64 <= ovl) {
+        v[r] = c_add(v[r], *reinterpret_cast<const float2*>(carry + e));
+      } else if (w0 < ovl) {
+        if (e < ovl) v[r].x += carry[e];
+        if (e + 1 < ovl) v[r].y += carry[e + 1];
+      }
     }
     __syncthreads();  // carry reads and this block's smem reads are done
     const int lo = static_cast<int>(max(own_lo - start, -1ll));
@@ -230,17 +283,28 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
     float pb[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int r = 0; r < R0; ++r) {
+      const int e = 2 * (t + S0 * r), w0 = 2 * (wt + S0 * r), w1 = w0 + 64;
+      if (w1 <= fe && w0 >= lo && w1 <= hi) {  // final and owned
+        yb[e] = v[r].x;
+        yb[e + 1] = v[r].y;
+        pb[(r & 1) * 2] = fmaf(v[r].x, v[r].x, pb[(r & 1) * 2]);
+        pb[(r & 1) * 2 + 1] = fmaf(v[r].y, v[r].y, pb[(r & 1) * 2 + 1]);
+      } else if (w0 >= fe) {  // carried into the next block
+        carry[e - L] = v[r].x;
+        carry[e + 1 - L] = v[r].y;
+      } else {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int e = 2 * (t + S0 * r) + h;
-        const float val = h ? v[r].y : v[r].x;
-        if (e < fe) {
-          if (e >= lo && e < hi) {
-            yb[e] = val;
-            pb[(r & 1) * 2 + h] = fmaf(val, val, pb[(r & 1) * 2 + h]);
+        for (int h = 0; h < 2; ++h) {
+          const int eh = e + h;
+          const float val = h ? v[r].y : v[r].x;
+          if (eh < fe) {
+            if (eh >= lo && eh < hi) {
+              yb[eh] = val;
+              pb[(r & 1) * 2 + h] = fmaf(val, val, pb[(r & 1) * 2 + h]);
+            }
+          } else {
+            carry[eh - L] = val;
           }
-        } else {
-          carry[e - L] = val;
         }
       }
     }
@@ -275,36 +339,45 @@ cudaError_t ip_t(const OlaArgs& a, int ccap, cudaStream_t st) {
 
 }  // namespace
 
+#define RSG_IP_DISPATCH(L, CALL)                     \
+  switch (L) {                                       \
+    case 12: { constexpr int M = 4096; return CALL; }  \
+    case 13: { constexpr int M = 8192; return CALL; }  \
+    case 14: { constexpr int M = 16384; return CALL; } \
+  }
+
+namespace {
+int ccap_of(int64_t max_nh) { return static_cast<int>((std::max<int64_t>(max_nh - 1, 1) + 3) & ~int64_t(3)); }
+size_t ip_smem_of(int log2m, int ccap) {
+  RSG_IP_DISPATCH(log2m, ip_smem<M>(ccap))
+  return 0;
+}
+int ip_threads_of(int log2m) {
+  RSG_IP_DISPATCH(log2m, IpPlan<M>::T)
+  return 0;
+}
+}  // namespace
+
 // Sizes (log2 M) with an in-place K4 and the largest N_h - 1 its carry can hold.
 bool ip_supported(int log2m, int64_t max_nh) {
+  if (ip_threads_of(log2m) == 0) return false;
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const int ccap = static_cast<int>((std::max<int64_t>(max_nh - 1, 1) + 3) & ~int64_t(3));
-  switch (log2m) {
-    case 13: return ip_smem<8192>(ccap) + 1024 <= static_cast<size_t>(optin);
-    case 14: return ip_smem<16384>(ccap) + 1024 <= static_cast<size_t>(optin);
-    default: return false;
-  }
+  return ip_smem_of(log2m, ccap_of(max_nh)) + 1024 <= static_cast<size_t>(optin);
 }
 
 int ip_resident(int log2m, int64_t max_nh) {
-  const int ccap = static_cast<int>((std::max<int64_t>(max_nh - 1, 1) + 3) & ~int64_t(3));
-  const size_t per_sm = 228 * 1024;
-  const size_t need = (log2m == 13 ? ip_smem<8192>(ccap) : ip_smem<16384>(ccap)) + 1024;
-  const int by_smem = static_cast<int>(per_sm / need);
-  const int by_threads = 2048 / (log2m == 13 ? IpPlan<8192>::T : IpPlan<16384>::T);
+  const size_t need = ip_smem_of(log2m, ccap_of(max_nh)) + 1024;
+  const int by_smem = static_cast<int>((228 * 1024) / need);
+  const int by_threads = 2048 / ip_threads_of(log2m);
   return std::max(1, std::min(by_smem, by_threads));
 }
 
 cudaError_t launch_ola_ip(int log2m, const OlaArgs& a, int64_t max_nh, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
-  const int ccap = static_cast<int>((std::max<int64_t>(max_nh - 1, 1) + 3) & ~int64_t(3));
-  switch (log2m) {
-    case 13: return ip_t<8192>(a, ccap, s);
-    case 14: return ip_t<16384>(a, ccap, s);
-    default: return cudaErrorInvalidValue;
-  }
+  RSG_IP_DISPATCH(log2m, ip_t<M>(a, ccap_of(max_nh), s))
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace rsg
