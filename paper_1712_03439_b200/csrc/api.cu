@@ -394,7 +394,7 @@ bool use_large(int l) {
 bool use_ip(int l, int64_t max_nh) {
   static const std::pair<int, int> r = [] {
     const char* e = std::getenv("RSG_IP");
-    int lo = 13, hi = 14;
+    int lo = 12, hi = 14;
     if (e) std::sscanf(e, "%d,%d", &lo, &hi);
     return std::make_pair(lo, hi);
   }();
@@ -446,9 +446,20 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
   for (int l : order) {
     auto& v = bucket[l];
     if (v.empty()) continue;
-    int64_t bucket_nh = 1;
-    for (int32_t p : v) bucket_nh = std::max<int64_t>(bucket_nh, plans[p].nh);
-    const bool ip = use_ip(l, bucket_nh);
+    int64_t bucket_nh = 1, bucket_blocks = 0, bucket_pre = 1;
+    for (int32_t p : v) {
+      bucket_nh = std::max<int64_t>(bucket_nh, plans[p].nh);
+      bucket_blocks += plans[p].B;
+      const int64_t n = int64_t(1) << plans[p].log2n;
+      bucket_pre = std::max<int64_t>(bucket_pre, (n - 1) / plans[p].L);
+    }
+    // The in-place K4 runs one work item per CTA; below M = 16384 (where it is the only
+    // fast path) it needs enough items to fill the GPU twice, else the four-step path or
+    // the small-M kernel (which split every block or pack several items per CTA) win.
+    bool ip = use_ip(l, bucket_nh);
+    if (ip && l < kMaxLog2M &&
+        bucket_blocks / (16 * bucket_pre) < 2 * 148LL * ip_resident(l, bucket_nh))
+      ip = false;
     if (!ip && use_large(l)) {  // four-step path, batched by scratch size
       Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
               static_cast<int64_t>(fp.items.size()), 0, true, false};
