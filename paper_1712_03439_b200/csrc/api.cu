@@ -359,6 +359,7 @@ struct Span {
   bool large;  // four-step path (large.cu)
   bool two;    // two-stream K4 (ola2.cu): items in FilterPlan::items2
   bool ip = false;     // in-place large-transform K4 (big.cu)
+  bool w = false;      // two-stream items on the warp-per-transform K4 (warp.cu)
   int64_t max_nh = 1;  // largest N_h of the span (in-place K4 carry size)
 };
 
@@ -399,6 +400,18 @@ bool use_ip(int l, int64_t max_nh) {
     return std::make_pair(lo, hi);
   }();
   return l >= r.first && l <= r.second && ip_supported(l, max_nh);
+}
+// Real FFT sizes (log2 N) that run the warp-per-transform two-stream K4 (warp.cu) when
+// their carries fit.  Off by default: measured 7-11% slower than the small-M K4 at
+// N = 512 / 1024 in the config-4 render; RSG_W="9,10" selects it.
+bool use_w(int log2n, int64_t max_nh) {
+  static const std::pair<int, int> r = [] {
+    const char* e = std::getenv("RSG_W");
+    int lo = 0, hi = -1;
+    if (e) std::sscanf(e, "%d,%d", &lo, &hi);
+    return std::make_pair(lo, hi);
+  }();
+  return log2n >= r.first && log2n <= r.second && w_supported(log2n, max_nh);
 }
 // Real FFT sizes (log2 N) that run the two-stream K4 (tuning override RSG_OLA2="lo,hi";
 // "0,0" disables it).
@@ -456,8 +469,9 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
     // The in-place K4 runs one work item per CTA; below M = 16384 (where it is the only
     // fast path) it needs enough items to fill the GPU twice, else the four-step path or
     // the small-M kernel (which split every block or pack several items per CTA) win.
+    static const bool ip_force = std::getenv("RSG_IP_FORCE") != nullptr;  // tests: skip the work test
     bool ip = use_ip(l, bucket_nh);
-    if (ip && l < kMaxLog2M &&
+    if (ip && l < kMaxLog2M && !ip_force &&
         bucket_blocks / (16 * bucket_pre) < 2 * 148LL * ip_resident(l, bucket_nh))
       ip = false;
     if (!ip && use_large(l)) {  // four-step path, batched by scratch size
@@ -497,17 +511,20 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
     }
     // largest pairs first (LPT) so the tail of the launch is short
     std::stable_sort(v.begin(), v.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
-    if (use_ola2(l + 1)) {  // two-stream K4: items are pairs of runs of one pair
+    const bool wk = !ip && use_w(l + 1, bucket_nh);
+    if (wk || use_ola2(l + 1)) {  // two-stream K4: items are pairs of runs of one pair
       int64_t total_blocks = 0, max_pre = 1;
       for (int32_t p : v) {
         total_blocks += plans[p].B;
         const int64_t n = int64_t(1) << plans[p].log2n;
         max_pre = std::max<int64_t>(max_pre, (n - plans[p].L + plans[p].L - 1) / plans[p].L);
       }
-      const int64_t slots = 148LL * ola2_resident_items(l + 1);
+      const int64_t slots = 148LL * (wk ? w_resident_items(l + 1, bucket_nh) : ola2_resident_items(l + 1));
       const int64_t run = std::max<int64_t>((total_blocks + 12 * slots - 1) / (12 * slots), 16 * max_pre);
       Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
               static_cast<int64_t>(fp.items2.size()), 0, false, true};
+      sp.w = wk;
+      sp.max_nh = bucket_nh;
       for (int32_t p : v) {
         PairPlan& pl = plans[p];
         const int64_t n = int64_t(1) << pl.log2n;
@@ -694,7 +711,10 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
                fb.part.as<double>() + fp.items.size() + sp.item_off, c->tw2f[sp.l + 1], c->tw2i[sp.l + 1],
                static_cast<int32_t>((std::max<int64_t>(max_nh - 1, 1) + 3) & ~int64_t(3)),
                static_cast<int32_t>((max_l + 8 + 3) & ~int64_t(3))};
-    RS_CUDA(launch_ola2(sp.l + 1, a, side_for(false)));
+    if (sp.w)
+      RS_CUDA(launch_ola_w(sp.l + 1, a, side_for(false)));
+    else
+      RS_CUDA(launch_ola2(sp.l + 1, a, side_for(false)));
     ++c->launches;
   }
   for (const Span& sp : fp.spans) {

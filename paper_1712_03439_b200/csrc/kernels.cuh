@@ -165,6 +165,10 @@ struct Ola2Args {
   int32_t scap;         // floats per input window: >= max L + 8 of the launch, multiple of 4
 };
 constexpr int kOla2MinLog2N = 5, kOla2MaxLog2N = 12;
+// Two-stream, warp-per-transform K4 for N = 512, 1024 (warp.cu), on Ola2Args (twf/twi unused).
+bool w_supported(int log2n, int64_t max_nh);
+int w_resident_items(int log2n, int64_t max_nh);  // work items resident per SM
+cudaError_t launch_ola_w(int log2n, const Ola2Args& a, cudaStream_t s);
 bool ola2_supported(int log2n);
 int ola2_resident_items(int log2n);
 int ola2_tw_total(int log2n, bool rev);

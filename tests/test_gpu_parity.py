@@ -181,6 +181,41 @@ def test_two_stream_k4_all_sizes():
     assert float(r.stdout.strip().splitlines()[-1]) <= WAVE_TOL
 
 
+@pytest.mark.parametrize("env,sizes", [
+    ({"RSG_W": "9,10"}, (9, 10)),           # warp-per-transform two-stream K4 (warp.cu)
+    ({"RSG_IP": "12,14", "RSG_IP_FORCE": "1"}, (13, 14, 15)),  # in-place K4 (big.cu), every size
+])
+def test_k4_variants(env, sizes):
+    """Opt-in K4 variants in a fresh process (their selection is read once per process):
+    single pairs with several runs per item at every N_h regime, and a render."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import numpy as np, oracle\n"
+        "from paper_1712_03439_b200 import roomsim as rs, scenes\n"
+        "ctx = rs.Context(0); port = oracle.port(); rng = np.random.default_rng(9); worst = 0.0\n"
+        f"for k in {tuple(sizes)!r}:\n"
+        "    n = 2 ** k\n"
+        "    for nh in (1, n // 4 + 1, n // 2, n - 3):\n"
+        "        x, h = rng.standard_normal(23 * n + 13), rng.standard_normal(max(nh, 1))\n"
+        "        want = port.convolve_ola(x, h, n); got = rs.convolve_ola(x, h, n, ctx=ctx)\n"
+        "        worst = max(worst, float(np.abs(got - want).max() / np.abs(want).max()))\n"
+        "b = scenes.config3(n_utt=4, seed=33)\n"
+        "g = rs.render_batch(b, ctx=ctx); o = port.render_batch(b, threads=8)\n"
+        "assert np.allclose(g.power, o[4], rtol=1e-5), (g.power, o[4])\n"
+        "for u in range(b.n_utt):\n"
+        "    for j in range(int(b.mic_begin[u + 1] - b.mic_begin[u])):\n"
+        "        a_ = b.channel(g.out, u, j, g.out_len[u]); w_ = b.channel(o[0], u, j, o[1][u])\n"
+        "        worst = max(worst, float(np.abs(a_ - w_).max() / np.abs(w_).max()))\n"
+        "print(worst)\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= WAVE_TOL
+
+
 def test_four_step_path_small_sizes(tmp_path):
     """Route every size >= 2^7 through the four-step path (RSG_LARGE_MIN) in a fresh
     process and check it against the oracle at sizes where K4 normally runs."""
