@@ -395,7 +395,7 @@ bool use_large(int l) {
 bool use_ip(int l, int64_t max_nh) {
   static const std::pair<int, int> r = [] {
     const char* e = std::getenv("RSG_IP");
-    int lo = 12, hi = 14;
+    int lo = 10, hi = 14;
     if (e) std::sscanf(e, "%d,%d", &lo, &hi);
     return std::make_pair(lo, hi);
   }();

@@ -26,9 +26,10 @@
 //            barrier, carry writes), every owned output written once, FP32 per-block
 //            power partials folded into FP64 in a fixed order (deterministic).
 //
-// Slot of element i: i + i/16 + i/S_0.  With the radix orders below every access of
-// every pass (strides S_p, the S = 1 blocks, and the pairing's k -> digit-reversed
-// slot, which moves by S_0 per k) is bank-conflict free on 64-bit accesses.
+// Slot of element i: i + i/16 + i/2^LS0 with 2^LS0 = max(256, S_0).  With the radix orders
+// below every access of every pass (strides S_p, the S = 1 blocks, and the pairing's
+// k -> digit-reversed slot, which moves by S_0 per k) is bank-conflict free on 64-bit
+// accesses.
 #include <cmath>
 
 #include "fft.cuh"
@@ -50,6 +51,21 @@ struct IpPlan<8192> {
   __host__ __device__ static constexpr int radix(int p) { return p == 0 ? 32 : 16; }
 };
 template <>
+struct IpPlan<512> {
+  static constexpr int NP = 3, T = 32, MINB = 16, LS0 = 8;
+  __host__ __device__ static constexpr int radix(int p) { return p == 1 ? 2 : 16; }
+};
+template <>
+struct IpPlan<1024> {
+  static constexpr int NP = 3, T = 64, MINB = 8, LS0 = 8;
+  __host__ __device__ static constexpr int radix(int p) { return p == 1 ? 4 : 16; }
+};
+template <>
+struct IpPlan<2048> {
+  static constexpr int NP = 3, T = 128, MINB = 4, LS0 = 8;
+  __host__ __device__ static constexpr int radix(int p) { return p == 1 ? 8 : 16; }
+};
+template <>
 struct IpPlan<4096> {
   static constexpr int NP = 3, T = 256, MINB = 2, LS0 = 8;
   __host__ __device__ static constexpr int radix(int p) { return 16; }
@@ -63,6 +79,9 @@ struct IpShape {
   // twiddle-base table: pass p (p < NP - 1) holds S_p bases exp(-2 pi i j / (R_p S_p))
   __host__ __device__ static constexpr int tw_off(int p) { return p == 0 ? 0 : tw_off(p - 1) + stride(p - 1); }
   static constexpr int TWN = tw_off(PL::NP - 1);
+  // smem-staged filter G (M + 1 bins) and pairing table W (M/2 + 1), float2, even counts
+  static constexpr bool GS = M <= 4096;
+  static constexpr int GSN = (M + 2) & ~1, WSN = (M / 2 + 2) & ~1;
   static constexpr int SLOTS = M + M / 16 + (M >> PL::LS0);
   static_assert(stride(0) == PL::T && stride(PL::NP - 1) == 1, "plan shape");
 };
@@ -88,10 +107,18 @@ __device__ __forceinline__ int ip_pos(unsigned k) {
 // (D <= S) or is constant over the butterfly (D >= R*S, powers of two), so the
 // offsets are compile-time constants and a pass needs one slot computation per
 // butterfly.
-template <class PL, int R, int S>
-__host__ __device__ constexpr int ip_off(int r) {
-  return r * S + (16 <= S ? r * S / 16 : 0) + ((1 << PL::LS0) <= S ? (r * S) >> PL::LS0 : 0);
+template <int D, int R, int S, int M>
+__host__ __device__ constexpr int ip_off_d(int r) {
+  // D <= S: distributes; D >= R S: constant over the butterfly; otherwise only a pass with
+  // a single block (R S = M, j < S, S | D) adds no carry into bit log2(D)
+  return D <= S ? r * S / D : (D >= R * S ? 0 : r * S / D);
 }
+template <class PL, int R, int S, int M>
+__host__ __device__ constexpr int ip_off(int r) {
+  return r * S + ip_off_d<16, R, S, M>(r) + ip_off_d<(1 << PL::LS0), R, S, M>(r);
+}
+template <int D, int R, int S, int M>
+__host__ __device__ constexpr bool ip_off_ok() { return D <= S || D >= R * S || (R * S == M && D % S == 0); }
 
 // In-place pass p of the forward (DIF) or inverse (DIT) transform.
 template <class PL, int M, int P, bool INV>
@@ -99,7 +126,7 @@ __device__ __forceinline__ void ip_pass(float2* s, const float2* tws, int t) {
   using SH = IpShape<PL, M>;
   constexpr int R = PL::radix(P), S = SH::stride(P), NB = M / (R * PL::T);
   static_assert(NB >= 1 && M % (R * PL::T) == 0, "pass shape");
-  static_assert((16 <= S || 16 >= R * S) && ((1 << PL::LS0) <= S || (1 << PL::LS0) >= R * S),
+  static_assert(ip_off_ok<16, R, S, M>() && ip_off_ok<(1 << PL::LS0), R, S, M>(),
                 "padding terms distribute over the butterfly");
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
@@ -108,7 +135,7 @@ __device__ __forceinline__ void ip_pass(float2* s, const float2* tws, int t) {
     const int pb = ipad<PL>(static_cast<int>((u / unsigned(S)) * unsigned(R * S) + j));
     float2 v[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = s[pb + ip_off<PL, R, S>(r)];
+    for (int r = 0; r < R; ++r) v[r] = s[pb + ip_off<PL, R, S, M>(r)];
     if constexpr (!INV) {
       Dft<R, false>::run(v);
       if constexpr (S > 1) apply_twiddles<R, false>(v, tws[SH::tw_off(P) + j]);
@@ -117,7 +144,7 @@ __device__ __forceinline__ void ip_pass(float2* s, const float2* tws, int t) {
       Dft<R, true>::run(v);
     }
 #pragma unroll
-    for (int r = 0; r < R; ++r) s[pb + ip_off<PL, R, S>(r)] = v[r];
+    for (int r = 0; r < R; ++r) s[pb + ip_off<PL, R, S, M>(r)] = v[r];
   }
 }
 
@@ -141,21 +168,22 @@ __device__ __forceinline__ void ip_inverse_rest(float2* s, const float2* tws, in
 
 // One pair (k, M - k) of the spectral step (spectral_multiply, fft.cuh); k = M - k
 // pairs only with itself (k = 0: partner slot 0 and G[M]; k = M/2).
-template <class PL, int M>
+template <class PL, int M, bool GS>
 __device__ __forceinline__ void ip_pair(float2* s, int k, const float2* __restrict__ G,
                                         const float2* __restrict__ W) {
+  auto ld = [](const float2* p) { return GS ? *p : ld_tw(p); };  // smem-staged or global
   const int km = (M - k) & (M - 1);
   const int pa = ipad<PL>(ip_pos<PL, M>(static_cast<unsigned>(k)));
   const int pb = ipad<PL>(ip_pos<PL, M>(static_cast<unsigned>(km)));
   const float2 a = s[pa];
   const float2 b = c_conj(s[pb]);
-  const float2 w = ld_tw(W + k);
+  const float2 w = ld(W + k);
   const float2 S = c_add(a, b);
   const float2 D = c_rot<false>(c_sub(a, b));
   const float2 wD = c_mul(w, D);
   const float2 X2 = c_add(S, wD), X2m = c_sub(S, wD);
-  const float2 P = c_mul(X2, ld_tw(G + k));
-  const float2 Q = c_mulc(X2m, ld_tw(G + (M - k)));
+  const float2 P = c_mul(X2, ld(G + k));
+  const float2 Q = c_mulc(X2m, ld(G + (M - k)));
   const float2 U = c_add(P, Q);
   const float2 V = c_mulc(c_sub(P, Q), w);
   s[pa] = make_float2(U.x - V.y, U.y + V.x);
@@ -183,7 +211,11 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
   extern __shared__ __align__(16) float2 smem[];
   float2* s = smem;
   float2* tws = smem + SH::SLOTS;
-  float* carry = reinterpret_cast<float*>(tws + ((SH::TWN + 1) & ~1));
+  // sizes up to M = 4096 also stage the pair's G and the pairing table W in smem
+  constexpr bool GS = SH::GS;
+  float2* gs = tws + ((SH::TWN + 1) & ~1);
+  float2* ws = gs + (GS ? SH::GSN : 0);
+  float* carry = reinterpret_cast<float*>(ws + (GS ? SH::WSN : 0));
   __shared__ double red[T / 32];
   const int t = threadIdx.x;
   const OlaItem it = a.items[blockIdx.x];
@@ -191,8 +223,10 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
   const PairMeta& pm = a.pair[it.pair];
   const float* __restrict__ x = a.signals + pm.sig_off;
   const long long nx = pm.nx;
-  const float2* __restrict__ G = a.spec + pl.spec_off;
-  const float2* __restrict__ W = a.tw + Plan<M>::TW_PASS;  // pairing table W^k, k <= M/2
+  const float2* __restrict__ Gg = a.spec + pl.spec_off;
+  const float2* __restrict__ Wg = a.tw + Plan<M>::TW_PASS;  // pairing table W^k, k <= M/2
+  const float2* G = GS ? gs : Gg;
+  const float2* W = GS ? ws : Wg;
   float* __restrict__ y = a.y + pl.y_off;
   const int L = static_cast<int>(pl.L);
   const int B = static_cast<int>(pl.B);
@@ -212,8 +246,12 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
     tws[i] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
   }
   for (int i = t; i < ovl; i += T) carry[i] = 0.f;
+  if constexpr (GS) {
+    for (int i = t; i <= M; i += T) gs[i] = ld_tw(Gg + i);
+    for (int i = t; i <= M / 2; i += T) ws[i] = ld_tw(Wg + i);
+  }
   if (t == 0) {  // the pair's filter and the run's first block
-    prefetch_l2(G, (M + 1) * sizeof(float2));
+    if (!GS) prefetch_l2(Gg, (M + 1) * sizeof(float2));
     const long long s0 = static_cast<long long>(it.b_begin) * L;
     prefetch_l2(x + s0, 4 * (nx - s0 < L ? nx - s0 : L));
   }
@@ -245,20 +283,20 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
       Dft<R0, false>::run(v);
       apply_twiddles<R0, false>(v, tws[t]);
 #pragma unroll
-      for (int r = 0; r < R0; ++r) s[ipad<PL>(t) + ip_off<PL, R0, S0>(r)] = v[r];
+      for (int r = 0; r < R0; ++r) s[ipad<PL>(t) + ip_off<PL, R0, S0, M>(r)] = v[r];
     }
     __syncthreads();
     ip_forward_rest<PL, M, 1>(s, tws, t);
     // pairs (k, M - k), k in [0, M/2]: consecutive k on consecutive threads
 #pragma unroll 2
-    for (int k = t; k < M / 2; k += T) ip_pair<PL, M>(s, k, G, W);
-    if (t == 0) ip_pair<PL, M>(s, M / 2, G, W);
+    for (int k = t; k < M / 2; k += T) ip_pair<PL, M, GS>(s, k, G, W);
+    if (t == 0) ip_pair<PL, M, GS>(s, M / 2, G, W);
     __syncthreads();
     ip_inverse_rest<PL, M, PL::NP - 1>(s, tws, t);
     // inverse pass 0: outputs c = t + S_0 r in registers
     float2 v[R0];
 #pragma unroll
-    for (int r = 0; r < R0; ++r) v[r] = s[ipad<PL>(t) + ip_off<PL, R0, S0>(r)];
+    for (int r = 0; r < R0; ++r) v[r] = s[ipad<PL>(t) + ip_off<PL, R0, S0, M>(r)];
     apply_twiddles<R0, true>(v, tws[t]);
     Dft<R0, true>::run(v);
     // Warp-uniform classification per r: the warp's 64 samples e in [w0, w0 + 64)
@@ -323,7 +361,8 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
 template <int M>
 size_t ip_smem(int ccap) {
   using SH = IpShape<IpPlan<M>, M>;
-  return (static_cast<size_t>(SH::SLOTS) + ((SH::TWN + 1) & ~1)) * sizeof(float2) +
+  return (static_cast<size_t>(SH::SLOTS) + ((SH::TWN + 1) & ~1) + (SH::GS ? SH::GSN + SH::WSN : 0)) *
+             sizeof(float2) +
          static_cast<size_t>(ccap) * sizeof(float);
 }
 
@@ -341,6 +380,9 @@ cudaError_t ip_t(const OlaArgs& a, int ccap, cudaStream_t st) {
 
 #define RSG_IP_DISPATCH(L, CALL)                     \
   switch (L) {                                       \
+    case 9: { constexpr int M = 512; return CALL; }    \
+    case 10: { constexpr int M = 1024; return CALL; }  \
+    case 11: { constexpr int M = 2048; return CALL; }  \
     case 12: { constexpr int M = 4096; return CALL; }  \
     case 13: { constexpr int M = 8192; return CALL; }  \
     case 14: { constexpr int M = 16384; return CALL; } \
@@ -355,6 +397,10 @@ size_t ip_smem_of(int log2m, int ccap) {
 int ip_threads_of(int log2m) {
   RSG_IP_DISPATCH(log2m, IpPlan<M>::T)
   return 0;
+}
+int ip_minb_of(int log2m) {  // CTAs per SM the register budget is set for
+  RSG_IP_DISPATCH(log2m, IpPlan<M>::MINB)
+  return 1;
 }
 }  // namespace
 
@@ -371,7 +417,7 @@ int ip_resident(int log2m, int64_t max_nh) {
   const size_t need = ip_smem_of(log2m, ccap_of(max_nh)) + 1024;
   const int by_smem = static_cast<int>((228 * 1024) / need);
   const int by_threads = 2048 / ip_threads_of(log2m);
-  return std::max(1, std::min(by_smem, by_threads));
+  return std::max(1, std::min(std::min(by_smem, by_threads), ip_minb_of(log2m)));
 }
 
 cudaError_t launch_ola_ip(int log2m, const OlaArgs& a, int64_t max_nh, cudaStream_t s) {
