@@ -183,7 +183,7 @@ def test_two_stream_k4_all_sizes():
 
 @pytest.mark.parametrize("env,sizes", [
     ({"RSG_W": "9,10"}, (9, 10)),           # warp-per-transform two-stream K4 (warp.cu)
-    ({"RSG_IP": "12,14", "RSG_IP_FORCE": "1"}, (13, 14, 15)),  # in-place K4 (big.cu), every size
+    ({"RSG_IP": "9,14", "RSG_IP_FORCE": "1"}, (10, 11, 12, 13, 14, 15)),  # in-place K4 (big.cu), every size
 ])
 def test_k4_variants(env, sizes):
     """Opt-in K4 variants in a fresh process (their selection is read once per process):
