@@ -343,7 +343,7 @@ def ours(args, rank, world, local_rank):
         "bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
         "frac": achieved / fp32_peak if achieved else None, "traffic": traffic,
         "traffic_unit": "DRAM bytes per step (all K4 launches)", "traffic_source": traffic_src,
-        "kernel": "ola_kernel<M> (K4), all FFT sizes of one render",
+        "kernel": "K4 (ola_small_kernel<M>, ola_ip_kernel<M>, ola2_kernel<N>, four-step stages), all FFT sizes of one render",
         "ola_ms_per_step": ola_ms / args.steps,
         "alg_flops_per_step": per_step_flops,
         "alg_bytes_per_step": alg_bytes,

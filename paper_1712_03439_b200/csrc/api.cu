@@ -467,12 +467,12 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
       bucket_pre = std::max<int64_t>(bucket_pre, (n - 1) / plans[p].L);
     }
     // The in-place K4 runs one work item per CTA; below M = 16384 (where it is the only
-    // fast path) it needs enough items to fill the GPU twice, else the four-step path or
+    // fast path) it needs enough items to fill the GPU once, else the four-step path or
     // the small-M kernel (which split every block or pack several items per CTA) win.
     static const bool ip_force = std::getenv("RSG_IP_FORCE") != nullptr;  // tests: skip the work test
     bool ip = use_ip(l, bucket_nh);
     if (ip && l < kMaxLog2M && !ip_force &&
-        bucket_blocks / (16 * bucket_pre) < 2 * 148LL * ip_resident(l, bucket_nh))
+        bucket_blocks / (16 * bucket_pre) < 148LL * ip_resident(l, bucket_nh))
       ip = false;
     if (!ip && use_large(l)) {  // four-step path, batched by scratch size
       Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
