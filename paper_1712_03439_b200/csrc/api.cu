@@ -466,12 +466,11 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
       const int64_t n = int64_t(1) << plans[p].log2n;
       bucket_pre = std::max<int64_t>(bucket_pre, (n - 1) / plans[p].L);
     }
-    // The in-place K4 runs one work item per CTA; below M = 16384 (where it is the only
-    // fast path) it needs enough items to fill the GPU once, else the four-step path or
-    // the small-M kernel (which split every block or pack several items per CTA) win.
+    // The in-place K4 runs one work item per CTA; at M = 8192 it needs enough items to
+    // fill the GPU once, else the four-step path (which splits every block) wins.
     static const bool ip_force = std::getenv("RSG_IP_FORCE") != nullptr;  // tests: skip the work test
     bool ip = use_ip(l, bucket_nh);
-    if (ip && l < kMaxLog2M && !ip_force &&
+    if (ip && l == 13 && !ip_force &&
         bucket_blocks / (16 * bucket_pre) < 148LL * ip_resident(l, bucket_nh))
       ip = false;
     if (!ip && use_large(l)) {  // four-step path, batched by scratch size

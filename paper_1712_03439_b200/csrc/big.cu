@@ -38,36 +38,63 @@
 namespace rsg {
 namespace {
 
+// Per-size tuning (CTAs per SM the register budget is set for; G and the pairing
+// table staged in smem or read through L1): measured on B200, config-4 render.
+#ifndef RSG_IP_MINB_1024
+#define RSG_IP_MINB_1024 8
+#endif
+#ifndef RSG_IP_GS_1024
+#define RSG_IP_GS_1024 true
+#endif
+#ifndef RSG_IP_MINB_2048
+#define RSG_IP_MINB_2048 6
+#endif
+#ifndef RSG_IP_GS_2048
+#define RSG_IP_GS_2048 false
+#endif
+#ifndef RSG_IP_MINB_4096
+#define RSG_IP_MINB_4096 3
+#endif
+#ifndef RSG_IP_GS_4096
+#define RSG_IP_GS_4096 false
+#endif
+
 template <int M>
 struct IpPlan;
 template <>
 struct IpPlan<16384> {
   static constexpr int NP = 3, T = 512, MINB = 1, LS0 = 9;
+  static constexpr bool GS = false;
   __host__ __device__ static constexpr int radix(int p) { return p == 2 ? 16 : 32; }
 };
 template <>
 struct IpPlan<8192> {
   static constexpr int NP = 3, T = 256, MINB = 2, LS0 = 8;
+  static constexpr bool GS = false;
   __host__ __device__ static constexpr int radix(int p) { return p == 0 ? 32 : 16; }
 };
 template <>
 struct IpPlan<512> {
   static constexpr int NP = 3, T = 32, MINB = 16, LS0 = 8;
+  static constexpr bool GS = true;
   __host__ __device__ static constexpr int radix(int p) { return p == 1 ? 2 : 16; }
 };
 template <>
 struct IpPlan<1024> {
-  static constexpr int NP = 3, T = 64, MINB = 8, LS0 = 8;
+  static constexpr int NP = 3, T = 64, MINB = RSG_IP_MINB_1024, LS0 = 8;
+  static constexpr bool GS = RSG_IP_GS_1024;
   __host__ __device__ static constexpr int radix(int p) { return p == 1 ? 4 : 16; }
 };
 template <>
 struct IpPlan<2048> {
-  static constexpr int NP = 3, T = 128, MINB = 4, LS0 = 8;
+  static constexpr int NP = 3, T = 128, MINB = RSG_IP_MINB_2048, LS0 = 8;
+  static constexpr bool GS = RSG_IP_GS_2048;
   __host__ __device__ static constexpr int radix(int p) { return p == 1 ? 8 : 16; }
 };
 template <>
 struct IpPlan<4096> {
-  static constexpr int NP = 3, T = 256, MINB = 2, LS0 = 8;
+  static constexpr int NP = 3, T = 256, MINB = RSG_IP_MINB_4096, LS0 = 8;
+  static constexpr bool GS = RSG_IP_GS_4096;
   __host__ __device__ static constexpr int radix(int p) { return 16; }
 };
 template <class PL, int M>
@@ -80,7 +107,7 @@ struct IpShape {
   __host__ __device__ static constexpr int tw_off(int p) { return p == 0 ? 0 : tw_off(p - 1) + stride(p - 1); }
   static constexpr int TWN = tw_off(PL::NP - 1);
   // smem-staged filter G (M + 1 bins) and pairing table W (M/2 + 1), float2, even counts
-  static constexpr bool GS = M <= 4096;
+  static constexpr bool GS = PL::GS;
   static constexpr int GSN = (M + 2) & ~1, WSN = (M / 2 + 2) & ~1;
   static constexpr int SLOTS = M + M / 16 + (M >> PL::LS0);
   static_assert(stride(0) == PL::T && stride(PL::NP - 1) == 1, "plan shape");
