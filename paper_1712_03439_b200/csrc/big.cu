@@ -345,18 +345,29 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
     const int hi = static_cast<int>(min(own_hi - start, static_cast<long long>(N)));
     const int fe = b == B - 1 ? N : L;  // e < fe: final after this block
     float* yb = y + start;
+    // 8-byte stores where the block start allows (measured: pays at M >= 8192 only)
+    const bool y_al = M >= 8192 && (reinterpret_cast<uintptr_t>(yb) & 7) == 0;  // block-uniform
+    const bool c_al = M >= 8192 && (L & 1) == 0;
     float pb[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int r = 0; r < R0; ++r) {
       const int e = 2 * (t + S0 * r), w0 = 2 * (wt + S0 * r), w1 = w0 + 64;
       if (w1 <= fe && w0 >= lo && w1 <= hi) {  // final and owned
-        yb[e] = v[r].x;
-        yb[e + 1] = v[r].y;
+        if (y_al) {
+          *reinterpret_cast<float2*>(yb + e) = v[r];
+        } else {
+          yb[e] = v[r].x;
+          yb[e + 1] = v[r].y;
+        }
         pb[(r & 1) * 2] = fmaf(v[r].x, v[r].x, pb[(r & 1) * 2]);
         pb[(r & 1) * 2 + 1] = fmaf(v[r].y, v[r].y, pb[(r & 1) * 2 + 1]);
       } else if (w0 >= fe) {  // carried into the next block
-        carry[e - L] = v[r].x;
-        carry[e + 1 - L] = v[r].y;
+        if (c_al) {
+          *reinterpret_cast<float2*>(carry + e - L) = v[r];
+        } else {
+          carry[e - L] = v[r].x;
+          carry[e + 1 - L] = v[r].y;
+        }
       } else {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
