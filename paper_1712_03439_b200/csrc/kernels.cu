@@ -1015,41 +1015,67 @@ cudaError_t launch_gain(const GainArgs& a, cudaStream_t s) {
 // K6: the mix y_j[n] = Σ_i alpha_ij (h_ij * x_i)[n], zero-padded, summed in
 // source order in FP64, stored FP32.
 // ============================================================================
+constexpr int kMixMaxI = 8;  // sources whose metadata is cached per CTA (more: read per use)
+
+// One source row's quad at n (zero past the row's end).
+__device__ __forceinline__ float4 mix_quad(const float* row, long long ol, long long n) {
+  if (n + 3 < ol) return __ldcs(reinterpret_cast<const float4*>(row + n));
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (n < ol) v.x = row[n];
+  if (n + 1 < ol) v.y = row[n + 1];
+  if (n + 2 < ol) v.z = row[n + 2];
+  return v;
+}
+
 __global__ void __launch_bounds__(256) mix_kernel(MixArgs a) {
   const long long ch = blockIdx.y;
   const long long u = a.chan_utt[ch];
-  const int j = a.chan_mic[ch];
-  const long long len = a.utt_len[u];
   const long long stride = a.utt_stride[u];
   const long long n0 = blockIdx.x * a.tile;
   if (n0 >= stride) return;
+  const int j = a.chan_mic[ch];
+  const long long len = a.utt_len[u];
   const long long n1 = n0 + a.tile < stride ? n0 + a.tile : stride;
   const int I = a.utt_I[u], J = a.utt_J[u];
   const long long pair0 = a.utt_pair0[u];
+  // the channel's per-source row / length / gain, read once per CTA (no dependent
+  // metadata loads in the sample loop)
+  __shared__ const float* s_row[kMixMaxI];
+  __shared__ long long s_len[kMixMaxI];
+  __shared__ double s_gain[kMixMaxI];
+  if (threadIdx.x < kMixMaxI && threadIdx.x < I) {
+    const long long p = pair0 + static_cast<long long>(threadIdx.x) * J + j;
+    s_row[threadIdx.x] = a.y + a.plan[p].y_off;
+    s_len[threadIdx.x] = a.plan[p].out_len;
+    s_gain[threadIdx.x] = a.gain[p];
+  }
+  __syncthreads();
+  const int Ic = I < kMixMaxI ? I : kMixMaxI;
   float* out = a.out + a.chan_out[ch];
   const bool out16 = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
   // four consecutive samples per thread: float4 loads of every source's row (rows are
-  // 16-byte aligned, y_off % 4 == 0), FP64 sums in source order, one float4 store
+  // 16-byte aligned, y_off % 4 == 0), two sources' loads in flight at a time, FP64 sums in
+  // source order, one float4 store
   for (long long n = n0 + 4 * threadIdx.x; n < n1; n += 4 * blockDim.x) {
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    auto add = [&](double g, float4 v) {
+      acc0 = fma(g, static_cast<double>(v.x), acc0);
+      acc1 = fma(g, static_cast<double>(v.y), acc1);
+      acc2 = fma(g, static_cast<double>(v.z), acc2);
+      acc3 = fma(g, static_cast<double>(v.w), acc3);
+    };
     if (n < len) {
-      for (int i = 0; i < I; ++i) {
+      int i = 0;
+      for (; i + 1 < Ic; i += 2) {
+        const float4 va = mix_quad(s_row[i], s_len[i], n);
+        const float4 vb = mix_quad(s_row[i + 1], s_len[i + 1], n);
+        add(s_gain[i], va);
+        add(s_gain[i + 1], vb);
+      }
+      if (i < Ic) add(s_gain[i], mix_quad(s_row[i], s_len[i], n));
+      for (i = kMixMaxI; i < I; ++i) {  // beyond the cached sources
         const long long p = pair0 + static_cast<long long>(i) * J + j;
-        const long long ol = a.plan[p].out_len;
-        if (n >= ol) continue;
-        const double g = a.gain[p];
-        const float* yr = a.y + a.plan[p].y_off;
-        if (n + 3 < ol) {
-          const float4 v = __ldcs(reinterpret_cast<const float4*>(yr + n));
-          acc0 = fma(g, static_cast<double>(v.x), acc0);
-          acc1 = fma(g, static_cast<double>(v.y), acc1);
-          acc2 = fma(g, static_cast<double>(v.z), acc2);
-          acc3 = fma(g, static_cast<double>(v.w), acc3);
-        } else {  // the row ends inside this quad
-          acc0 = fma(g, static_cast<double>(yr[n]), acc0);
-          if (n + 1 < ol) acc1 = fma(g, static_cast<double>(yr[n + 1]), acc1);
-          if (n + 2 < ol) acc2 = fma(g, static_cast<double>(yr[n + 2]), acc2);
-        }
+        add(a.gain[p], mix_quad(a.y + a.plan[p].y_off, a.plan[p].out_len, n));
       }
     }
     // samples in [len, stride) are the zero-filled tail (acc stays 0 there)
