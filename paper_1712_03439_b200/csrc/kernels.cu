@@ -61,6 +61,9 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   static_assert(NW >= 2 && NW <= 32 && (NW & (NW - 1)) == 0, "power-of-two warp count");
   constexpr int OB = NW == 2 ? 1 : NW == 4 ? 2 : NW == 8 ? 3 : NW == 16 ? 4 : 5;  // owner bits
   constexpr int NQ = (NV + 3) / 4;  // 4-byte words per owner's count row
+  // row stride in bytes: 16-byte aligned (uint4 row loads) and an odd number of 16-byte
+  // units, so the owners' rows start in different banks (8-way conflicts otherwise)
+  constexpr int RS = 16 * ((((4 * NQ + 15) / 16) % 2 == 0) ? (4 * NQ + 15) / 16 + 1 : (4 * NQ + 15) / 16);
   const SynthItem it = a.items[blockIdx.x];
   const PairMeta& pm = a.pair[it.pair];
   const UttMeta& um = a.utt[pm.utt];
@@ -72,7 +75,9 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   double* ent_a = rg + (3 * K + 1);              // [CH] owner-major sorted amplitudes
   int* ent_d = reinterpret_cast<int*>(ent_a + CH);           // [CH] their bins
   // [NW owner][NV virtual warp] entry counts, one byte each (<= 32), 16-byte aligned rows
-  unsigned char* cnt8 = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(ent_d + CH) + 15) & ~uintptr_t(15));
+  // of RS bytes (offset arithmetic keeps the accesses in the shared window: STS/LDS)
+  const uintptr_t cnt_off = (reinterpret_cast<uintptr_t>(ent_d + CH) - reinterpret_cast<uintptr_t>(sm) + 15) & ~uintptr_t(15);
+  unsigned char* cnt8 = sm + cnt_off;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lo = it.slice_lo, len = it.slice_len;
   for (int l = tid; l < len; l += NT) bins[l] = 0.0;
@@ -151,7 +156,7 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
         mine[h] &= ((owner[h] >> k) & 1) ? bk : ~bk;
         row &= ((lane >> k) & 1) ? bk : ~bk;
       }
-      if (lane < NW) cnt8[lane * (4 * NQ) + h * NW + warp] = static_cast<unsigned char>(__popc(row));
+      if (lane < NW) cnt8[lane * RS + h * NW + warp] = static_cast<unsigned char>(__popc(row));
     }
     __syncthreads();
     // ---- stable counting sort into owner-major lists (order: slot, warp, lane) ----
@@ -161,7 +166,7 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
 #pragma unroll
     for (int h = 0; h < IPT; ++h) ub[h] = 0u;
     if (lane < NW) {
-      const unsigned* rowp = reinterpret_cast<const unsigned*>(cnt8 + lane * (4 * NQ));
+      const unsigned* rowp = reinterpret_cast<const unsigned*>(cnt8 + lane * RS);
 #pragma unroll
       for (int q4 = 0; q4 < NQ; q4 += 4) {  // 16-byte loads (a strided 4-byte loop is conflicted)
         unsigned rv[4];
@@ -243,8 +248,10 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
 
 size_t synth_smem_bytes(int max_order, int slice, int nt, int ipt) {
   const int W = 2 * max_order + 1, nw = nt / 32, ch = ipt * nt, nv = ipt * nw;
+  const int u16 = (4 * ((nv + 3) / 4) + 15) / 16;  // count-row stride (kernel's RS)
+  const int rs = 16 * (u16 % 2 == 0 ? u16 + 1 : u16);
   return sizeof(double) * (static_cast<size_t>(slice) + 3 * W + 3 * max_order + 1 + ch) + sizeof(int) * ch +
-         static_cast<size_t>(nw) * 4 * ((nv + 3) / 4) + 16 + 16;
+         static_cast<size_t>(nw) * rs + 16 + 16;
 }
 
 cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice, cudaStream_t s,
