@@ -51,6 +51,19 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// FP64 load from a 32-bit shared address (tables written before a __syncthreads)
+__device__ __forceinline__ double lds_f64(unsigned a) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+// *(double*)shared[a] = *(double*)shared[a] + v, round to nearest (no contraction)
+__device__ __forceinline__ void shared_add_rn(unsigned a, double v) {
+  double cur;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cur) : "r"(a) : "memory");
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(__dadd_rn(cur, v)) : "memory");
+}
+
 // IPT = images per thread per chunk (4 measured best; 2 where 4 would cost occupancy)
 template <int NT, int IPT>
 __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_cap) {
@@ -80,6 +93,12 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   unsigned char* cnt8 = sm + cnt_off;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lo = it.slice_lo, len = it.slice_len;
+  // 32-bit shared address of the bins, computed once (laundered through asm: otherwise the
+  // compiler re-derives the CTA's shared window, S2UR SR_CgaCtaId, at every use)
+  unsigned bins_s;
+  asm volatile("mov.b32 %0, %1;" : "=r"(bins_s) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(bins))));
+  const unsigned ax_s = bins_s + 8u * static_cast<unsigned>(slice_cap);
+  const unsigned rg_s = ax_s + 8u * static_cast<unsigned>(3 * W);
   for (int l = tid; l < len; l += NT) bins[l] = 0.0;
   for (int idx = tid; idx < 3 * W; idx += NT) {
     const int axis = idx / W, n = idx - axis * W - K;
@@ -116,7 +135,8 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
       amp[h] = 0.0;
       if (i < V) {
         // norm: sqrt((x*x + y*y) + z*z), room_model.hpp:43
-        const double d2 = __dadd_rn(__dadd_rn(ax[ix], ax[W + iy]), ax[2 * W + iz]);
+        const double d2 = __dadd_rn(__dadd_rn(lds_f64(ax_s + 8u * ix), lds_f64(ax_s + 8u * (W + iy))),
+                                    lds_f64(ax_s + 8u * (2 * W + iz)));
         const double d = __dsqrt_rn(d2);
         if (d <= 0.0) geo = 1;                     // :157-158
         const double dl = ceil(__dmul_rn(d, spm));  // :159-160
@@ -125,7 +145,7 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
         const long long rel = static_cast<long long>(D) - lo;
         if (rel >= 0 && rel < len) {
           const int g = abs(ix - K) + abs(iy - K) + abs(iz - K);
-          amp[h] = __ddiv_rn(rg[g], d);  // :161-162 pow(r, g) / d
+          amp[h] = __ddiv_rn(lds_f64(rg_s + 8u * g), d);  // :161-162 pow(r, g) / d
           rel_bin[h] = static_cast<int>(rel);
         }
       }
@@ -222,10 +242,13 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
       const unsigned grp = __match_any_sync(0xffffffffu, bn);
       const int rank = __popc(grp & lt);
       const int rounds = __reduce_max_sync(0xffffffffu, valid ? __popc(grp) : 0);
-      if (valid && rank == 0) bins[bn] = __dadd_rn(bins[bn], av);
+      // bins[bn] += av through a 32-bit shared address (a generic pointer re-derives the
+      // CTA's shared window every iteration: S2UR on the critical path)
+      const unsigned ba = bins_s + 8u * static_cast<unsigned>(bn);
+      if (valid && rank == 0) shared_add_rn(ba, av);
       for (int r = 1; r < rounds; ++r) {
         __syncwarp();
-        if (valid && rank == r) bins[bn] = __dadd_rn(bins[bn], av);
+        if (valid && rank == r) shared_add_rn(ba, av);
       }
       __syncwarp();
     }
