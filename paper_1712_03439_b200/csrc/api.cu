@@ -928,13 +928,27 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
   ch.P = static_cast<int64_t>(ch.pair.size());
   // K1 launch classes: (threads, slice size).  Small lattices (K <= 12) use
   // 128-thread CTAs; slices are grouped so the dynamic smem fits the class.
-  static const int kClass[3] = {2048, 6144, kSynthSlice};
-  std::vector<SynthItem> cls[2][3];
+  // A RIR of (14400, kSynthBig] bins (> 0.9 s at 16 kHz) is synthesized by one CTA (one per SM): every slice
+  // CTA enumerates the whole image lattice, so two near-equal slices cost twice the image
+  // work (config 5: K1 -18%).  Shorter RIRs keep two slices at two CTAs per SM, which
+  // measured faster (config 4).  Tuning override RSG_SYNTH_BIG = "lo,hi" bins.
+  static const std::pair<int64_t, int64_t> big = [] {
+    const char* e = std::getenv("RSG_SYNTH_BIG");
+    long long lo = 14400, hi = kSynthBig;
+    if (e) std::sscanf(e, "%lld,%lld", &lo, &hi);
+    return std::make_pair(static_cast<int64_t>(lo), static_cast<int64_t>(hi));
+  }();
+  static const int kClass[4] = {2048, 6144, kSynthSlice, kSynthBig};
+  std::vector<SynthItem> cls[2][4];
   for (int64_t p = 0; p < ch.P; ++p) {
     if (ch.place_err[p]) continue;
     const int64_t cap = ch.pair[p].rir_cap;
     const int K = ch.utt[ch.pair[p].utt].order;
     const int small = K <= 12 ? 1 : 0;  // measured crossover of the 128- and 512-thread K1
+    if (cap > std::max<int64_t>(kSynthSlice, big.first) && cap <= big.second) {
+      cls[small][3].push_back(SynthItem{static_cast<int32_t>(p), 0, static_cast<int32_t>(cap), 0});
+      continue;
+    }
     for (int64_t lo = 0; lo < cap; lo += kSynthSlice) {
       const int64_t len = std::min<int64_t>(kSynthSlice, cap - lo);
       const int k = len <= kClass[0] ? 0 : (len <= kClass[1] ? 1 : 2);
@@ -943,7 +957,7 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
   }
   ch.synth_class.clear();
   for (int small = 0; small < 2; ++small)
-    for (int k = 2; k >= 0; --k) {  // large lattices and slices first
+    for (int k = 3; k >= 0; --k) {  // large lattices and slices first
       int cap = 1;
       for (const auto& itm : cls[small][k]) cap = std::max(cap, itm.slice_len);
       ch.synth_class.emplace_back(static_cast<int64_t>(ch.items.size()), static_cast<int64_t>(cls[small][k].size()),

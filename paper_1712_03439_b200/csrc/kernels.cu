@@ -280,8 +280,11 @@ size_t synth_smem_bytes(int max_order, int slice, int nt, int ipt) {
 cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice, cudaStream_t s,
                          int nt) {
   if (n_items == 0) return cudaSuccess;
-  // 4 images per thread unless that would drop a 512-thread CTA below 2 per SM
-  const int ipt = (nt == 512 && 2 * synth_smem_bytes(max_order, slice, nt, 4) > 227 * 1024) ? 2 : 4;
+  // 4 images per thread unless that would drop a 512-thread CTA below 2 per SM (when not
+  // even 2 images per thread keep 2 per SM, 4)
+  const bool two4 = 2 * synth_smem_bytes(max_order, slice, nt, 4) <= 227 * 1024;
+  const bool two2 = 2 * synth_smem_bytes(max_order, slice, nt, 2) <= 227 * 1024;
+  const int ipt = (nt == 512 && !two4 && two2) ? 2 : 4;
   const size_t smem = synth_smem_bytes(max_order, slice, nt, ipt);
   auto go = [&](auto kern, int threads) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
