@@ -1,5 +1,7 @@
-// big.cu — K4 for the large one-CTA transform sizes (M = N/2 = 8192, 16384): an
-// in-place mixed-radix FFT, one work item (a run of OLA blocks of one pair) per CTA.
+// big.cu — K4 in place: a mixed-radix FFT that rewrites every butterfly's own slots, one
+// work item (a run of OLA blocks of one pair) per CTA, for M = N/2 = 1024 … 16384 (the
+// planner's default; M = 512 is supported and opt-in: RSG_IP="9,14" — measured slower than
+// ola_small_kernel<512>).
 //
 // Reference: convolve_ola (convolution.hpp:219-255) with RadixTwoRealFft
 // (fft.hpp:57-169): per block, the real N-point transform of the zero-padded
