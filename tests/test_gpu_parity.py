@@ -405,3 +405,32 @@ def test_render_errors(rs, ctx):
     b.plan_rule, b.forced_fft_size = scenes.PLAN_FORCED, 16
     with pytest.raises(rs.PlanError):
         rs.render_batch(b, ctx=ctx)
+
+
+@pytest.mark.parametrize("cfg,n_utt,seed", [("config5", 1, 24), ("config4", 4, 26), ("config2", 4, 33)])
+def test_render_rirs_bit_exact(rs, ctx, port, cfg, n_utt, seed):
+    """Every pair's RIR as the batched render synthesized it (K1, through its launch
+    classes: the 128- / 512-thread lattices, the sliced and the one-CTA long RIRs) equals
+    the reference synthesize_rir (room_model.hpp:141-174) bit for bit."""
+    from paper_1712_03439_b200 import scenes
+
+    b = getattr(scenes, cfg)(n_utt=n_utt, seed=seed)
+    g = rs.render_batch(b, ctx=ctx)
+    I, J = np.diff(b.src_begin), np.diff(b.mic_begin)
+    checked = 0
+    for u in range(b.n_utt):
+        for i in range(I[u]):
+            for j in range(J[u]):
+                p = int(b.pair_begin[u] + i * J[u] + j)
+                want = port.synthesize_rir(b.room_dims[u], float(b.reflection[u]), int(b.image_order[u]),
+                                           b.src_pos[b.src_begin[u] + i], b.mic_pos[b.mic_begin[u] + j],
+                                           fs=float(b.sample_rate[u]), c0=float(b.speed_of_sound[u]),
+                                           max_taps=int(b.max_taps[u]))
+                assert want.size == g.layout["rir_len"][p], (p, want.size)
+                if b.eta_db > 0:  # the render keeps the truncated RIR (room_model.hpp:203-213)
+                    want = port.truncate_rir(want, b.eta_db)[0]
+                got = rs.last_pair_rir(p, want.size + 8, ctx=ctx)
+                assert got.size == want.size == g.layout["rir_keep"][p], (p, got.size, want.size)
+                assert (got.view(np.uint64) == want.view(np.uint64)).all(), p
+                checked += 1
+    assert checked == b.n_pairs
