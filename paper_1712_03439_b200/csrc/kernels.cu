@@ -632,10 +632,31 @@ ola_small_kernel(OlaArgs a) {
   }
   cp_async_wait_all();
   __syncthreads();  // per-CTA twiddles, G, carry and barriers in place (all threads)
+  // Up to M = RSG_K4_DIRECT_MAX pass 0 reads the block straight from the signal
+  // (L2-prefetched two blocks ahead by one thread) instead of the TMA stage: measured
+  // 2-27% faster at M <= 256, 5% slower at M = 512
+#ifndef RSG_K4_DIRECT_MAX
+#define RSG_K4_DIRECT_MAX 256
+#endif
+  constexpr bool kDirect = M <= RSG_K4_DIRECT_MAX;
+  auto prefetch_l2_block = [&](int b) {
+    if (b < it.b_end && t == 0) {
+      const long long st = static_cast<long long>(b) * L;
+      const long long n = nx - st < L ? nx - st : L;
+      const uintptr_t a0 = reinterpret_cast<uintptr_t>(x + st) & ~uintptr_t(15);
+      const uintptr_t a1 = (reinterpret_cast<uintptr_t>(x + st + n) + 15) & ~uintptr_t(15);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(static_cast<unsigned>(a1 - a0)) : "memory");
+    }
+  };
 #ifndef RSG_X_NOLOAD
   if (has) {
-    prefetch(0);
-    if (it.b_begin + 1 < it.b_end) prefetch(1);
+    if constexpr (kDirect) {
+      prefetch_l2_block(it.b_begin);
+      prefetch_l2_block(it.b_begin + 1);
+    } else {
+      prefetch(0);
+      if (it.b_begin + 1 < it.b_end) prefetch(1);
+    }
   }
 #endif
   double pw = 0.0;
@@ -649,7 +670,9 @@ ola_small_kernel(OlaArgs a) {
     int d = 0, take = 0;
     bool bulk = false;
     float* stage = stage_of(k);
-    if (active) {
+    if (kDirect) {
+      take = active ? (nx - start < L ? nx - start : L) : 0;
+    } else if (active) {
       window(b, d, take, bulk);
 #ifndef RSG_X_NOLOAD
       if (bulk) {
@@ -666,9 +689,13 @@ ola_small_kernel(OlaArgs a) {
 #endif
     }
     bar();
-    first_pass<M, float, GroupBar<T>, false>(s, t, active, stage + d, take, bar);
+    first_pass<M, float, GroupBar<T>, false>(s, t, active, kDirect ? x + start : stage + d, take, bar);
 #if !defined(RSG_NO_PREFETCH) && !defined(RSG_X_NOLOAD)
-    if (active && b + 2 < it.b_end) prefetch(k + 2);  // lands while blocks b, b+1 are transformed
+    if constexpr (kDirect) {
+      if (active) prefetch_l2_block(b + 2);
+    } else {
+      if (active && b + 2 < it.b_end) prefetch(k + 2);  // lands while blocks b, b+1 are transformed
+    }
 #endif
 #ifndef RSG_NO_FUSED_PAIR
     if constexpr (M == 512) {  // last forward pass + pairing + first inverse pass in registers
