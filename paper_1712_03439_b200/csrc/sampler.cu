@@ -44,21 +44,34 @@ struct SrcInfo {
   int32_t local, pad;
 };
 
-// grid.y = source, grid.x = tiles of 4 * blockDim.x sample pairs
+// Persistent grid over (source, tile) work units: unit u of the flat list belongs to the
+// source whose tile prefix `first_tile` brackets it (binary search); a tile is 4 *
+// blockDim.x sample pairs.  (A 2-D grid sized by the longest source launched millions
+// of empty CTAs for the short ones.)
+constexpr int kSigTile = 4 * 256;
 __global__ void __launch_bounds__(256) signals_kernel(SamplerSpecD sp, uint64_t seed, int64_t epoch,
-                                                      const SrcInfo* src, float* out) {
-  const SrcInfo si = src[blockIdx.y];
-  const Stream g(seed ^ 0x5EED5EED5EEDull, static_cast<uint64_t>(si.utt), static_cast<uint64_t>(epoch),
-                 kTagSignal + static_cast<uint32_t>(si.local));
-  const int64_t npairs = (si.len + 1) / 2;
-  float* o = out + si.off;
-  for (int k = 0; k < 4; ++k) {
-    const int64_t p = (static_cast<int64_t>(blockIdx.x) * 4 + k) * blockDim.x + threadIdx.x;
-    if (p >= npairs) return;
-    float z0, z1;
-    signal_pair(sp, g, static_cast<uint64_t>(p), &z0, &z1);
-    o[2 * p] = z0;
-    if (2 * p + 1 < si.len) o[2 * p + 1] = z1;
+                                                      const SrcInfo* src, const int64_t* first_tile,
+                                                      int64_t n_src, int64_t n_tiles, float* out) {
+  for (int64_t u = blockIdx.x; u < n_tiles; u += gridDim.x) {
+    int64_t lo = 0, hi = n_src - 1;  // last source with first_tile <= u
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) / 2;
+      if (first_tile[mid] <= u) lo = mid; else hi = mid - 1;
+    }
+    const SrcInfo si = src[lo];
+    const Stream g(seed ^ 0x5EED5EED5EEDull, static_cast<uint64_t>(si.utt), static_cast<uint64_t>(epoch),
+                   kTagSignal + static_cast<uint32_t>(si.local));
+    const int64_t npairs = (si.len + 1) / 2;
+    float* o = out + si.off;
+    const int64_t tile = u - first_tile[lo];
+    for (int k = 0; k < 4; ++k) {
+      const int64_t p = (tile * 4 + k) * blockDim.x + threadIdx.x;
+      if (p >= npairs) break;
+      float z0, z1;
+      signal_pair(sp, g, static_cast<uint64_t>(p), &z0, &z1);
+      o[2 * p] = z0;
+      if (2 * p + 1 < si.len) o[2 * p + 1] = z1;
+    }
   }
 }
 
@@ -165,29 +178,29 @@ int rs_generate_signals(const rs_sampler_spec* spec, uint64_t seed, int64_t epoc
                         const int64_t* sig_len, float* out_dev, void* stream) {
   if (int st = check_spec(spec)) return st;
   if (n_src <= 0) return RS_OK;
-  if (n_src > 65535) {  // grid.y limit: split
-    for (int64_t s0 = 0; s0 < n_src; s0 += 65535) {
-      const int64_t m = std::min<int64_t>(65535, n_src - s0);
-      if (int st = rs_generate_signals(spec, seed, epoch, m, utt_of_src + s0, src_local + s0, sig_off + s0,
-                                       sig_len + s0, out_dev, stream))
-        return st;
-    }
-    return RS_OK;
-  }
-  std::vector<SrcInfo> info(n_src);
-  int64_t max_pairs = 1;
+  // one table: n_src SrcInfo, then the n_src tile prefixes
+  const size_t info_bytes = static_cast<size_t>(n_src) * sizeof(SrcInfo);
+  std::vector<unsigned char> table(info_bytes + static_cast<size_t>(n_src) * sizeof(int64_t));
+  SrcInfo* info = reinterpret_cast<SrcInfo*>(table.data());
+  int64_t* first = reinterpret_cast<int64_t*>(table.data() + info_bytes);
+  int64_t n_tiles = 0;
   for (int64_t s = 0; s < n_src; ++s) {
     info[s] = SrcInfo{utt_of_src[s], sig_off[s], sig_len[s], src_local[s], 0};
-    max_pairs = std::max<int64_t>(max_pairs, (sig_len[s] + 1) / 2);
+    first[s] = n_tiles;
+    n_tiles += ((sig_len[s] + 1) / 2 + kSigTile - 1) / kSigTile;
   }
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  SrcInfo* d = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), info.size() * sizeof(SrcInfo), st);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(d, info.data(), info.size() * sizeof(SrcInfo), cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) {
-    const dim3 grid(static_cast<unsigned>((max_pairs + 1023) / 1024), static_cast<unsigned>(n_src));
-    signals_kernel<<<grid, 256, 0, st>>>(spec_of(spec), seed, epoch, d, out_dev);
+  unsigned char* d = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), table.size(), st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d, table.data(), table.size(), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && n_tiles > 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t grid = std::min<int64_t>(n_tiles, static_cast<int64_t>(sms) * 8);
+    signals_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(
+        spec_of(spec), seed, epoch, reinterpret_cast<const SrcInfo*>(d),
+        reinterpret_cast<const int64_t*>(d + info_bytes), n_src, n_tiles, out_dev);
     e = cudaGetLastError();
   }
   if (d) cudaFreeAsync(d, st);
