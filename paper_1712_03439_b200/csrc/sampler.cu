@@ -46,7 +46,7 @@ struct SrcInfo {
 
 // Persistent grid over (source, tile) work units: unit u of the flat list belongs to the
 // source whose tile prefix `first_tile` brackets it (binary search); a tile is 4 *
-// blockDim.x sample pairs.  (A 2-D grid sized by the longest source launched millions
+// blockDim.x sample quads.  (A 2-D grid sized by the longest source launched millions
 // of empty CTAs for the short ones.)
 constexpr int kSigTile = 4 * 256;
 __global__ void __launch_bounds__(256) signals_kernel(SamplerSpecD sp, uint64_t seed, int64_t epoch,
@@ -61,16 +61,17 @@ __global__ void __launch_bounds__(256) signals_kernel(SamplerSpecD sp, uint64_t 
     const SrcInfo si = src[lo];
     const Stream g(seed ^ 0x5EED5EED5EEDull, static_cast<uint64_t>(si.utt), static_cast<uint64_t>(epoch),
                    kTagSignal + static_cast<uint32_t>(si.local));
-    const int64_t npairs = (si.len + 1) / 2;
+    const int64_t nquads = (si.len + 3) / 4;
     float* o = out + si.off;
     const int64_t tile = u - first_tile[lo];
     for (int k = 0; k < 4; ++k) {
-      const int64_t p = (tile * 4 + k) * blockDim.x + threadIdx.x;
-      if (p >= npairs) break;
-      float z0, z1;
-      signal_pair(sp, g, static_cast<uint64_t>(p), &z0, &z1);
-      o[2 * p] = z0;
-      if (2 * p + 1 < si.len) o[2 * p + 1] = z1;
+      const int64_t q = (tile * 4 + k) * blockDim.x + threadIdx.x;
+      if (q >= nquads) break;
+      float z[4];
+      signal_quad(sp, g, static_cast<uint64_t>(q), z);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (4 * q + i < si.len) o[4 * q + i] = z[i];
     }
   }
 }
@@ -163,11 +164,11 @@ int rs_generate_signals_host(const rs_sampler_spec* spec, uint64_t seed, int64_t
                    kTagSignal + static_cast<uint32_t>(src_local[s]));
     float* o = out + sig_off[s];
     const int64_t len = sig_len[s];
-    for (int64_t p = 0; 2 * p < len; ++p) {
-      float z0, z1;
-      signal_pair(sp, g, static_cast<uint64_t>(p), &z0, &z1);
-      o[2 * p] = z0;
-      if (2 * p + 1 < len) o[2 * p + 1] = z1;
+    for (int64_t q = 0; 4 * q < len; ++q) {
+      float z[4];
+      signal_quad(sp, g, static_cast<uint64_t>(q), z);
+      for (int i = 0; i < 4; ++i)
+        if (4 * q + i < len) o[4 * q + i] = z[i];
     }
   }
   return RS_OK;
@@ -187,7 +188,7 @@ int rs_generate_signals(const rs_sampler_spec* spec, uint64_t seed, int64_t epoc
   for (int64_t s = 0; s < n_src; ++s) {
     info[s] = SrcInfo{utt_of_src[s], sig_off[s], sig_len[s], src_local[s], 0};
     first[s] = n_tiles;
-    n_tiles += ((sig_len[s] + 1) / 2 + kSigTile - 1) / kSigTile;
+    n_tiles += ((sig_len[s] + 3) / 4 + kSigTile - 1) / kSigTile;
   }
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   unsigned char* d = nullptr;

@@ -350,19 +350,25 @@ RSH void psincosf_(float x, float* sn, float* cs) {  // x in [0, 2 pi)
   *cs = q == 0 ? c : (q == 1 ? -s : (q == 2 ? -c : s));
 }
 
-// Samples 2p, 2p+1 of a source stream: N(0, std) by Box-Muller in FP32 from two 24-bit
-// uniforms (counter p of the stream's Philox sequence).
-RSH void signal_pair(const SamplerSpecD& sp, const Stream& g, uint64_t p, float* z0, float* z1) {
-  const U4 w = philox4x32_10(U4{static_cast<uint32_t>(p), static_cast<uint32_t>(p >> 32), g.tag, 0x51A1u},
-                             g.k0, g.k1);
-  const float u0 = static_cast<float>(w.x >> 8) * 0x1.0p-24f;  // exact, [0, 1)
-  const float u1 = static_cast<float>(w.y >> 8) * 0x1.0p-24f;
+// Two samples N(0, std) by Box-Muller in FP32 from two 24-bit uniforms.
+RSH void box_muller(float sd, uint32_t a, uint32_t b, float* z0, float* z1) {
+  const float u0 = static_cast<float>(a >> 8) * 0x1.0p-24f;  // exact, [0, 1)
+  const float u1 = static_cast<float>(b >> 8) * 0x1.0p-24f;
   const float r = RF_SQRT(RF_MUL(-2.0f, plogf_(RF_SUB(1.0f, u0))));  // 1 - u0 in (0, 1]
   float sn, cs;
   psincosf_(RF_MUL(6.28318548f, u1), &sn, &cs);
-  const float sd = static_cast<float>(sp.signal_std);
   *z0 = RF_MUL(sd, RF_MUL(r, cs));
   *z1 = RF_MUL(sd, RF_MUL(r, sn));
+}
+
+// Samples 4q .. 4q+3 of a source stream: counter q of the stream's Philox sequence gives
+// four 32-bit words, two Box-Muller pairs.
+RSH void signal_quad(const SamplerSpecD& sp, const Stream& g, uint64_t q, float* z) {
+  const U4 w = philox4x32_10(U4{static_cast<uint32_t>(q), static_cast<uint32_t>(q >> 32), g.tag, 0x51A1u},
+                             g.k0, g.k1);
+  const float sd = static_cast<float>(sp.signal_std);
+  box_muller(sd, w.x, w.y, z, z + 1);
+  box_muller(sd, w.z, w.w, z + 2, z + 3);
 }
 
 }  // namespace rsg
