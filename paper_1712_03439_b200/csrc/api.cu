@@ -562,7 +562,15 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
       max_pre = std::max<int64_t>(max_pre, (n - plans[p].L + plans[p].L - 1) / plans[p].L);
     }
     const int64_t slots = 148LL * (ip ? ip_resident(l, bucket_nh) : ola_resident_groups(l));
-    const int64_t run = std::max<int64_t>((total_blocks + 6 * slots - 1) / (6 * slots), 16 * max_pre);
+    // work items per resident slot (measured, config 4): the in-place K4 prefers long runs
+    // (each item stages its filter and twiddles), ola_small<512> too, the M <= 256 sizes
+    // more items (shorter tails)
+    static const int64_t run_div_env = [] {
+      const char* e = std::getenv("RSG_RUN_DIV");  // tuning override
+      return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(0);
+    }();
+    const int64_t run_div = run_div_env ? run_div_env : (ip ? 2 : (l <= 8 ? 12 : 3));
+    const int64_t run = std::max<int64_t>((total_blocks + run_div * slots - 1) / (run_div * slots), 16 * max_pre);
     Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
             static_cast<int64_t>(fp.items.size()), 0, false, false};
     sp.ip = ip;
