@@ -5,30 +5,26 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC,-O2,-ffp-contract=off
 SRC := paper_1712_03439_b200/csrc
 OUT := paper_1712_03439_b200/_lib
-OBJS := $(OUT)/kernels.o $(OUT)/big.o $(OUT)/warp.o $(OUT)/large.o $(OUT)/ola2.o $(OUT)/sampler.o $(OUT)/features.o $(OUT)/api.o
+OBJS := $(OUT)/kernels.o $(OUT)/big.o $(OUT)/large.o $(OUT)/ola2.o $(OUT)/sampler.o $(OUT)/features.o $(OUT)/api.o
 
 REF_INC ?= /root/reference/proj/include
 ADAPTER := tests/cpp/_build/adapter_test
 
 all: $(OUT)/libroomsim_gpu.so oracle adapter
 
-$(OUT)/kernels.o: $(SRC)/kernels.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh $(SRC)/async.cuh
+$(OUT)/kernels.o: $(SRC)/kernels.cu $(SRC)/kernels.cuh $(SRC)/power.cuh $(SRC)/fft.cuh $(SRC)/async.cuh
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/kernels.ptxas.log || (cat $(OUT)/kernels.ptxas.log; false)
 
-$(OUT)/large.o: $(SRC)/large.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh $(SRC)/async.cuh
+$(OUT)/large.o: $(SRC)/large.cu $(SRC)/kernels.cuh $(SRC)/power.cuh $(SRC)/fft.cuh $(SRC)/async.cuh
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/large.ptxas.log || (cat $(OUT)/large.ptxas.log; false)
 
-$(OUT)/big.o: $(SRC)/big.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh
+$(OUT)/big.o: $(SRC)/big.cu $(SRC)/kernels.cuh $(SRC)/power.cuh $(SRC)/fft.cuh
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/big.ptxas.log || (cat $(OUT)/big.ptxas.log; false)
 
-$(OUT)/warp.o: $(SRC)/warp.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh
-	@mkdir -p $(OUT)
-	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/warp.ptxas.log || (cat $(OUT)/warp.ptxas.log; false)
-
-$(OUT)/ola2.o: $(SRC)/ola2.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh $(SRC)/fft2.cuh $(SRC)/async.cuh
+$(OUT)/ola2.o: $(SRC)/ola2.cu $(SRC)/kernels.cuh $(SRC)/power.cuh $(SRC)/fft.cuh $(SRC)/fft2.cuh $(SRC)/async.cuh
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/ola2.ptxas.log || (cat $(OUT)/ola2.ptxas.log; false)
 
@@ -36,11 +32,11 @@ $(OUT)/sampler.o: $(SRC)/sampler.cu $(SRC)/sampler.cuh include/roomsim_gpu.h
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(OUT)/features.o: $(SRC)/features.cu $(SRC)/kernels.cuh $(SRC)/fft.cuh
+$(OUT)/features.o: $(SRC)/features.cu $(SRC)/kernels.cuh $(SRC)/power.cuh $(SRC)/fft.cuh
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(OUT)/api.o: $(SRC)/api.cu $(SRC)/kernels.cuh include/roomsim_gpu.h
+$(OUT)/api.o: $(SRC)/api.cu $(SRC)/kernels.cuh $(SRC)/power.cuh include/roomsim_gpu.h
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 

@@ -113,7 +113,16 @@ int rs_truncate_rir(rs_ctx* ctx, const double* h, size_t n, double eta_db,
 
 /* ---- convolution (convolution.hpp:164-271) -------------------------------
  * x: nx doubles (mono AudioBuffer), h: nh doubles (Rir.samples), out:
- * nx+nh-1 doubles.  FP32 on the device.                                    */
+ * nx+nh-1 doubles.  The FFT strategies compute in FP32 on the device
+ * (max |err| <= 1e-5 of the peak); convolve_direct in FP64, bit-exact.
+ * rs_convolve dispatches on strategy like roomsim::convolve
+ * (convolution.hpp:258-271): RS_DIRECT -> rs_convolve_direct, RS_FULL_FFT ->
+ * rs_convolve_full_fft, RS_OVERLAP_ADD -> rs_convolve_ola (fft_size 0 is a
+ * PlanError, "overlap-add plan is missing an FFT size").                    */
+/* convolve_direct (convolution.hpp:164-179): the definition sum, FP64, with the
+ * reference's accumulation order (bit-exact). */
+int rs_convolve_direct(rs_ctx* ctx, const double* x, size_t nx, const double* h, size_t nh,
+                       double* out);
 int rs_convolve_ola(rs_ctx* ctx, const double* x, size_t nx, const double* h, size_t nh,
                     size_t fft_size, double* out);
 int rs_convolve_full_fft(rs_ctx* ctx, const double* x, size_t nx, const double* h,

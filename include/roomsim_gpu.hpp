@@ -8,6 +8,7 @@
 //   roomsim::gpu::truncate_rir      replaces roomsim::truncate_rir     (room_model.hpp:203-213)
 //   roomsim::gpu::convolve_ola      replaces roomsim::convolve_ola     (convolution.hpp:219-255)
 //   roomsim::gpu::convolve_full_fft replaces roomsim::convolve_full_fft(convolution.hpp:182-212)
+//   roomsim::gpu::convolve_direct   replaces roomsim::convolve_direct  (convolution.hpp:164-179), FP64 bit-exact
 //   roomsim::gpu::convolve          replaces roomsim::convolve         (convolution.hpp:258-271)
 //   roomsim::gpu::CudaRealFft       a RealFftEngine (fft.hpp:38-49) for the templated reference
 //                                   functions: roomsim::convolve_ola<roomsim::gpu::CudaRealFft>
@@ -143,10 +144,19 @@ inline AudioBuffer convolve_full_fft(const AudioBuffer& x, const Rir& h, Context
   return AudioBuffer::mono(std::move(out), x.sample_rate);
 }
 
+inline AudioBuffer convolve_direct(const AudioBuffer& x, const Rir& h, Context& ctx = default_context()) {
+  detail::check_io(x, h);
+  std::vector<double> out(x.num_frames() + h.samples.size() - 1);
+  check(rs_convolve_direct(ctx.get(), x.channel(0).data(), x.num_frames(), h.samples.data(),
+                           h.samples.size(), out.data()));
+  return AudioBuffer::mono(std::move(out), x.sample_rate);
+}
+
 inline AudioBuffer convolve(const AudioBuffer& x, const Rir& h, const ConvolutionPlan& plan,
                             Context& ctx = default_context()) {
   switch (plan.strategy) {
     case Strategy::direct:
+      return convolve_direct(x, h, ctx);
     case Strategy::full_fft:
       return convolve_full_fft(x, h, ctx);
     case Strategy::overlap_add:

@@ -350,17 +350,19 @@ double pair_flops(const PairPlan& p) {
 }
 
 // ---- stage B: spectrum + OLA over planned pairs --------------------------------
-// Pairs are bucketed by transform size; buckets run largest work first.  Each
-// pair's blocks are split into runs (K4 work items) long enough that the
+// Every pair's K4 variant is a function of its own (N, N_h) only (so are its power
+// partials, power.cuh): a pair renders to the same bytes whatever else shares its chunk.
+// Pairs are bucketed by (transform size, variant); buckets run largest work first.
+// Each pair's blocks are split into runs (K4 work items) long enough that the
 // recomputed overlap blocks cost <= ~6%, short enough to fill the GPU.
+enum K4Variant { kVarSmall = 0, kVarIp = 1, kVarOla2 = 2, kVarLarge = 3, kVarCount = 4 };
+
 struct Span {
   int l;
+  int var;
   int64_t list_off, list_n, item_off, item_n;
-  bool large;  // four-step path (large.cu)
-  bool two;    // two-stream K4 (ola2.cu): items in FilterPlan::items2
-  bool ip = false;     // in-place large-transform K4 (big.cu)
-  bool w = false;      // two-stream items on the warp-per-transform K4 (warp.cu)
-  int64_t max_nh = 1;  // largest N_h of the span (in-place K4 carry size)
+  int64_t max_nh = 1;  // largest N_h of the span (in-place / two-stream carry size)
+  int64_t max_l = 1;   // largest L of the span (two-stream input window)
 };
 
 // A batch of one large span (four-step path): pairs [pair_lo, pair_hi) of the
@@ -372,46 +374,54 @@ struct FilterPlan {
   std::vector<int32_t> lists;
   std::vector<OlaItem> items;
   std::vector<Span> spans;
-  std::vector<OlaItem2> items2;     // two-stream spans (part index = items.size() + i)
+  std::vector<OlaItem2> items2;     // two-stream spans
   std::vector<int2> units;          // large spans: (pair, block)
   std::vector<LargeBatch> batches;
   int64_t max_scratch = 0;          // complex elements of the largest batch's scratch
-  int64_t spec_total = 0, y_total = 0;
+  int64_t spec_total = 0, y_total = 0, part_total = 0;
   double flops = 0;
 };
 
-// Sizes that take the four-step path: measured faster than the one-CTA kernel at
-// M = 8192 and for every M > 16384 (tuning override: RSG_LARGE_MIN = smallest log2 M).
+// Sizes that take the four-step path: every M > 16384 and M = 8192 (measured faster than
+// the one-CTA kernel in the config-4 render, where few pairs have that size).  Tuning
+// override RSG_LARGE_MIN = smallest log2 M; RSG_IP_FORCE keeps M = 8192 in place (tests).
 bool use_large(int l) {
   static const int v = [] {
     const char* e = std::getenv("RSG_LARGE_MIN");
     return e ? std::atoi(e) : -1;
   }();
+  static const bool ip_force = std::getenv("RSG_IP_FORCE") != nullptr;
   if (l > kMaxLog2M) return true;
-  return v >= 0 ? l >= v : l == 13;
+  if (v >= 0) return l >= v;
+  return l == 13 && !ip_force;
 }
-// Sizes (log2 M) that take the in-place one-CTA K4 (big.cu) when its carry fits in
+// Largest N_h whose overlap carry fits next to the in-place K4's transform (0: none).
+int64_t ip_max_nh(int l) {
+  static int64_t cache[kMaxLog2M + 1];
+  static bool init = false;
+  if (!init) {
+    for (int k = 0; k <= kMaxLog2M; ++k) {
+      int64_t lo = 0, hi = int64_t(2) << k;  // N_h <= N
+      while (lo < hi) {  // largest nh with ip_supported(k, nh)
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (ip_supported(k, mid)) lo = mid; else hi = mid - 1;
+      }
+      cache[k] = lo;
+    }
+    init = true;
+  }
+  return l >= 0 && l <= kMaxLog2M ? cache[l] : 0;
+}
+// Sizes (log2 M) that take the in-place one-CTA K4 (big.cu) when the pair's carry fits in
 // shared memory (tuning override RSG_IP="lo,hi"; "0,0" disables it).
-bool use_ip(int l, int64_t max_nh) {
+bool use_ip(int l, int64_t nh) {
   static const std::pair<int, int> r = [] {
     const char* e = std::getenv("RSG_IP");
     int lo = 10, hi = 14;
     if (e) std::sscanf(e, "%d,%d", &lo, &hi);
     return std::make_pair(lo, hi);
   }();
-  return l >= r.first && l <= r.second && ip_supported(l, max_nh);
-}
-// Real FFT sizes (log2 N) that run the warp-per-transform two-stream K4 (warp.cu) when
-// their carries fit.  Off by default: measured 7-11% slower than the small-M K4 at
-// N = 512 / 1024 in the config-4 render; RSG_W="9,10" selects it.
-bool use_w(int log2n, int64_t max_nh) {
-  static const std::pair<int, int> r = [] {
-    const char* e = std::getenv("RSG_W");
-    int lo = 0, hi = -1;
-    if (e) std::sscanf(e, "%d,%d", &lo, &hi);
-    return std::make_pair(lo, hi);
-  }();
-  return log2n >= r.first && log2n <= r.second && w_supported(log2n, max_nh);
+  return l >= r.first && l <= r.second && nh <= ip_max_nh(l);
 }
 // Real FFT sizes (log2 N) that run the two-stream K4 (tuning override RSG_OLA2="lo,hi";
 // "0,0" disables it).
@@ -428,27 +438,42 @@ bool use_ola2(int log2n) {
   // (ncu launch list, B200); elsewhere K4 is as fast or faster
   return log2n == 8;
 }
+constexpr int kSmallMaxLog2MHost = 12;  // ola_small_kernel<M> sizes (kernels.cu)
+int k4_variant(int l, int64_t nh) {
+  if (use_large(l)) return kVarLarge;
+  if (use_ola2(l + 1)) return kVarOla2;
+  if (use_ip(l, nh)) return kVarIp;
+  if (l <= kSmallMaxLog2MHost) return kVarSmall;
+  return kVarLarge;  // M >= 8192 whose overlap carry does not fit in shared memory
+}
 
 constexpr int64_t kLargeScratchBytes = int64_t(1) << 31;  // per batch (16 M bytes per unit)
 
+// Blocks before a run start whose tails overlap it: ceil((N_h - 1) / L).
+int64_t pre_blocks(const PairPlan& p) {
+  const int64_t n = int64_t(1) << p.log2n;
+  return (n - p.L + p.L - 1) / p.L;
+}
+
 int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
   const int64_t n_pairs = static_cast<int64_t>(plans.size());
-  std::vector<std::vector<int32_t>> bucket(kLargeMaxLog2M + 1);
+  constexpr int NB = (kLargeMaxLog2M + 1) * kVarCount;
+  std::vector<std::vector<int32_t>> bucket(NB);
   std::vector<double> work(n_pairs);
   fp.flops = 0;
   for (int64_t p = 0; p < n_pairs; ++p) {
     const int l = plans[p].log2n - 1;
     if (l < 0 || l > kLargeMaxLog2M) return fail(RS_ERR_UNSUPPORTED, "FFT size outside the supported range");
-    bucket[l].push_back(static_cast<int32_t>(p));
+    bucket[l * kVarCount + k4_variant(l, plans[p].nh)].push_back(static_cast<int32_t>(p));
     work[p] = pair_flops(plans[p]);
     fp.flops += work[p];
   }
-  std::vector<int> order(kLargeMaxLog2M + 1);
+  std::vector<int> order(NB);
   std::iota(order.begin(), order.end(), 0);
-  std::vector<double> bucket_work(kLargeMaxLog2M + 1, 0.0);
-  for (int l = 0; l <= kLargeMaxLog2M; ++l)
-    for (int32_t p : bucket[l]) bucket_work[l] += work[p];
-  std::sort(order.begin(), order.end(), [&](int a, int b) { return bucket_work[a] > bucket_work[b]; });
+  std::vector<double> bucket_work(NB, 0.0);
+  for (int k = 0; k < NB; ++k)
+    for (int32_t p : bucket[k]) bucket_work[k] += work[p];
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return bucket_work[a] > bucket_work[b]; });
   fp.lists.clear();
   fp.items.clear();
   fp.spans.clear();
@@ -456,26 +481,21 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
   fp.items2.clear();
   fp.batches.clear();
   fp.max_scratch = 0;
-  for (int l : order) {
-    auto& v = bucket[l];
+  int64_t part_acc = 0;
+  for (int key : order) {
+    auto& v = bucket[key];
     if (v.empty()) continue;
-    int64_t bucket_nh = 1, bucket_blocks = 0, bucket_pre = 1;
+    const int l = key / kVarCount, var = key % kVarCount;
+    Span sp{l, var, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()), 0, 0};
+    int64_t total_blocks = 0, max_pre = 1;
     for (int32_t p : v) {
-      bucket_nh = std::max<int64_t>(bucket_nh, plans[p].nh);
-      bucket_blocks += plans[p].B;
-      const int64_t n = int64_t(1) << plans[p].log2n;
-      bucket_pre = std::max<int64_t>(bucket_pre, (n - 1) / plans[p].L);
+      sp.max_nh = std::max<int64_t>(sp.max_nh, plans[p].nh);
+      sp.max_l = std::max<int64_t>(sp.max_l, plans[p].L);
+      total_blocks += plans[p].B;
+      max_pre = std::max<int64_t>(max_pre, pre_blocks(plans[p]));
     }
-    // The in-place K4 runs one work item per CTA; at M = 8192 it needs enough items to
-    // fill the GPU once, else the four-step path (which splits every block) wins.
-    static const bool ip_force = std::getenv("RSG_IP_FORCE") != nullptr;  // tests: skip the work test
-    bool ip = use_ip(l, bucket_nh);
-    if (ip && l == 13 && !ip_force &&
-        bucket_blocks / (16 * bucket_pre) < 148LL * ip_resident(l, bucket_nh))
-      ip = false;
-    if (!ip && use_large(l)) {  // four-step path, batched by scratch size
-      Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
-              static_cast<int64_t>(fp.items.size()), 0, true, false};
+    if (var == kVarLarge) {  // four-step path, batched by scratch size
+      sp.item_off = static_cast<int64_t>(fp.items.size());
       const int64_t m = int64_t(1) << l;
       const int64_t per_batch = std::max<int64_t>(1, kLargeScratchBytes / (16 * m));
       LargeBatch bt{static_cast<int>(fp.spans.size()), 0, 0, static_cast<int64_t>(fp.units.size()), 0,
@@ -497,9 +517,11 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
         if (static_cast<int64_t>(fp.units.size()) - bt.unit_lo + pl.B > per_batch) close(i);
         const int64_t unit0 = static_cast<int64_t>(fp.units.size()) - bt.unit_lo;
         for (int64_t b = 0; b < pl.B; ++b) fp.units.push_back(make_int2(v[i], static_cast<int>(b)));
-        pl.item0 = static_cast<int64_t>(fp.items.size());
-        pl.nitems = (pl.out_len + large_tile() - 1) / large_tile();
-        for (int64_t tl = 0; tl < pl.nitems; ++tl)
+        const int64_t tiles = (pl.out_len + large_tile() - 1) / large_tile();
+        pl.part0 = part_acc;
+        pl.npart = static_cast<int32_t>(tiles);
+        part_acc += tiles;
+        for (int64_t tl = 0; tl < tiles; ++tl)
           fp.items.push_back(OlaItem{v[i], static_cast<int32_t>(tl), static_cast<int32_t>(unit0), 0});
       }
       close(static_cast<int64_t>(v.size()));
@@ -510,29 +532,22 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
     }
     // largest pairs first (LPT) so the tail of the launch is short
     std::stable_sort(v.begin(), v.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
-    const bool wk = !ip && use_w(l + 1, bucket_nh);
-    if (wk || use_ola2(l + 1)) {  // two-stream K4: items are pairs of runs of one pair
-      int64_t total_blocks = 0, max_pre = 1;
-      for (int32_t p : v) {
-        total_blocks += plans[p].B;
-        const int64_t n = int64_t(1) << plans[p].log2n;
-        max_pre = std::max<int64_t>(max_pre, (n - plans[p].L + plans[p].L - 1) / plans[p].L);
-      }
-      const int64_t slots = 148LL * (wk ? w_resident_items(l + 1, bucket_nh) : ola2_resident_items(l + 1));
-      const int64_t run = std::max<int64_t>((total_blocks + 12 * slots - 1) / (12 * slots), 16 * max_pre);
-      Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
-              static_cast<int64_t>(fp.items2.size()), 0, false, true};
-      sp.w = wk;
-      sp.max_nh = bucket_nh;
+    if (var == kVarOla2) {  // two-stream K4: an item is a pair of runs of one pair
+      // Runs of a fixed length per pair (>= 16 overlap blocks' worth, >= 24 blocks): the
+      // two runs sharing a complex transform round into each other, so which blocks pair
+      // up must not depend on the rest of the chunk.
+      sp.item_off = static_cast<int64_t>(fp.items2.size());
+      const int ppb = ola2_parts_per_block(l + 1);
       for (int32_t p : v) {
         PairPlan& pl = plans[p];
-        const int64_t n = int64_t(1) << pl.log2n;
-        const int64_t pre = (n - pl.L + pl.L - 1) / pl.L;
+        const int64_t pre = pre_blocks(pl);
+        const int64_t run = std::max<int64_t>(16 * pre, 24);
         int64_t nr = (pl.B + run - 1) / run;
         if (nr > 1 && (nr & 1)) ++nr;  // an even number of runs: two per item
         const int64_t len = (pl.B + nr - 1) / nr;
-        pl.item0 = -1 - static_cast<int64_t>(fp.items2.size());  // fixed up below
-        pl.nitems = 0;
+        pl.part0 = part_acc;
+        pl.npart = static_cast<int32_t>(pl.B * ppb);
+        part_acc += pl.B * ppb;
         for (int64_t r = 0; r < nr; r += 2) {
           OlaItem2 it{p, 0, 0, 0, static_cast<int32_t>(pl.B), static_cast<int32_t>(pl.B),
                       static_cast<int32_t>(pl.B), 0};
@@ -547,7 +562,6 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
             }
           }
           fp.items2.push_back(it);
-          ++pl.nitems;
         }
       }
       sp.item_n = static_cast<int64_t>(fp.items2.size()) - sp.item_off;
@@ -555,13 +569,8 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
       fp.lists.insert(fp.lists.end(), v.begin(), v.end());
       continue;
     }
-    int64_t total_blocks = 0, max_pre = 1;
-    for (int32_t p : v) {
-      total_blocks += plans[p].B;
-      const int64_t n = int64_t(1) << plans[p].log2n;
-      max_pre = std::max<int64_t>(max_pre, (n - plans[p].L + plans[p].L - 1) / plans[p].L);
-    }
-    const int64_t slots = 148LL * (ip ? ip_resident(l, bucket_nh) : ola_resident_groups(l));
+    const bool ip = var == kVarIp;
+    const int64_t slots = 148LL * (ip ? ip_resident(l, sp.max_nh) : ola_resident_groups(l));
     // work items per resident slot (measured, config 4): the in-place K4 prefers long runs
     // (each item stages its filter and twiddles), ola_small<512> too, the M <= 256 sizes
     // more items (shorter tails)
@@ -571,29 +580,25 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
     }();
     const int64_t run_div = run_div_env ? run_div_env : (ip ? 2 : (l <= 8 ? 12 : 3));
     const int64_t run = std::max<int64_t>((total_blocks + run_div * slots - 1) / (run_div * slots), 16 * max_pre);
-    Span sp{l, static_cast<int64_t>(fp.lists.size()), static_cast<int64_t>(v.size()),
-            static_cast<int64_t>(fp.items.size()), 0, false, false};
-    sp.ip = ip;
-    sp.max_nh = bucket_nh;
+    const int ppb = ip ? ip_parts_per_block(l) : small_parts_per_block(l);
+    sp.item_off = static_cast<int64_t>(fp.items.size());
     for (int32_t p : v) {
       PairPlan& pl = plans[p];
-      const int64_t n = int64_t(1) << pl.log2n;
-      const int64_t pre = (n - pl.L + pl.L - 1) / pl.L;  // ceil((N_h - 1) / L)
-      pl.item0 = static_cast<int64_t>(fp.items.size());
-      pl.nitems = 0;
+      const int64_t pre = pre_blocks(pl);
+      pl.part0 = part_acc;
+      pl.npart = static_cast<int32_t>(pl.B * ppb);
+      part_acc += pl.B * ppb;
       for (int64_t r0 = 0; r0 < pl.B; r0 += run) {
         const int64_t r1 = std::min<int64_t>(pl.B, r0 + run);
         const int64_t b0 = r0 == 0 ? 0 : std::max<int64_t>(0, r0 - pre);
         fp.items.push_back(OlaItem{p, static_cast<int32_t>(b0), static_cast<int32_t>(r0), static_cast<int32_t>(r1)});
-        ++pl.nitems;
       }
     }
     sp.item_n = static_cast<int64_t>(fp.items.size()) - sp.item_off;
     fp.spans.push_back(sp);
     fp.lists.insert(fp.lists.end(), v.begin(), v.end());
   }
-  for (auto& q : plans)  // two-stream items: part indices after the K4 / stage-D items
-    if (q.item0 < 0) q.item0 = static_cast<int64_t>(fp.items.size()) + (-1 - q.item0);
+  fp.part_total = part_acc;
   fp.spec_total = fp.y_total = 0;
   for (const auto& q : plans) {
     fp.spec_total = std::max<int64_t>(fp.spec_total, q.spec_off + (int64_t(1) << (q.log2n - 1)) + 1);
@@ -659,7 +664,7 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
   RS_TRY(upload_on(fb.olaitems, fp.items, st, arena));
   RS_TRY(fb.spec.ensure(std::max<int64_t>(fp.spec_total, 1) * sizeof(float2)));
   RS_TRY(fb.y.ensure(std::max<int64_t>(fp.y_total, 1) * sizeof(float)));
-  RS_TRY(fb.part.ensure(std::max<size_t>(fp.items.size() + fp.items2.size(), 1) * sizeof(double)));
+  RS_TRY(fb.part.ensure(std::max<int64_t>(fp.part_total, 1) * sizeof(double)));
   if (!fp.items2.empty()) RS_TRY(upload_on(fb.olaitems2, fp.items2, st, arena));
   if (!fp.batches.empty()) {
     RS_TRY(upload_on(fb.units, fp.units, st, arena));
@@ -667,8 +672,9 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
     RS_TRY(fb.yblk.ensure(fp.max_scratch * 2 * sizeof(float)));
   }
   const int32_t* d_lists = fb.lists.as<int32_t>();
+  double* d_part = fb.part.as<double>();
   for (const Span& sp : fp.spans) {
-    if (sp.large) continue;  // spectrum inside the four-step batches
+    if (sp.var == kVarLarge) continue;  // spectrum inside the four-step batches
     SpecArgs a{d_lists + sp.list_off, static_cast<int32_t>(sp.list_n), d_pair, fb.plan.as<PairPlan>(),
                d_rir, fb.spec.as<float2>(), c->tw[sp.l]};
     RS_CUDA(launch_spectrum(sp.l, a, st));
@@ -680,8 +686,7 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
   RS_CUDA(cudaEventRecord(c->side_fork, st));
   bool used[rs_ctx::kSide] = {};
   int next_side = 0;
-  auto side_for = [&](bool fresh) -> cudaStream_t {
-    static_cast<void>(fresh);
+  auto side_for = [&]() -> cudaStream_t {
     const int i = next_side++ % rs_ctx::kSide;
     if (!used[i]) {
       cudaStreamWaitEvent(c->side[i], c->side_fork, 0);
@@ -689,7 +694,7 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
     }
     return c->side[i];
   };
-  cudaStream_t large_st = fp.batches.empty() ? st : side_for(true);
+  cudaStream_t large_st = fp.batches.empty() ? st : side_for();
   for (const LargeBatch& bt : fp.batches) {
     const Span& sp = fp.spans[bt.span];
     int l1, l2;
@@ -697,7 +702,7 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
     LargeArgs a{fb.units.as<int2>() + bt.unit_lo, d_lists + sp.list_off + bt.pair_lo,
                 static_cast<int32_t>(bt.unit_hi - bt.unit_lo), static_cast<int32_t>(bt.pair_hi - bt.pair_lo),
                 d_pair, fb.plan.as<PairPlan>(), d_signals, d_rir, fb.spec.as<float2>(), fb.scratch.as<float2>(),
-                fb.yblk.as<float>(), fb.y.as<float>(), fb.part.as<double>() + bt.item_lo,
+                fb.yblk.as<float>(), fb.y.as<float>(), d_part,
                 fb.olaitems.as<OlaItem>() + bt.item_lo, static_cast<int32_t>(bt.item_hi - bt.item_lo),
                 c->tw[l1], c->tw[l2]};
     for (int stage = 0; stage < 6; ++stage) {
@@ -706,34 +711,23 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
     }
   }
   for (const Span& sp : fp.spans) {
-    if (!sp.two) continue;
-    int64_t max_nh = 1, max_l = 1;
-    for (int64_t i = 0; i < sp.list_n; ++i) {
-      const PairPlan& q = plans[fp.lists[sp.list_off + i]];
-      max_nh = std::max<int64_t>(max_nh, q.nh);
-      max_l = std::max<int64_t>(max_l, q.L);
+    if (sp.var == kVarOla2) {
+      Ola2Args a{fb.olaitems2.as<OlaItem2>() + sp.item_off, static_cast<int32_t>(sp.item_n), d_pair,
+                 fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(), d_part,
+                 c->tw2f[sp.l + 1], c->tw2i[sp.l + 1],
+                 static_cast<int32_t>((std::max<int64_t>(sp.max_nh - 1, 1) + 3) & ~int64_t(3)),
+                 static_cast<int32_t>((sp.max_l + 8 + 3) & ~int64_t(3))};
+      RS_CUDA(launch_ola2(sp.l + 1, a, side_for()));
+      ++c->launches;
+    } else if (sp.var == kVarSmall || sp.var == kVarIp) {
+      OlaArgs a{fb.olaitems.as<OlaItem>() + sp.item_off, static_cast<int32_t>(sp.item_n), d_pair,
+                fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(), d_part, c->tw[sp.l]};
+      if (sp.var == kVarIp)
+        RS_CUDA(launch_ola_ip(sp.l, a, sp.max_nh, side_for()));
+      else
+        RS_CUDA(launch_ola(sp.l, a, side_for()));
+      ++c->launches;
     }
-    Ola2Args a{fb.olaitems2.as<OlaItem2>() + sp.item_off, static_cast<int32_t>(sp.item_n), d_pair,
-               fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(),
-               fb.part.as<double>() + fp.items.size() + sp.item_off, c->tw2f[sp.l + 1], c->tw2i[sp.l + 1],
-               static_cast<int32_t>((std::max<int64_t>(max_nh - 1, 1) + 3) & ~int64_t(3)),
-               static_cast<int32_t>((max_l + 8 + 3) & ~int64_t(3))};
-    if (sp.w)
-      RS_CUDA(launch_ola_w(sp.l + 1, a, side_for(false)));
-    else
-      RS_CUDA(launch_ola2(sp.l + 1, a, side_for(false)));
-    ++c->launches;
-  }
-  for (const Span& sp : fp.spans) {
-    if (sp.large || sp.two) continue;
-    OlaArgs a{fb.olaitems.as<OlaItem>() + sp.item_off, static_cast<int32_t>(sp.item_n), d_pair,
-              fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(),
-              fb.part.as<double>() + sp.item_off, c->tw[sp.l]};
-    if (sp.ip)
-      RS_CUDA(launch_ola_ip(sp.l, a, sp.max_nh, side_for(false)));
-    else
-      RS_CUDA(launch_ola(sp.l, a, side_for(false)));
-    ++c->launches;
   }
   for (int i = 0; i < rs_ctx::kSide; ++i)  // join
     if (used[i]) {
@@ -1121,7 +1115,7 @@ int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO
               ch.d_utt_J.as<int32_t>(), ch.fb.part.as<double>(), ch.d_snr.as<double>() - s_first,
               ch.d_gain.as<double>(), ch.d_power.as<double>(), ch.d_flags.as<int32_t>(), ch.P};
   RS_CUDA(launch_gain(ga, sB));
-  ++c->launches;
+  c->launches += 2;
   MixArgs ma{ch.d_chan_utt.as<int64_t>(), ch.d_chan_mic.as<int32_t>(), ch.d_chan_out.as<int64_t>(),
              ch.d_utt_len.as<int64_t>(), ch.d_utt_stride.as<int64_t>(), ch.d_utt_pair0.as<int64_t>(),
              ch.d_utt_I.as<int32_t>(), ch.d_utt_J.as<int32_t>(), ch.fb.plan.as<PairPlan>(), ch.fb.y.as<float>(),
@@ -1691,11 +1685,36 @@ int rs_convolve_full_fft(rs_ctx* c, const double* x, size_t nx, const double* h,
   return convolve_host(c, x, nx, h, nh, fft_size_for(nx + nh - 1), out);
 }
 
+int rs_convolve_direct(rs_ctx* c, const double* x, size_t nx, const double* h, size_t nh, double* out) {
+  RS_TRY(check_ctx(c));
+  if (nx == 0) return fail(RS_ERR_DEGENERATE, "convolution input must be non-empty mono audio");
+  if (nh == 0) return fail(RS_ERR_DEGENERATE, "empty impulse response");
+  const size_t ol = nx + nh - 1;
+  RS_TRY(c->scratch_a.ensure((nx + nh) * sizeof(double)));
+  RS_TRY(c->scratch_b.ensure(ol * sizeof(double)));
+  double* dx = c->scratch_a.as<double>();
+  double* dh = dx + nx;
+  RS_CUDA(cudaMemcpyAsync(dx, x, nx * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  RS_CUDA(cudaMemcpyAsync(dh, h, nh * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  if (c->profiling) RS_CUDA(cudaEventRecord(c->ev0, c->stream));
+  RS_CUDA(launch_direct_conv(dx, static_cast<int64_t>(nx), dh, static_cast<int64_t>(nh), c->scratch_b.as<double>(),
+                             c->stream));
+  if (c->profiling) RS_CUDA(cudaEventRecord(c->ev1, c->stream));
+  RS_CUDA(cudaMemcpyAsync(out, c->scratch_b.p, ol * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  RS_CUDA(cudaStreamSynchronize(c->stream));
+  RS_TRY(finish_timing(c));
+  c->launches = 1;
+  c->ola_flops = 2.0 * static_cast<double>(nx) * static_cast<double>(nh);
+  c->alg_bytes = 8.0 * (nx + nh + ol);
+  return RS_OK;
+}
+
 int rs_convolve(rs_ctx* c, const double* x, size_t nx, const double* h, size_t nh, int strategy,
                 size_t fft_size, double* out) {
   RS_TRY(check_ctx(c));
   switch (strategy) {
     case RS_DIRECT:
+      return rs_convolve_direct(c, x, nx, h, nh, out);
     case RS_FULL_FFT:
       return rs_convolve_full_fft(c, x, nx, h, nh, out);
     case RS_OVERLAP_ADD:

@@ -36,6 +36,7 @@
 
 #include "fft.cuh"
 #include "kernels.cuh"
+#include "power.cuh"
 
 namespace rsg {
 namespace {
@@ -245,7 +246,6 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
   float2* gs = tws + ((SH::TWN + 1) & ~1);
   float2* ws = gs + (GS ? SH::GSN : 0);
   float* carry = reinterpret_cast<float*>(ws + (GS ? SH::WSN : 0));
-  __shared__ double red[T / 32];
   const int t = threadIdx.x;
   const OlaItem it = a.items[blockIdx.x];
   const PairPlan& pl = a.plan[it.pair];
@@ -285,7 +285,6 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
     prefetch_l2(x + s0, 4 * (nx - s0 < L ? nx - s0 : L));
   }
   __syncthreads();
-  double pw = 0.0;
 #pragma unroll 1
   for (int b = it.b_begin; b < it.b_end; ++b) {
     const long long start = static_cast<long long>(b) * L;
@@ -386,15 +385,8 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
         }
       }
     }
-    pw += static_cast<double>((pb[0] + pb[1]) + (pb[2] + pb[3]));
-  }
-  for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
-  if ((t & 31) == 0) red[t >> 5] = pw;
-  __syncthreads();
-  if (t == 0) {
-    double tot = 0.0;
-    for (int w = 0; w < T / 32; ++w) tot += red[w];
-    a.part[blockIdx.x] = tot;
+    store_block_power<T>(a.part + pl.part0 + static_cast<long long>(b) * parts_per_block_of(T),
+                         (pb[0] + pb[1]) + (pb[2] + pb[3]), t, b >= it.b_own);
   }
 }
 
@@ -458,6 +450,11 @@ int ip_resident(int log2m, int64_t max_nh) {
   const int by_smem = static_cast<int>((228 * 1024) / need);
   const int by_threads = 2048 / ip_threads_of(log2m);
   return std::max(1, std::min(std::min(by_smem, by_threads), ip_minb_of(log2m)));
+}
+
+int ip_parts_per_block(int log2m) {
+  RSG_IP_DISPATCH(log2m, parts_per_block_of(IpPlan<M>::T))
+  return 0;
 }
 
 cudaError_t launch_ola_ip(int log2m, const OlaArgs& a, int64_t max_nh, cudaStream_t s) {

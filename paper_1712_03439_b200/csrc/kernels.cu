@@ -14,6 +14,7 @@
 #include "async.cuh"
 #include "fft.cuh"
 #include "kernels.cuh"
+#include "power.cuh"
 
 #ifndef RSG_E
 #define RSG_E 16
@@ -22,9 +23,6 @@
 #define RSG_E_SMALL 8
 #endif
 
-#ifndef RSG_OLA_MINB
-#define RSG_OLA_MINB 1
-#endif
 
 namespace rsg {
 
@@ -659,9 +657,6 @@ ola_small_kernel(OlaArgs a) {
     }
   }
 #endif
-  double pw = 0.0;
-  constexpr int R = PL::radix(PL::NP - 1);
-  constexpr int NB = PL::E / R;
 #pragma unroll 1
   for (int k = 0; k < trips; ++k) {
     const int b = it.b_begin + k;
@@ -744,117 +739,10 @@ ola_small_kernel(OlaArgs a) {
       }
     };
     stockham_emit_pass<M, GroupBar<T>, decltype(emit_fn), true, false>(s, t, tws, active, bar, emit_fn);
-    pw += static_cast<double>((pb[0] + pb[1]) + (pb[2] + pb[3]));
+    store_block_power<T>(a.part + pl.part0 + static_cast<long long>(b) * parts_per_block_of(T),
+                         (pb[0] + pb[1]) + (pb[2] + pb[3]), t, active && b >= it.b_own);
     // (N_h - 1 > L, three or more overlapping blocks, needs no extra step: the
     // old carry at e in [L, N_h - 1) comes from the other buffer.)
-  }
-  // Σ y^2 of the group (fixed order: deterministic) -> part[item]
-  if constexpr (T >= 32) {
-    __shared__ double red[CTA / 32];
-    for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pw;
-    bar();
-    if (t == 0 && has) {
-      double tot = 0.0;
-      for (int w = 0; w < T / 32; ++w) tot += red[g * (T / 32) + w];
-      a.part[item] = tot;
-    }
-  } else {
-    for (int o = T / 2; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
-    if (t == 0 && has) a.part[item] = pw;
-  }
-}
-
-template <int M>
-__global__ void __launch_bounds__(cta_threads_of(Plan<M>::LOG), (M >= 8192 ? 1 : RSG_OLA_MINB))
-ola_kernel(OlaArgs a) {
-  using PL = Plan<M>;
-  extern __shared__ __align__(16) float2 smem[];
-  constexpr int T = PL::T;
-  constexpr int G = groups_of<M>();
-  constexpr int N = 2 * M;
-  const int g = threadIdx.x / T, t0 = threadIdx.x % T;
-  const int item = blockIdx.x * G + g;
-  const bool has = item < a.count;
-  const OlaItem it = a.items[has ? item : 0];
-  const PairPlan& pl = a.plan[it.pair];
-  const PairMeta& pm = a.pair[it.pair];
-  const float* __restrict__ x = a.signals + pm.sig_off;
-  const long long nx = pm.nx;
-  const float2* __restrict__ Gs = a.spec + pl.spec_off;
-  const float2* W = a.tw + PL::TW_PASS;
-  float* __restrict__ y = a.y + pl.y_off;
-  const int L = static_cast<int>(pl.L);
-  const int B = static_cast<int>(pl.B);
-  const int out_len = static_cast<int>(pl.out_len);
-  const int ovl = N - L;  // N_h - 1 samples overlap the next block
-  float2* s = smem + g * PL::PADDED;
-  const GroupBar<T> bar{1 + g};
-  int trips = has ? it.b_end - it.b_begin : 0;
-  if constexpr (T < 32 && T > 1) trips = __reduce_max_sync(0xffffffffu, trips);
-  if constexpr (T == 1) trips = __reduce_max_sync(0xffffffffu, trips);
-  const long long own_lo = static_cast<long long>(it.b_own) * L;
-  const long long own_hi = it.b_end == B ? out_len : static_cast<long long>(it.b_end) * L;
-  double pw = 0.0;
-#pragma unroll 1
-  for (int k = 0; k < trips; ++k) {
-    const int b = it.b_begin + k;
-    const bool active = has && b < it.b_end;
-    const long long start = static_cast<long long>(b) * L;
-    const int take = active ? static_cast<int>(nx - start < L ? nx - start : L) : 0;
-    // the thread index laundered per block: keeps the compiler from hoisting every
-    // pass's loop-invariant smem addresses out of the block loop (which spills)
-    int t;
-    asm volatile("mov.b32 %0, %1;" : "=r"(t) : "r"(t0));
-    first_pass<M>(s, t, active, x + start, take, bar);
-#ifndef RSG_NO_FWD
-    forward_rest<M>(s, t, a.tw, active, bar);
-#endif
-#ifndef RSG_NO_MUL
-    spectral_multiply<M>(s, t, Gs, W, active, bar);
-#endif
-#ifndef RSG_NO_INV
-    inverse_but_last<M>(s, t, a.tw, active, bar);
-#endif
-    const bool rmw = b > it.b_begin;  // this item's previous block wrote the overlap
-    float* yb = y + start;
-    // element offsets e in [0, N) relative to the block start (32-bit)
-    const int lo = static_cast<int>(max(own_lo - start, -1ll));
-    const int hi = static_cast<int>(min(own_hi - start, static_cast<long long>(N)));
-    const int fe = (b == B - 1) ? N : L;  // e < fe: final after block b
-    const int rmw_end = rmw ? ovl : 0;
-    stockham_emit_pass<M>(s, t, a.tw, active, bar, [&](int, int, int c, float2 v) {
-#ifdef RSG_TRIVIAL_EMIT
-      yb[2 * c] = v.x; yb[2 * c + 1] = v.y;
-#else
-      const int e0 = 2 * c, e1 = e0 + 1;
-      if (e0 >= lo && e0 < hi) {
-        const float acc = e0 < rmw_end ? yb[e0] + v.x : v.x;
-        yb[e0] = acc;
-        if (e0 < fe) pw = fma(static_cast<double>(acc), static_cast<double>(acc), pw);
-      }
-      if (e1 >= lo && e1 < hi) {
-        const float acc = e1 < rmw_end ? yb[e1] + v.y : v.y;
-        yb[e1] = acc;
-        if (e1 < fe) pw = fma(static_cast<double>(acc), static_cast<double>(acc), pw);
-      }
-#endif
-    });
-  }
-  // Σ y^2 of the group (fixed order: deterministic) -> part[item]
-  if constexpr (T >= 32) {
-    __shared__ double red[cta_threads_of(PL::LOG) / 32];
-    for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pw;
-    bar();
-    if (t0 == 0 && has) {
-      double tot = 0.0;
-      for (int w = 0; w < T / 32; ++w) tot += red[g * (T / 32) + w];
-      a.part[item] = tot;
-    }
-  } else {
-    for (int o = T / 2; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
-    if (t0 == 0 && has) a.part[item] = pw;
   }
 }
 
@@ -941,9 +829,6 @@ static cudaError_t set_attrs() {
     if ((e = cudaFuncSetAttribute(ola_small_kernel<M>, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
     if ((e = cudaFuncSetAttribute(ola_small_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(k4_smem_bytes(Plan<M>::LOG))))) return e;
-  } else {
-    if ((e = cudaFuncSetAttribute(ola_kernel<M>, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
-    if ((e = cudaFuncSetAttribute(ola_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   }
   if ((e = cudaFuncSetAttribute(rir_spectrum_kernel<M>, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
   if ((e = cudaFuncSetAttribute(rir_spectrum_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
@@ -975,12 +860,12 @@ static cudaError_t ola_t(const OlaArgs& a, cudaStream_t s) {
   if constexpr (Plan<M>::LOG <= kSmallMaxLog2M) {
     constexpr int CTA = k4_cta_of(Plan<M>::LOG), G = CTA / Plan<M>::T;
     ola_small_kernel<M><<<(a.count + G - 1) / G, CTA, k4_smem_bytes(Plan<M>::LOG), s>>>(a);
-  } else {
-    constexpr int G = groups_of<M>();
-    ola_kernel<M><<<(a.count + G - 1) / G, cta_threads_of(Plan<M>::LOG), k4_smem_bytes(Plan<M>::LOG), s>>>(a);
+    return cudaGetLastError();
   }
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;  // M > 4096: the in-place (big.cu) or four-step (large.cu) K4
 }
+
+int small_parts_per_block(int log2m) { return parts_per_block_of((1 << log2m) / e_of(log2m)); }
 
 template <int M>
 static cudaError_t rfft_t(bool inverse, const float* in_real, const float2* in_spec,
@@ -1037,26 +922,33 @@ cudaError_t launch_rfft(int log2m, bool inverse, const float* in_real, const flo
 // K5: SNR gains.  alpha_ij = sqrt(P_0j / (P_ij 10^(snr_i/10)))
 // with P = mean_power (audio_buffer.hpp:66-75) = Σy^2 / len; alpha_0j = 1.
 // ============================================================================
-__device__ __forceinline__ double pair_sumsq(const GainArgs& a, long long p) {
+// K5a: mean power of every pair from its K4 partials (power.cuh): a warp per pair, lane l
+// summing partials l, l + 32, ... then a fixed butterfly — one order per pair.
+__global__ void __launch_bounds__(256) power_kernel(GainArgs a) {
+  const long long p = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= a.n_pairs) return;  // warp-uniform
   const PairPlan& pl = a.plan[p];
+  const double* part = a.part + pl.part0;
   double s = 0.0;
-  for (int k = 0; k < pl.nitems; ++k) s += a.part[pl.item0 + k];  // item order: deterministic
-  return s;
+  for (int k = lane; k < pl.npart; k += 32) s += part[k];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) a.power[p] = s / static_cast<double>(pl.out_len);
 }
 
+// K5b: gains from the powers; alpha_0j = 1.
 __global__ void gain_kernel(GainArgs a) {
   const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (p >= a.n_pairs) return;
   const PairMeta& pm = a.pair[p];
   const long long p0 = a.utt_pair0[pm.utt] + pm.mic_local;  // target pair at mic j
-  const double P = pair_sumsq(a, p) / static_cast<double>(a.plan[p].out_len);
-  a.power[p] = P;
+  const double P = a.power[p];
   if (pm.src_local == 0) {
     a.gain[p] = 1.0;
     if (!(P > 0.0)) a.flags[p] |= 4;
     return;
   }
-  const double Pt = pair_sumsq(a, p0) / static_cast<double>(a.plan[p0].out_len);
+  const double Pt = a.power[p0];
   if (!(P > 0.0) || !(Pt > 0.0)) {
     a.flags[p] |= 4;
     a.gain[p] = 0.0;
@@ -1067,6 +959,7 @@ __global__ void gain_kernel(GainArgs a) {
 
 cudaError_t launch_gain(const GainArgs& a, cudaStream_t s) {
   if (a.n_pairs == 0) return cudaSuccess;
+  power_kernel<<<static_cast<unsigned>((a.n_pairs + 7) / 8), 256, 0, s>>>(a);
   gain_kernel<<<static_cast<unsigned>((a.n_pairs + 255) / 256), 256, 0, s>>>(a);
   return cudaGetLastError();
 }
@@ -1181,6 +1074,55 @@ cudaError_t launch_pcie_copy(void* dst, const void* src, size_t bytes, cudaStrea
   const size_t n16 = bytes / 16 + 1;
   const unsigned blocks = static_cast<unsigned>(std::min<size_t>((n16 + 255) / 256, 148 * 4));
   pcie_copy_kernel<<<blocks, 256, 0, s>>>(static_cast<char*>(dst), static_cast<const char*>(src), bytes);
+  return cudaGetLastError();
+}
+
+// ---- convolve_direct (convolution.hpp:164-179), FP64, bit-exact ----------------------
+// The reference accumulates out[i + j] += x[i] * h[j] with i outermost, so out[n] receives
+// x[i] * h[n - i] for ascending i, starting from 0.0.  One thread per output sample adds
+// the same products in the same order with round-to-nearest multiply and add (no FMA
+// contraction): the result equals the reference bit for bit.  The h window of a CTA's 256
+// outputs and the x samples it needs are staged through shared memory in 256-sample tiles.
+__global__ void __launch_bounds__(256) direct_conv_kernel(const double* __restrict__ x, int64_t nx,
+                                                          const double* __restrict__ h, int64_t nh,
+                                                          double* __restrict__ out) {
+  __shared__ double xs[256];
+  __shared__ double hs[512];
+  const int64_t n0 = static_cast<int64_t>(blockIdx.x) * 256;
+  const int64_t n = n0 + threadIdx.x;
+  const int64_t out_len = nx + nh - 1;
+  // i ranges over [max(0, n - nh + 1), min(n, nx - 1)]; the CTA's union:
+  const int64_t i_lo = n0 - nh + 1 > 0 ? n0 - nh + 1 : 0;
+  const int64_t i_hi = (n0 + 255 < nx - 1 ? n0 + 255 : nx - 1);
+  double acc = 0.0;
+  for (int64_t i0 = i_lo; i0 <= i_hi; i0 += 256) {
+    __syncthreads();
+    const int64_t i = i0 + threadIdx.x;
+    xs[threadIdx.x] = i <= i_hi ? x[i] : 0.0;
+    // h[n - i] for this tile: n - i in (n0 - i0 - 256, n0 + 255 - i0]; stage 512 taps
+    // starting at j0 = n0 - i0 - 255
+    const int64_t j0 = n0 - i0 - 255;
+    for (int k = threadIdx.x; k < 512; k += 256) {
+      const int64_t j = j0 + k;
+      hs[k] = (j >= 0 && j < nh) ? h[j] : 0.0;
+    }
+    __syncthreads();
+    if (n < out_len) {
+      const int64_t a = n - nh + 1 > i0 ? n - nh + 1 : i0;        // first i of this tile for n
+      const int64_t bnd = n < i0 + 255 ? n : i0 + 255;
+      const int64_t b = bnd < i_hi ? bnd : i_hi;                  // last i
+      for (int64_t ii = a; ii <= b; ++ii)
+        acc = __dadd_rn(acc, __dmul_rn(xs[ii - i0], hs[(n - ii) - j0]));
+    }
+  }
+  if (n < out_len) out[n] = acc;
+}
+
+cudaError_t launch_direct_conv(const double* x, int64_t nx, const double* h, int64_t nh, double* out,
+                               cudaStream_t s) {
+  const int64_t out_len = nx + nh - 1;
+  if (out_len <= 0) return cudaSuccess;
+  direct_conv_kernel<<<static_cast<unsigned>((out_len + 255) / 256), 256, 0, s>>>(x, nx, h, nh, out);
   return cudaGetLastError();
 }
 

@@ -50,8 +50,8 @@ struct PairPlan {
   int64_t B;         // block count
   int64_t out_len;   // N_x + N_h - 1
   int32_t log2n;     // N = 2^log2n
-  int32_t nitems;    // K4 work items of this pair (consecutive)
-  int64_t item0;     // global index of the pair's first work item
+  int32_t npart;     // power partials of this pair (consecutive, see power.cuh)
+  int64_t part0;     // index of the pair's first power partial
 };
 
 // K4 work item: a run of OLA blocks of one pair.  The item owns output
@@ -108,7 +108,7 @@ struct OlaArgs {
   const float* signals;
   const float2* spec;
   float* y;             // reverberant pair signals
-  double* part;         // per item Σ y^2 over its final samples (FP64)
+  double* part;         // power partials: block b, warp w of a pair at plan.part0 + b * ppb + w
   const float2* tw;
 };
 
@@ -133,7 +133,7 @@ struct GainArgs {
   const PairPlan* plan;
   const int64_t* utt_pair0;
   const int32_t* utt_J;
-  const double* part;         // per K4 item Σ y^2; summed per pair in item order
+  const double* part;         // power partials (PairPlan::part0 / npart), summed in a fixed order
   const double* snr_lin;      // per global source: pow(10, snr/10) (host std::pow)
   double* gain;
   double* power;
@@ -158,17 +158,13 @@ struct Ola2Args {
   const float* signals;
   const float2* spec;   // K3's G = H / (2N), k in [0, N/2]
   float* y;
-  double* part;         // per item: Σ y^2 over both runs' owned samples
+  double* part;         // power partials (as OlaArgs::part, per run's block)
   const float2* twf;    // PlanC<N, false> pass tables
   const float2* twi;    // PlanC<N, true> pass tables
   int32_t ccap;         // floats per carry buffer: >= max N_h - 1 of the launch, multiple of 4
   int32_t scap;         // floats per input window: >= max L + 8 of the launch, multiple of 4
 };
 constexpr int kOla2MinLog2N = 5, kOla2MaxLog2N = 12;
-// Two-stream, warp-per-transform K4 for N = 512, 1024 (warp.cu), on Ola2Args (twf/twi unused).
-bool w_supported(int log2n, int64_t max_nh);
-int w_resident_items(int log2n, int64_t max_nh);  // work items resident per SM
-cudaError_t launch_ola_w(int log2n, const Ola2Args& a, cudaStream_t s);
 bool ola2_supported(int log2n);
 int ola2_resident_items(int log2n);
 int ola2_tw_total(int log2n, bool rev);
@@ -211,7 +207,7 @@ struct LargeArgs {
   float2* scratch;           // per unit: M complex
   float* yblk;               // per unit: N = 2M block output samples
   float* y;
-  double* part;              // per stage-D item (indexed like `items`)
+  double* part;              // power partials: one per stage-D tile at plan.part0 + tile
   const OlaItem* items;      // stage-D tiles: {pair, tile, unit of block 0, 0}
   int32_t n_items;
   const float2* tw1;         // Plan<M1> twiddle tables
@@ -227,6 +223,12 @@ cudaError_t launch_large(int log2m, const LargeArgs& a, int stage, cudaStream_t 
 cudaError_t launch_large_rfft(int log2m, bool inverse, const float* in_real, const float2* in_spec,
                               float* out_real, float2* out_spec, int count, float2* scratch,
                               const float2* tw1, const float2* tw2, cudaStream_t s);
+
+// Power partials per OLA block of each K4 variant (one per warp of the group that
+// transforms the block; power.cuh).
+int small_parts_per_block(int log2m);  // ola_small_kernel<M>
+int ip_parts_per_block(int log2m);     // ola_ip_kernel<M>
+int ola2_parts_per_block(int log2n);   // ola2_kernel<N> (per run's block)
 
 // ---- launchers (kernels.cu) --------------------------------------------------
 // In-place one-CTA K4 for M = 8192, 16384 (big.cu); the carry (N_h - 1 floats) must fit
@@ -255,7 +257,7 @@ cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int sli
 cudaError_t launch_cut(const CutArgs& a, int n_pairs, cudaStream_t s);
 cudaError_t launch_spectrum(int log2m, const SpecArgs& a, cudaStream_t s);
 cudaError_t launch_ola(int log2m, const OlaArgs& a, cudaStream_t s);
-cudaError_t launch_gain(const GainArgs& a, cudaStream_t s);
+cudaError_t launch_gain(const GainArgs& a, cudaStream_t s);  // K5: power (warp per pair) + gains
 cudaError_t launch_mix(const MixArgs& a, int64_t n_chan, int64_t max_len, cudaStream_t s);
 // dst/src: device or mapped-pinned-host pointers, 16-byte aligned
 cudaError_t launch_pcie_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
@@ -263,6 +265,9 @@ cudaError_t launch_pcie_copy(void* dst, const void* src, size_t bytes, cudaStrea
 cudaError_t launch_rfft(int log2m, bool inverse, const float* in_real, const float2* in_spec,
                         float* out_real, float2* out_spec, int count, const float2* tw,
                         cudaStream_t s);
+// convolve_direct (convolution.hpp:164-179): FP64, bit-exact, out has nx + nh - 1 doubles
+cudaError_t launch_direct_conv(const double* x, int64_t nx, const double* h, int64_t nh, double* out,
+                               cudaStream_t s);
 cudaError_t launch_convert_d2f(const double* in, float* out, int64_t n, cudaStream_t s);
 cudaError_t launch_convert_f2d(const float* in, double* out, int64_t n, cudaStream_t s);
 

@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(256) large_ola_sum(LargeArgs a, long long n_ff
     y[n] = acc;
     pw = fma(static_cast<double>(acc), static_cast<double>(acc), pw);
   }
+  // the tile's partial (fixed order) -> the pair's slot of this tile (power.cuh)
   __shared__ double red[8];
   for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pw;
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(256) large_ola_sum(LargeArgs a, long long n_ff
   if (threadIdx.x == 0) {
     double tot = 0.0;
     for (int w = 0; w < 8; ++w) tot += red[w];
-    a.part[item] = tot;
+    a.part[pl.part0 + it.b_begin] = tot;
   }
 }
 

@@ -15,6 +15,7 @@
 #include "async.cuh"
 #include "fft2.cuh"
 #include "kernels.cuh"
+#include "power.cuh"
 
 namespace rsg {
 namespace {
@@ -142,7 +143,6 @@ __global__ void __launch_bounds__(ola2_cta(ilog2(N)), ola2_minb(ilog2(N))) ola2_
     prefetch(0, 0);
     prefetch(1, 0);
   }
-  double pw = 0.0;
 #pragma unroll 1
   for (int k = 0; k < trips; ++k) {
     int b[2], d[2] = {0, 0}, take[2] = {0, 0};
@@ -208,22 +208,10 @@ __global__ void __launch_bounds__(ola2_cta(ilog2(N)), ola2_minb(ilog2(N))) ola2_
         }
       }
     });
-    pw += static_cast<double>(pb[0] + pb[1]);
-  }
-  // Σ y^2 of both runs' owned samples (fixed order) -> part[item]
-  if constexpr (T >= 32) {
-    for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
-    __shared__ double red[CTA / 32];
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pw;
-    __syncthreads();
-    if (t == 0 && has) {
-      double tot = 0.0;
-      for (int w = 0; w < T / 32; ++w) tot += red[g * (T / 32) + w];
-      a.part[item] = tot;
-    }
-  } else {
-    for (int o = T / 2; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
-    if (t == 0 && has) a.part[item] = pw;
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+      store_block_power<T>(a.part + pl.part0 + static_cast<long long>(b[r]) * parts_per_block_of(T), pb[r], t,
+                           act[r] && b[r] >= ro[r]);
   }
 }
 
@@ -265,6 +253,8 @@ void fill_c(float2* h) {
 }  // namespace
 
 bool ola2_supported(int log2n) { return log2n >= kOla2MinLog2N && log2n <= kOla2MaxLog2N; }
+
+int ola2_parts_per_block(int log2n) { return parts_per_block_of(ola2_t_of(log2n)); }
 
 int ola2_resident_items(int log2n) {
   const int cta = ola2_cta(log2n), t = ola2_t_of(log2n);

@@ -96,7 +96,7 @@ ABI_SYMBOLS = [
     "rs_ctx_synchronize", "rs_ctx_last_timing", "rs_ctx_stage_times", "rs_ctx_set_profiling", "rs_cost_direct",
     "rs_cost_full_fft", "rs_cost_ola", "rs_ola_block_count", "rs_plan_for", "rs_choose_plan",
     "rs_rfft_forward", "rs_rfft_inverse", "rs_synthesize_rir", "rs_truncate_rir",
-    "rs_convolve_ola", "rs_convolve_full_fft", "rs_convolve", "rs_batch_num_pairs",
+    "rs_convolve_ola", "rs_convolve_full_fft", "rs_convolve_direct", "rs_convolve", "rs_batch_num_pairs",
     "rs_render_batch", "rs_render_batch_device", "rs_last_pair_signal", "rs_last_pair_rir",
     "rs_sampler_counts", "rs_sample_scenes", "rs_sampler_counts_device", "rs_sample_scenes_device",
     "rs_generate_signals_host", "rs_generate_signals", "rs_logmel_shape", "rs_logmel_device",
@@ -150,6 +150,7 @@ def load_library() -> C.CDLL:
         "rs_truncate_rir": (C.c_int, [vp, vp, sz, d, szp, szp, dp]),
         "rs_convolve_ola": (C.c_int, [vp, vp, sz, vp, sz, sz, vp]),
         "rs_convolve_full_fft": (C.c_int, [vp, vp, sz, vp, sz, vp]),
+        "rs_convolve_direct": (C.c_int, [vp, vp, sz, vp, sz, vp]),
         "rs_convolve": (C.c_int, [vp, vp, sz, vp, sz, C.c_int, sz, vp]),
         "rs_batch_num_pairs": (i64, [vp]),
         "rs_render_batch": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
@@ -378,6 +379,11 @@ def convolve_full_fft(x, h, ctx: Optional[Context] = None) -> np.ndarray:
     return _conv(load_library().rs_convolve_full_fft, x, h, ctx=ctx)
 
 
+def convolve_direct(x, h, ctx: Optional[Context] = None) -> np.ndarray:
+    """roomsim::convolve_direct (convolution.hpp:164-179): FP64 on the device, bit-exact."""
+    return _conv(load_library().rs_convolve_direct, x, h, ctx=ctx)
+
+
 def convolve(x, h, plan: ConvolutionPlan, ctx: Optional[Context] = None) -> np.ndarray:
     """roomsim::convolve (convolution.hpp:258-271)."""
     return _conv(load_library().rs_convolve, x, h, int(plan.strategy), int(plan.fft_size or 0), ctx=ctx)
@@ -486,20 +492,27 @@ def sample_batch(spec: RsSamplerSpec, n_utt: int, *, seed: int, first_utt: int =
         reflection=refl, sample_rate=np.full(n_utt, spec.fs), speed_of_sound=np.full(n_utt, spec.c0),
         image_order=order, max_taps=taps, src_pos=src, mic_pos=mic, snr_db=snr,
         sig_off=np.concatenate([[0], np.cumsum(sig_len)[:-1]]).astype(np.int64), sig_len=sig_len,
-        signals=None, eta_db=eta_db, plan_rule=plan_rule, forced_fft_size=forced_fft_size, seed=seed)
+        signals=None, eta_db=eta_db, plan_rule=plan_rule, forced_fft_size=forced_fft_size, seed=seed,
+        utt_ids=first_utt + np.arange(n_utt, dtype=np.int64))
 
 
-def _signal_meta(batch, first_utt: int):
+def _signal_meta(batch, first_utt: Optional[int]):
+    """(global utterance id, source index within it) of every source of ``batch``: the
+    generator's keys.  ``first_utt`` given: utterances first_utt.. (a contiguous batch);
+    else the batch's own ids (``SceneBatch.ids``: subsets and shards keep theirs)."""
     I = np.diff(batch.src_begin)
-    utt = (np.repeat(np.arange(batch.n_utt), I) + first_utt).astype(np.int64)
+    ids = (np.arange(batch.n_utt, dtype=np.int64) + first_utt) if first_utt is not None else batch.ids
+    utt = np.repeat(ids, I).astype(np.int64)
     local = (np.arange(batch.n_src) - np.repeat(batch.src_begin[:-1], I)).astype(np.int32)
     return utt, local
 
 
-def generate_signals(spec: RsSamplerSpec, batch, *, seed: int, first_utt: int = 0, epoch: int = 0,
+def generate_signals(spec: RsSamplerSpec, batch, *, seed: int, first_utt: Optional[int] = None, epoch: int = 0,
                      device_ptr: Optional[int] = None, stream: int = 0) -> Optional[np.ndarray]:
     """Synthetic N(0, std^2) source signals of ``batch``: on the host (returns the array)
-    or straight into device memory at ``device_ptr`` (returns None)."""
+    or straight into device memory at ``device_ptr`` (returns None).  Keyed by each
+    source's global utterance id (``batch.ids`` unless ``first_utt`` is given), so a
+    subset or a shard gets the same samples as the full batch."""
     L = load_library()
     utt, local = _signal_meta(batch, first_utt)
     off = np.ascontiguousarray(batch.sig_off, np.int64)

@@ -141,10 +141,16 @@ class SceneBatch:
     forced_fft_size: int = 0
     name: str = ""
     seed: int = 1
+    utt_ids: Optional[np.ndarray] = None  # global utterance ids (sampler keys); None: 0..n_utt-1
 
     @property
     def n_utt(self) -> int:
         return int(self.room_dims.shape[0])
+
+    @property
+    def ids(self) -> np.ndarray:
+        """Global utterance id of every utterance of the batch (what the samplers key on)."""
+        return np.arange(self.n_utt, dtype=np.int64) if self.utt_ids is None else np.asarray(self.utt_ids, np.int64)
 
     @property
     def n_src(self) -> int:
@@ -262,6 +268,7 @@ class SceneBatch:
             sig_off=offs,
             sig_len=lens.astype(np.int64),
             signals=sig,
+            utt_ids=self.ids[utts],
         )
 
 
@@ -293,6 +300,7 @@ def make_batch(spec: SamplerSpec, n_utt: int, *, epoch: int = 0, first_utt: int 
         forced_fft_size=forced_fft_size,
         name=name,
         seed=spec.seed,
+        utt_ids=first_utt + np.arange(n_utt, dtype=np.int64),
     )
     if signals:
         b.signals = host_signals(b, spec.seed, epoch, first_utt)

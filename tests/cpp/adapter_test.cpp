@@ -65,6 +65,30 @@ int main() {
     EXPECT(p.fft_size == q.fft_size && p.predicted_cost == q.predicted_cost && p.strategy == q.strategy,
            "choose_plan differs case %d", t);
   }
+  // convolve dispatch (convolution.hpp:258-271): direct is FP64 and bit-exact, the FFT
+  // strategies FP32 within 1e-5 of the peak
+  for (int t = 0; t < 6; ++t) {
+    std::vector<double> x(300 + 611 * t), hs(20 + 131 * t);
+    for (auto& v : x) v = Nd(g);
+    for (auto& v : hs) v = Nd(g);
+    const auto xb = AudioBuffer::mono(x, 16000.0);
+    Rir h;
+    h.samples = hs;
+    const AudioBuffer dw = convolve_direct(xb, h), dg = gpu::convolve_direct(xb, h);
+    EXPECT(dw.channel(0) == dg.channel(0), "gpu::convolve_direct bits differ case %d", t);
+    const ConvolutionPlan plans[3] = {plan_for(CostInputs{1.0, 1.0, x.size(), hs.size()}, Strategy::direct),
+                                      plan_for(CostInputs{1.0, 1.0, x.size(), hs.size()}, Strategy::full_fft),
+                                      plan_for(CostInputs{1.0, 1.0, x.size(), hs.size()}, Strategy::overlap_add)};
+    for (const ConvolutionPlan& p : plans) {
+      const AudioBuffer want = convolve(xb, h, p), got = gpu::convolve(xb, h, p);
+      EXPECT(got.channel(0).size() == want.channel(0).size(), "gpu::convolve length case %d", t);
+      if (p.strategy == Strategy::direct)
+        EXPECT(got.channel(0) == want.channel(0), "gpu::convolve(direct) bits case %d", t);
+      else
+        EXPECT(rel_err(got.channel(0), want.channel(0)) <= 1e-5, "gpu::convolve strategy %d case %d",
+               static_cast<int>(p.strategy), t);
+    }
+  }
   // error taxonomy
   bool threw = false;
   try {

@@ -182,8 +182,8 @@ def test_two_stream_k4_all_sizes():
 
 
 @pytest.mark.parametrize("env,sizes", [
-    ({"RSG_W": "9,10"}, (9, 10)),           # warp-per-transform two-stream K4 (warp.cu)
     ({"RSG_IP": "9,14", "RSG_IP_FORCE": "1"}, (10, 11, 12, 13, 14, 15)),  # in-place K4 (big.cu), every size
+    ({"RSG_IP": "0,0"}, (10, 11, 12, 13)),  # in-place K4 off: ola_small_kernel up to M = 4096, four-step above
 ])
 def test_k4_variants(env, sizes):
     """Opt-in K4 variants in a fresh process (their selection is read once per process):
