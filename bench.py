@@ -8,20 +8,28 @@ utterances x (1 target + 5 noises) x 2 mics, image-method RIRs truncated at
 
   python bench.py [--gpus N --steps K --warmup W]          # our CUDA path
   python bench.py --impl reference [...]                    # the reference's CPU path
+  python bench.py --gpus 2 --dry-run                        # CPU: spawn/shard/reduce only
 
 Our arm prints `value` (inputs resident in HBM, CUDA events on the launching
 stream, max over ranks), `e2e` (host pinned buffers through the C-ABI with
-H2D/D2H in the timed region), the OLA kernel's `roofline`, the reference
-CPU `cpu_baseline` (rank 0, N = 1, bounded sample), `clocks` and
-`gpu_launches`.  Multi-GPU: one process per GPU (torchrun), utterances sharded
-with no collective on the data path ("scaling": "weak" by default: every
-rank renders its own 4096 utterances).
+H2D/D2H in the timed region), the OLA kernel's `roofline` (with a per-size
+breakdown), the reference CPU `cpu_baseline` (rank 0, N = 1, bounded sample),
+`parity` (that sample rendered on the GPU against the reference), `clocks` and
+`gpu_launches`.
+
+Multi-GPU: one process per GPU — torchrun's ranks, or, when WORLD_SIZE is
+unset and --gpus N > 1, N processes spawned here (127.0.0.1 rendezvous).
+Utterances are sharded with no collective on the data path: "scaling":
+"strong" by default (the config's 4096 utterances LPT-partitioned over the
+ranks by predicted work), "weak" on request (every rank renders
+its own set of utterance ids).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -36,23 +44,61 @@ METRIC = "simulated audio-sec/sec"
 UNIT = "audio-s/s"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="config4", choices=["config2", "config3", "config4", "config5"])
-    ap.add_argument("--utterances", type=int, default=0, help="per GPU (weak) or total (strong); 0 = config default")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--utterances", type=int, default=0, help="total (strong) or per GPU (weak); 0 = config default")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong",
+                    help="strong (default): the config's utterances sharded over the GPUs (BASELINE config 4: "
+                         "4096 utterances over 1/2/4/8 B200); weak: every GPU renders its own set")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU only (gloo): spawn / shard / max-over-ranks logic without rendering")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-utts", type=int, default=0)
     ap.add_argument("--seed", type=int, default=4)
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 DEFAULT_UTTS = {"config2": 128, "config3": 128, "config4": 4096, "config5": 512}
+
+
+# ---- the workload and its shards ------------------------------------------------
+def n_config(args) -> int:
+    return args.utterances or DEFAULT_UTTS[args.config]
+
+
+def full_batch(args, signals=False, first_utt=0):
+    from paper_1712_03439_b200 import scenes
+
+    return scenes.CONFIGS[args.config](n_utt=n_config(args), seed=args.seed, signals=signals, first_utt=first_utt)
+
+
+def rank_batch(args, rank, world):
+    """The scenes rank `rank` renders: its LPT shard of the workload (strong) or its
+    own block of utterance ids (weak).  Returns (batch, total utterances of the job)."""
+    from paper_1712_03439_b200 import shard
+
+    n = n_config(args)
+    if args.scaling == "weak":
+        return full_batch(args, first_utt=rank * n), n * world
+    b, _ = shard.shard_batch(full_batch(args), rank, world)
+    return b, n
+
+
+def workload_config(args, world):
+    """The `config` object both arms print (same keys, same values)."""
+    from paper_1712_03439_b200 import scenes
+
+    b = scenes.CONFIGS[args.config](n_utt=1, seed=args.seed, signals=False)
+    n = n_config(args)
+    return {"workload": args.config, "utterances": n * world if args.scaling == "weak" else n,
+            "scaling": args.scaling, "seed": args.seed, "eta_db": b.eta_db,
+            "fft_rule": {0: "choose_plan", 1: f"forced {b.forced_fft_size}", 2: "bit_ceil(2*N_h)"}[b.plan_rule]}
 
 
 # ---- clocks (sampled during the timed region) -----------------------------------
@@ -113,61 +159,59 @@ class ClockSampler:
 
 
 # ---- CPU reference runs -------------------------------------------------------
-def cpu_sample(batch_fn, n_utt: int, want: int):
-    """Deterministic subsample of the workload (every k-th utterance), host signals."""
-    from paper_1712_03439_b200 import scenes
-
-    k = max(1, n_utt // max(want, 1))
-    ids = np.arange(0, n_utt, k)[:want]
-    full = batch_fn(signals=False)
+def cpu_sample(args, want: int):
+    """Deterministic subsample of the whole workload (every k-th utterance) with host
+    N(0, 0.1) signals: what the CPU baseline renders (and the GPU, for `parity`)."""
+    full = full_batch(args)
+    k = max(1, full.n_utt // max(want, 1))
+    ids = np.arange(0, full.n_utt, k)[:want]
     sub = full.subset(ids)
-    sub.signals = np.empty(sub.total_samples, np.float32)
     g = np.random.Generator(np.random.Philox(key=99))
-    sub.signals[:] = g.standard_normal(sub.total_samples, dtype=np.float32) * np.float32(0.1)
+    sub.signals = g.standard_normal(sub.total_samples, dtype=np.float32) * np.float32(0.1)
     return sub, k
 
 
-def run_cpu_reference(sub, threads: int):
+def run_cpu_reference(sub, threads: int, tuned: bool = True):
+    """The reference (oracle/_ref: the unmodified reference headers, compiled) renders
+    `sub` on `threads` host threads; the C restatement if that build is absent."""
     import oracle
 
     kind = "reference" if oracle.reference_available() else "port"
     lib = oracle.reference() if kind == "reference" else oracle.port()
     if kind == "reference":
-        lib.lib.ref_set_malloc_tuning(1)
+        lib.lib.ref_set_malloc_tuning(1 if tuned else 0)
     t0 = time.perf_counter()
-    lib.render_batch(sub, threads=threads)
+    res = lib.render_batch(sub, threads=threads)
     dt = time.perf_counter() - t0
-    return sub.audio_seconds / dt, dt, kind
+    return sub.audio_seconds / dt, dt, kind, res
 
 
 def reference_arm(args, rank, world):
-    """--impl reference: the reference's own CPU path (oracle/_ref) on the host cores."""
+    """--impl reference: the reference's own CPU path (oracle/_ref) on all host cores,
+    on our arm's config / metric / unit; each step renders a bounded deterministic
+    sample of the workload.  Rank 0 alone runs it."""
     if rank != 0:
         return
-    from paper_1712_03439_b200 import scenes
-
-    n_utt = args.utterances or DEFAULT_UTTS[args.config]
     threads = os.cpu_count() or 1
     # each step ~3-5 s of the host's cores: the whole K+W run stays within minutes
     want = args.cpu_sample_utts or max(16, 24 * threads)
-    fn = lambda signals=False: scenes.CONFIGS[args.config](n_utt=n_utt, seed=args.seed, signals=signals)  # noqa: E731
-    sub, k = cpu_sample(fn, n_utt, want)
+    sub, k = cpu_sample(args, want)
     for _ in range(args.warmup):
         run_cpu_reference(sub, threads)
-    vals, secs = [], []
+    secs = []
     kind = None
     for _ in range(args.steps):
-        v, dt, kind = run_cpu_reference(sub, threads)
-        vals.append(v)
+        _, dt, kind, _ = run_cpu_reference(sub, threads)
         secs.append(dt)
     value = float(sub.audio_seconds * args.steps / sum(secs))
-    sample = (f"{sub.n_utt} of {n_utt} {args.config} utterances (every {k}th, "
+    sample = (f"{sub.n_utt} of {n_config(args)} {args.config} utterances (every {k}th, "
               f"{sub.audio_seconds:.1f} audio-s, {sub.n_pairs} pairs) per step")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / args.steps,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": args.config, "utterances": n_utt},
+        "data": "synthetic: seeded N(0,0.1) signals, sampled image-method rooms",
+        "config": workload_config(args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
                          "note": "reference radix-2 CPU path (FFTW3 unavailable); malloc mmap_threshold=64MiB"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -175,21 +219,47 @@ def reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def dry_run(args, rank, world):
+    """CPU check of the multi-rank plumbing (gloo): every rank builds its shard; rank 0
+    checks the union covers every utterance exactly once and prints the shards."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1712_03439_b200 import shard
+
+    b, total = rank_batch(args, rank, world)
+    ids = [int(u) for u in b.ids]
+    w = shard.predicted_work(b)
+    mine = (ids, float(b.audio_seconds), int(b.n_pairs), float(w.sum()), float(w.max()) if w.size else 0.0)
+    got = [None] * world
+    if world > 1:
+        dist.all_gather_object(got, mine)
+    else:
+        got = [mine]
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)  # stands in for a rank's step time
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        allids = sorted(u for g in got for u in g[0])
+        want = list(range(total))
+        line = {"dry_run": True, "n_gpus": world, "scaling": args.scaling, "config": workload_config(args, world),
+                "shard_utterances": [len(g[0]) for g in got], "shard_pairs": [g[2] for g in got],
+                "shard_audio_seconds": [round(g[1], 3) for g in got],
+                "shard_predicted_work": [g[3] for g in got], "max_utterance_work": max(g[4] for g in got),
+                "covers_every_utterance_once": allids == want, "max_over_ranks": float(t[0])}
+        print(json.dumps(line), flush=True)
+
+
 # ---- our arm ---------------------------------------------------------------------
 def ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
-    from paper_1712_03439_b200 import roomsim, scenes, shard
+    from paper_1712_03439_b200 import roomsim, scenes
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    n_cfg = args.utterances or DEFAULT_UTTS[args.config]
-    if args.scaling == "weak":
-        batch = scenes.CONFIGS[args.config](n_utt=n_cfg, seed=args.seed, signals=False, first_utt=rank * n_cfg)
-    else:
-        full = scenes.CONFIGS[args.config](n_utt=n_cfg, seed=args.seed, signals=False)
-        batch, _ = shard.shard_batch(full, rank, world)
+    batch, total_utts = rank_batch(args, rank, world)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 + rank)
     signals = torch.randn(max(batch.total_samples, 1), generator=gen, device=dev, dtype=torch.float32).mul_(0.1)
@@ -207,6 +277,12 @@ def ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(v) for v in t]
+
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -219,7 +295,7 @@ def ours(args, rank, world, local_rank):
     stages = {}
     e0.record(stream)
     for _ in range(args.steps):
-        res = step()
+        step()
         t = ctx.last_timing()
         ola_ms += t["ola_ms"]
         flops += t["ola_flops"]
@@ -232,14 +308,23 @@ def ours(args, rank, world, local_rank):
     clocks = clk.stop()
     ms = e0.elapsed_time(e1) / args.steps
     alg_bytes = ctx.last_timing()["alg_bytes"]
-    t = torch.tensor([ms, ola_ms / args.steps], device=dev, dtype=torch.float64)
-    aud = torch.tensor([batch.audio_seconds], device=dev, dtype=torch.float64)
+    ms_max, ola_ms_max = max_over_ranks([ms, ola_ms / args.steps])
+    aud = torch.tensor([batch.audio_seconds, batch.n_pairs], device=dev, dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(aud, op=dist.ReduceOp.SUM)
-    ms_max, ola_ms_max = float(t[0]), float(t[1])
-    total_audio = float(aud[0])
+    total_audio, total_pairs = float(aud[0]), int(aud[1])
     value = total_audio / (ms_max / 1e3)
+
+    # ---- per-size K4 breakdown: one diagnostic render with the K4 launches serialized and
+    # timed one by one (outside the timed region) --------------------------------------
+    k4_sizes = None
+    try:
+        ctx.set_profiling(2)
+        step()
+        k4_sizes = ctx.k4_breakdown()
+        ctx.set_profiling(True)
+    except AttributeError:
+        pass
 
     # ---- e2e: host pinned buffers through rs_render_batch (H2D + D2H inside) ----
     e2e = None
@@ -260,43 +345,39 @@ def ours(args, rank, world, local_rank):
         torch.cuda.synchronize(dev)
         wall = (time.perf_counter() - t0) / args.steps * 1e3
         ev = e0.elapsed_time(e1) / args.steps
-        te = torch.tensor([max(wall, ev)], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": total_audio / (float(te[0]) / 1e3), "unit": UNIT,
+        te = max_over_ranks([max(wall, ev)])[0]
+        e2e = {"value": total_audio / (te / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(4 * batch.total_samples), "d2h_bytes_per_step": int(4 * batch.out_total),
-               "ms_per_step": float(te[0])}
+               "ms_per_step": te, "what": "rs_render_batch with pinned host signals/outputs: per-chunk H2D of the "
+                                          "signals and D2H of the mixed channels inside the timed region"}
         batch.signals = None
 
     # ---- epoch loop: source signals generated in HBM (rs_generate_signals, SURVEY.md §8f
     # row 1) + the render, per step; no host staging of the 12.6 GB of inputs ----------------
     epoch_loop = None
-    if not args.no_e2e and args.config != "config1":
+    if not args.no_e2e:
         spec = roomsim.sampler_spec(getattr(scenes, "spec_" + args.config)(args.seed))
-        gen_ms = 0.0
+        gen_plan = roomsim.SignalPlan(spec, batch, seed=args.seed)  # per-batch tables, built once
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
         def epoch_step(ep):
             g0.record(stream)
-            roomsim.generate_signals(spec, batch, seed=args.seed, epoch=ep, first_utt=rank * n_cfg,
-                                     device_ptr=signals.data_ptr(), stream=stream.cuda_stream)
+            gen_plan.generate(signals.data_ptr(), epoch=ep, stream=stream.cuda_stream)
             g1.record(stream)
             return step()
+
         epoch_step(0)
         barrier()
         torch.cuda.synchronize(dev)
         e0.record(stream)
         for k in range(args.steps):
             epoch_step(k + 1)
-            torch.cuda.synchronize(dev)
-            gen_ms += g0.elapsed_time(g1)
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        ms_ep = e0.elapsed_time(e1) / args.steps
-        te = torch.tensor([ms_ep], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        epoch_loop = {"value": total_audio / (float(te[0]) / 1e3), "unit": UNIT, "ms_per_step": float(te[0]),
-                      "signal_gen_ms": gen_ms / args.steps,
+        gen_ms = g0.elapsed_time(g1)
+        ms_ep = max_over_ranks([e0.elapsed_time(e1) / args.steps])[0]
+        epoch_loop = {"value": total_audio / (ms_ep / 1e3), "unit": UNIT, "ms_per_step": ms_ep,
+                      "signal_gen_ms": gen_ms,
                       "what": "per step: N(0, 0.1) source signals generated in HBM by rs_generate_signals "
                               "(Philox, bit-exact with the host fixture generator) + rs_render_batch_device; "
                               "scene metadata from the host sampler; no host<->device staging of samples"}
@@ -322,6 +403,7 @@ def ours(args, rank, world, local_rank):
                   "frames_per_s": frames / (lm_ms / args.steps / 1e3) if lm_ms > 0 else None,
                   "what": "128 log-Mel, 32 ms Hann / 10 ms hop, 125-7500 Hz, 4-frame stacks every 3rd "
                           "(PAPER.md:452-460) of every rendered channel; device-timed kernel"}
+        del feat
 
     # ---- roofline of the OLA filter kernels (K4) -------------------------------------
     props = torch.cuda.get_device_properties(dev)
@@ -337,13 +419,17 @@ def ours(args, rank, world, local_rank):
     achieved = per_step_flops / (ola_ms / args.steps / 1e3) / 1e12 if ola_ms > 0 else None
     hbm = float(peaks.get("hbm_gbs") or 6543.1)
     traffic, traffic_src = None, None
-    if args.config == "config4" and n_cfg == DEFAULT_UTTS["config4"]:
-        try:  # K4 DRAM bytes per render, from the committed ncu launch list of this workload
-            with open(os.path.join(ROOT, "profiles", "r01_k4_traffic.json")) as f:
-                tj = json.load(f)
+    try:  # K4 DRAM bytes per render, from the committed ncu launch list of this workload
+        with open(os.path.join(ROOT, "profiles", "k4_traffic.json")) as f:
+            tj = json.load(f)
+        if tj.get("workload") == args.config and tj.get("utterances_per_rank") == batch.n_utt:
             traffic, traffic_src = tj["dram_bytes_per_render"], tj["source"] + "; " + tj["note"]
-        except Exception:
-            pass
+    except Exception:
+        pass
+    if k4_sizes:
+        for r in k4_sizes:
+            r["tflops"] = r["flops"] / (r["ms"] / 1e3) / 1e12 if r["ms"] > 0 else None
+            r["frac"] = r["tflops"] / fp32_peak if r["tflops"] else None
     roofline = {
         "bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
         "frac": achieved / fp32_peak if achieved else None, "traffic": traffic,
@@ -355,58 +441,112 @@ def ours(args, rank, world, local_rank):
         "hbm_time_ms": alg_bytes / (hbm * 1e9) * 1e3,
         "peak_source": f"derived: {props.multi_processor_count} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz "
                        "(sm_max_mhz of MEASURED_PEAKS.json); FFT flops = 5 N log2 N per real transform",
+        "by_size": k4_sizes,
+        "by_size_note": "one extra render with the K4 launches serialized, each timed with CUDA events "
+                        "(algorithmic flops of its pairs / its time); the headline frac is the concurrent "
+                        "launches' aggregate",
     }
 
-    cpu = None
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         want = args.cpu_sample_utts or max(32, 64 * threads)  # ~10 s of the host's cores
-        fn = lambda signals=False: scenes.CONFIGS[args.config](n_utt=n_cfg, seed=args.seed, signals=signals)  # noqa: E731
-        sub, k = cpu_sample(fn, n_cfg, want)
-        v, dt, kind = run_cpu_reference(sub, threads)
+        sub, k = cpu_sample(args, want)
+        v, dt, kind, ref_res = run_cpu_reference(sub, threads)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
-               "sample": f"{sub.n_utt} of {n_cfg} {args.config} utterances (every {k}th), "
+               "sample": f"{sub.n_utt} of {n_config(args)} {args.config} utterances (every {k}th), "
                          f"{sub.audio_seconds:.1f} audio-s, {dt:.1f} s wall",
-               "note": "reference radix-2 CPU path (FFTW3 unavailable)"}
+               "note": "reference radix-2 CPU path (FFTW3 unavailable); malloc mmap_threshold=64MiB"}
+        # the same sample through our path: layouts bit-exact, waveforms within 1e-5 of the peak
+        g = roomsim.render_batch(sub, ctx=ctx)
+        o_out, o_len, o_lay, o_gain, o_pow = ref_res
+        lay_ok = all(bool((g.layout[f] == o_lay[f]).all()) for f in
+                     ("rir_len", "rir_keep", "cutoff", "fft_size", "block_len", "n_blocks", "out_len"))
+        J = np.diff(sub.mic_begin)
+        worst = 0.0
+        for u in range(sub.n_utt):
+            w_ = np.concatenate([sub.channel(o_out, u, j, o_len[u]) for j in range(J[u])])
+            g_ = np.concatenate([sub.channel(g.out, u, j, o_len[u]) for j in range(J[u])]).astype(np.float64)
+            worst = max(worst, float(np.abs(g_ - w_).max() / np.abs(w_).max()))
+        parity = {"checked_against": kind, "utterances": sub.n_utt, "pairs": sub.n_pairs,
+                  "layouts_bit_exact": lay_ok, "max_rel_wave_err": worst,
+                  "max_rel_gain_err": float(np.max(np.abs(g.gains - o_gain) / np.abs(o_gain))),
+                  "pass": bool(lay_ok and worst <= 1e-5)}
 
     if rank == 0:
+        cfg = workload_config(args, world)
+        cfg.update({"pairs": total_pairs, "audio_seconds": total_audio,
+                    "per_rank": {"utterances": batch.n_utt, "pairs": batch.n_pairs},
+                    "l2": "inputs (%.1f GB per GPU) >> L2 (126 MB): no flush needed" % (4 * batch.total_samples / 1e9)})
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: seeded N(0,0.1) fp32 signals, sampled image-method rooms",
-            "config": {"workload": args.config, "utterances_per_gpu" if args.scaling == "weak" else "utterances": n_cfg,
-                       "pairs_per_gpu": batch.n_pairs, "audio_seconds_total": total_audio,
-                       "eta_db": batch.eta_db, "fft_rule": {0: "choose_plan", 1: f"forced {batch.forced_fft_size}",
-                                                             2: "bit_ceil(2*N_h)"}[batch.plan_rule],
-                       "l2": "inputs (%.1f GB/GPU) >> L2 (126 MB): no flush needed" % (4 * batch.total_samples / 1e9)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "epoch_loop": epoch_loop, "logmel": logmel,
-            "gpu_launches": launches, "clocks": clocks,
+            "config": cfg, "roofline": roofline, "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
+            "epoch_loop": epoch_loop, "logmel": logmel, "gpu_launches": launches, "clocks": clocks,
             "stage_ms": {k: round(v, 3) for k, v in stages.items()},
         }
         print(json.dumps(line), flush=True)
     ctx.close()
 
 
-def main():
-    args = parse()
+def _free_port() -> int:
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def run_rank(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one process per GPU "
+                 f"(torchrun --nproc-per-node {args.gpus}) or leave WORLD_SIZE unset to spawn here")
     if args.impl == "reference":
         reference_arm(args, rank, world)
         return
-    if world > 1:
-        import torch
-        import torch.distributed as dist
+    import torch
+    import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    ours(args, rank, world, local_rank)
     if world > 1:
-        import torch.distributed as dist
+        if args.dry_run:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        if args.dry_run:
+            dry_run(args, rank, world)
+        else:
+            ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
 
-        dist.destroy_process_group()
+
+def _spawned(local_rank, argv, world, port):
+    os.environ.update(RANK=str(local_rank), LOCAL_RANK=str(local_rank), WORLD_SIZE=str(world),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    run_rank(parse(argv))
+
+
+def main():
+    argv = sys.argv[1:]
+    args = parse(argv)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if args.impl == "reference":  # rank 0 alone runs the CPU reference: no processes to spawn
+            os.environ.update(RANK="0", LOCAL_RANK="0", WORLD_SIZE=str(args.gpus))
+            reference_arm(args, 0, args.gpus)
+            return
+        import torch.multiprocessing as mp
+
+        mp.spawn(_spawned, args=(argv, args.gpus, _free_port()), nprocs=args.gpus, join=True)
+        return
+    run_rank(args)
 
 
 if __name__ == "__main__":

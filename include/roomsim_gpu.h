@@ -73,8 +73,16 @@ int rs_ctx_last_timing(rs_ctx* ctx, double* ola_ms, double* ola_flops,
  * overlapped with the other stream); host_plan_ms = host wall time of the
  * planner.  Entries are -1 when unavailable. */
 int rs_ctx_stage_times(rs_ctx* ctx, double* ms, int n, double* host_plan_ms);
-/* Enable event timing of the OLA kernels (adds events; off by default). */
+/* Enable event timing of the OLA kernels (adds events; off by default).  Level 2
+ * (diagnostic) also serializes the K4 launches of each chunk on one stream and times
+ * every (FFT size, kernel variant) span separately: rs_ctx_k4_breakdown. */
 int rs_ctx_set_profiling(rs_ctx* ctx, int enabled);
+/* Per-(log2 N, variant) rows of the last render at profiling level 2 (variant: 0
+ * ola_small_kernel, 1 in-place ola_ip_kernel, 2 two-stream ola2_kernel, 3 four-step):
+ * pairs, algorithmic FFT flops ((2B+1) 5 N log2 N per pair) and device ms.  Returns the
+ * row count (rows beyond `cap` are not written); negative on error. */
+int rs_ctx_k4_breakdown(rs_ctx* ctx, int cap, int32_t* log2n, int32_t* variant, int64_t* pairs,
+                        double* flops, double* ms);
 
 /* ---- host-side planner (convolution.hpp:72-161), exact FP64 mirror -------- */
 double rs_cost_direct(double num_sources, double num_mics, size_t nx, size_t nh);
@@ -249,6 +257,15 @@ int rs_generate_signals_host(const rs_sampler_spec* spec, uint64_t seed, int64_t
 int rs_generate_signals(const rs_sampler_spec* spec, uint64_t seed, int64_t epoch, int64_t n_src,
                         const int64_t* utt_of_src, const int32_t* src_local, const int64_t* sig_off,
                         const int64_t* sig_len, float* out_dev, void* stream);
+/* The same generator for a fixed batch across epochs: the per-source table is built and
+ * uploaded once (create); each epoch is then one kernel launch on `stream` with no host
+ * work, allocation or synchronisation (generate).  Bit-exact with the calls above. */
+typedef struct rs_signal_plan rs_signal_plan;
+int rs_signal_plan_create(const rs_sampler_spec* spec, uint64_t seed, int64_t n_src,
+                          const int64_t* utt_of_src, const int32_t* src_local,
+                          const int64_t* sig_off, const int64_t* sig_len, rs_signal_plan** out);
+int rs_signal_plan_generate(rs_signal_plan* plan, int64_t epoch, float* out_dev, void* stream);
+int rs_signal_plan_destroy(rs_signal_plan* plan);
 
 /* ---- log-Mel front end -------------------
  * 128 log-Mel energies per 32 ms frame (512 samples, periodic Hann) every 10 ms (160

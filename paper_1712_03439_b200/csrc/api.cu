@@ -6,6 +6,7 @@
 // the kernel sequence K1 -> K2 -> plan -> K3 -> K4 -> K5 -> K6.
 #include <algorithm>
 #include <chrono>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -293,6 +294,23 @@ struct rs_ctx {
   // log-Mel front end tables (built on first use)
   DevBuf lm_window, lm_ptr, lm_bin, lm_w, lm_tiles;
   bool lm_ready = false;
+  // profiling level 2: K4 launches serialized on the filter stream, one event pair per
+  // (size, variant) span; rows of the last render, merged by (log2 N, variant)
+  int prof_level = 0;
+  struct K4Span { int log2n, var; int64_t pairs; double flops; cudaEvent_t a, b; };
+  std::vector<K4Span> k4_spans;      // this render's spans (events pending)
+  std::vector<cudaEvent_t> ev_pool;  // reusable events
+  size_t ev_used = 0;
+  struct K4Row { int log2n, var; int64_t pairs; double flops, ms; };
+  std::vector<K4Row> k4_rows;
+  cudaEvent_t pool_event() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
 };
 
 namespace {
@@ -686,7 +704,7 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
   RS_CUDA(cudaEventRecord(c->side_fork, st));
   bool used[rs_ctx::kSide] = {};
   int next_side = 0;
-  auto side_for = [&]() -> cudaStream_t {
+  std::function<cudaStream_t()> side_for = [&]() -> cudaStream_t {
     const int i = next_side++ % rs_ctx::kSide;
     if (!used[i]) {
       cudaStreamWaitEvent(c->side[i], c->side_fork, 0);
@@ -694,9 +712,31 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
     }
     return c->side[i];
   };
+  const bool serial = c->prof_level >= 2;  // diagnostic: one stream, one event pair per span
+  auto span_flops = [&](const Span& sp) {
+    double f = 0;
+    for (int64_t i = 0; i < sp.list_n; ++i) f += pair_flops(plans[fp.lists[sp.list_off + i]]);
+    return f;
+  };
+  auto span_begin = [&](const Span& sp) {
+    if (!serial) return;
+    rs_ctx::K4Span k{sp.l + 1, sp.var, sp.list_n, span_flops(sp), c->pool_event(), c->pool_event()};
+    cudaEventRecord(k.a, st);
+    c->k4_spans.push_back(k);
+  };
+  auto span_end = [&]() {
+    if (serial) cudaEventRecord(c->k4_spans.back().b, st);
+  };
+  if (serial) side_for = [&]() -> cudaStream_t { return st; };
   cudaStream_t large_st = fp.batches.empty() ? st : side_for();
+  int open_span = -1;
   for (const LargeBatch& bt : fp.batches) {
     const Span& sp = fp.spans[bt.span];
+    if (bt.span != open_span) {
+      if (open_span >= 0) span_end();
+      span_begin(sp);
+      open_span = bt.span;
+    }
     int l1, l2;
     large_split(sp.l, &l1, &l2);
     LargeArgs a{fb.units.as<int2>() + bt.unit_lo, d_lists + sp.list_off + bt.pair_lo,
@@ -710,7 +750,9 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
       ++c->launches;
     }
   }
+  if (open_span >= 0) span_end();
   for (const Span& sp : fp.spans) {
+    if (sp.var != kVarLarge) span_begin(sp);
     if (sp.var == kVarOla2) {
       Ola2Args a{fb.olaitems2.as<OlaItem2>() + sp.item_off, static_cast<int32_t>(sp.item_n), d_pair,
                  fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(), d_part,
@@ -728,6 +770,7 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
         RS_CUDA(launch_ola(sp.l, a, side_for()));
       ++c->launches;
     }
+    if (sp.var != kVarLarge) span_end();
   }
   for (int i = 0; i < rs_ctx::kSide; ++i)  // join
     if (used[i]) {
@@ -736,6 +779,26 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
     }
   if (ev_k4b) RS_CUDA(cudaEventRecord(ev_k4b, st));
   return RS_OK;
+}
+
+// Profiling level 2: turn the render's per-span events into rows merged by (N, variant).
+void collect_k4_rows(rs_ctx* c) {
+  c->k4_rows.clear();
+  for (const auto& k : c->k4_spans) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, k.a, k.b);
+    bool merged = false;
+    for (auto& r : c->k4_rows)
+      if (r.log2n == k.log2n && r.var == k.var) {
+        r.pairs += k.pairs;
+        r.flops += k.flops;
+        r.ms += ms;
+        merged = true;
+      }
+    if (!merged) c->k4_rows.push_back(rs_ctx::K4Row{k.log2n, k.var, k.pairs, k.flops, ms});
+  }
+  c->k4_spans.clear();
+  c->ev_used = 0;
 }
 
 int finish_timing(rs_ctx* c) {
@@ -1321,6 +1384,7 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
   if (c->profiling) cudaEventRecord(c->st[6], c->stream);
   RS_CUDA(cudaStreamSynchronize(c->stream));
   R.hmark("sync done");
+  if (c->prof_level >= 2) collect_k4_rows(c);
   c->launches += g_copy_launches;
   g_kernel_copies = false;
   R.dump();
@@ -1431,6 +1495,7 @@ int convolve_host(rs_ctx* c, const double* x, size_t nx, const double* h, size_t
   RS_CUDA(launch_convert_f2d(fb.y.as<float>(), c->scratch_b.as<double>(), static_cast<int64_t>(ol), c->stream));
   RS_CUDA(cudaMemcpyAsync(out, c->scratch_b.p, ol * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   RS_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->prof_level >= 2) collect_k4_rows(c);
   RS_TRY(finish_timing(c));
   c->ola_flops = flops;
   c->alg_bytes = 4.0 * (nx + nh + ol);
@@ -1476,6 +1541,7 @@ int rs_ctx_destroy(rs_ctx* c) {
     if (c->side_join[i]) cudaEventDestroy(c->side_join[i]);
   }
   if (c->side_fork) cudaEventDestroy(c->side_fork);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   for (auto& e : c->st)
@@ -1507,7 +1573,23 @@ int rs_ctx_stage_times(rs_ctx* c, double* ms, int n, double* host_plan_ms) {
 int rs_ctx_set_profiling(rs_ctx* c, int enabled) {
   RS_TRY(check_ctx(c));
   c->profiling = enabled != 0;
+  c->prof_level = enabled;
   return RS_OK;
+}
+
+int rs_ctx_k4_breakdown(rs_ctx* c, int cap, int32_t* log2n, int32_t* variant, int64_t* pairs, double* flops,
+                        double* ms) {
+  if (!c) return -fail(RS_ERR_CONFIG, "null context");
+  const int n = static_cast<int>(c->k4_rows.size());
+  for (int i = 0; i < n && i < cap; ++i) {
+    const auto& r = c->k4_rows[i];
+    if (log2n) log2n[i] = r.log2n;
+    if (variant) variant[i] = r.var;
+    if (pairs) pairs[i] = r.pairs;
+    if (flops) flops[i] = r.flops;
+    if (ms) ms[i] = r.ms;
+  }
+  return n;
 }
 
 int rs_ctx_last_timing(rs_ctx* c, double* ola_ms, double* ola_flops, double* alg_bytes,

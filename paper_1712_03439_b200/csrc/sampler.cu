@@ -174,38 +174,84 @@ int rs_generate_signals_host(const rs_sampler_spec* spec, uint64_t seed, int64_t
   return RS_OK;
 }
 
+}  // extern "C"
+
+// A batch's per-source generator table, on the device once: every epoch's signals are then
+// one kernel launch with no host work, no allocation and no synchronisation.
+struct rs_signal_plan {
+  SamplerSpecD spec;
+  uint64_t seed = 0;
+  int64_t n_src = 0, n_tiles = 0, grid = 0;
+  unsigned char* d = nullptr;  // n_src SrcInfo, then the n_src tile prefixes
+  size_t info_bytes = 0;
+};
+
+extern "C" {
+
+int rs_signal_plan_create(const rs_sampler_spec* spec, uint64_t seed, int64_t n_src, const int64_t* utt_of_src,
+                          const int32_t* src_local, const int64_t* sig_off, const int64_t* sig_len,
+                          rs_signal_plan** out) {
+  if (!out) return sfail(RS_ERR_CONFIG, "null output pointer");
+  if (int st = check_spec(spec)) return st;
+  auto* p = new rs_signal_plan();
+  p->spec = spec_of(spec);
+  p->seed = seed;
+  p->n_src = n_src < 0 ? 0 : n_src;
+  p->info_bytes = static_cast<size_t>(p->n_src) * sizeof(SrcInfo);
+  std::vector<unsigned char> table(p->info_bytes + static_cast<size_t>(p->n_src) * sizeof(int64_t));
+  SrcInfo* info = reinterpret_cast<SrcInfo*>(table.data());
+  int64_t* first = reinterpret_cast<int64_t*>(table.data() + p->info_bytes);
+  for (int64_t s = 0; s < p->n_src; ++s) {
+    info[s] = SrcInfo{utt_of_src[s], sig_off[s], sig_len[s], src_local[s], 0};
+    first[s] = p->n_tiles;
+    p->n_tiles += ((sig_len[s] + 3) / 4 + kSigTile - 1) / kSigTile;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  p->grid = std::min<int64_t>(p->n_tiles, static_cast<int64_t>(sms) * 8);
+  cudaError_t e = cudaSuccess;
+  if (!table.empty()) {
+    e = cudaMalloc(reinterpret_cast<void**>(&p->d), table.size());
+    if (e == cudaSuccess) e = cudaMemcpy(p->d, table.data(), table.size(), cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) {
+    if (p->d) cudaFree(p->d);
+    delete p;
+    return sfail(e == cudaErrorMemoryAllocation ? RS_ERR_OOM : RS_ERR_CUDA, cudaGetErrorString(e));
+  }
+  *out = p;
+  return RS_OK;
+}
+
+int rs_signal_plan_generate(rs_signal_plan* p, int64_t epoch, float* out_dev, void* stream) {
+  if (!p) return sfail(RS_ERR_CONFIG, "null signal plan");
+  if (p->n_tiles == 0) return RS_OK;
+  signals_kernel<<<static_cast<unsigned>(p->grid), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      p->spec, p->seed, epoch, reinterpret_cast<const SrcInfo*>(p->d),
+      reinterpret_cast<const int64_t*>(p->d + p->info_bytes), p->n_src, p->n_tiles, out_dev);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? RS_OK : sfail(RS_ERR_CUDA, cudaGetErrorString(e));
+}
+
+int rs_signal_plan_destroy(rs_signal_plan* p) {
+  if (!p) return RS_OK;
+  if (p->d) cudaFree(p->d);
+  delete p;
+  return RS_OK;
+}
+
 int rs_generate_signals(const rs_sampler_spec* spec, uint64_t seed, int64_t epoch, int64_t n_src,
                         const int64_t* utt_of_src, const int32_t* src_local, const int64_t* sig_off,
                         const int64_t* sig_len, float* out_dev, void* stream) {
   if (int st = check_spec(spec)) return st;
   if (n_src <= 0) return RS_OK;
-  // one table: n_src SrcInfo, then the n_src tile prefixes
-  const size_t info_bytes = static_cast<size_t>(n_src) * sizeof(SrcInfo);
-  std::vector<unsigned char> table(info_bytes + static_cast<size_t>(n_src) * sizeof(int64_t));
-  SrcInfo* info = reinterpret_cast<SrcInfo*>(table.data());
-  int64_t* first = reinterpret_cast<int64_t*>(table.data() + info_bytes);
-  int64_t n_tiles = 0;
-  for (int64_t s = 0; s < n_src; ++s) {
-    info[s] = SrcInfo{utt_of_src[s], sig_off[s], sig_len[s], src_local[s], 0};
-    first[s] = n_tiles;
-    n_tiles += ((sig_len[s] + 3) / 4 + kSigTile - 1) / kSigTile;
-  }
-  const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  unsigned char* d = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), table.size(), st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d, table.data(), table.size(), cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess && n_tiles > 0) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t grid = std::min<int64_t>(n_tiles, static_cast<int64_t>(sms) * 8);
-    signals_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(
-        spec_of(spec), seed, epoch, reinterpret_cast<const SrcInfo*>(d),
-        reinterpret_cast<const int64_t*>(d + info_bytes), n_src, n_tiles, out_dev);
-    e = cudaGetLastError();
-  }
-  if (d) cudaFreeAsync(d, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the host table must outlive the copy
+  rs_signal_plan* p = nullptr;
+  if (int st = rs_signal_plan_create(spec, seed, n_src, utt_of_src, src_local, sig_off, sig_len, &p)) return st;
+  int st = rs_signal_plan_generate(p, epoch, out_dev, stream);
+  const cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));  // before the table is freed
+  rs_signal_plan_destroy(p);
+  if (st) return st;
   return e == cudaSuccess ? RS_OK : sfail(RS_ERR_CUDA, cudaGetErrorString(e));
 }
 

@@ -93,13 +93,15 @@ LAYOUT_DTYPE = np.dtype([("rir_len", np.int64), ("rir_keep", np.int64), ("cutoff
 # Every symbol include/roomsim_gpu.h declares (checked by tests/test_abi.py).
 ABI_SYMBOLS = [
     "rs_last_error", "rs_version", "rs_ctx_create", "rs_ctx_destroy", "rs_ctx_set_stream",
-    "rs_ctx_synchronize", "rs_ctx_last_timing", "rs_ctx_stage_times", "rs_ctx_set_profiling", "rs_cost_direct",
+    "rs_ctx_synchronize", "rs_ctx_last_timing", "rs_ctx_stage_times", "rs_ctx_set_profiling",
+    "rs_ctx_k4_breakdown", "rs_cost_direct",
     "rs_cost_full_fft", "rs_cost_ola", "rs_ola_block_count", "rs_plan_for", "rs_choose_plan",
     "rs_rfft_forward", "rs_rfft_inverse", "rs_synthesize_rir", "rs_truncate_rir",
     "rs_convolve_ola", "rs_convolve_full_fft", "rs_convolve_direct", "rs_convolve", "rs_batch_num_pairs",
     "rs_render_batch", "rs_render_batch_device", "rs_last_pair_signal", "rs_last_pair_rir",
     "rs_sampler_counts", "rs_sample_scenes", "rs_sampler_counts_device", "rs_sample_scenes_device",
-    "rs_generate_signals_host", "rs_generate_signals", "rs_logmel_shape", "rs_logmel_device",
+    "rs_generate_signals_host", "rs_generate_signals", "rs_signal_plan_create", "rs_signal_plan_generate",
+    "rs_signal_plan_destroy", "rs_logmel_shape", "rs_logmel_device",
 ]
 
 
@@ -138,6 +140,7 @@ def load_library() -> C.CDLL:
         "rs_ctx_last_timing": (C.c_int, [vp, dp, dp, dp, C.POINTER(i64)]),
         "rs_ctx_set_profiling": (C.c_int, [vp, C.c_int]),
         "rs_ctx_stage_times": (C.c_int, [vp, dp, C.c_int, dp]),
+        "rs_ctx_k4_breakdown": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp]),
         "rs_cost_direct": (d, [d, d, sz, sz]),
         "rs_cost_full_fft": (d, [d, d, sz, sz, sz]),
         "rs_cost_ola": (d, [d, d, sz, sz, sz]),
@@ -163,6 +166,9 @@ def load_library() -> C.CDLL:
         "rs_sample_scenes_device": (C.c_int, [vp, C.c_uint64, i64, i64, i64] + [vp] * 10),
         "rs_generate_signals_host": (C.c_int, [vp, C.c_uint64, i64, i64, vp, vp, vp, vp, vp]),
         "rs_generate_signals": (C.c_int, [vp, C.c_uint64, i64, i64, vp, vp, vp, vp, vp, vp]),
+        "rs_signal_plan_create": (C.c_int, [vp, C.c_uint64, i64, vp, vp, vp, vp, C.POINTER(vp)]),
+        "rs_signal_plan_generate": (C.c_int, [vp, i64, vp, vp]),
+        "rs_signal_plan_destroy": (C.c_int, [vp]),
         "rs_logmel_shape": (C.c_int, [i64, C.POINTER(i64), C.POINTER(i64)]),
         "rs_logmel_device": (C.c_int, [vp, vp, i64, vp, vp, vp, vp]),
     }
@@ -258,8 +264,27 @@ class Context:
     def set_stream(self, stream_handle: int) -> None:
         _check(load_library().rs_ctx_set_stream(self.h, C.c_void_p(stream_handle)))
 
-    def set_profiling(self, on: bool) -> None:
+    def set_profiling(self, on) -> None:
+        """True/1: event timing of the stages; 2: also the per-(size, variant) K4
+        breakdown (K4 launches serialized — a diagnostic render, not a timed one)."""
         _check(load_library().rs_ctx_set_profiling(self.h, int(on)))
+
+    K4_VARIANTS = ("ola_small", "ola_ip", "ola2", "four_step")
+
+    def k4_breakdown(self) -> list:
+        """Rows of the last render at profiling level 2: N, variant, pairs, flops, ms."""
+        L = load_library()
+        n = L.rs_ctx_k4_breakdown(self.h, 0, None, None, None, None, None)
+        if n < 0:
+            _check(-n)
+        lg = np.zeros(n, np.int32)
+        var = np.zeros(n, np.int32)
+        pairs = np.zeros(n, np.int64)
+        fl = np.zeros(n)
+        ms = np.zeros(n)
+        L.rs_ctx_k4_breakdown(self.h, n, _ptr(lg), _ptr(var), _ptr(pairs), _ptr(fl), _ptr(ms))
+        return [{"fft_size": 1 << int(lg[i]), "kernel": self.K4_VARIANTS[int(var[i])], "pairs": int(pairs[i]),
+                 "flops": float(fl[i]), "ms": float(ms[i])} for i in np.argsort(-fl)]
 
     def synchronize(self) -> None:
         _check(load_library().rs_ctx_synchronize(self.h))
@@ -525,6 +550,36 @@ def generate_signals(spec: RsSamplerSpec, batch, *, seed: int, first_utt: Option
     _check(L.rs_generate_signals(C.byref(spec), seed, epoch, batch.n_src, _ptr(utt), _ptr(local), _ptr(off),
                                  _ptr(ln), device_ptr, stream or None))
     return None
+
+
+class SignalPlan:
+    """rs_signal_plan: the generator table of a fixed batch on the device, built once;
+    ``generate(ptr, epoch)`` is then one kernel launch (no host work, no sync)."""
+
+    def __init__(self, spec: RsSamplerSpec, batch, *, seed: int, first_utt: Optional[int] = None):
+        L = load_library()
+        utt, local = _signal_meta(batch, first_utt)
+        off = np.ascontiguousarray(batch.sig_off, np.int64)
+        ln = np.ascontiguousarray(batch.sig_len, np.int64)
+        h = C.c_void_p()
+        _check(L.rs_signal_plan_create(C.byref(spec), seed, batch.n_src, _ptr(utt), _ptr(local), _ptr(off),
+                                       _ptr(ln), C.byref(h)))
+        self.h = h
+
+    def generate(self, device_ptr: int, *, epoch: int = 0, stream: int = 0) -> None:
+        _check(load_library().rs_signal_plan_generate(self.h, int(epoch), C.c_void_p(device_ptr),
+                                                      C.c_void_p(stream or None)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            load_library().rs_signal_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ---- log-Mel front end (SURVEY.md §8f row 4; PAPER.md:452-460) ---------------------------

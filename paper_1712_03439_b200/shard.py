@@ -14,12 +14,17 @@ import numpy as np
 
 
 def predicted_work(batch) -> np.ndarray:
-    """Per-utterance work proxy: Σ_pairs N_x * log-ish RIR factor (before the
-    RIR is known): I * J * N_x * (1 + horizon / 4096)."""
+    """Per-utterance device time proxy, known before any RIR is synthesized:
+    I * J * (N_x + 0.65 (2K + 1)^3).  The OLA filter costs ~20 N_x log2 N flops per pair
+    with log2 N ~ 10 at config 4 (the truncated N_h is not known yet; its log barely
+    moves the cost), the image-method synthesis ~(2K + 1)^3 images per pair; the 0.65
+    weight is their measured ratio on B200 (config 4: K4 27 ms for 1.05e12 flops, K1
+    5.8 ms for 2.1e9 images)."""
     I = np.diff(batch.src_begin)
     J = np.diff(batch.mic_begin)
     nx = batch.sig_len[batch.src_begin[:-1]].astype(np.float64)
-    return I * J * nx * (1.0 + batch.max_taps / 4096.0)
+    images = (2.0 * batch.image_order.astype(np.float64) + 1.0) ** 3
+    return I * J * (nx + 0.65 * images)
 
 
 def lpt_partition(work: np.ndarray, world: int) -> list:

@@ -88,3 +88,39 @@ def test_gloo_two_ranks_match_single_process():
         for j, ch in enumerate(merged[u]):
             want = full.channel(out, u, j, out_len[u])
             assert (ch.view(np.uint64) == want.view(np.uint64)).all()
+
+
+def _bench_json(args, env=None):
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    e.update(env or {})
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py")] + args, cwd=root, env=e,
+                       capture_output=True, text=True, timeout=600)
+    return r, [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+
+
+@pytest.mark.parametrize("scaling,world", [("strong", 2), ("weak", 2), ("strong", 4)])
+def test_bench_spawns_ranks_and_covers_the_workload(scaling, world):
+    """`python bench.py --gpus N` with WORLD_SIZE unset spawns N ranks (here on CPU with
+    gloo, --dry-run): every utterance of the job lands on exactly one rank, the timing
+    reduction is the max over ranks, and rank 0 alone prints."""
+    r, lines = _bench_json(["--gpus", str(world), "--dry-run", "--scaling", scaling, "--utterances", "256"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert len(lines) == 1, r.stdout
+    d = lines[0]
+    assert d["n_gpus"] == world and d["covers_every_utterance_once"] and d["max_over_ranks"] == float(world)
+    assert len(d["shard_utterances"]) == world
+    total = 256 * (world if scaling == "weak" else 1)
+    assert sum(d["shard_utterances"]) == total == d["config"]["utterances"]
+    if scaling == "strong":  # LPT bound: shards within one utterance's predicted work of each other
+        a = np.array(d["shard_predicted_work"])
+        assert a.max() - a.min() <= d["max_utterance_work"] * (1 + 1e-9)
+
+
+def test_bench_rejects_gpus_world_mismatch():
+    r, _ = _bench_json(["--gpus", "2", "--dry-run"], env={"WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr
