@@ -19,6 +19,7 @@
 
 #include "../../include/roomsim_gpu.h"
 #include "kernels.cuh"
+#include "power.cuh"
 
 using namespace rsg;
 
@@ -551,7 +552,7 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
     // largest pairs first (LPT) so the tail of the launch is short
     std::stable_sort(v.begin(), v.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
     if (var == kVarOla2) {  // two-stream K4: an item is a pair of runs of one pair
-      // Runs of a fixed length per pair (>= 16 overlap blocks' worth, >= 24 blocks): the
+      // Runs of a fixed length per pair (16 overlap blocks' worth, whole power segments): the
       // two runs sharing a complex transform round into each other, so which blocks pair
       // up must not depend on the rest of the chunk.
       sp.item_off = static_cast<int64_t>(fp.items2.size());
@@ -559,13 +560,12 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
       for (int32_t p : v) {
         PairPlan& pl = plans[p];
         const int64_t pre = pre_blocks(pl);
-        const int64_t run = std::max<int64_t>(16 * pre, 24);
-        int64_t nr = (pl.B + run - 1) / run;
-        if (nr > 1 && (nr & 1)) ++nr;  // an even number of runs: two per item
-        const int64_t len = (pl.B + nr - 1) / nr;
+        const int64_t len = kPowerSeg * pre;  // >= 16 overlap blocks' worth, a whole number of segments
+        int64_t nr = (pl.B + len - 1) / len;
+        if (nr > 1 && (nr & 1)) ++nr;  // an even number of runs: two per item (the last may be empty)
         pl.part0 = part_acc;
-        pl.npart = static_cast<int32_t>(pl.B * ppb);
-        part_acc += pl.B * ppb;
+        pl.npart = static_cast<int32_t>(power_segments(pl.B) * ppb);
+        part_acc += pl.npart;
         for (int64_t r = 0; r < nr; r += 2) {
           OlaItem2 it{p, 0, 0, 0, static_cast<int32_t>(pl.B), static_cast<int32_t>(pl.B),
                       static_cast<int32_t>(pl.B), 0};
@@ -597,15 +597,16 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
       return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(0);
     }();
     const int64_t run_div = run_div_env ? run_div_env : (ip ? 2 : (l <= 8 ? 12 : 3));
-    const int64_t run = std::max<int64_t>((total_blocks + run_div * slots - 1) / (run_div * slots), 16 * max_pre);
+    int64_t run = std::max<int64_t>((total_blocks + run_div * slots - 1) / (run_div * slots), 16 * max_pre);
+    run = (run + kPowerSeg - 1) / kPowerSeg * kPowerSeg;  // runs start on power-segment boundaries
     const int ppb = ip ? ip_parts_per_block(l) : small_parts_per_block(l);
     sp.item_off = static_cast<int64_t>(fp.items.size());
     for (int32_t p : v) {
       PairPlan& pl = plans[p];
       const int64_t pre = pre_blocks(pl);
       pl.part0 = part_acc;
-      pl.npart = static_cast<int32_t>(pl.B * ppb);
-      part_acc += pl.B * ppb;
+      pl.npart = static_cast<int32_t>(power_segments(pl.B) * ppb);
+      part_acc += pl.npart;
       for (int64_t r0 = 0; r0 < pl.B; r0 += run) {
         const int64_t r1 = std::min<int64_t>(pl.B, r0 + run);
         const int64_t b0 = r0 == 0 ? 0 : std::max<int64_t>(0, r0 - pre);
@@ -1272,7 +1273,15 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
     const char* e = std::getenv("RSG_CHUNK_PAIRS");  // tuning override
     return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(0);
   }();
-  const int64_t chunk_pairs = chunk_env ? chunk_env : (host_io ? kChunkPairsHost : kChunkPairsDevice);
+  int64_t total_pairs = 0;
+  for (int64_t u = 0; u < U; ++u)
+    total_pairs += (b->src_begin[u + 1] - b->src_begin[u]) * (b->mic_begin[u + 1] - b->mic_begin[u]);
+  // Device renders of fewer than 2 full chunks (e.g. one rank's share under strong scaling)
+  // still get two chunks, so the host planner of one overlaps the other's kernels.
+  const int64_t dev_chunk = total_pairs > 2 * kChunkPairsDevice
+                                ? kChunkPairsDevice
+                                : std::max<int64_t>(2048, (total_pairs + 1) / 2);
+  const int64_t chunk_pairs = chunk_env ? chunk_env : (host_io ? kChunkPairsHost : dev_chunk);
   // Host path: the last chunk_pairs are split C/2, C/4, C/4 so the pipeline drains
   // quickly (only the final chunk's filter and download follow the last upload).
   std::vector<std::pair<int64_t, int64_t>> ranges;

@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
     prefetch_l2(x + s0, 4 * (nx - s0 < L ? nx - s0 : L));
   }
   __syncthreads();
+  double pw = 0.0;  // this lane's Σ y² of the current power segment
 #pragma unroll 1
   for (int b = it.b_begin; b < it.b_end; ++b) {
     const long long start = static_cast<long long>(b) * L;
@@ -385,8 +386,13 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
         }
       }
     }
-    store_block_power<T>(a.part + pl.part0 + static_cast<long long>(b) * parts_per_block_of(T),
-                         (pb[0] + pb[1]) + (pb[2] + pb[3]), t, b >= it.b_own);
+    // power: per-lane FP64 sum over the segment, stored at its end (power.cuh)
+    pw += static_cast<double>((pb[0] + pb[1]) + (pb[2] + pb[3]));
+    if (closes_segment(b, it.b_end)) {
+      store_segment_power<T>(a.part + pl.part0 + static_cast<long long>(b / kPowerSeg) * parts_per_block_of(T), pw,
+                             t, b >= it.b_own);
+      pw = 0.0;
+    }
   }
 }
 

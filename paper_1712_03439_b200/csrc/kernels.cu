@@ -630,6 +630,7 @@ ola_small_kernel(OlaArgs a) {
   }
   cp_async_wait_all();
   __syncthreads();  // per-CTA twiddles, G, carry and barriers in place (all threads)
+  double pw = 0.0;  // this lane's Σ y² of the current power segment
   // Up to M = RSG_K4_DIRECT_MAX pass 0 reads the block straight from the signal
   // (L2-prefetched two blocks ahead by one thread) instead of the TMA stage: measured
   // 2-27% faster at M <= 256, 5% slower at M = 512
@@ -739,8 +740,14 @@ ola_small_kernel(OlaArgs a) {
       }
     };
     stockham_emit_pass<M, GroupBar<T>, decltype(emit_fn), true, false>(s, t, tws, active, bar, emit_fn);
-    store_block_power<T>(a.part + pl.part0 + static_cast<long long>(b) * parts_per_block_of(T),
-                         (pb[0] + pb[1]) + (pb[2] + pb[3]), t, active && b >= it.b_own);
+    // power: per-lane FP64 sum over the segment, stored at its end (power.cuh)
+    pw += static_cast<double>((pb[0] + pb[1]) + (pb[2] + pb[3]));
+    const bool seg_end = active && closes_segment(b, it.b_end);
+    if (__any_sync(0xffffffffu, seg_end)) {
+      store_segment_power<T>(a.part + pl.part0 + static_cast<long long>(b / kPowerSeg) * parts_per_block_of(T), pw,
+                             t, seg_end && b >= it.b_own);
+      if (seg_end) pw = 0.0;
+    }
     // (N_h - 1 > L, three or more overlapping blocks, needs no extra step: the
     // old carry at e in [L, N_h - 1) comes from the other buffer.)
   }

@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(ola2_cta(ilog2(N)), ola2_minb(ilog2(N))) ola2_
     prefetch(0, 0);
     prefetch(1, 0);
   }
+  double pw[2] = {0.0, 0.0};  // per run: this lane's Σ y² of the current power segment
 #pragma unroll 1
   for (int k = 0; k < trips; ++k) {
     int b[2], d[2] = {0, 0}, take[2] = {0, 0};
@@ -208,10 +209,17 @@ __global__ void __launch_bounds__(ola2_cta(ilog2(N)), ola2_minb(ilog2(N))) ola2_
         }
       }
     });
+    // power: per-lane FP64 sums over each run's segment, stored at its end (power.cuh)
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
-      store_block_power<T>(a.part + pl.part0 + static_cast<long long>(b[r]) * parts_per_block_of(T), pb[r], t,
-                           act[r] && b[r] >= ro[r]);
+    for (int r = 0; r < 2; ++r) {
+      pw[r] += static_cast<double>(pb[r]);
+      const bool seg_end = act[r] && closes_segment(b[r], re_[r]);
+      if (__any_sync(0xffffffffu, seg_end)) {
+        store_segment_power<T>(a.part + pl.part0 + static_cast<long long>(b[r] / kPowerSeg) * parts_per_block_of(T),
+                               pw[r], t, seg_end && b[r] >= ro[r]);
+        if (seg_end) pw[r] = 0.0;
+      }
+    }
   }
 }
 

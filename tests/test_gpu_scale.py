@@ -111,7 +111,7 @@ def test_config4_full_scale_device_and_host():
     # subsample: every 64th utterance + first / last utterance of every chunk of both modes
     ppu = b.pairs_per_utt
     ids = set(range(0, b.n_utt, 64)) | {b.n_utt - 1}
-    for host_mode, cp in ((False, 16384), (True, 6144)):
+    for host_mode, cp in ((False, 16384), (True, 6144)):  # api.cu kChunkPairsDevice / kChunkPairsHost
         rng_ = chunk_ranges(ppu, cp, host_mode)
         assert len(rng_) >= (3 if not host_mode else 8), rng_
         for u0, u1 in rng_:
