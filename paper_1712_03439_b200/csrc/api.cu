@@ -560,7 +560,7 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
       for (int32_t p : v) {
         PairPlan& pl = plans[p];
         const int64_t pre = pre_blocks(pl);
-        const int64_t len = kPowerSeg * pre;  // >= 16 overlap blocks' worth, a whole number of segments
+        const int64_t len = kPowerSeg * std::max<int64_t>(pre, 1);  // 16 overlap blocks' worth, whole segments
         int64_t nr = (pl.B + len - 1) / len;
         if (nr > 1 && (nr & 1)) ++nr;  // an even number of runs: two per item (the last may be empty)
         pl.part0 = part_acc;
@@ -832,8 +832,11 @@ struct Chunk {
   std::vector<PairMeta> pair;
   std::vector<SynthItem> items;
   std::vector<std::tuple<int64_t, int64_t, int, int>> synth_class;  // (offset, count, slice cap, threads)
-  std::vector<int> place_err;
+  std::vector<int> place_err;            // per pair: config / placement error (K1 skips the pair)
   std::vector<std::string> place_msg;
+  std::vector<uint8_t> empty_sig;        // per pair: N_x == 0 (reported after the RIR's own errors)
+  std::vector<int> utt_err;              // per utterance: no target or no mic
+  std::vector<std::string> utt_msg;
   std::vector<PairPlan> plans;
   std::vector<int32_t> strategy;
   std::vector<int64_t> ulen;
@@ -922,15 +925,21 @@ int state_init(rs_ctx* c);
 // Host metadata of chunk k (validation with the reference's messages).
 int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
   ch.utt.clear(); ch.rg.clear(); ch.pair.clear(); ch.items.clear();
-  ch.place_err.clear(); ch.place_msg.clear();
+  ch.place_err.clear(); ch.place_msg.clear(); ch.empty_sig.clear(); ch.utt_err.clear(); ch.utt_msg.clear();
   ch.max_order = 0; ch.slice = 1; ch.rir_total = 0;
   for (int64_t u = ch.u0; u < ch.u1; ++u) {
     const double* L = b->room_dims + 3 * u;
-    const int K = b->image_order[u];
-    RS_TRY(room_validate(L, b->reflection[u], b->sample_rate[u], b->speed_of_sound[u], K));
     const int64_t s0 = b->src_begin[u], I = b->src_begin[u + 1] - s0;
     const int64_t m0 = b->mic_begin[u], J = b->mic_begin[u + 1] - m0;
-    if (I < 1 || J < 1) return fail(RS_ERR_CONFIG, "scene needs a target and a microphone");
+    // Errors are recorded, not returned: plan_chunk reports the first one in the order the
+    // reference meets them (utterance, then pair; per pair: RoomConfig::validate and the
+    // placements inside synthesize_rir, geometry, truncation, then the convolution).
+    ch.utt_err.push_back(I < 1 || J < 1 ? RS_ERR_CONFIG : RS_OK);
+    ch.utt_msg.push_back(I < 1 || J < 1 ? "scene needs a target and a microphone" : "");
+    int K = b->image_order[u];
+    const int cfg_err = room_validate(L, b->reflection[u], b->sample_rate[u], b->speed_of_sound[u], K);
+    const std::string cfg_msg = cfg_err ? g_err : std::string();
+    if (cfg_err) K = 0;  // no lattice for an invalid room: its pairs carry the config error
     UttMeta um{};
     for (int a = 0; a < 3; ++a) um.dims[a] = L[a];
     um.spm = b->sample_rate[u] / b->speed_of_sound[u];  // room_model.hpp:150
@@ -966,8 +975,8 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
         pm.sig_off = b->sig_off[s0 + i];
         pm.nx = b->sig_len[s0 + i];
         // RIR length = min(max_delay + 1, horizon), known exactly before the synth
-        int64_t pcap = cap;
-        if (strictly_inside(L, sp) && strictly_inside(L, mp)) {
+        int64_t pcap = cfg_err ? 1 : cap;
+        if (!cfg_err && strictly_inside(L, sp) && strictly_inside(L, mp)) {
           const int64_t md = static_cast<int64_t>(lattice_max_delay(L, sp, mp, K, um.spm)) + 1;
           pcap = um.max_taps > 0 ? std::min<int64_t>(md, um.max_taps) : md;
         }
@@ -976,18 +985,19 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
         ch.rir_total += pcap;
         int err = RS_OK;
         std::string msg;
-        if (!strictly_inside(L, sp)) {  // room_model.hpp:144-145
+        if (cfg_err) {  // room_model.hpp:143 (validate first)
+          err = cfg_err;
+          msg = cfg_msg;
+        } else if (!strictly_inside(L, sp)) {  // room_model.hpp:144-145
           err = RS_ERR_PLACEMENT;
           msg = "source must lie strictly inside the room";
         } else if (!strictly_inside(L, mp)) {  // :146-147
           err = RS_ERR_PLACEMENT;
           msg = "microphone must lie strictly inside the room";
-        } else if (pm.nx <= 0) {
-          err = RS_ERR_DEGENERATE;
-          msg = "convolution input must be non-empty mono audio";
         }
         ch.place_err.push_back(err);
         ch.place_msg.push_back(msg);
+        ch.empty_sig.push_back(pm.nx <= 0 ? 1 : 0);
         ch.pair.push_back(pm);
       }
   }
@@ -1078,7 +1088,15 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
   ch.strategy.assign(ch.P, RS_OVERLAP_ADD);
   ch.ulen.assign(ch.u1 - ch.u0, 0);
   int64_t spec_off = 0, y_off = 0;
+  // utterance-level errors (no target / mic) of utterances [next_utt, upto), in order
+  int64_t next_utt = 0;
+  auto utt_check = [&](int64_t upto) -> int {
+    for (; next_utt < upto; ++next_utt)
+      if (ch.utt_err[next_utt]) return fail(ch.utt_err[next_utt], ch.utt_msg[next_utt]);
+    return RS_OK;
+  };
   for (int64_t p = 0; p < ch.P; ++p) {
+    RS_TRY(utt_check(ch.pair[p].utt + 1));
     if (ch.place_err[p]) return fail(ch.place_err[p], ch.place_msg[p]);
     const PairRir& r = ch.h_rir[p];
     if (r.flags & 1) return fail(RS_ERR_GEOMETRY, "microphone coincides with an image source");
@@ -1091,16 +1109,20 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
     int s = RS_OVERLAP_ADD;
     double cost;
     if (b->plan_rule == RS_PLAN_CHOOSE) {
+      // choose_plan validates the lengths before convolve sees the signal (convolution.hpp:94-98)
       RS_TRY(choose_plan_impl(1.0, 1.0, nx, nh, &s, &n, &cost));
       if (s == RS_FULL_FFT) n = fft_size_for(nx + nh - 1);
     } else if (b->plan_rule == RS_PLAN_FORCED) {
       n = static_cast<size_t>(b->forced_fft_size);
+      // convolve_ola checks its input before the FFT size (convolution.hpp:221-227)
+      if (ch.empty_sig[p]) return fail(RS_ERR_DEGENERATE, "convolution input must be non-empty mono audio");
       RS_TRY(checked_fft_size(n, nh, "overlap-add"));
     } else if (b->plan_rule == RS_PLAN_POW2_TWICE) {
       n = bit_ceil_sz(2 * nh);
     } else {
       return fail(RS_ERR_CONFIG, "unknown plan rule");
     }
+    if (ch.empty_sig[p]) return fail(RS_ERR_DEGENERATE, "convolution input must be non-empty mono audio");
     if (n < 2 || n > (static_cast<size_t>(2) << kLargeMaxLog2M))
       return fail(RS_ERR_UNSUPPORTED, "FFT size " + std::to_string(n) + " not supported by the device kernels");
     ch.strategy[p] = s;
@@ -1117,6 +1139,7 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
     int64_t& ul = ch.ulen[ch.pair[p].utt];
     ul = std::max(ul, pl.out_len);
   }
+  RS_TRY(utt_check(static_cast<int64_t>(ch.utt_err.size())));  // trailing utterances without pairs
   for (int64_t u = ch.u0; u < ch.u1; ++u)
     if (out_stride[u] < ch.ulen[u - ch.u0]) return fail(RS_ERR_CONFIG, "output stride too small");
   return plan_filter(ch.plans, ch.fp);

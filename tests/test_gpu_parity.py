@@ -434,3 +434,52 @@ def test_render_rirs_bit_exact(rs, ctx, port, cfg, n_utt, seed):
                 assert (got.view(np.uint64) == want.view(np.uint64)).all(), p
                 checked += 1
     assert checked == b.n_pairs
+
+
+def test_render_error_order_matches_reference(rs, ctx):
+    """The first error of a render is the one the reference meets first: utterance
+    order, then pair order; per pair RoomConfig::validate and the placements inside
+    synthesize_rir, then geometry, then the convolution's own checks."""
+    import oracle
+    from paper_1712_03439_b200 import scenes
+
+    ref = oracle.reference() if oracle.reference_available() else oracle.port()
+    codes = {rs.PlacementError: 1, rs.GeometryError: 2, rs.DegenerateInputError: 3, rs.PlanError: 4,
+             rs.ConfigError: 5}
+
+    def run_both(b):
+        try:
+            rs.render_batch(b, ctx=ctx)
+            got = 0
+        except rs.Error as e:
+            got = codes[type(e)]
+        try:
+            ref.render_batch(b)
+            want = 0
+        except oracle.OracleError as e:
+            want = e.code
+        return got, want
+
+    cases = []
+    b = scenes.config3(n_utt=3, seed=81)       # utt 0 pair (1, *): placement; utt 1: bad room
+    b.src_pos[b.src_begin[0] + 1] = [0.0, 1.0, 1.0]
+    b.reflection[1] = 1.5
+    cases.append((b, 1))
+    b = scenes.config3(n_utt=3, seed=81)       # utt 1: bad room before utt 2's placement error
+    b.reflection[1] = 1.5
+    b.mic_pos[b.mic_begin[2]] = [-1.0, 1.0, 1.0]
+    cases.append((b, 5))
+    b = scenes.config3(n_utt=2, seed=82)       # mic on the source (geometry) beats its empty signal
+    b.image_order[1] = 0
+    s = b.src_begin[1]
+    b.mic_pos[b.mic_begin[1]] = b.src_pos[s]
+    b.sig_len = b.sig_len.copy()
+    b.sig_len[s] = 0
+    cases.append((b, 2))
+    b = scenes.config3(n_utt=2, seed=83)       # an empty signal alone: DegenerateInputError
+    b.sig_len = b.sig_len.copy()
+    b.sig_len[b.src_begin[1] + 1] = 0
+    cases.append((b, 3))
+    for k, (b, want_code) in enumerate(cases):
+        got, want = run_both(b)
+        assert got == want == want_code, (k, got, want)
