@@ -852,12 +852,12 @@ struct Chunk {
   double* h_gain = nullptr;
   double* h_power = nullptr;
   cudaEvent_t ev_rir = nullptr, ev_syn0 = nullptr, ev_syn1 = nullptr, ev_k4a = nullptr, ev_k4b = nullptr,
-              ev_mix0 = nullptr, ev_mix1 = nullptr, ev_sig = nullptr, ev_out = nullptr, ev_filtered = nullptr;
+              ev_mix0 = nullptr, ev_mix1 = nullptr, ev_sig = nullptr, ev_out = nullptr;
   int init_events() {
     cudaEvent_t* evs[] = {&ev_rir, &ev_syn0, &ev_syn1, &ev_k4a, &ev_k4b, &ev_mix0, &ev_mix1};
     for (auto* e : evs)
       if (!*e) RS_CUDA(cudaEventCreate(e));
-    cudaEvent_t* sync_only[] = {&ev_sig, &ev_out, &ev_filtered};
+    cudaEvent_t* sync_only[] = {&ev_sig, &ev_out};
     for (auto* e : sync_only)
       if (!*e) RS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     return RS_OK;
@@ -870,7 +870,7 @@ struct Chunk {
     for (DevBuf* b : bufs) b->release();
     hA.release();
     hB.release();
-    cudaEvent_t evs[] = {ev_rir, ev_syn0, ev_syn1, ev_k4a, ev_k4b, ev_mix0, ev_mix1, ev_sig, ev_out, ev_filtered};
+    cudaEvent_t evs[] = {ev_rir, ev_syn0, ev_syn1, ev_k4a, ev_k4b, ev_mix0, ev_mix1, ev_sig, ev_out};
     for (auto e : evs)
       if (e) cudaEventDestroy(e);
   }
@@ -884,8 +884,7 @@ struct rs_render_state {
   std::vector<int64_t> pair_chunk;  // global pair -> chunk
   // sA: K1/K2 and RIR summaries; sB: K3-K6; sH/sD: host<->device copies of the
   // signals and outputs, so the PCIe transfers run back to back under the kernels.
-  cudaStream_t sA = nullptr, sB = nullptr, sH = nullptr, sD = nullptr, sM = nullptr;
-  cudaEvent_t ev_endM = nullptr;
+  cudaStream_t sA = nullptr, sB = nullptr, sH = nullptr, sD = nullptr;
   cudaEvent_t ev_start = nullptr, ev_endA = nullptr, ev_endB = nullptr, ev_endH = nullptr, ev_endD = nullptr;
   // RSG_TRACE=1: per-chunk timeline of the pipeline (device events + host marks) on stderr
   bool tracing = false;
@@ -1148,8 +1147,7 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
 
 // Stream B: K3, K4, K5, K6 (+ output download on the host path).
 int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO& io, const int64_t* out_off,
-                   const int64_t* out_stride, cudaStream_t sB, cudaStream_t sD, cudaStream_t sM,
-                   cudaEvent_t ev_filtered) {
+                   const int64_t* out_stride, cudaStream_t sB, cudaStream_t sD) {
   const int64_t U = ch.u1 - ch.u0;
   std::vector<double> snr_lin(b->src_begin[ch.u1] - b->src_begin[ch.u0]);
   const int64_t s_first = b->src_begin[ch.u0];
@@ -1186,46 +1184,42 @@ int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO
   if (io.h_signals) RS_CUDA(cudaStreamWaitEvent(sB, ch.ev_sig, 0));
   RS_TRY(launch_filter(c, ch.fb, ch.fp, ch.plans, ch.d_pair.as<PairMeta>(), ch.d_rir.as<double>(), io.d_signals,
                        sB, &ch.hB, ch.ev_k4a, ch.ev_k4b));
-  // gains + mix on their own (high-priority) stream: chunk k's mix streams through HBM
-  // while chunk k+1's filter keeps the FP32 pipes busy (RSG_MIX_SAME_STREAM=1: sB)
-  RS_CUDA(cudaEventRecord(ev_filtered, sB));
-  RS_CUDA(cudaStreamWaitEvent(sM, ev_filtered, 0));
-  if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_mix0, sM));
-  RS_TRY(upload_on(ch.d_snr, snr_lin, sM, &ch.hB));
-  RS_TRY(upload_on(ch.d_utt_pair0, pair0, sM, &ch.hB));
-  RS_TRY(upload_on(ch.d_utt_I, uI, sM, &ch.hB));
-  RS_TRY(upload_on(ch.d_utt_J, uJ, sM, &ch.hB));
-  RS_TRY(upload_on(ch.d_chan_utt, ch_utt, sM, &ch.hB));
-  RS_TRY(upload_on(ch.d_chan_mic, ch_mic, sM, &ch.hB));
-  RS_TRY(upload_on(ch.d_chan_out, ch_out, sM, &ch.hB));
-  RS_TRY(upload_on(ch.d_utt_len, ch.ulen, sM, &ch.hB));
-  RS_TRY(upload_on(ch.d_utt_stride, ustride, sM, &ch.hB));
+  if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_mix0, sB));
+  RS_TRY(upload_on(ch.d_snr, snr_lin, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_utt_pair0, pair0, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_utt_I, uI, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_utt_J, uJ, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_chan_utt, ch_utt, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_chan_mic, ch_mic, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_chan_out, ch_out, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_utt_len, ch.ulen, sB, &ch.hB));
+  RS_TRY(upload_on(ch.d_utt_stride, ustride, sB, &ch.hB));
   RS_TRY(ch.d_gain.ensure(std::max<int64_t>(ch.P, 1) * sizeof(double)));
   RS_TRY(ch.d_power.ensure(std::max<int64_t>(ch.P, 1) * sizeof(double)));
   RS_TRY(ch.d_flags.ensure(std::max<int64_t>(ch.P, 1) * sizeof(int32_t)));
-  RS_CUDA(cudaMemsetAsync(ch.d_flags.p, 0, std::max<int64_t>(ch.P, 1) * sizeof(int32_t), sM));
+  RS_CUDA(cudaMemsetAsync(ch.d_flags.p, 0, std::max<int64_t>(ch.P, 1) * sizeof(int32_t), sB));
   GainArgs ga{ch.d_pair.as<PairMeta>(), ch.fb.plan.as<PairPlan>(), ch.d_utt_pair0.as<int64_t>(),
               ch.d_utt_J.as<int32_t>(), ch.fb.part.as<double>(), ch.d_snr.as<double>() - s_first,
               ch.d_gain.as<double>(), ch.d_power.as<double>(), ch.d_flags.as<int32_t>(), ch.P};
-  RS_CUDA(launch_gain(ga, sM));
+  RS_CUDA(launch_gain(ga, sB));
   c->launches += 2;
   MixArgs ma{ch.d_chan_utt.as<int64_t>(), ch.d_chan_mic.as<int32_t>(), ch.d_chan_out.as<int64_t>(),
              ch.d_utt_len.as<int64_t>(), ch.d_utt_stride.as<int64_t>(), ch.d_utt_pair0.as<int64_t>(),
              ch.d_utt_I.as<int32_t>(), ch.d_utt_J.as<int32_t>(), ch.fb.plan.as<PairPlan>(), ch.fb.y.as<float>(),
              ch.d_gain.as<double>(), io.d_out, 4096};
-  RS_CUDA(launch_mix(ma, static_cast<int64_t>(ch_utt.size()), max_stride, sM));
+  RS_CUDA(launch_mix(ma, static_cast<int64_t>(ch_utt.size()), max_stride, sB));
   ++c->launches;
-  if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_mix1, sM));
+  if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_mix1, sB));
   ch.h_flags = ch.hB.alloc<int32_t>(ch.P);
   ch.h_gain = ch.hB.alloc<double>(ch.P);
   ch.h_power = ch.hB.alloc<double>(ch.P);
   if (ch.P) {
     RS_TRY(small_copy(ch.h_flags, ch.hB.dev(ch.h_flags), ch.d_flags.p, ch.d_flags.p, ch.P * sizeof(int32_t),
-                      cudaMemcpyDeviceToHost, sM));
+                      cudaMemcpyDeviceToHost, sB));
     RS_TRY(small_copy(ch.h_gain, ch.hB.dev(ch.h_gain), ch.d_gain.p, ch.d_gain.p, ch.P * sizeof(double),
-                      cudaMemcpyDeviceToHost, sM));
+                      cudaMemcpyDeviceToHost, sB));
     RS_TRY(small_copy(ch.h_power, ch.hB.dev(ch.h_power), ch.d_power.p, ch.d_power.p, ch.P * sizeof(double),
-                      cudaMemcpyDeviceToHost, sM));
+                      cudaMemcpyDeviceToHost, sB));
   }
   if (io.h_out) {  // host path: this chunk's output span, on the download stream
     int64_t lo = INT64_MAX, hi = 0;
@@ -1234,7 +1228,7 @@ int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO
       hi = std::max(hi, out_off[u] + (b->mic_begin[u + 1] - b->mic_begin[u]) * out_stride[u]);
     }
     if (hi > lo) {
-      RS_CUDA(cudaEventRecord(ch.ev_out, sM));
+      RS_CUDA(cudaEventRecord(ch.ev_out, sB));
       RS_CUDA(cudaStreamWaitEvent(sD, ch.ev_out, 0));
       RS_CUDA(cudaMemcpyAsync(io.h_out + lo, io.d_out + lo, (hi - lo) * sizeof(float), cudaMemcpyDeviceToHost, sD));
     }
@@ -1251,14 +1245,6 @@ int state_init(rs_ctx* c) {
   c->rs = new rs_render_state();
   RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sA, cudaStreamNonBlocking));
   RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sB, cudaStreamNonBlocking));
-  {
-    static const bool same = std::getenv("RSG_MIX_SAME_STREAM") != nullptr;  // A/B measurement
-    int lo = 0, hi = 0;
-    RS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    if (same) c->rs->sM = c->rs->sB;
-    else RS_CUDA(cudaStreamCreateWithPriority(&c->rs->sM, cudaStreamNonBlocking, hi));
-  }
-  RS_CUDA(cudaEventCreateWithFlags(&c->rs->ev_endM, cudaEventDisableTiming));
   RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sH, cudaStreamNonBlocking));
   RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sD, cudaStreamNonBlocking));
   cudaEvent_t* evs[] = {&c->rs->ev_start, &c->rs->ev_endA, &c->rs->ev_endB, &c->rs->ev_endH, &c->rs->ev_endD};
@@ -1269,7 +1255,7 @@ int state_init(rs_ctx* c) {
 void destroy_state(rs_ctx* c) {
   if (!c->rs) return;
   rs_render_state* r = c->rs;
-  cudaStream_t ss[] = {r->sA, r->sB, r->sH, r->sD, r->sM == r->sB ? nullptr : r->sM};
+  cudaStream_t ss[] = {r->sA, r->sB, r->sH, r->sD};
   for (auto st : ss)
     if (st) cudaStreamSynchronize(st);
   for (auto& ch : r->chunks) ch.release();
@@ -1279,7 +1265,7 @@ void destroy_state(rs_ctx* c) {
   for (DevBuf* b : bufs) b->release();
   for (auto st : ss)
     if (st) cudaStreamDestroy(st);
-  cudaEvent_t evs[] = {r->ev_start, r->ev_endA, r->ev_endB, r->ev_endH, r->ev_endD, r->ev_endM};
+  cudaEvent_t evs[] = {r->ev_start, r->ev_endA, r->ev_endB, r->ev_endH, r->ev_endD};
   for (auto e : evs)
     if (e) cudaEventDestroy(e);
   delete r;
@@ -1368,7 +1354,6 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
   }
   RS_CUDA(cudaStreamWaitEvent(R.sA, R.ev_start, 0));
   RS_CUDA(cudaStreamWaitEvent(R.sB, R.ev_start, 0));
-  RS_CUDA(cudaStreamWaitEvent(R.sM, R.ev_start, 0));
   RS_CUDA(cudaStreamWaitEvent(R.sH, R.ev_start, 0));
   RS_CUDA(cudaStreamWaitEvent(R.sD, R.ev_start, 0));
   if (c->profiling) RS_CUDA(cudaEventRecord(c->st[0], c->stream));
@@ -1413,7 +1398,7 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
     R.hmark("plan done " + std::to_string(k));
     t_plan += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (status) break;
-    status = enqueue_filter(c, b, R.chunks[k], io, out_off, out_stride, R.sB, R.sD, R.sM, R.chunks[k].ev_filtered);
+    status = enqueue_filter(c, b, R.chunks[k], io, out_off, out_stride, R.sB, R.sD);
     R.mark(R.sB, "filter+mix enq-end " + std::to_string(k));
     R.mark(R.sD, "d2h done " + std::to_string(k));
     R.mark(R.sA, "sA at " + std::to_string(k));
@@ -1422,8 +1407,6 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
   // ---- join back into the caller's stream -------------------------------------------
   cudaEventRecord(R.ev_endA, R.sA);
   cudaEventRecord(R.ev_endB, R.sB);
-  cudaEventRecord(R.ev_endM, R.sM);
-  cudaStreamWaitEvent(c->stream, R.ev_endM, 0);
   cudaEventRecord(R.ev_endH, R.sH);
   cudaEventRecord(R.ev_endD, R.sD);
   cudaStreamWaitEvent(c->stream, R.ev_endA, 0);
