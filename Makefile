@@ -5,7 +5,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC,-O2,-ffp-contract=off
 SRC := paper_1712_03439_b200/csrc
 OUT := paper_1712_03439_b200/_lib
-OBJS := $(OUT)/synth_cut.o $(OUT)/kernels.o $(OUT)/big.o $(OUT)/large.o $(OUT)/ola2.o $(OUT)/sampler.o $(OUT)/features.o $(OUT)/api.o
+OBJS := $(OUT)/kernels.o $(OUT)/big.o $(OUT)/large.o $(OUT)/ola2.o $(OUT)/sampler.o $(OUT)/features.o $(OUT)/api.o
 
 REF_INC ?= /root/reference/proj/include
 ADAPTER := tests/cpp/_build/adapter_test
@@ -15,10 +15,6 @@ all: $(OUT)/libroomsim_gpu.so oracle adapter
 $(OUT)/kernels.o: $(SRC)/kernels.cu $(SRC)/kernels.cuh $(SRC)/power.cuh $(SRC)/fft.cuh $(SRC)/async.cuh
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/kernels.ptxas.log || (cat $(OUT)/kernels.ptxas.log; false)
-
-$(OUT)/synth_cut.o: $(SRC)/synth_cut.cu $(SRC)/kernels.cuh
-	@mkdir -p $(OUT)
-	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/synth_cut.ptxas.log || (cat $(OUT)/synth_cut.ptxas.log; false)
 
 $(OUT)/large.o: $(SRC)/large.cu $(SRC)/kernels.cuh $(SRC)/power.cuh $(SRC)/fft.cuh $(SRC)/async.cuh
 	@mkdir -p $(OUT)

@@ -832,8 +832,6 @@ struct Chunk {
   std::vector<PairMeta> pair;
   std::vector<SynthItem> items;
   std::vector<std::tuple<int64_t, int64_t, int, int>> synth_class;  // (offset, count, slice cap, threads)
-  std::vector<int32_t> cut_pairs;                                    // truncated renders: synth_cut.cu
-  std::vector<std::tuple<int64_t, int64_t, int, int>> cut_class;     // (offset, count, cap, window)
   std::vector<int> place_err;            // per pair: config / placement error (K1 skips the pair)
   std::vector<std::string> place_msg;
   std::vector<uint8_t> empty_sig;        // per pair: N_x == 0 (reported after the RIR's own errors)
@@ -845,7 +843,7 @@ struct Chunk {
   FilterPlan fp;
   int max_order = 0, slice = 1;
   int64_t rir_total = 0;
-  DevBuf d_utt, d_pair, d_rg, d_items, d_cut, d_rir, d_rirout, d_gain, d_power, d_flags, d_snr, d_chan_utt,
+  DevBuf d_utt, d_pair, d_rg, d_items, d_rir, d_rirout, d_gain, d_power, d_flags, d_snr, d_chan_utt,
       d_chan_mic, d_chan_out, d_utt_len, d_utt_stride, d_utt_pair0, d_utt_I, d_utt_J;
   FilterBufs fb;
   PinnedArena hA, hB;
@@ -865,7 +863,7 @@ struct Chunk {
     return RS_OK;
   }
   void release() {
-    DevBuf* bufs[] = {&d_utt, &d_pair, &d_rg, &d_items, &d_cut, &d_rir, &d_rirout, &d_gain, &d_power, &d_flags,
+    DevBuf* bufs[] = {&d_utt, &d_pair, &d_rg, &d_items, &d_rir, &d_rirout, &d_gain, &d_power, &d_flags,
                       &d_snr, &d_chan_utt, &d_chan_mic, &d_chan_out, &d_utt_len, &d_utt_stride,
                       &d_utt_pair0, &d_utt_I, &d_utt_J, &fb.plan, &fb.lists, &fb.olaitems, &fb.spec,
                       &fb.y, &fb.part, &fb.units, &fb.scratch, &fb.yblk, &fb.olaitems2};
@@ -1018,23 +1016,8 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
   }();
   static const int kClass[4] = {2048, 6144, kSynthSlice, kSynthBig};
   std::vector<SynthItem> cls[2][4];
-  // Truncated renders: K1 synthesizes only the bins truncate_rir can keep (synth_cut.cu),
-  // one CTA per pair, launch classes by RIR length (RSG_SYNTH_CUT=0: the full K1).
-  static const bool cut_off = [] {
-    const char* e = std::getenv("RSG_SYNTH_CUT");
-    return e && e[0] == '0';
-  }();
-  static const int kCutCap[3] = {8192, 16384, 32768};
-  std::vector<int32_t> cut_cls[3];
-  ch.cut_pairs.clear();
-  ch.cut_class.clear();
   for (int64_t p = 0; p < ch.P; ++p) {
     if (ch.place_err[p]) continue;
-    if (b->eta_db > 0.0 && !cut_off && ch.pair[p].rir_cap <= kCutCap[2]) {
-      const int64_t cap = ch.pair[p].rir_cap;
-      cut_cls[cap <= kCutCap[0] ? 0 : (cap <= kCutCap[1] ? 1 : 2)].push_back(static_cast<int32_t>(p));
-      continue;
-    }
     const int64_t cap = ch.pair[p].rir_cap;
     const int K = ch.utt[ch.pair[p].utt].order;
     const int small = K <= 12 ? 1 : 0;  // measured crossover of the 128- and 512-thread K1
@@ -1047,12 +1030,6 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
       const int k = len <= kClass[0] ? 0 : (len <= kClass[1] ? 1 : 2);
       cls[small][k].push_back(SynthItem{static_cast<int32_t>(p), static_cast<int32_t>(lo), static_cast<int32_t>(len), 0});
     }
-  }
-  for (int k = 2; k >= 0; --k) {  // longest RIRs first
-    if (cut_cls[k].empty()) continue;
-    ch.cut_class.emplace_back(static_cast<int64_t>(ch.cut_pairs.size()), static_cast<int64_t>(cut_cls[k].size()),
-                              kCutCap[k], kCutCap[k] / 2);
-    ch.cut_pairs.insert(ch.cut_pairs.end(), cut_cls[k].begin(), cut_cls[k].end());
   }
   ch.synth_class.clear();
   for (int small = 0; small < 2; ++small)
@@ -1071,7 +1048,6 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
 int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, cudaStream_t sA) {
   RS_TRY(ch.init_events());
   size_t need = staged_bytes(ch.utt) + staged_bytes(ch.pair) + staged_bytes(ch.rg) + staged_bytes(ch.items) +
-                staged_bytes(ch.cut_pairs) +
                 ((std::max<int64_t>(ch.P, 1) * sizeof(PairRir) + 63) & ~size_t(63)) + 64;
   RS_TRY(ch.hA.reserve(need));
   ch.hA.reset();
@@ -1080,7 +1056,6 @@ int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, cudaStream_t sA
   RS_TRY(upload_on(ch.d_pair, ch.pair, sA, &ch.hA));
   RS_TRY(upload_on(ch.d_rg, ch.rg, sA, &ch.hA));
   RS_TRY(upload_on(ch.d_items, ch.items, sA, &ch.hA));
-  if (!ch.cut_pairs.empty()) RS_TRY(upload_on(ch.d_cut, ch.cut_pairs, sA, &ch.hA));
   RS_TRY(ch.d_rir.ensure(std::max<int64_t>(ch.rir_total, 1) * sizeof(double)));
   RS_TRY(ch.d_rirout.ensure(std::max<int64_t>(ch.P, 1) * sizeof(PairRir)));
   RS_CUDA(cudaMemsetAsync(ch.d_rirout.p, 0, std::max<int64_t>(ch.P, 1) * sizeof(PairRir), sA));
@@ -1094,13 +1069,6 @@ int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, cudaStream_t sA
     ++c->launches;
   }
   const double eta_factor = b->eta_db > 0.0 ? std::pow(10.0, -b->eta_db / 10.0) : 0.0;
-  constexpr int kCandCap = 8192;  // candidate entries per window pass (synth_cut.cu)
-  for (const auto& [off, n, cap, win] : ch.cut_class) {
-    SynthCutArgs sc{ch.d_utt.as<UttMeta>(), ch.d_pair.as<PairMeta>(), ch.d_rg.as<double>(),
-                    ch.d_cut.as<int32_t>() + off, ch.d_rir.as<double>(), ch.d_rirout.as<PairRir>(), eta_factor};
-    RS_CUDA(launch_synth_cut(sc, static_cast<int>(n), cap, win, ch.max_order, kCandCap, sA));
-    ++c->launches;
-  }
   CutArgs ca{ch.d_pair.as<PairMeta>(), ch.d_utt.as<UttMeta>(), ch.d_rir.as<double>(), ch.d_rirout.as<PairRir>(),
              eta_factor};
   RS_CUDA(launch_cut(ca, static_cast<int>(ch.P), sA));

@@ -323,10 +323,8 @@ __global__ void __launch_bounds__(256) rir_cut_kernel(CutArgs a) {
     }
     return;
   }
-  // bins at and beyond exact_len were not synthesized: all provably below the threshold
-  const long long scan = (r.exact_len > 0 && r.exact_len < len) ? r.exact_len : len;
   double mx = 0.0;
-  for (long long n = tid; n < scan; n += 256) mx = fmax(mx, __dmul_rn(h[n], h[n]));
+  for (long long n = tid; n < len; n += 256) mx = fmax(mx, __dmul_rn(h[n], h[n]));
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if (lane == 0) red_d[warp] = mx;
   __syncthreads();
@@ -334,7 +332,7 @@ __global__ void __launch_bounds__(256) rir_cut_kernel(CutArgs a) {
   for (int w = 1; w < 8; ++w) mx = fmax(mx, red_d[w]);
   const double th = __dmul_rn(mx, a.eta_factor);  // room_model.hpp:184
   long long last = -1;
-  for (long long n = tid; n < scan; n += 256)
+  for (long long n = tid; n < len; n += 256)
     if (__dmul_rn(h[n], h[n]) >= th) last = n;  // room_model.hpp:193-195
   for (int o = 16; o > 0; o >>= 1) {
     const long long other = __shfl_xor_sync(0xffffffffu, last, o);

@@ -38,8 +38,7 @@ struct PairRir {
   int64_t cutoff;                // n_c
   double threshold;              // p_th (room_model.hpp:184)
   int32_t flags;                 // 1: geometry error (d <= 0), 2: degenerate (all-zero)
-  int32_t exact_len;             // > 0: only bins [0, exact_len) were synthesized (synth_cut.cu);
-                                 // every later bin is provably below the cut threshold
+  int32_t pad;
 };
 
 // Per pair, written by the host planner (after K2) and consumed by K3/K4/mix.
@@ -82,20 +81,6 @@ struct SynthArgs {
   double* rir;
   PairRir* out;
 };
-
-// K1 for truncated renders (synth_cut.cu): one CTA per pair of `pairs`.
-struct SynthCutArgs {
-  const UttMeta* utt;
-  const PairMeta* pair;
-  const double* rg;
-  const int32_t* pairs;
-  double* rir;
-  PairRir* out;
-  double eta_factor;  // pow(10, -eta/10), host std::pow
-};
-size_t synth_cut_smem_bytes(int cap, int win, int max_order, int cand_cap);
-cudaError_t launch_synth_cut(const SynthCutArgs& a, int n_pairs, int cap, int win, int max_order, int cand_cap,
-                             cudaStream_t s);
 
 struct CutArgs {
   const PairMeta* pair;
