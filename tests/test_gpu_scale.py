@@ -249,3 +249,28 @@ def test_convolve_dispatch(rs, ctx):
         rs.convolve(np.ones(10), np.ones(3), rs.ConvolutionPlan(rs.OVERLAP_ADD, None), ctx=ctx)
     with pytest.raises(rs.DegenerateInputError):
         rs.convolve(np.ones(0), np.ones(3), rs.ConvolutionPlan(rs.DIRECT), ctx=ctx)
+
+
+@pytest.mark.parametrize("eta", [3.0, 20.0, 45.0, 80.0])
+def test_truncation_any_eta(rs, ctx, eta):
+    """K1 + K2 at shallow and deep cuts: cut indices, kept taps (bit-exact against the
+    reference synthesize_rir + truncate_rir) and the renders."""
+    from paper_1712_03439_b200 import scenes
+
+    b = scenes.config3(n_utt=6, seed=int(eta) + 100)
+    b.eta_db = eta
+    g = rs.render_batch(b, ctx=ctx)
+    ref = checker()
+    want = ref.render_batch(b, threads=os.cpu_count() or 8)
+    compare_subset(b, g.out, g.out_len, g.layout, g.gains, g.power, np.arange(b.n_utt), want)
+    I, J = np.diff(b.src_begin), np.diff(b.mic_begin)
+    for u in range(b.n_utt):
+        for i in range(I[u]):
+            for j in range(J[u]):
+                p = int(b.pair_begin[u] + i * J[u] + j)
+                full = ref.synthesize_rir(b.room_dims[u], float(b.reflection[u]), int(b.image_order[u]),
+                                          b.src_pos[b.src_begin[u] + i], b.mic_pos[b.mic_begin[u] + j],
+                                          max_taps=int(b.max_taps[u]))
+                kept = ref.truncate_rir(full, eta)[0]
+                got = rs.last_pair_rir(p, kept.size + 8, ctx=ctx)
+                assert got.size == kept.size and (got.view(np.uint64) == kept.view(np.uint64)).all(), (p, eta)
