@@ -111,10 +111,7 @@ struct IpShape {
   static constexpr int TWN = tw_off(PL::NP - 1);
   // smem-staged filter G (M + 1 bins) and pairing table W (M/2 + 1), float2, even counts
   static constexpr bool GS = PL::GS;
-  // unit order (IpUnits): 2 bins per pairing unit, NU = (M/32 - 1) 16 + 32 units (the two
-  // special groups keep idle lanes)
-  static constexpr int NU = (M / (2 * PL::radix(PL::NP - 1)) - 1) * PL::radix(PL::NP - 1) + 2 * PL::radix(PL::NP - 1);
-  static constexpr int GSN = 2 * NU, WSN = (NU + 1) & ~1;
+  static constexpr int GSN = (M + 2) & ~1, WSN = (M / 2 + 2) & ~1;  // unit order: 2 (M/2 + 1), M/2 + 1
   static constexpr int SLOTS = M + M / 16 + (M >> PL::LS0);
   static_assert(stride(0) == PL::T && stride(PL::NP - 1) == 1, "plan shape");
 };
@@ -322,7 +319,6 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
   for (int i = t; i < ovl; i += T) carry[i] = 0.f;
   if constexpr (GS) {  // unit order (IpUnits): gs[2u] = G[k], gs[2u + 1] = G[M - k], ws[u] = W^k
     using UN = IpUnits<PL, M>;
-    static_assert(UN::NU == SH::NU, "unit-order smem size");
     for (int i = t; i <= M; i += T) {  // coalesced reads, scattered smem writes
       int role;
       const int u = UN::unit_of(i, role);

@@ -452,7 +452,7 @@ __device__ __forceinline__ void stockham_pass(float2* s, int t, const float2* __
 // at or beyond `take` are the zero padding.  Writes smem, then syncs.
 template <int M, class Src, class Bar = CtaBar, bool NOCHK = false>
 __device__ __forceinline__ void first_pass(float2* s, int t, bool active, const Src* x, int take,
-                                           Bar bar = Bar(), bool pair_al = false) {
+                                           Bar bar = Bar()) {
   using PL = Plan<M>;
   constexpr int R = PL::radix(0), T = PL::T, NB = PL::E / R, STRIDE = M / R;
   if (active) {
@@ -468,12 +468,6 @@ __device__ __forceinline__ void first_pass(float2* s, int t, bool active, const 
         if constexpr (NOCHK) {  // zero padding already in the source buffer
           v[r].x = static_cast<float>(xb[off]);
           v[r].y = static_cast<float>(xb[off + 1]);
-        } else if (sizeof(Src) == 4 && pair_al) {
-          // x is an 8-byte aligned buffer readable past `take` (a TMA stage): one 64-bit
-          // load per complex instead of two stride-2 32-bit loads (half the wavefronts)
-          const float2 pv = *reinterpret_cast<const float2*>(xb + off);
-          v[r].x = off < lim ? pv.x : 0.f;
-          v[r].y = off + 1 < lim ? pv.y : 0.f;
         } else {
           v[r].x = off < lim ? static_cast<float>(xb[off]) : 0.f;
           v[r].y = off + 1 < lim ? static_cast<float>(xb[off + 1]) : 0.f;

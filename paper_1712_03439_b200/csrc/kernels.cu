@@ -685,9 +685,7 @@ ola_small_kernel(OlaArgs a) {
 #endif
     }
     bar();
-    // stage reads as 64-bit pairs when the block landed on an even float (d even)
-    first_pass<M, float, GroupBar<T>, false>(s, t, active, kDirect ? x + start : stage + d, take, bar,
-                                             !kDirect && (d & 1) == 0);
+    first_pass<M, float, GroupBar<T>, false>(s, t, active, kDirect ? x + start : stage + d, take, bar);
 #if !defined(RSG_NO_PREFETCH) && !defined(RSG_X_NOLOAD)
     if constexpr (kDirect) {
       if (active) prefetch_l2_block(b + 2);
@@ -719,26 +717,10 @@ ola_small_kernel(OlaArgs a) {
     // this block's power partials (FP32, <= 2E terms over four independent chains so the
     // FMAs do not serialise), folded into FP64 below in a fixed order
     float pb[4] = {0.f, 0.f, 0.f, 0.f};
-    // 64-bit stores where both halves go the same way and the destination is 8-byte aligned
-    // (output: the block starts on an even float; carry: L even), else two 32-bit stores
-    const bool y_al = (reinterpret_cast<uintptr_t>(yb) & 7) == 0, c_al = (L & 1) == 0;
     auto emit_fn = [&](int q, int r, int c, float2 v) {
       const int e0 = 2 * c;
       const float2 ci = *reinterpret_cast<const float2*>(cin + e0);
       const float2 acc = make_float2(ci.x + v.x, ci.y + v.y);
-      const bool fin0 = e0 < L || last, fin1 = e0 + 1 < L || last;
-      if (fin0 && fin1 && y_al && e0 >= lo && e0 + 1 < hi) {
-#ifndef RSG_X_NOSTORE
-        *reinterpret_cast<float2*>(yb + e0) = acc;
-#endif
-        pb[2 * (r & 1)] = fmaf(acc.x, acc.x, pb[2 * (r & 1)]);
-        pb[2 * (r & 1) + 1] = fmaf(acc.y, acc.y, pb[2 * (r & 1) + 1]);
-        return;
-      }
-      if (!fin0 && c_al) {  // e0 >= L and L even: both halves carried
-        *reinterpret_cast<float2*>(carry + (e0 - L)) = acc;
-        return;
-      }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int e = e0 + h;
