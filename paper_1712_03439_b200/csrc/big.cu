@@ -111,7 +111,7 @@ struct IpShape {
   static constexpr int TWN = tw_off(PL::NP - 1);
   // smem-staged filter G (M + 1 bins) and pairing table W (M/2 + 1), float2, even counts
   static constexpr bool GS = PL::GS;
-  static constexpr int GSN = (M + 2) & ~1, WSN = (M / 2 + 2) & ~1;  // unit order: 2 (M/2 + 1), M/2 + 1
+  static constexpr int GSN = (M + 2) & ~1, WSN = (M / 2 + 2) & ~1;
   static constexpr int SLOTS = M + M / 16 + (M >> PL::LS0);
   static_assert(stride(0) == PL::T && stride(PL::NP - 1) == 1, "plan shape");
 };
@@ -196,71 +196,29 @@ __device__ __forceinline__ void ip_inverse_rest(float2* s, const float2* tws, in
   }
 }
 
-// One pair (k, M - k) of the spectral step (spectral_multiply, fft.cuh) with its filter
-// bins gk = G[k], gm = G[M - k] and twiddle w = W^k; k = M - k pairs only with itself
-// (k = 0: partner slot 0 and G[M]; k = M/2).
-template <class PL, int M>
-__device__ __forceinline__ void ip_pair_v(float2* s, int k, float2 gk, float2 gm, float2 w) {
+// One pair (k, M - k) of the spectral step (spectral_multiply, fft.cuh); k = M - k
+// pairs only with itself (k = 0: partner slot 0 and G[M]; k = M/2).
+template <class PL, int M, bool GS>
+__device__ __forceinline__ void ip_pair(float2* s, int k, const float2* __restrict__ G,
+                                        const float2* __restrict__ W) {
+  auto ld = [](const float2* p) { return GS ? *p : ld_tw(p); };  // smem-staged or global
   const int km = (M - k) & (M - 1);
   const int pa = ipad<PL>(ip_pos<PL, M>(static_cast<unsigned>(k)));
   const int pb = ipad<PL>(ip_pos<PL, M>(static_cast<unsigned>(km)));
   const float2 a = s[pa];
   const float2 b = c_conj(s[pb]);
+  const float2 w = ld(W + k);
   const float2 S = c_add(a, b);
   const float2 D = c_rot<false>(c_sub(a, b));
   const float2 wD = c_mul(w, D);
   const float2 X2 = c_add(S, wD), X2m = c_sub(S, wD);
-  const float2 P = c_mul(X2, gk);
-  const float2 Q = c_mulc(X2m, gm);
+  const float2 P = c_mul(X2, ld(G + k));
+  const float2 Q = c_mulc(X2m, ld(G + (M - k)));
   const float2 U = c_add(P, Q);
   const float2 V = c_mulc(c_sub(P, Q), w);
   s[pa] = make_float2(U.x - V.y, U.y + V.x);
   if (k != 0 && km != k) s[pb] = make_float2(U.x + V.y, V.x - U.y);
 }
-template <class PL, int M>
-__device__ __forceinline__ void ip_pair(float2* s, int k, const float2* __restrict__ G,
-                                        const float2* __restrict__ W) {
-  ip_pair_v<PL, M>(s, k, ld_tw(G + k), ld_tw(G + (M - k)), ld_tw(W + k));
-}
-
-// Pairing units (GS sizes): pair (k, M - k) with k = c + WL l, l the last DIF digit (slot
-// stride 1): the 16 lanes of a half-warp take consecutive l, so k and M - k = (WL - c) +
-// WL (RL - 1 - l) both hit 16 consecutive slots — conflict-free 64-bit accesses
-// (consecutive k on consecutive lanes put the partners' digit-reversed slots on a 2-way
-// conflict).  Units: groups c = 1 .. WL/2 - 1 (RL lanes each), then c = WL/2 (pairs l and
-// RL-1-l) and c = 0 (pairs l and RL - l; k = 0 and M/2 pair with themselves), each on its
-// own half-warp.  The filter bins and twiddles are staged in smem in unit order.
-template <class PL, int M>
-struct IpUnits {
-  static constexpr int RL = PL::radix(PL::NP - 1), WL = M / RL;
-  static constexpr int NREG = (WL / 2 - 1) * RL, NU = NREG + 2 * RL;
-  static_assert(RL == 16 && PL::T % 16 == 0, "half-warp per pairing group");
-  // canonical k of unit u, or -1 (idle lane of a special group)
-  __device__ __forceinline__ static int k_of(int u) {
-    if (u < NREG) return 1 + u / RL + WL * (u % RL);
-    if (u < NREG + RL) {
-      const int l = u - NREG;
-      return l < RL / 2 ? WL / 2 + WL * l : -1;
-    }
-    const int l = u - NREG - RL;
-    return l <= RL / 2 ? WL * l : -1;
-  }
-  // unit of natural bin k in [0, M] and its role: 0 = the unit's k, 1 = its partner M - k
-  __device__ __forceinline__ static int unit_of(int k, int& role) {
-    if (k == M) { role = 1; return NREG + RL; }  // partner of k = 0
-    const int c = k % WL, l = k / WL;
-    if (c >= 1 && c < WL / 2) { role = 0; return (c - 1) * RL + l; }
-    if (c > WL / 2) { role = 1; return (WL - c - 1) * RL + (RL - 1 - l); }
-    if (c == WL / 2) {
-      if (l < RL / 2) { role = 0; return NREG + l; }
-      role = 1;
-      return NREG + (RL - 1 - l);
-    }
-    if (l <= RL / 2) { role = 0; return NREG + RL + l; }
-    role = 1;
-    return NREG + RL + (RL - l);
-  }
-};
 
 // One thread: pull [p, p + bytes) into L2 ahead of use (1-D bulk prefetch; the window
 // is widened to 16-byte alignment).
@@ -317,21 +275,9 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
     tws[i] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
   }
   for (int i = t; i < ovl; i += T) carry[i] = 0.f;
-  if constexpr (GS) {  // unit order (IpUnits): gs[2u] = G[k], gs[2u + 1] = G[M - k], ws[u] = W^k
-    using UN = IpUnits<PL, M>;
-    for (int i = t; i <= M; i += T) {  // coalesced reads, scattered smem writes
-      int role;
-      const int u = UN::unit_of(i, role);
-      const float2 g = ld_tw(Gg + i);
-      gs[2 * u + role] = g;
-      if (i == M / 2) gs[2 * u + 1] = g;  // self-paired: G[M - M/2] = G[M/2]
-    }
-    for (int i = t; i <= M / 2; i += T) {
-      int role;
-      const int u = UN::unit_of(i, role);
-      const float2 w = ld_tw(Wg + i);
-      ws[u] = role ? make_float2(-w.x, w.y) : w;  // W^(M - i) = -conj(W^i)
-    }
+  if constexpr (GS) {
+    for (int i = t; i <= M; i += T) gs[i] = ld_tw(Gg + i);
+    for (int i = t; i <= M / 2; i += T) ws[i] = ld_tw(Wg + i);
   }
   if (t == 0) {  // the pair's filter and the run's first block
     if (!GS) prefetch_l2(Gg, (M + 1) * sizeof(float2));
@@ -370,21 +316,10 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
     }
     __syncthreads();
     ip_forward_rest<PL, M, 1>(s, tws, t);
-    if constexpr (GS) {  // conflict-free unit order, filter and twiddles from smem (IpUnits)
-      using UN = IpUnits<PL, M>;
+    // pairs (k, M - k), k in [0, M/2]: consecutive k on consecutive threads
 #pragma unroll 2
-      for (int u = t; u < UN::NU; u += T) {
-        const int k = UN::k_of(u);
-        if (k >= 0) {
-          const float4 g = *reinterpret_cast<const float4*>(gs + 2 * u);
-          ip_pair_v<PL, M>(s, k, make_float2(g.x, g.y), make_float2(g.z, g.w), ws[u]);
-        }
-      }
-    } else {  // consecutive k on consecutive threads (coalesced filter reads through L1)
-#pragma unroll 2
-      for (int k = t; k < M / 2; k += T) ip_pair<PL, M>(s, k, G, W);
-      if (t == 0) ip_pair<PL, M>(s, M / 2, G, W);
-    }
+    for (int k = t; k < M / 2; k += T) ip_pair<PL, M, GS>(s, k, G, W);
+    if (t == 0) ip_pair<PL, M, GS>(s, M / 2, G, W);
     __syncthreads();
     ip_inverse_rest<PL, M, PL::NP - 1>(s, tws, t);
     // inverse pass 0: outputs c = t + S_0 r in registers
@@ -454,9 +389,8 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
     // power: per-lane FP64 sum over the segment, stored at its end (power.cuh)
     pw += static_cast<double>((pb[0] + pb[1]) + (pb[2] + pb[3]));
     if (closes_segment(b, it.b_end)) {
-      const long long part0 = __ldg(&a.plan[it.pair].part0);  // reloaded: nothing 64-bit lives across blocks
-      store_segment_power<T>(a.part + part0 + static_cast<long long>(b / kPowerSeg) * parts_per_block_of(T), pw, t,
-                             b >= it.b_own);
+      store_segment_power<T>(a.part + pl.part0 + static_cast<long long>(b / kPowerSeg) * parts_per_block_of(T), pw,
+                             t, b >= it.b_own);
       pw = 0.0;
     }
   }
