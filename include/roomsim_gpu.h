@@ -277,6 +277,16 @@ int rs_signal_plan_destroy(rs_signal_plan* plan);
 int rs_logmel_shape(int64_t n_samples, int64_t* n_frames, int64_t* n_stacked);
 int rs_logmel_device(rs_ctx* ctx, const float* wave_dev, int64_t n_chan, const int64_t* chan_off,
                      const int64_t* chan_len, float* feat_dev, const int64_t* feat_off);
+/* The render with the log-Mel front end fused into the mix (one kernel per chunk: each
+ * output tile is mixed into shared memory and the frames starting in it are featurized
+ * there): rs_render_batch_device's arguments plus feat_dev / feat_off (per output channel,
+ * utterance-major then mic; capacity from rs_logmel_shape(out_stride[u])).  out_dev may be
+ * NULL: the waveforms are then never written to HBM.  Features are bit-identical to
+ * rs_logmel_device on the rendered channels. */
+int rs_render_features_device(rs_ctx* ctx, const rs_scene_batch* batch, float* out_dev,
+                              const int64_t* out_off, const int64_t* out_stride, int64_t* out_len,
+                              rs_pair_layout* layout, double* gains, double* power, float* feat_dev,
+                              const int64_t* feat_off);
 
 #ifdef __cplusplus
 }

@@ -820,9 +820,11 @@ int finish_timing(rs_ctx* c) {
 // nothing), so results do not depend on the chunking.
 struct RenderIO {
   const float* d_signals;  // device signals (sig_off indexes them)
-  float* d_out;            // device output base (out_off indexes it)
+  float* d_out;            // device output base (out_off indexes it); null: features only
   const float* h_signals;  // host path: upload per chunk into d_signals
   float* h_out;            // host path: download per chunk from d_out
+  float* d_feat = nullptr;            // features mode: stacked log-Mel vectors (mix_logmel_kernel)
+  const int64_t* feat_off = nullptr;  // per output channel (utterance-major, then mic), host
 };
 
 struct Chunk {
@@ -843,6 +845,7 @@ struct Chunk {
   FilterPlan fp;
   int max_order = 0, slice = 1;
   int64_t rir_total = 0;
+  DevBuf d_chan_feat;
   DevBuf d_utt, d_pair, d_rg, d_items, d_rir, d_rirout, d_gain, d_power, d_flags, d_snr, d_chan_utt,
       d_chan_mic, d_chan_out, d_utt_len, d_utt_stride, d_utt_pair0, d_utt_I, d_utt_J;
   FilterBufs fb;
@@ -863,7 +866,7 @@ struct Chunk {
     return RS_OK;
   }
   void release() {
-    DevBuf* bufs[] = {&d_utt, &d_pair, &d_rg, &d_items, &d_rir, &d_rirout, &d_gain, &d_power, &d_flags,
+    DevBuf* bufs[] = {&d_chan_feat, &d_utt, &d_pair, &d_rg, &d_items, &d_rir, &d_rirout, &d_gain, &d_power, &d_flags,
                       &d_snr, &d_chan_utt, &d_chan_mic, &d_chan_out, &d_utt_len, &d_utt_stride,
                       &d_utt_pair0, &d_utt_I, &d_utt_J, &fb.plan, &fb.lists, &fb.olaitems, &fb.spec,
                       &fb.y, &fb.part, &fb.units, &fb.scratch, &fb.yblk, &fb.olaitems2};
@@ -1178,7 +1181,8 @@ int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO
                 staged_bytes(ch.fp.items2) + staged_bytes(ch.fp.units) +
                 staged_bytes(snr_lin) + staged_bytes(pair0) + staged_bytes(uI) + staged_bytes(uJ) +
                 staged_bytes(ch_utt) + staged_bytes(ch_mic) + staged_bytes(ch_out) + staged_bytes(ch.ulen) +
-                staged_bytes(ustride) + 3 * (((std::max<int64_t>(ch.P, 1) * 8) + 63) & ~size_t(63)) + 256;
+                staged_bytes(ustride) + 3 * (((std::max<int64_t>(ch.P, 1) * 8) + 63) & ~size_t(63)) + 256 +
+                (io.d_feat ? staged_bytes(ch_out) : 0);
   RS_TRY(ch.hB.reserve(need));
   ch.hB.reset();
   if (io.h_signals) RS_CUDA(cudaStreamWaitEvent(sB, ch.ev_sig, 0));
@@ -1207,7 +1211,17 @@ int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO
              ch.d_utt_len.as<int64_t>(), ch.d_utt_stride.as<int64_t>(), ch.d_utt_pair0.as<int64_t>(),
              ch.d_utt_I.as<int32_t>(), ch.d_utt_J.as<int32_t>(), ch.fb.plan.as<PairPlan>(), ch.fb.y.as<float>(),
              ch.d_gain.as<double>(), io.d_out, 4096};
-  RS_CUDA(launch_mix(ma, static_cast<int64_t>(ch_utt.size()), max_stride, sB));
+  if (io.d_feat) {  // features mode: mix + log-Mel in one kernel (features.cu)
+    std::vector<int64_t> ch_feat(ch_utt.size());
+    const int64_t c0 = b->mic_begin[ch.u0];  // global index of the chunk's first channel
+    for (size_t k = 0; k < ch_feat.size(); ++k) ch_feat[k] = io.feat_off[c0 + static_cast<int64_t>(k)];
+    RS_TRY(upload_on(ch.d_chan_feat, ch_feat, sB, &ch.hB));
+    const MixFeatArgs lf{io.d_feat, ch.d_chan_feat.as<int64_t>(), c->lm_window.as<float>(), c->lm_ptr.as<int32_t>(),
+                         c->lm_bin.as<int32_t>(), c->lm_w.as<float>(), c->tw[8], 1e-10f};
+    RS_CUDA(launch_mix_logmel(ma, lf, static_cast<int64_t>(ch_utt.size()), max_stride, sB));
+  } else {
+    RS_CUDA(launch_mix(ma, static_cast<int64_t>(ch_utt.size()), max_stride, sB));
+  }
   ++c->launches;
   if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_mix1, sB));
   ch.h_flags = ch.hB.alloc<int32_t>(ch.P);
@@ -1908,17 +1922,11 @@ int rs_last_pair_rir(rs_ctx* c, int64_t pair, double* out, size_t cap, size_t* l
   return RS_OK;
 }
 
-// ---- log-Mel front end (SURVEY.md §8f row 4; PAPER.md:452-460) ----------------------
-int rs_logmel_shape(int64_t n_samples, int64_t* n_frames, int64_t* n_stacked) {
-  const int64_t F = n_samples >= 512 ? 1 + (n_samples - 512) / 160 : 0;
-  if (n_frames) *n_frames = F;
-  if (n_stacked) *n_stacked = F >= 4 ? (F - 4) / 3 + 1 : 0;
-  return RS_OK;
-}
+}  // extern "C"
 
-int rs_logmel_device(rs_ctx* c, const float* wave_dev, int64_t n_chan, const int64_t* chan_off,
-                     const int64_t* chan_len, float* feat_dev, const int64_t* feat_off) {
-  RS_TRY(check_ctx(c));
+namespace {
+// Periodic Hann window and the HTK-mel filterbank (FP64 on the host, once per context).
+int logmel_tables(rs_ctx* c) {
   if (!c->lm_ready) {  // periodic Hann window and the HTK-mel filterbank, FP64 on the host
     const double pi = 3.14159265358979323846;
     std::vector<float> win(512);
@@ -1949,6 +1957,24 @@ int rs_logmel_device(rs_ctx* c, const float* wave_dev, int64_t n_chan, const int
     RS_TRY(upload(c, c->lm_w, w));
     c->lm_ready = true;
   }
+  return RS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+// ---- log-Mel front end (SURVEY.md §8f row 4; PAPER.md:452-460) ----------------------
+int rs_logmel_shape(int64_t n_samples, int64_t* n_frames, int64_t* n_stacked) {
+  const int64_t F = n_samples >= 512 ? 1 + (n_samples - 512) / 160 : 0;
+  if (n_frames) *n_frames = F;
+  if (n_stacked) *n_stacked = F >= 4 ? (F - 4) / 3 + 1 : 0;
+  return RS_OK;
+}
+
+int rs_logmel_device(rs_ctx* c, const float* wave_dev, int64_t n_chan, const int64_t* chan_off,
+                     const int64_t* chan_len, float* feat_dev, const int64_t* feat_off) {
+  RS_TRY(check_ctx(c));
+  RS_TRY(logmel_tables(c));
   std::vector<LogMelTile> tiles;
   for (int64_t ch = 0; ch < n_chan; ++ch) {
     int64_t F, S;
@@ -1975,6 +2001,19 @@ int rs_logmel_device(rs_ctx* c, const float* wave_dev, int64_t n_chan, const int
     c->ola_ms = ms;
   }
   return RS_OK;
+}
+
+int rs_render_features_device(rs_ctx* c, const rs_scene_batch* b, float* out_dev, const int64_t* out_off,
+                              const int64_t* out_stride, int64_t* out_len, rs_pair_layout* layout, double* gains,
+                              double* power, float* feat_dev, const int64_t* feat_off) {
+  RS_TRY(check_ctx(c));
+  if (!b) return fail(RS_ERR_CONFIG, "invalid scene batch");
+  if (!feat_dev || !feat_off) return fail(RS_ERR_CONFIG, "features mode needs a feature buffer and offsets");
+  RS_TRY(logmel_tables(c));
+  RenderIO io{b->signals, out_dev, nullptr, nullptr};
+  io.d_feat = feat_dev;
+  io.feat_off = feat_off;
+  return render_impl(c, b, io, out_off, out_stride, out_len, layout, gains, power);
 }
 
 }  // extern "C"

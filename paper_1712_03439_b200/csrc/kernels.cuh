@@ -192,6 +192,19 @@ struct LogMelArgs {
   float log_floor;
 };
 cudaError_t launch_logmel(const LogMelArgs& a, cudaStream_t s);
+// Mix + log-Mel fused (features.cu): MixArgs::out may be null (waveforms not written).
+struct MixFeatArgs {
+  float* feat;
+  const int64_t* feat_off;  // per output channel of the launch (device)
+  const float* window;
+  const int32_t* mel_ptr;
+  const int32_t* mel_bin;
+  const float* mel_w;
+  const float2* tw;         // Plan<256> tables
+  float log_floor;
+};
+cudaError_t launch_mix_logmel(const MixArgs& a, const MixFeatArgs& lf, int64_t n_chan, int64_t max_len,
+                              cudaStream_t s);
 
 // Large transforms (large.cu): four-step FFT through global scratch.
 struct LargeArgs {

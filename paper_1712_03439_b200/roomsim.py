@@ -101,7 +101,7 @@ ABI_SYMBOLS = [
     "rs_render_batch", "rs_render_batch_device", "rs_last_pair_signal", "rs_last_pair_rir",
     "rs_sampler_counts", "rs_sample_scenes", "rs_sampler_counts_device", "rs_sample_scenes_device",
     "rs_generate_signals_host", "rs_generate_signals", "rs_signal_plan_create", "rs_signal_plan_generate",
-    "rs_signal_plan_destroy", "rs_logmel_shape", "rs_logmel_device",
+    "rs_signal_plan_destroy", "rs_logmel_shape", "rs_logmel_device", "rs_render_features_device",
 ]
 
 
@@ -171,6 +171,7 @@ def load_library() -> C.CDLL:
         "rs_signal_plan_destroy": (C.c_int, [vp]),
         "rs_logmel_shape": (C.c_int, [i64, C.POINTER(i64), C.POINTER(i64)]),
         "rs_logmel_device": (C.c_int, [vp, vp, i64, vp, vp, vp, vp]),
+        "rs_render_features_device": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -598,3 +599,35 @@ def logmel_device(wave_ptr: int, chan_off, chan_len, feat_ptr: int, feat_off,
     cl = np.ascontiguousarray(chan_len, np.int64)
     fo = np.ascontiguousarray(feat_off, np.int64)
     _check(load_library().rs_logmel_device(ctx.h, wave_ptr, co.size, _ptr(co), _ptr(cl), feat_ptr, _ptr(fo)))
+
+
+def feature_layout(batch):
+    """(per-channel offsets, total floats) of a features buffer sized from the channel
+    capacities (out_stride), channels utterance-major then mic."""
+    J = np.diff(batch.mic_begin)
+    caps = np.repeat(batch.out_stride, J)
+    S = np.array([logmel_shape(int(n))[1] for n in caps], np.int64)
+    off = np.concatenate([[0], np.cumsum(S * 512)[:-1]]).astype(np.int64) if S.size else np.zeros(0, np.int64)
+    return off, int((S * 512).sum())
+
+
+def render_features(batch, *, device_signals_ptr: int, feat_ptr: int, feat_off, device_out_ptr: Optional[int] = None,
+                    ctx: Optional[Context] = None) -> RenderResult:
+    """The render with the log-Mel fused into the mix (rs_render_features_device); with
+    device_out_ptr None the waveforms are not written."""
+    ctx = ctx or default_context()
+    L = load_library()
+    b, keep = batch.as_struct(RsSceneBatch, signals_ptr=device_signals_ptr)
+    out_off = np.ascontiguousarray(batch.out_off, np.int64)
+    out_stride = np.ascontiguousarray(batch.out_stride, np.int64)
+    out_len = np.zeros(batch.n_utt, np.int64)
+    layout = np.zeros(batch.n_pairs, LAYOUT_DTYPE)
+    gains = np.zeros(batch.n_pairs)
+    power = np.zeros(batch.n_pairs)
+    fo = np.ascontiguousarray(feat_off, np.int64)
+    st = L.rs_render_features_device(ctx.h, C.byref(b), C.c_void_p(device_out_ptr), _ptr(out_off), _ptr(out_stride),
+                                     _ptr(out_len), _ptr(layout), _ptr(gains), _ptr(power), C.c_void_p(feat_ptr),
+                                     _ptr(fo))
+    del keep
+    _check(st)
+    return RenderResult(None, out_len, layout, gains, power)

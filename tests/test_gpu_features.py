@@ -65,3 +65,39 @@ def test_render_to_wav_roundtrip(rs, ctx, tmp_path):
         assert x.shape == (2, g.out_len[u])
         for j in range(2):
             assert np.array_equal(x[j].astype(np.float32), b.channel(g.out, u, j, g.out_len[u]))
+
+
+def test_fused_mix_logmel_matches_separate(rs, ctx):
+    """rs_render_features_device (log-Mel fused into the mix) gives the same waveforms and
+    bit-identical features as the render followed by rs_logmel_device — and without an
+    output buffer the waveforms are never written."""
+    import torch
+
+    from paper_1712_03439_b200 import scenes
+
+    b = scenes.config4(n_utt=6, seed=47)
+    sig = torch.from_numpy(b.signals).cuda()
+    out = torch.zeros(b.out_total, dtype=torch.float32, device="cuda")
+    r = rs.render_batch(b, ctx=ctx, device_signals_ptr=sig.data_ptr(), device_out_ptr=out.data_ptr())
+    foff, ftot = rs.feature_layout(b)
+    J = np.diff(b.mic_begin)
+    ch_off = np.concatenate([b.out_off[u] + np.arange(J[u]) * b.out_stride[u] for u in range(b.n_utt)])
+    ch_len = np.repeat(r.out_len, J)
+    sep = torch.full((max(ftot, 1),), float("nan"), dtype=torch.float32, device="cuda")
+    rs.logmel_device(out.data_ptr(), ch_off, ch_len, sep.data_ptr(), foff, ctx=ctx)
+    out2 = torch.full((b.out_total,), float("nan"), dtype=torch.float32, device="cuda")
+    fused = torch.full((max(ftot, 1),), float("nan"), dtype=torch.float32, device="cuda")
+    r2 = rs.render_features(b, device_signals_ptr=sig.data_ptr(), feat_ptr=fused.data_ptr(), feat_off=foff,
+                            device_out_ptr=out2.data_ptr(), ctx=ctx)
+    fused_only = torch.full((max(ftot, 1),), float("nan"), dtype=torch.float32, device="cuda")
+    rs.render_features(b, device_signals_ptr=sig.data_ptr(), feat_ptr=fused_only.data_ptr(), feat_off=foff, ctx=ctx)
+    torch.cuda.synchronize()
+    assert (r2.out_len == r.out_len).all() and (r2.gains == r.gains).all()
+    assert (out2.cpu().numpy().view(np.uint32) == out.cpu().numpy().view(np.uint32)).all()
+    S = np.array([rs.logmel_shape(int(n))[1] for n in ch_len], np.int64)
+    a, c, d = sep.cpu().numpy(), fused.cpu().numpy(), fused_only.cpu().numpy()
+    for o, s_ in zip(foff, S):
+        seg = slice(o, o + s_ * 512)
+        assert np.isfinite(a[seg]).all()
+        assert (a[seg].view(np.uint32) == c[seg].view(np.uint32)).all()
+        assert (a[seg].view(np.uint32) == d[seg].view(np.uint32)).all()
