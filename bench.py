@@ -398,12 +398,31 @@ def ours(args, rank, world, local_rank):
             roomsim.logmel_device(out.data_ptr(), ch_off, ch_len, feat.data_ptr(), f_off, ctx=ctx)
             lm_ms += ctx.last_timing()["ola_ms"]
         frames = int(sum(3 * (s_ - 1) + 4 for s_ in S if s_ > 0))
+        # the render with the log-Mel fused into the mix, waveforms never written (features only)
+        foff, ftot = roomsim.feature_layout(batch)
+        fused = torch.empty(max(ftot, 1), dtype=torch.float32, device=dev)
+        fstep = lambda: roomsim.render_features(batch, device_signals_ptr=signals.data_ptr(),  # noqa: E731
+                                                feat_ptr=fused.data_ptr(), feat_off=foff, ctx=ctx)
+        fstep()
+        barrier()
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(args.steps):
+            fstep()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms_f = max_over_ranks([e0.elapsed_time(e1) / args.steps])[0]
         logmel = {"ms_per_step": lm_ms / args.steps, "channels": int(ch_len.size), "frames": frames,
                   "stacked_vectors": int(S.sum()),
                   "frames_per_s": frames / (lm_ms / args.steps / 1e3) if lm_ms > 0 else None,
                   "what": "128 log-Mel, 32 ms Hann / 10 ms hop, 125-7500 Hz, 4-frame stacks every 3rd "
-                          "(PAPER.md:452-460) of every rendered channel; device-timed kernel"}
-        del feat
+                          "(PAPER.md:452-460) of every rendered channel; device-timed kernel",
+                  "fused_render_features": {
+                      "ms_per_step": ms_f, "value": total_audio / (ms_f / 1e3), "unit": UNIT,
+                      "vs_render_plus_logmel_ms": ms_max + lm_ms / args.steps,
+                      "what": "rs_render_features_device: the whole render with the log-Mel computed inside the "
+                              "mix kernel from shared memory; waveforms not written (features only)"}}
+        del feat, fused
 
     # ---- roofline of the OLA filter kernels (K4) -------------------------------------
     props = torch.cuda.get_device_properties(dev)
