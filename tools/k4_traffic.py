@@ -2,7 +2,7 @@
 (gpu__time_duration.sum, dram__bytes_read.sum, dram__bytes_write.sum), as JSON for
 bench.py's roofline `traffic` field.
 
-usage: python tools/k4_traffic.py launches.csv renders source-note > profiles/rNN_k4_traffic.json
+usage: python tools/k4_traffic.py launches.csv renders source-note [utterances] > profiles/k4_traffic.json
 """
 import csv
 import json
@@ -15,7 +15,7 @@ from launch_summary import SCALE
 K4 = re.compile(r"ola_small_kernel|ola_ip_kernel|ola_w_kernel|ola2_kernel|ola_kernel|large_(rows|cols|ola)")
 
 
-def main(path, renders, source):
+def main(path, renders, source, utts=4096):
     with open(path) as f:
         lines = [l for l in f if l.startswith('"')]
     per = defaultdict(dict)
@@ -25,6 +25,7 @@ def main(path, renders, source):
     ms = sum(m.get("gpu__time_duration.sum", 0.0) for m in per.values())
     by = sum(m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0) for m in per.values())
     print(json.dumps({
+        "workload": "config4", "utterances_per_rank": utts,
         "kernel": "K4 (ola_small_kernel / ola_ip_kernel / ola2_kernel / four-step stages), all launches of one config-4 render",
         "dram_bytes_per_render": by / renders,
         "device_ms_per_render": ms / renders,
@@ -36,4 +37,4 @@ def main(path, renders, source):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]), sys.argv[3])
+    main(sys.argv[1], int(sys.argv[2]), sys.argv[3], int(sys.argv[4]) if len(sys.argv) > 4 else 4096)
