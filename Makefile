@@ -38,10 +38,10 @@ $(OUT)/features.o: $(SRC)/features.cu $(SRC)/kernels.cuh $(SRC)/power.cuh $(SRC)
 
 $(OUT)/api.o: $(SRC)/api.cu $(SRC)/kernels.cuh $(SRC)/power.cuh include/roomsim_gpu.h
 	@mkdir -p $(OUT)
-	$(NVCC) $(NVFLAGS) -c $< -o $@
+	$(NVCC) $(NVFLAGS) -Xcompiler -fopenmp -c $< -o $@
 
 $(OUT)/libroomsim_gpu.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -lgomp
 
 oracle:
 	$(MAKE) -s -C oracle

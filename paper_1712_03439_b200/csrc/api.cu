@@ -217,6 +217,24 @@ int choose_plan_impl(double I, double J, size_t nx, size_t nh, int* s, size_t* n
   return RS_OK;
 }
 
+// Host loops over utterances / pairs on a few threads (OpenMP; the planner's glibc pow and
+// exact lattice maxima would otherwise keep the first chunk's kernels waiting).  Every
+// iteration writes only its own slots, so the result does not depend on the thread count.
+template <class F>
+void host_parallel_for(int64_t n, F&& f) {
+  static const int nthr = [] {
+    const char* e = std::getenv("RSG_HOST_THREADS");
+    int v = e ? std::atoi(e) : 8;
+    return std::max(1, v);
+  }();
+  if (n < 64 || nthr == 1) {
+    for (int64_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+#pragma omp parallel for num_threads(nthr) schedule(static, 16)
+  for (int64_t i = 0; i < n; ++i) f(i);
+}
+
 // Exact max over the image lattice of ceil(|image - mic| * fs/c0): the squared
 // distance is a sum of per-axis terms and every rounded operation on the way
 // (fl(x*x), fl(a+b), sqrt, fl(d*spm), ceil) is monotone, so the maximum is the
@@ -927,30 +945,54 @@ int state_init(rs_ctx* c);
 
 // Host metadata of chunk k (validation with the reference's messages).
 int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
-  ch.utt.clear(); ch.rg.clear(); ch.pair.clear(); ch.items.clear();
-  ch.place_err.clear(); ch.place_msg.clear(); ch.empty_sig.clear(); ch.utt_err.clear(); ch.utt_msg.clear();
+  ch.items.clear();
   ch.max_order = 0; ch.slice = 1; ch.rir_total = 0;
-  for (int64_t u = ch.u0; u < ch.u1; ++u) {
+  const int64_t U = ch.u1 - ch.u0;
+  // serial: per-utterance pair and r^g-table extents (prefix sums)
+  std::vector<int64_t> pair_start(U + 1, 0), rg_start(U + 1, 0);
+  for (int64_t lu = 0; lu < U; ++lu) {
+    const int64_t u = ch.u0 + lu;
+    const int64_t I = b->src_begin[u + 1] - b->src_begin[u], J = b->mic_begin[u + 1] - b->mic_begin[u];
+    const int K = b->image_order[u];
+    const bool bad = room_validate(b->room_dims + 3 * u, b->reflection[u], b->sample_rate[u], b->speed_of_sound[u], K);
+    pair_start[lu + 1] = pair_start[lu] + std::max<int64_t>(I, 0) * std::max<int64_t>(J, 0);
+    rg_start[lu + 1] = rg_start[lu] + 3 * (bad ? 0 : K) + 1;
+    if (!bad) ch.max_order = std::max(ch.max_order, K);
+  }
+  const int64_t P = pair_start[U];
+  ch.utt.assign(U, UttMeta{});
+  ch.rg.assign(rg_start[U], 0.0);
+  ch.pair.assign(P, PairMeta{});
+  ch.place_err.assign(P, RS_OK);
+  ch.place_msg.assign(P, std::string());
+  ch.empty_sig.assign(P, 0);
+  ch.utt_err.assign(U, RS_OK);
+  ch.utt_msg.assign(U, std::string());
+  // parallel over utterances: tables, pair metadata, exact RIR lengths, recorded errors
+  // (glibc pow for r^g and the exact lattice maxima dominate the host's share of a render)
+  host_parallel_for(U, [&](int64_t lu) {
+    const int64_t u = ch.u0 + lu;
     const double* L = b->room_dims + 3 * u;
     const int64_t s0 = b->src_begin[u], I = b->src_begin[u + 1] - s0;
     const int64_t m0 = b->mic_begin[u], J = b->mic_begin[u + 1] - m0;
     // Errors are recorded, not returned: plan_chunk reports the first one in the order the
     // reference meets them (utterance, then pair; per pair: RoomConfig::validate and the
     // placements inside synthesize_rir, geometry, truncation, then the convolution).
-    ch.utt_err.push_back(I < 1 || J < 1 ? RS_ERR_CONFIG : RS_OK);
-    ch.utt_msg.push_back(I < 1 || J < 1 ? "scene needs a target and a microphone" : "");
+    if (I < 1 || J < 1) {
+      ch.utt_err[lu] = RS_ERR_CONFIG;
+      ch.utt_msg[lu] = "scene needs a target and a microphone";
+    }
     int K = b->image_order[u];
     const int cfg_err = room_validate(L, b->reflection[u], b->sample_rate[u], b->speed_of_sound[u], K);
-    const std::string cfg_msg = cfg_err ? g_err : std::string();
+    const std::string cfg_msg = cfg_err ? g_err : std::string();  // g_err is thread-local
     if (cfg_err) K = 0;  // no lattice for an invalid room: its pairs carry the config error
-    UttMeta um{};
+    UttMeta& um = ch.utt[lu];
     for (int a = 0; a < 3; ++a) um.dims[a] = L[a];
     um.spm = b->sample_rate[u] / b->speed_of_sound[u];  // room_model.hpp:150
     um.order = K;
-    um.rg_off = static_cast<int32_t>(ch.rg.size());
+    um.rg_off = static_cast<int32_t>(rg_start[lu]);
     um.max_taps = b->max_taps ? b->max_taps[u] : 0;
-    for (int g = 0; g <= 3 * K; ++g) ch.rg.push_back(std::pow(b->reflection[u], static_cast<double>(g)));
-    ch.max_order = std::max(ch.max_order, K);
+    for (int g = 0; g <= 3 * K; ++g) ch.rg[rg_start[lu] + g] = std::pow(b->reflection[u], static_cast<double>(g));
     int64_t cap = um.max_taps;
     if (cap <= 0) {  // bound on the farthest lattice image
       double d2 = 0;
@@ -960,18 +1002,17 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
       }
       cap = static_cast<int64_t>(std::ceil(std::sqrt(d2) * um.spm)) + 2;
     }
-    const int32_t lu = static_cast<int32_t>(ch.utt.size());
-    ch.utt.push_back(um);
+    int64_t p = pair_start[lu];
     for (int64_t i = 0; i < I; ++i)
-      for (int64_t j = 0; j < J; ++j) {
-        PairMeta pm{};
+      for (int64_t j = 0; j < J; ++j, ++p) {
+        PairMeta& pm = ch.pair[p];
         const double* sp = b->src_pos + 3 * (s0 + i);
         const double* mp = b->mic_pos + 3 * (m0 + j);
         for (int a = 0; a < 3; ++a) {
           pm.src[a] = sp[a];
           pm.mic[a] = mp[a];
         }
-        pm.utt = lu;
+        pm.utt = static_cast<int32_t>(lu);
         pm.src_idx = static_cast<int32_t>(s0 + i);
         pm.mic_local = static_cast<int32_t>(j);
         pm.src_local = static_cast<int32_t>(i);
@@ -983,26 +1024,23 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
           const int64_t md = static_cast<int64_t>(lattice_max_delay(L, sp, mp, K, um.spm)) + 1;
           pcap = um.max_taps > 0 ? std::min<int64_t>(md, um.max_taps) : md;
         }
-        pm.rir_off = ch.rir_total;
         pm.rir_cap = pcap;
-        ch.rir_total += pcap;
-        int err = RS_OK;
-        std::string msg;
         if (cfg_err) {  // room_model.hpp:143 (validate first)
-          err = cfg_err;
-          msg = cfg_msg;
+          ch.place_err[p] = cfg_err;
+          ch.place_msg[p] = cfg_msg;
         } else if (!strictly_inside(L, sp)) {  // room_model.hpp:144-145
-          err = RS_ERR_PLACEMENT;
-          msg = "source must lie strictly inside the room";
+          ch.place_err[p] = RS_ERR_PLACEMENT;
+          ch.place_msg[p] = "source must lie strictly inside the room";
         } else if (!strictly_inside(L, mp)) {  // :146-147
-          err = RS_ERR_PLACEMENT;
-          msg = "microphone must lie strictly inside the room";
+          ch.place_err[p] = RS_ERR_PLACEMENT;
+          ch.place_msg[p] = "microphone must lie strictly inside the room";
         }
-        ch.place_err.push_back(err);
-        ch.place_msg.push_back(msg);
-        ch.empty_sig.push_back(pm.nx <= 0 ? 1 : 0);
-        ch.pair.push_back(pm);
+        ch.empty_sig[p] = pm.nx <= 0 ? 1 : 0;
       }
+  });
+  for (int64_t p = 0; p < P; ++p) {  // RIR regions (serial prefix)
+    ch.pair[p].rir_off = ch.rir_total;
+    ch.rir_total += ch.pair[p].rir_cap;
   }
   ch.P = static_cast<int64_t>(ch.pair.size());
   // K1 launch classes: (threads, slice size).  Small lattices (K <= 12) use
