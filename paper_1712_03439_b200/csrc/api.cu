@@ -221,17 +221,17 @@ int choose_plan_impl(double I, double J, size_t nx, size_t nh, int* s, size_t* n
 // exact lattice maxima would otherwise keep the first chunk's kernels waiting).  Every
 // iteration writes only its own slots, so the result does not depend on the thread count.
 template <class F>
-void host_parallel_for(int64_t n, F&& f) {
+void host_parallel_for(int64_t n, F&& f, int64_t min_n = 64) {
   static const int nthr = [] {
     const char* e = std::getenv("RSG_HOST_THREADS");
     int v = e ? std::atoi(e) : 8;
     return std::max(1, v);
   }();
-  if (n < 64 || nthr == 1) {
+  if (n < min_n || nthr == 1) {
     for (int64_t i = 0; i < n; ++i) f(i);
     return;
   }
-#pragma omp parallel for num_threads(nthr) schedule(static, 16)
+#pragma omp parallel for num_threads(nthr) schedule(dynamic, 1)
   for (int64_t i = 0; i < n; ++i) f(i);
 }
 
@@ -505,6 +505,12 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
     work[p] = pair_flops(plans[p]);
     fp.flops += work[p];
   }
+  // largest pairs first (LPT) within every one-CTA bucket so each launch's tail is short; the
+  // order is scheduling only (a pair's bytes do not depend on it), sorted on host threads
+  host_parallel_for(NB, [&](int64_t key) {
+    if (key % kVarCount != kVarLarge && bucket[key].size() > 1)
+      std::stable_sort(bucket[key].begin(), bucket[key].end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
+  }, 1);
   std::vector<int> order(NB);
   std::iota(order.begin(), order.end(), 0);
   std::vector<double> bucket_work(NB, 0.0);
@@ -567,8 +573,6 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
       fp.lists.insert(fp.lists.end(), v.begin(), v.end());
       continue;
     }
-    // largest pairs first (LPT) so the tail of the launch is short
-    std::stable_sort(v.begin(), v.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
     if (var == kVarOla2) {  // two-stream K4: an item is a pair of runs of one pair
       // Runs of a fixed length per pair (16 overlap blocks' worth, whole power segments): the
       // two runs sharing a complex transform round into each other, so which blocks pair
