@@ -721,6 +721,28 @@ ola_small_kernel(OlaArgs a) {
       const int e0 = 2 * c;
       const float2 ci = *reinterpret_cast<const float2*>(cin + e0);
       const float2 acc = make_float2(ci.x + v.x, ci.y + v.y);
+#ifndef RSG_EMIT_NOFAST
+      if constexpr (T >= 32 && PL::E == 8) {
+        // A warp's elements of one r are 64 consecutive samples [w0, w0 + 64): classify them
+        // once, warp-uniformly (the per-element tests below were a quarter of the kernel's
+        // instructions: branches, predicates, divergence bookkeeping)
+        const int w0 = 2 * (c & ~31);
+        if (w0 >= lo && w0 + 64 <= hi && (w0 + 64 <= L || last)) {  // all final and owned
+#ifndef RSG_X_NOSTORE
+          yb[e0] = acc.x;
+          yb[e0 + 1] = acc.y;
+#endif
+          pb[2 * (r & 1)] = fmaf(acc.x, acc.x, pb[2 * (r & 1)]);
+          pb[2 * (r & 1) + 1] = fmaf(acc.y, acc.y, pb[2 * (r & 1) + 1]);
+          return;
+        }
+        if (w0 >= L && !last) {  // all carried into the next block
+          carry[e0 - L] = acc.x;
+          carry[e0 + 1 - L] = acc.y;
+          return;
+        }
+      }
+#endif
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int e = e0 + h;
