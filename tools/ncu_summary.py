@@ -1,6 +1,7 @@
 """Key metrics of an `ncu --set full` report, one block per kernel launch.
 
-usage: python tools/ncu_summary.py report.ncu-rep
+usage: python tools/ncu_summary.py report.ncu-rep|report_raw.csv [...]
+(a `_raw.csv` is `ncu -i report.ncu-rep --page raw --csv`, exported on the GPU box)
 """
 import csv
 import io
@@ -27,7 +28,11 @@ KEYS = [
 
 
 def main(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):
+        with open(path) as f:
+            raw = f.read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     ix = {h: i for i, h in enumerate(hdr)}
@@ -44,4 +49,5 @@ def main(path):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    for p in sys.argv[1:]:
+        main(p)

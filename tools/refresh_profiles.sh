@@ -25,8 +25,15 @@ for k in "ola_small_kernel<.int.512>" "ola_ip_kernel<.int.1024>" "ola_ip_kernel<
   timeout 600 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:$k" \
     --launch-skip 2 -c 1 -o $O/${R}_full_$n python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > $O/ncu_$n.log 2>&1
   echo "$n rc=$?"
+  # the copy-back limit is 64 MiB: raw metrics as CSV for every capture, the report itself
+  # only for the two largest K4 kernels
+  ncu -i $O/${R}_full_$n.ncu-rep --page raw --csv > $O/${R}_full_${n}_raw.csv 2>/dev/null
+  case $n in ola_small_kernelint512|ola_ip_kernelint1024) ;; *) rm -f $O/${R}_full_$n.ncu-rep ;; esac
 done
 timeout 600 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:ola_ip_kernel<.int.16384>" \
   --launch-skip 2 -c 1 -o $O/${R}_full_ip16384_config5 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --config config5 > $O/ncu_ip16384.log 2>&1
 echo "ip16384 rc=$?"
+ncu -i $O/${R}_full_ip16384_config5.ncu-rep --page raw --csv > $O/${R}_full_ip16384_config5_raw.csv 2>/dev/null
+rm -f $O/${R}_full_ip16384_config5.ncu-rep
+du -sh $O
 ls -la $O
