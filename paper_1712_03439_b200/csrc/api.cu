@@ -334,29 +334,15 @@ struct rs_ctx {
 
 namespace {
 
-// The library's own streams run at the device's greatest priority: work the caller queues on
-// default-priority streams (e.g. the next epoch's signal generation) only fills the SM slots
-// a render leaves idle (RSG_STREAM_PRIORITY=0: default priority).
-int hot_priority() {
-  static const int prio = [] {
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    const char* e = std::getenv("RSG_STREAM_PRIORITY");
-    return (e && e[0] == '0') ? lo : hi;
-  }();
-  return prio;
-}
-cudaError_t hot_stream(cudaStream_t* s) { return cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, hot_priority()); }
-
 int ctx_init(rs_ctx* c) {
   RS_CUDA(cudaSetDevice(c->device));
-  RS_CUDA(hot_stream(&c->own));
+  RS_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
   c->stream = c->own;
   RS_CUDA(cudaEventCreate(&c->ev0));
   RS_CUDA(cudaEventCreate(&c->ev1));
   for (auto& e : c->st) RS_CUDA(cudaEventCreate(&e));
   for (int i = 0; i < rs_ctx::kSide; ++i) {
-    RS_CUDA(hot_stream(&c->side[i]));
+    RS_CUDA(cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking));
     RS_CUDA(cudaEventCreateWithFlags(&c->side_join[i], cudaEventDisableTiming));
   }
   RS_CUDA(cudaEventCreateWithFlags(&c->side_fork, cudaEventDisableTiming));
@@ -1313,10 +1299,10 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
 int state_init(rs_ctx* c) {
   if (c->rs) return RS_OK;
   c->rs = new rs_render_state();
-  RS_CUDA(hot_stream(&c->rs->sA));
-  RS_CUDA(hot_stream(&c->rs->sB));
-  RS_CUDA(hot_stream(&c->rs->sH));
-  RS_CUDA(hot_stream(&c->rs->sD));
+  RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sA, cudaStreamNonBlocking));
+  RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sB, cudaStreamNonBlocking));
+  RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sH, cudaStreamNonBlocking));
+  RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sD, cudaStreamNonBlocking));
   cudaEvent_t* evs[] = {&c->rs->ev_start, &c->rs->ev_endA, &c->rs->ev_endB, &c->rs->ev_endH, &c->rs->ev_endD};
   for (auto* e : evs) RS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   return RS_OK;

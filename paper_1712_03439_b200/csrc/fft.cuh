@@ -468,10 +468,6 @@ __device__ __forceinline__ void first_pass(float2* s, int t, bool active, const 
         if constexpr (NOCHK) {  // zero padding already in the source buffer
           v[r].x = static_cast<float>(xb[off]);
           v[r].y = static_cast<float>(xb[off + 1]);
-        } else if (T >= 32 && 2 * (j & ~31) + off + 64 <= take) {
-          // the warp's 64 samples of this r are all inside the block (warp-uniform test)
-          v[r].x = static_cast<float>(xb[off]);
-          v[r].y = static_cast<float>(xb[off + 1]);
         } else {
           v[r].x = off < lim ? static_cast<float>(xb[off]) : 0.f;
           v[r].y = off + 1 < lim ? static_cast<float>(xb[off + 1]) : 0.f;
