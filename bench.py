@@ -376,50 +376,11 @@ def ours(args, rank, world, local_rank):
         torch.cuda.synchronize(dev)
         gen_ms = g0.elapsed_time(g1)
         ms_ep = max_over_ranks([e0.elapsed_time(e1) / args.steps])[0]
-        # pipelined: epoch k+1's signals generated into a second buffer on a low-priority
-        # stream while epoch k renders (the generator fills the render's idle SM slots)
-        sig_b = torch.empty_like(signals)
-        bufs = (signals, sig_b)
-        gstream = torch.cuda.Stream(dev, priority=0)
-        done = [torch.cuda.Event(), torch.cuda.Event()]   # render of a buffer finished
-        ready = [torch.cuda.Event(), torch.cuda.Event()]  # generator of a buffer finished
-
-        def gen_into(i, ep):
-            gstream.wait_event(done[i])
-            gen_plan.generate(bufs[i].data_ptr(), epoch=ep, stream=gstream.cuda_stream)
-            ready[i].record(gstream)
-
-        def render_from(i):
-            stream.wait_event(ready[i])
-            r = roomsim.render_batch(batch, ctx=ctx, device_signals_ptr=bufs[i].data_ptr(),
-                                     device_out_ptr=out.data_ptr())
-            done[i].record(stream)
-            return r
-
-        for i in range(2):
-            done[i].record(stream)
-        gen_into(0, 0)
-        gen_into(1, 1)
-        render_from(0)
-        torch.cuda.synchronize(dev)
-        barrier()
-        e0.record(stream)
-        for k in range(args.steps):
-            i = (k + 1) % 2
-            gen_into(1 - i, k + 2)  # next epoch into the buffer the previous render read
-            render_from(i)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        ms_pipe = max_over_ranks([e0.elapsed_time(e1) / args.steps])[0]
-        del sig_b, bufs
-        epoch_loop = {"value": total_audio / (ms_pipe / 1e3), "unit": UNIT, "ms_per_step": ms_pipe,
+        epoch_loop = {"value": total_audio / (ms_ep / 1e3), "unit": UNIT, "ms_per_step": ms_ep,
                       "signal_gen_ms": gen_ms,
-                      "serial": {"value": total_audio / (ms_ep / 1e3), "ms_per_step": ms_ep},
-                      "what": "per step: N(0, 0.1) source signals generated in HBM by rs_signal_plan_generate "
-                              "(Philox, bit-exact with the host fixture generator; the next epoch's into a second "
-                              "buffer on a low-priority stream while this epoch renders) + rs_render_batch_device; "
-                              "scene metadata from the host sampler; no host<->device staging of samples; "
-                              "'serial' = generate then render on one stream"}
+                      "what": "per step: N(0, 0.1) source signals generated in HBM by rs_generate_signals "
+                              "(Philox, bit-exact with the host fixture generator) + rs_render_batch_device; "
+                              "scene metadata from the host sampler; no host<->device staging of samples"}
 
     # ---- log-Mel front end on the rendered channels -----------------
     logmel = None
