@@ -361,14 +361,135 @@ RSH void box_muller(float sd, uint32_t a, uint32_t b, float* z0, float* z1) {
   *z1 = RF_MUL(sd, RF_MUL(r, sn));
 }
 
+#ifdef __CUDA_ARCH__
+// ---- device: the two Box-Muller pairs of a quad in the two halves of packed FP32x2 ops ----
+// Every half executes box_muller's exact IEEE operation sequence (round to nearest), so the
+// samples equal the host's bit for bit.  Products go through fma.rn.f32x2(a, b, -0): that
+// is round(a*b) exactly (also for signed zeros), and unlike mul.rn.f32x2 ptxas cannot fuse
+// it with the following add into an FFMA2 (which would skip a rounding).
+struct F2 {
+  float x, y;
+};
+__device__ __forceinline__ unsigned long long f2b(F2 a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ F2 b2f(unsigned long long v) {
+  F2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+// The -0 addend must be a run-time value: with an immediate, ptxas rewrites the fma into a
+// multiply and then contracts multiply + add into one FFMA2 after all.
+__device__ __forceinline__ F2 pmul(F2 a, F2 b, unsigned long long nz) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2b(a)), "l"(f2b(b)), "l"(nz));
+  return b2f(d);
+}
+__device__ __forceinline__ F2 padd(F2 a, F2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2b(a)), "l"(f2b(b)));
+  return b2f(d);
+}
+__device__ __forceinline__ F2 psub(F2 a, F2 b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2b(a)), "l"(f2b(b)));
+  return b2f(d);
+}
+__device__ __forceinline__ F2 bc(float v) { return F2{v, v}; }
+
+// plogf_ on both halves (x in (0, 1])
+__device__ __forceinline__ F2 plogf2(F2 x, unsigned long long nz) {
+  float mv[2];
+  float ev[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t b = __float_as_uint(h ? x.y : x.x);
+    int e = static_cast<int>((b >> 23) & 0xff) - 127;
+    b = (b & 0x007FFFFFu) | 0x3F800000u;
+    float m = __uint_as_float(b);
+    if (m > 1.41421356f) {
+      m = __fmul_rn(m, 0.5f);
+      e += 1;
+    }
+    mv[h] = m;
+    ev[h] = static_cast<float>(e);
+  }
+  const F2 m{mv[0], mv[1]};
+  const F2 num = psub(m, bc(1.0f)), den = padd(m, bc(1.0f));
+  const F2 sv{__fdiv_rn(num.x, den.x), __fdiv_rn(num.y, den.y)};
+  const F2 s2 = pmul(sv, sv, nz);
+  F2 p = bc(1.0f / 11.0f);
+  p = padd(bc(1.0f / 9.0f), pmul(s2, p, nz));
+  p = padd(bc(1.0f / 7.0f), pmul(s2, p, nz));
+  p = padd(bc(1.0f / 5.0f), pmul(s2, p, nz));
+  p = padd(bc(1.0f / 3.0f), pmul(s2, p, nz));
+  p = padd(bc(1.0f), pmul(s2, p, nz));
+  return padd(pmul(F2{ev[0], ev[1]}, bc(0.693147182f), nz), pmul(pmul(bc(2.0f), sv, nz), p, nz));
+}
+
+// psincosf_ on both halves (x in [0, 2 pi))
+__device__ __forceinline__ void psincosf2(F2 x, F2* sn, F2* cs, unsigned long long nz) {
+  const F2 kk = padd(pmul(x, bc(0.636619772f), nz), bc(0.5f));
+  const F2 k{floorf(kk.x), floorf(kk.y)};
+  const F2 r = psub(psub(x, pmul(k, bc(1.5703125f), nz)), pmul(k, bc(4.83826794e-4f), nz));
+  const F2 r2 = pmul(r, r, nz);
+  F2 s = bc(1.0f / 362880.0f);
+  s = padd(bc(-1.0f / 5040.0f), pmul(r2, s, nz));
+  s = padd(bc(1.0f / 120.0f), pmul(r2, s, nz));
+  s = padd(bc(-1.0f / 6.0f), pmul(r2, s, nz));
+  s = padd(r, pmul(pmul(r, r2, nz), s, nz));
+  F2 c = bc(1.0f / 3628800.0f);
+  c = padd(bc(-1.0f / 40320.0f), pmul(r2, c, nz));
+  c = padd(bc(1.0f / 720.0f), pmul(r2, c, nz));
+  c = padd(bc(-1.0f / 24.0f), pmul(r2, c, nz));
+  c = padd(bc(0.5f), pmul(r2, c, nz));
+  c = psub(bc(1.0f), pmul(r2, c, nz));
+  float so[2], co[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float sh = h ? s.y : s.x, ch = h ? c.y : c.x;
+    const int q = static_cast<int>(h ? k.y : k.x) & 3;
+    so[h] = q == 0 ? sh : (q == 1 ? ch : (q == 2 ? -sh : -ch));
+    co[h] = q == 0 ? ch : (q == 1 ? -sh : (q == 2 ? -ch : sh));
+  }
+  *sn = F2{so[0], so[1]};
+  *cs = F2{co[0], co[1]};
+}
+
+// box_muller(sd, a0, b0) -> z[0], z[1] and box_muller(sd, a1, b1) -> z[2], z[3]
+__device__ __forceinline__ void box_muller2(float sd, uint32_t a0, uint32_t b0, uint32_t a1, uint32_t b1, float* z) {
+  // -0 in both halves, from the run-time standard deviation (ptxas cannot fold it)
+  const float nzf = __fmul_rn(-0.0f, fabsf(sd));
+  const unsigned long long nz = f2b(F2{nzf, nzf});
+  const F2 u0{static_cast<float>(a0 >> 8) * 0x1.0p-24f, static_cast<float>(a1 >> 8) * 0x1.0p-24f};  // exact
+  const F2 u1{static_cast<float>(b0 >> 8) * 0x1.0p-24f, static_cast<float>(b1 >> 8) * 0x1.0p-24f};
+  const F2 lg = plogf2(psub(bc(1.0f), u0), nz);
+  const F2 t = pmul(bc(-2.0f), lg, nz);
+  const F2 r{__fsqrt_rn(t.x), __fsqrt_rn(t.y)};
+  F2 sn, cs;
+  psincosf2(pmul(bc(6.28318548f), u1, nz), &sn, &cs, nz);
+  const F2 zc = pmul(bc(sd), pmul(r, cs, nz), nz), zs = pmul(bc(sd), pmul(r, sn, nz), nz);
+  z[0] = zc.x;
+  z[1] = zs.x;
+  z[2] = zc.y;
+  z[3] = zs.y;
+}
+#endif
+
 // Samples 4q .. 4q+3 of a source stream: counter q of the stream's Philox sequence gives
 // four 32-bit words, two Box-Muller pairs.
 RSH void signal_quad(const SamplerSpecD& sp, const Stream& g, uint64_t q, float* z) {
   const U4 w = philox4x32_10(U4{static_cast<uint32_t>(q), static_cast<uint32_t>(q >> 32), g.tag, 0x51A1u},
                              g.k0, g.k1);
   const float sd = static_cast<float>(sp.signal_std);
+#ifdef __CUDA_ARCH__
+  box_muller2(sd, w.x, w.y, w.z, w.w, z);
+#else
   box_muller(sd, w.x, w.y, z, z + 1);
   box_muller(sd, w.z, w.w, z + 2, z + 3);
+#endif
 }
 
 }  // namespace rsg
