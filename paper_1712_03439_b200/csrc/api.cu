@@ -1442,8 +1442,11 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
     if (!status) status = enqueue_synth(c, b, R.chunks[0], R.sA);
   }
   for (int k = 0; k < kSigAhead && !status; ++k) status = enqueue_sig(k);
+  // Profiling level 2 (the per-size K4 breakdown) serializes the whole render: chunk k+1's
+  // synth waits for chunk k's filter, so no K1 runs beside the K4 launches being timed.
+  const bool serial = c->prof_level >= 2;
   for (int k = 0; k < nch && !status; ++k) {
-    if (k + 1 < nch) {
+    if (k + 1 < nch && !serial) {
       status = prep_chunk(b, R.chunks[k + 1]);
       if (!status) status = enqueue_synth(c, b, R.chunks[k + 1], R.sA);
       if (status) break;
@@ -1455,6 +1458,12 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
     t_plan += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (status) break;
     status = enqueue_filter(c, b, R.chunks[k], io, out_off, out_stride, R.sB, R.sD);
+    if (serial && !status && k + 1 < nch) {
+      RS_CUDA(cudaEventRecord(R.chunks[k].ev_out, R.sB));
+      RS_CUDA(cudaStreamWaitEvent(R.sA, R.chunks[k].ev_out, 0));
+      status = prep_chunk(b, R.chunks[k + 1]);
+      if (!status) status = enqueue_synth(c, b, R.chunks[k + 1], R.sA);
+    }
     R.mark(R.sB, "filter+mix enq-end " + std::to_string(k));
     R.mark(R.sD, "d2h done " + std::to_string(k));
     R.mark(R.sA, "sA at " + std::to_string(k));
