@@ -163,6 +163,10 @@ def build_batch(m: Manifest, recs: list, eta_db: float):
     I = np.array([s.src.shape[0] for s in scs])
     J = np.array([s.mic.shape[0] for s in scs])
     lens = np.array([s.size for s in sigs], np.int64)
+    offs = scenes.signal_offsets(lens)
+    buf = np.zeros(int((offs + lens).max()), np.float32)
+    for o, x in zip(offs, sigs):
+        buf[o : o + x.size] = x
     b = scenes.SceneBatch(
         src_begin=np.concatenate([[0], np.cumsum(I)]).astype(np.int64),
         mic_begin=np.concatenate([[0], np.cumsum(J)]).astype(np.int64),
@@ -171,8 +175,7 @@ def build_batch(m: Manifest, recs: list, eta_db: float):
         image_order=np.array([s.order for s in scs], np.int32), max_taps=np.array([s.horizon for s in scs], np.int64),
         src_pos=np.concatenate([s.src for s in scs]), mic_pos=np.concatenate([s.mic for s in scs]),
         snr_db=np.concatenate([s.snr_db for s in scs]),
-        sig_off=np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64), sig_len=lens,
-        signals=np.concatenate(sigs).astype(np.float32), eta_db=eta_db, plan_rule=plan_rule,
+        sig_off=offs, sig_len=lens, signals=buf, eta_db=eta_db, plan_rule=plan_rule,
         forced_fft_size=forced, name="manifest", seed=m.seed)
     return b, ok, failed
 

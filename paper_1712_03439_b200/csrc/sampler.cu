@@ -45,33 +45,47 @@ struct SrcInfo {
 };
 
 // Persistent grid over (source, tile) work units: unit u of the flat list belongs to the
-// source whose tile prefix `first_tile` brackets it (binary search); a tile is 4 *
-// blockDim.x sample quads.  (A 2-D grid sized by the longest source launched millions
-// of empty CTAs for the short ones.)
-constexpr int kSigTile = 4 * 256;
-__global__ void __launch_bounds__(256) signals_kernel(SamplerSpecD sp, uint64_t seed, int64_t epoch,
-                                                      const SrcInfo* src, const int64_t* first_tile,
-                                                      int64_t n_src, int64_t n_tiles, float* out) {
+// source whose tile prefix `first_tile` brackets it (binary search, one thread per CTA); a
+// tile is kSigQuads quads per thread.  (A 2-D grid sized by the longest source launched
+// millions of empty CTAs for the short ones.)
+constexpr int kSigThreads = 256, kSigQuads = 8;
+constexpr int kSigTile = kSigQuads * kSigThreads;  // quads per tile
+__global__ void __launch_bounds__(kSigThreads) signals_kernel(SamplerSpecD sp, uint64_t seed, int64_t epoch,
+                                                              const SrcInfo* src, const int64_t* first_tile,
+                                                              int64_t n_src, int64_t n_tiles, float* out) {
+  __shared__ int64_t s_src;
   for (int64_t u = blockIdx.x; u < n_tiles; u += gridDim.x) {
-    int64_t lo = 0, hi = n_src - 1;  // last source with first_tile <= u
-    while (lo < hi) {
-      const int64_t mid = (lo + hi + 1) / 2;
-      if (first_tile[mid] <= u) lo = mid; else hi = mid - 1;
+    __syncthreads();  // the previous tile's s_src is consumed
+    if (threadIdx.x == 0) {
+      int64_t lo = 0, hi = n_src - 1;  // last source with first_tile <= u
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (first_tile[mid] <= u) lo = mid; else hi = mid - 1;
+      }
+      s_src = lo;
     }
+    __syncthreads();
+    const int64_t lo = s_src;
     const SrcInfo si = src[lo];
     const Stream g(seed ^ 0x5EED5EED5EEDull, static_cast<uint64_t>(si.utt), static_cast<uint64_t>(epoch),
                    kTagSignal + static_cast<uint32_t>(si.local));
     const int64_t nquads = (si.len + 3) / 4;
     float* o = out + si.off;
+    const bool al16 = (reinterpret_cast<uintptr_t>(o) & 15u) == 0;
     const int64_t tile = u - first_tile[lo];
-    for (int k = 0; k < 4; ++k) {
-      const int64_t q = (tile * 4 + k) * blockDim.x + threadIdx.x;
+#pragma unroll 1
+    for (int k = 0; k < kSigQuads; ++k) {
+      const int64_t q = (tile * kSigQuads + k) * kSigThreads + threadIdx.x;
       if (q >= nquads) break;
       float z[4];
       signal_quad(sp, g, static_cast<uint64_t>(q), z);
+      if (al16 && 4 * q + 3 < si.len) {
+        *reinterpret_cast<float4*>(o + 4 * q) = make_float4(z[0], z[1], z[2], z[3]);
+      } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (4 * q + i < si.len) o[4 * q + i] = z[i];
+        for (int i = 0; i < 4; ++i)
+          if (4 * q + i < si.len) o[4 * q + i] = z[i];
+      }
     }
   }
 }

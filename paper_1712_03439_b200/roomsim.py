@@ -517,7 +517,7 @@ def sample_batch(spec: RsSamplerSpec, n_utt: int, *, seed: int, first_utt: int =
         src_begin=src_begin, mic_begin=(np.arange(n_utt + 1) * J).astype(np.int64), room_dims=room,
         reflection=refl, sample_rate=np.full(n_utt, spec.fs), speed_of_sound=np.full(n_utt, spec.c0),
         image_order=order, max_taps=taps, src_pos=src, mic_pos=mic, snr_db=snr,
-        sig_off=np.concatenate([[0], np.cumsum(sig_len)[:-1]]).astype(np.int64), sig_len=sig_len,
+        sig_off=sc.signal_offsets(sig_len), sig_len=sig_len,
         signals=None, eta_db=eta_db, plan_rule=plan_rule, forced_fft_size=forced_fft_size, seed=seed,
         utt_ids=first_utt + np.arange(n_utt, dtype=np.int64))
 

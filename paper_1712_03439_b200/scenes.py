@@ -170,7 +170,8 @@ class SceneBatch:
 
     @property
     def total_samples(self) -> int:
-        return int(self.sig_len.sum())
+        """Extent of the signal buffer (sources start on 16-byte boundaries: `signal_offsets`)."""
+        return int((self.sig_off + self.sig_len).max()) if self.sig_len.size else 0
 
     @property
     def audio_seconds(self) -> float:
@@ -248,10 +249,12 @@ class SceneBatch:
             mb.append(mb[-1] + (m1 - m0))
         srcs = np.asarray(srcs, np.int64)
         lens = self.sig_len[srcs]
-        offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+        offs = signal_offsets(lens)
         sig = None
         if self.signals is not None:
-            sig = np.concatenate([self.signals[o : o + n] for o, n in zip(self.sig_off[srcs], lens)]) if len(srcs) else np.zeros(0, np.float32)
+            sig = np.zeros(int((offs + lens).max()) if len(srcs) else 0, np.float32)
+            for o_new, o, n in zip(offs, self.sig_off[srcs], lens):
+                sig[o_new : o_new + n] = self.signals[o : o + n]
         return dataclasses.replace(
             self,
             src_begin=np.asarray(sb, np.int64),
@@ -272,6 +275,14 @@ class SceneBatch:
         )
 
 
+def signal_offsets(lens) -> np.ndarray:
+    """Offsets of consecutive sources in one signal buffer, each rounded up to a multiple of
+    4 samples (16 bytes): vector loads and stores of a source start aligned."""
+    lens = np.asarray(lens, np.int64)
+    padded = (lens + 3) // 4 * 4
+    return np.concatenate([[0], np.cumsum(padded)[:-1]]).astype(np.int64) if lens.size else np.zeros(0, np.int64)
+
+
 def make_batch(spec: SamplerSpec, n_utt: int, *, epoch: int = 0, first_utt: int = 0,
                eta_db: float = 0.0, plan_rule: int = PLAN_CHOOSE, forced_fft_size: int = 0,
                signals: bool = True, name: str = "") -> SceneBatch:
@@ -279,7 +290,7 @@ def make_batch(spec: SamplerSpec, n_utt: int, *, epoch: int = 0, first_utt: int 
     I = np.array([s.src.shape[0] for s in scenes])
     J = np.array([s.mic.shape[0] for s in scenes])
     nx = np.repeat([s.n_samples for s in scenes], I).astype(np.int64)
-    off = np.concatenate([[0], np.cumsum(nx)[:-1]]).astype(np.int64)
+    off = signal_offsets(nx)
     b = SceneBatch(
         src_begin=np.concatenate([[0], np.cumsum(I)]).astype(np.int64),
         mic_begin=np.concatenate([[0], np.cumsum(J)]).astype(np.int64),
@@ -309,7 +320,7 @@ def make_batch(spec: SamplerSpec, n_utt: int, *, epoch: int = 0, first_utt: int 
 
 def host_signals(b: SceneBatch, seed: int, epoch: int = 0, first_utt: int = 0) -> np.ndarray:
     """i.i.d. N(0, 0.1) float32 per source, keyed by (seed, utterance, source)."""
-    out = np.empty(b.total_samples, np.float32)
+    out = np.zeros(b.total_samples, np.float32)
     for u in range(b.n_utt):
         for s in range(b.src_begin[u], b.src_begin[u + 1]):
             g = _rng(seed ^ 0x5EED, (first_utt + u) * 64 + int(s - b.src_begin[u]), epoch)
