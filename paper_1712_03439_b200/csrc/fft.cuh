@@ -703,4 +703,101 @@ __device__ __forceinline__ void fused_pair_512(float2* s, int t, const float2* t
   bar();
 }
 
+// ---- M = 256: the same fusion for the 8 x 8 x 4 plan (one warp per transform).  The last
+// forward pass (radix 4, NS = 64) gives thread t butterflies j = t and t + 32, i.e.
+// Z[t + 64 r] (b1) and Z[t + 32 + 64 r] (b2), r < 4; the inverse pass 0 (radix 8, NS = 1)
+// needs Z'[t + 32 r], r < 8 — the same eight bins.  The partner of k = t + 64 r is
+// M - k = (32 - t) + 32 + 64 (3 - r): lane 32 - t's b2[3 - r] (lanes l and 32 - l; lane
+// 16 is its own partner, lane 0 pairs within b1 and within b2).  Each lane computes the
+// pairs of its b1 from the partner's raw b2 (shuffled in) and returns the partner's new b2
+// (shuffled back).  Reads the Q layout (output of the NS = 8 pass), writes the PAD layout
+// inverse pass 1 reads.  Formulas as spectral_multiply.
+template <class Bar>
+__device__ __forceinline__ void fused_pair_256(float2* s, int t, const float2* tws, const float2* G,
+                                               const float2* W, bool active, Bar bar) {
+  using PL = Plan<256>;
+  constexpr int M = 256;
+  static_assert(PL::T == 32 && PL::NP == 3 && PL::radix(2) == 4 && PL::ns(2) == 64 && PL::q_in(2),
+                "plan shape");
+  float2 b1[4], b2[4];
+  if (active) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      b1[r] = s[q_slot<32>(t, 64 * r)];       // element t + 64 r
+      b2[r] = s[q_slot<32>(t, 32 + 64 * r)];  // element t + 32 + 64 r
+    }
+    apply_twiddles<4, false>(b1, tws[PL::tw_off(2) + t]);
+    Dft<4, false>::run(b1);  // b1[r] = Z[t + 64 r]
+    apply_twiddles<4, false>(b2, tws[PL::tw_off(2) + t + 32]);
+    Dft<4, false>::run(b2);  // b2[r] = Z[t + 32 + 64 r]
+  }
+  const int partner = (32 - t) & 31;
+  float2 pv[4];  // partner's raw b2 (all lanes shuffle; inactive lanes carry junk)
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    pv[r].x = __shfl_sync(0xffffffffu, b2[r].x, partner);
+    pv[r].y = __shfl_sync(0xffffffffu, b2[r].y, partner);
+  }
+  auto wk_of = [&](int k) {  // W^k = exp(-2 pi i k / 2M), k in [0, M]: table holds k <= M/2
+    if (k <= M / 2) return W[k];
+    const float2 w = W[M - k];
+    return make_float2(-w.x, w.y);
+  };
+  auto pair = [&](int k, float2 a, float2 b, float2& zk, float2& zm) {
+    const float2 wk = wk_of(k);
+    const float2 S = c_add(a, b);
+    const float2 D = c_rot<false>(c_sub(a, b));
+    const float2 wD = c_mul(wk, D);
+    const float2 X2 = c_add(S, wD), X2m = c_sub(S, wD);
+    const float2 P = c_mul(X2, G[k]);
+    const float2 Q = c_mulc(X2m, G[M - k]);
+    const float2 U = c_add(P, Q);
+    const float2 V = c_mulc(c_sub(P, Q), wk);
+    zk = make_float2(U.x - V.y, U.y + V.x);
+    zm = make_float2(U.x + V.y, V.x - U.y);
+  };
+  float2 o1[4], o2[4], back[4];
+  const bool self0 = t == 0;
+  if (active) {
+    if (!self0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        float2 zk, zm;
+        pair(t + 64 * r, b1[r], c_conj(pv[3 - r]), zk, zm);
+        o1[r] = zk;
+        back[3 - r] = zm;  // the partner's new b2[3 - r] (Z'[M - k])
+      }
+    } else {  // bins 64 r (b1) and 32 + 64 r (b2) pair within themselves
+      float2 zm;
+      pair(0, b1[0], c_conj(b1[0]), o1[0], zm);
+      pair(64, b1[1], c_conj(b1[3]), o1[1], o1[3]);
+      pair(M / 2, b1[2], c_conj(b1[2]), o1[2], zm);
+      pair(32, b2[0], c_conj(b2[3]), o2[0], o2[3]);
+      pair(96, b2[1], c_conj(b2[2]), o2[1], o2[2]);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) back[r] = make_float2(0.f, 0.f);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    float2 got;
+    got.x = __shfl_sync(0xffffffffu, back[r].x, partner);
+    got.y = __shfl_sync(0xffffffffu, back[r].y, partner);
+    if (!self0) o2[r] = got;
+  }
+  float2 v[8];  // Z'[t + 32 r], r < 8
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    v[2 * r] = o1[r];
+    v[2 * r + 1] = o2[r];
+  }
+  if (active) Dft<8, true>::run(v);  // inverse pass 0 (NS = 1)
+  bar();                             // every lane's reads of s are done
+  if (active) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) s[PAD(8 * t + r)] = v[r];
+  }
+  bar();
+}
+
 }  // namespace rsg

@@ -698,6 +698,10 @@ ola_small_kernel(OlaArgs a) {
       stockham_pass<M, 1, false, GroupBar<T>, true>(s, t, tws, active, bar);
       fused_pair_512(s, t, tws, gs, W, active, bar);
       stockham_pass<M, 1, true, GroupBar<T>, true, true>(s, t, tws, active, bar);
+    } else if constexpr (M == 256) {
+      stockham_pass<M, 1, false, GroupBar<T>, true>(s, t, tws, active, bar);
+      fused_pair_256(s, t, tws, gs, W, active, bar);
+      stockham_pass<M, 1, true, GroupBar<T>, true>(s, t, tws, active, bar);
     } else
 #endif
     {
