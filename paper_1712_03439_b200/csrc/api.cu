@@ -400,6 +400,7 @@ struct Span {
   int64_t list_off, list_n, item_off, item_n;
   int64_t max_nh = 1;  // largest N_h of the span (in-place / two-stream carry size)
   int64_t max_l = 1;   // largest L of the span (two-stream input window)
+  int seg = kPowerSeg; // OLA blocks per power segment
 };
 
 // A batch of one large span (four-step path): pairs [pair_lo, pair_hi) of the
@@ -419,18 +420,19 @@ struct FilterPlan {
   double flops = 0;
 };
 
-// Sizes that take the four-step path: every M > 16384 and M = 8192 (measured faster than
-// the one-CTA kernel in the config-4 render, where few pairs have that size).  Tuning
-// override RSG_LARGE_MIN = smallest log2 M; RSG_IP_FORCE keeps M = 8192 in place (tests).
+// Sizes that take the four-step path: every M > 16384 (and M = 8192 / 16384 pairs whose
+// overlap carry does not fit next to the in-place transform).  Tuning override
+// RSG_LARGE_MIN = smallest log2 M.
 bool use_large(int l) {
   static const int v = [] {
     const char* e = std::getenv("RSG_LARGE_MIN");
     return e ? std::atoi(e) : -1;
   }();
   static const bool ip_force = std::getenv("RSG_IP_FORCE") != nullptr;
+  static_cast<void>(ip_force);
   if (l > kMaxLog2M) return true;
   if (v >= 0) return l >= v;
-  return l == 13 && !ip_force;
+  return false;
 }
 // Largest N_h whose overlap carry fits next to the in-place K4's transform (0: none).
 int64_t ip_max_nh(int l) {
@@ -619,15 +621,21 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
       return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(0);
     }();
     const int64_t run_div = run_div_env ? run_div_env : (ip ? 2 : (l <= 8 ? 12 : 3));
-    int64_t run = std::max<int64_t>((total_blocks + run_div * slots - 1) / (run_div * slots), 16 * max_pre);
-    run = (run + kPowerSeg - 1) / kPowerSeg * kPowerSeg;  // runs start on power-segment boundaries
+    // the in-place K4 at M >= 8192: a few long blocks per pair — 2-block power segments and
+    // runs down to 2 (pre-)blocks, so even a small bucket fills the SMs (each run recomputes
+    // its overlap blocks: up to half the work of a 2-block run, paid only where it buys CTAs)
+    const int seg = (ip && l >= 13) ? kPowerSegLarge : kPowerSeg;
+    const int64_t min_run = (ip && l >= 13) ? 2 * max_pre : 16 * max_pre;
+    int64_t run = std::max<int64_t>((total_blocks + run_div * slots - 1) / (run_div * slots), min_run);
+    run = (run + seg - 1) / seg * seg;  // runs start on power-segment boundaries
+    sp.seg = seg;
     const int ppb = ip ? ip_parts_per_block(l) : small_parts_per_block(l);
     sp.item_off = static_cast<int64_t>(fp.items.size());
     for (int32_t p : v) {
       PairPlan& pl = plans[p];
       const int64_t pre = pre_blocks(pl);
       pl.part0 = part_acc;
-      pl.npart = static_cast<int32_t>(power_segments(pl.B) * ppb);
+      pl.npart = static_cast<int32_t>(power_segments(pl.B, seg) * ppb);
       part_acc += pl.npart;
       for (int64_t r0 = 0; r0 < pl.B; r0 += run) {
         const int64_t r1 = std::min<int64_t>(pl.B, r0 + run);
@@ -786,7 +794,8 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
       ++c->launches;
     } else if (sp.var == kVarSmall || sp.var == kVarIp) {
       OlaArgs a{fb.olaitems.as<OlaItem>() + sp.item_off, static_cast<int32_t>(sp.item_n), d_pair,
-                fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(), d_part, c->tw[sp.l]};
+                fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(), d_part, c->tw[sp.l],
+                sp.seg};
       if (sp.var == kVarIp)
         RS_CUDA(launch_ola_ip(sp.l, a, sp.max_nh, side_for()));
       else

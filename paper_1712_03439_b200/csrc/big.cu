@@ -388,9 +388,9 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
     }
     // power: per-lane FP64 sum over the segment, stored at its end (power.cuh)
     pw += static_cast<double>((pb[0] + pb[1]) + (pb[2] + pb[3]));
-    if (closes_segment(b, it.b_end)) {
+    if (closes_segment(b, it.b_end, a.seg)) {
       const long long part0 = __ldg(&a.plan[it.pair].part0);  // reloaded: nothing 64-bit lives across blocks
-      store_segment_power<T>(a.part + part0 + static_cast<long long>(b / kPowerSeg) * parts_per_block_of(T), pw, t,
+      store_segment_power<T>(a.part + part0 + static_cast<long long>(b / a.seg) * parts_per_block_of(T), pw, t,
                              b >= it.b_own);
       pw = 0.0;
     }

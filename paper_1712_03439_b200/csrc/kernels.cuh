@@ -108,8 +108,9 @@ struct OlaArgs {
   const float* signals;
   const float2* spec;
   float* y;             // reverberant pair signals
-  double* part;         // power partials: block b, warp w of a pair at plan.part0 + b * ppb + w
+  double* part;         // power partials: segment s, warp w of a pair at plan.part0 + s * ppb + w
   const float2* tw;
+  int32_t seg = 16;     // OLA blocks per power segment (power.cuh)
 };
 
 struct MixArgs {

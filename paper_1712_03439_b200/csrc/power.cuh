@@ -19,11 +19,14 @@ constexpr int kPowerSeg = 16;  // OLA blocks per power segment (runs start on mu
 
 // partials per segment: one per warp of the group (one for groups narrower than a warp)
 __host__ __device__ constexpr int parts_per_block_of(int T) { return T < 32 ? 1 : T / 32; }
-__host__ __device__ constexpr long long power_segments(long long B) { return (B + kPowerSeg - 1) / kPowerSeg; }
+__host__ __device__ constexpr long long power_segments(long long B, int seg = kPowerSeg) { return (B + seg - 1) / seg; }
+// The in-place K4 at M >= 8192 (few, long blocks per pair) uses 2-block segments, so its runs
+// can be short enough to spread a small bucket over the SMs.
+constexpr int kPowerSegLarge = 2;
 
-// true when block b closes a segment of a run ending at b_end
-__device__ __forceinline__ bool closes_segment(int b, int b_end) {
-  return (b + 1) % kPowerSeg == 0 || b + 1 == b_end;
+// true when block b closes a segment (of seg blocks) of a run ending at b_end
+__device__ __forceinline__ bool closes_segment(int b, int b_end, int seg = kPowerSeg) {
+  return (b + 1) % seg == 0 || b + 1 == b_end;
 }
 
 // v: this lane's FP64 Σ y² over one segment.  The group's T lanes (T < 32: a T-aligned
