@@ -471,11 +471,17 @@ def ours(args, rank, world, local_rank):
         threads = os.cpu_count() or 1
         want = args.cpu_sample_utts or max(32, 64 * threads)  # ~10 s of the host's cores
         sub, k = cpu_sample(args, want)
+        # glibc's default malloc first (SURVEY.md §8d asks for both; mallopt cannot be undone
+        # within the process): a quarter of the sample, so the baseline leg stays within seconds
+        sub_u = sub.subset(np.arange(0, sub.n_utt, 4))
+        v_u, dt_u, _, _ = run_cpu_reference(sub_u, threads, tuned=False)
         v, dt, kind, ref_res = run_cpu_reference(sub, threads)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
                "sample": f"{sub.n_utt} of {n_config(args)} {args.config} utterances (every {k}th), "
                          f"{sub.audio_seconds:.1f} audio-s, {dt:.1f} s wall",
-               "note": "reference radix-2 CPU path (FFTW3 unavailable); malloc mmap_threshold=64MiB"}
+               "note": "reference radix-2 CPU path (FFTW3 unavailable); malloc mmap_threshold=64MiB",
+               "value_default_malloc": v_u,
+               "default_malloc_sample": f"every 4th utterance of the sample ({sub_u.n_utt}), {dt_u:.1f} s wall"}
         # the same sample through our path: layouts bit-exact, waveforms within 1e-5 of the peak
         g = roomsim.render_batch(sub, ctx=ctx)
         o_out, o_len, o_lay, o_gain, o_pow = ref_res
