@@ -84,3 +84,53 @@ def test_render_from_device_generated_signals(rs, ctx, port):
             a = b.channel(go, u, j, o_len[u])
             w = b.channel(o_out, u, j, o_len[u])
             assert np.abs(a - w).max() <= 1e-5 * np.abs(w).max()
+
+
+def test_signal_plan_epochs_and_subsets(rs):
+    """rs_signal_plan (the table built once, one launch per epoch) equals the host generator
+    for several epochs, on a full batch and on a non-contiguous subset (shards keep their
+    utterance ids), including sources whose length is not a multiple of 4 (tail quads)."""
+    import torch
+    from paper_1712_03439_b200 import scenes
+
+    sp = rs.sampler_spec(scenes.spec_config4())
+    b = rs.sample_batch(sp, 40, seed=21, first_utt=7)
+    b.sig_len = b.sig_len.copy()
+    b.sig_len[::3] -= np.arange(b.sig_len[::3].size) % 4  # ragged tails
+    b.sig_off = scenes.signal_offsets(b.sig_len)
+    sub = b.subset([3, 11, 12, 30, 39])
+    for batch in (b, sub):
+        plan = rs.SignalPlan(sp, batch, seed=21)
+        dev = torch.full((batch.total_samples,), float("nan"), dtype=torch.float32, device="cuda")
+        for ep in (0, 3):
+            plan.generate(dev.data_ptr(), epoch=ep)
+            torch.cuda.synchronize()
+            host = rs.generate_signals(sp, batch, seed=21, epoch=ep)
+            d = dev.cpu().numpy()
+            for o, n in zip(batch.sig_off, batch.sig_len):
+                assert np.array_equal(d[o:o + n].view(np.uint32), host[o:o + n].view(np.uint32))
+        plan.close()
+    # the subset's samples are the full batch's (keyed by the global utterance ids)
+    full = rs.generate_signals(sp, b, seed=21)
+    part = rs.generate_signals(sp, sub, seed=21)
+    for k, u in enumerate([3, 11, 12, 30, 39]):
+        s_full, s_sub = b.src_begin[u], sub.src_begin[k]
+        n = int(b.sig_len[s_full])
+        assert np.array_equal(full[b.sig_off[s_full]:b.sig_off[s_full] + n],
+                              part[sub.sig_off[s_sub]:sub.sig_off[s_sub] + n])
+
+
+def test_k4_breakdown_rows(rs):
+    """Profiling level 2: per-(N, variant) rows whose flops sum to the render's K4 flops."""
+    from paper_1712_03439_b200 import scenes
+
+    c = rs.Context(0)
+    b = scenes.config3(n_utt=6, seed=55)
+    c.set_profiling(2)
+    rs.render_batch(b, ctx=c)
+    rows = c.k4_breakdown()
+    t = c.last_timing()
+    assert rows and sum(r["pairs"] for r in rows) == b.n_pairs
+    assert abs(sum(r["flops"] for r in rows) - t["ola_flops"]) <= 1e-6 * t["ola_flops"]
+    assert all(r["ms"] > 0 for r in rows)
+    c.close()
