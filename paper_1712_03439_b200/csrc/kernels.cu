@@ -89,6 +89,9 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   // of RS bytes (offset arithmetic keeps the accesses in the shared window: STS/LDS)
   const uintptr_t cnt_off = (reinterpret_cast<uintptr_t>(ent_d + CH) - reinterpret_cast<uintptr_t>(sm) + 15) & ~uintptr_t(15);
   unsigned char* cnt8 = sm + cnt_off;
+  // one byte per bin: the lane that last claimed it in the current fold round (distinctness test)
+  const unsigned tag_s = static_cast<unsigned>(__cvta_generic_to_shared(sm)) +
+                         static_cast<unsigned>(cnt_off + ((NW * RS + 15) & ~15));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lo = it.slice_lo, len = it.slice_len;
   // 32-bit shared address of the bins, computed once (laundered through asm: otherwise the
@@ -237,6 +240,23 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
       const bool valid = l < my_total;
       const int bn = valid ? ent_d[my_base + l] : -1 - lane;  // distinct dummy keys for idle lanes
       const double av = valid ? ent_a[my_base + l] : 0.0;
+      // Fast path: every lane claims its bin in a byte tag; if each valid lane reads back its
+      // own id the round's bins are distinct (the bins of one owner are touched by this warp
+      // only), so all entries apply at once.  A shared bin leaves some lane with another id:
+      // then match_any orders the round as below.  (MATCH.ANY's latency was the fold's
+      // largest stall.)
+      {
+        const unsigned ta = tag_s + static_cast<unsigned>(valid ? bn : 0);
+        if (valid) asm volatile("st.shared.u8 [%0], %1;" ::"r"(ta), "r"(lane) : "memory");
+        __syncwarp();
+        unsigned got = static_cast<unsigned>(lane);
+        if (valid) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(got) : "r"(ta) : "memory");
+        if (__all_sync(0xffffffffu, got == static_cast<unsigned>(lane))) {
+          if (valid) shared_add_rn(bins_s + 8u * static_cast<unsigned>(bn), av);
+          __syncwarp();
+          continue;
+        }
+      }
       const unsigned grp = __match_any_sync(0xffffffffu, bn);
       const int rank = __popc(grp & lt);
       const int rounds = __reduce_max_sync(0xffffffffu, valid ? __popc(grp) : 0);
@@ -272,7 +292,7 @@ size_t synth_smem_bytes(int max_order, int slice, int nt, int ipt) {
   const int u16 = (4 * ((nv + 3) / 4) + 15) / 16;  // count-row stride (kernel's RS)
   const int rs = 16 * (u16 % 2 == 0 ? u16 + 1 : u16);
   return sizeof(double) * (static_cast<size_t>(slice) + 3 * W + 3 * max_order + 1 + ch) + sizeof(int) * ch +
-         static_cast<size_t>(nw) * rs + 16 + 16;
+         ((static_cast<size_t>(nw) * rs + 15) & ~size_t(15)) + static_cast<size_t>(slice) + 16 + 16;  // + bin tags
 }
 
 cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice, cudaStream_t s,
@@ -282,7 +302,8 @@ cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int sli
   // even 2 images per thread keep 2 per SM, 4)
   const bool two4 = 2 * synth_smem_bytes(max_order, slice, nt, 4) <= 227 * 1024;
   const bool two2 = 2 * synth_smem_bytes(max_order, slice, nt, 2) <= 227 * 1024;
-  const int ipt = (nt == 512 && !two4 && two2) ? 2 : 4;
+  const bool one4 = synth_smem_bytes(max_order, slice, nt, 4) <= 227 * 1024;
+  const int ipt = (nt == 512 && ((!two4 && two2) || !one4)) ? 2 : 4;
   const size_t smem = synth_smem_bytes(max_order, slice, nt, ipt);
   auto go = [&](auto kern, int threads) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
