@@ -63,7 +63,9 @@ __device__ __forceinline__ void shared_add_rn(unsigned a, double v) {
 }
 
 // IPT = images per thread per chunk (4 measured best; 2 where 4 would cost occupancy)
-template <int NT, int IPT>
+// TAGS: the fold's distinct-bins fast path (byte tags per bin; the one-CTA long-RIR class,
+// where it measured 6% faster — the sliced classes were 3% slower with it)
+template <int NT, int IPT, bool TAGS>
 __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_cap) {
   extern __shared__ __align__(16) unsigned char sm[];
   constexpr int NW = NT / 32;  // warps = owner warps
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
       // only), so all entries apply at once.  A shared bin leaves some lane with another id:
       // then match_any orders the round as below.  (MATCH.ANY's latency was the fold's
       // largest stall.)
-      {
+      if constexpr (TAGS) {
         const unsigned ta = tag_s + static_cast<unsigned>(valid ? bn : 0);
         if (valid) asm volatile("st.shared.u8 [%0], %1;" ::"r"(ta), "r"(lane) : "memory");
         __syncwarp();
@@ -287,12 +289,12 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   }
 }
 
-size_t synth_smem_bytes(int max_order, int slice, int nt, int ipt) {
+size_t synth_smem_bytes(int max_order, int slice, int nt, int ipt, bool tags) {
   const int W = 2 * max_order + 1, nw = nt / 32, ch = ipt * nt, nv = ipt * nw;
   const int u16 = (4 * ((nv + 3) / 4) + 15) / 16;  // count-row stride (kernel's RS)
   const int rs = 16 * (u16 % 2 == 0 ? u16 + 1 : u16);
   return sizeof(double) * (static_cast<size_t>(slice) + 3 * W + 3 * max_order + 1 + ch) + sizeof(int) * ch +
-         ((static_cast<size_t>(nw) * rs + 15) & ~size_t(15)) + static_cast<size_t>(slice) + 16 + 16;  // + bin tags
+         ((static_cast<size_t>(nw) * rs + 15) & ~size_t(15)) + (tags ? static_cast<size_t>(slice) : 0) + 16 + 16;
 }
 
 cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice, cudaStream_t s,
@@ -300,19 +302,21 @@ cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int sli
   if (n_items == 0) return cudaSuccess;
   // 4 images per thread unless that would drop a 512-thread CTA below 2 per SM (when not
   // even 2 images per thread keep 2 per SM, 4)
-  const bool two4 = 2 * synth_smem_bytes(max_order, slice, nt, 4) <= 227 * 1024;
-  const bool two2 = 2 * synth_smem_bytes(max_order, slice, nt, 2) <= 227 * 1024;
-  const bool one4 = synth_smem_bytes(max_order, slice, nt, 4) <= 227 * 1024;
+  const bool tags = nt == 512 && slice > kSynthSlice;  // the one-CTA class
+  const bool two4 = 2 * synth_smem_bytes(max_order, slice, nt, 4, tags) <= 227 * 1024;
+  const bool two2 = 2 * synth_smem_bytes(max_order, slice, nt, 2, tags) <= 227 * 1024;
+  const bool one4 = synth_smem_bytes(max_order, slice, nt, 4, tags) <= 227 * 1024;
   const int ipt = (nt == 512 && ((!two4 && two2) || !one4)) ? 2 : 4;
-  const size_t smem = synth_smem_bytes(max_order, slice, nt, ipt);
+  const size_t smem = synth_smem_bytes(max_order, slice, nt, ipt, tags);
   auto go = [&](auto kern, int threads) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     kern<<<n_items, threads, smem, s>>>(a, slice);
     return cudaGetLastError();
   };
-  if (nt == 128) return go(rir_synth_kernel<128, 4>, 128);
-  return ipt == 4 ? go(rir_synth_kernel<512, 4>, 512) : go(rir_synth_kernel<512, 2>, 512);
+  if (nt == 128) return go(rir_synth_kernel<128, 4, false>, 128);
+  if (tags) return ipt == 4 ? go(rir_synth_kernel<512, 4, true>, 512) : go(rir_synth_kernel<512, 2, true>, 512);
+  return ipt == 4 ? go(rir_synth_kernel<512, 4, false>, 512) : go(rir_synth_kernel<512, 2, false>, 512);
 }
 
 // ============================================================================
