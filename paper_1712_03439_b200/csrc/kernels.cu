@@ -10,6 +10,7 @@
 //   rfft_*_kernel           RealFftEngine seam                        fft.hpp:38-49
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "async.cuh"
 #include "fft.cuh"
@@ -63,9 +64,11 @@ __device__ __forceinline__ void shared_add_rn(unsigned a, double v) {
 }
 
 // IPT = images per thread per chunk (4 measured best; 2 where 4 would cost occupancy)
-// TAGS: the fold's distinct-bins fast path (byte tags per bin; the one-CTA long-RIR class,
-// where it measured 6% faster — the sliced classes were 3% slower with it)
-template <int NT, int IPT, bool TAGS>
+// FOLD: how a round of an owner's list is ordered — 0: match_any groups (NT = 128: claims
+// measured 6% slower there); 2: ordered claims, no match_any (the 512-thread classes: K1 -15%
+// on the one-CTA class vs byte tags + match_any, -10% on the sliced one vs match_any)
+// HT: claim words per owner warp (FOLD 2; a power of two)
+template <int NT, int IPT, int FOLD, int HT = 256>
 __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_cap) {
   extern __shared__ __align__(16) unsigned char sm[];
   constexpr int NW = NT / 32;  // warps = owner warps
@@ -91,9 +94,14 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   // of RS bytes (offset arithmetic keeps the accesses in the shared window: STS/LDS)
   const uintptr_t cnt_off = (reinterpret_cast<uintptr_t>(ent_d + CH) - reinterpret_cast<uintptr_t>(sm) + 15) & ~uintptr_t(15);
   unsigned char* cnt8 = sm + cnt_off;
-  // one byte per bin: the lane that last claimed it in the current fold round (distinctness test)
+  // FOLD 2's claim words follow the count rows
   const unsigned tag_s = static_cast<unsigned>(__cvta_generic_to_shared(sm)) +
                          static_cast<unsigned>(cnt_off + ((NW * RS + 15) & ~15));
+  // per owner warp, HT 32-bit claim words, all ones between rounds
+  if constexpr (FOLD == 2) {
+    unsigned* cl = reinterpret_cast<unsigned*>(sm + cnt_off + ((NW * RS + 15) & ~15));
+    for (int i = threadIdx.x; i < NW * HT; i += NT) cl[i] = 0xffffffffu;
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lo = it.slice_lo, len = it.slice_len;
   // 32-bit shared address of the bins, computed once (laundered through asm: otherwise the
@@ -247,17 +255,32 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
       // only), so all entries apply at once.  A shared bin leaves some lane with another id:
       // then match_any orders the round as below.  (MATCH.ANY's latency was the fold's
       // largest stall.)
-      if constexpr (TAGS) {
-        const unsigned ta = tag_s + static_cast<unsigned>(valid ? bn : 0);
-        if (valid) asm volatile("st.shared.u8 [%0], %1;" ::"r"(ta), "r"(lane) : "memory");
-        __syncwarp();
-        unsigned got = static_cast<unsigned>(lane);
-        if (valid) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(got) : "r"(ta) : "memory");
-        if (__all_sync(0xffffffffu, got == static_cast<unsigned>(lane))) {
-          if (valid) shared_add_rn(bins_s + 8u * static_cast<unsigned>(bn), av);
+      if constexpr (FOLD == 2) {
+        // Ordered claims: every pending lane min-reduces its lane id into its bin's claim
+        // word (a hash of the bin; the owner's bins map 1:1 to bin >> 4); the lowest lane of
+        // each word wins, applies its entry and resets the word, the others retry.  Each bin
+        // therefore sees its entries in lane order; bins sharing a word only serialize.
+        // A round of distinct bins takes one pass; no match_any.
+        const unsigned cw = tag_s + 4u * static_cast<unsigned>(warp * HT + (((bn >> 4) ^ (bn >> 12)) & (HT - 1)));
+        const unsigned ba = bins_s + 8u * static_cast<unsigned>(bn);
+        bool pending = valid;
+        for (;;) {
+          if (pending) asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(cw), "r"(lane) : "memory");
           __syncwarp();
-          continue;
+          unsigned w = 0xffffffffu;
+          if (pending) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(cw) : "memory");
+          const bool win = pending && w == static_cast<unsigned>(lane);
+          __syncwarp();  // every claim word read before a winner resets it
+          if (win) {
+            shared_add_rn(ba, av);
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(cw), "r"(0xffffffffu) : "memory");
+          }
+          pending = pending && !win;
+          if (!__any_sync(0xffffffffu, pending)) break;
+          __syncwarp();
         }
+        __syncwarp();
+        continue;
       }
       const unsigned grp = __match_any_sync(0xffffffffu, bn);
       const int rank = __popc(grp & lt);
@@ -289,12 +312,12 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
   }
 }
 
-size_t synth_smem_bytes(int max_order, int slice, int nt, int ipt, bool tags) {
+size_t synth_smem_bytes(int max_order, int slice, int nt, int ipt, int fold, int ht) {
   const int W = 2 * max_order + 1, nw = nt / 32, ch = ipt * nt, nv = ipt * nw;
   const int u16 = (4 * ((nv + 3) / 4) + 15) / 16;  // count-row stride (kernel's RS)
   const int rs = 16 * (u16 % 2 == 0 ? u16 + 1 : u16);
   return sizeof(double) * (static_cast<size_t>(slice) + 3 * W + 3 * max_order + 1 + ch) + sizeof(int) * ch +
-         ((static_cast<size_t>(nw) * rs + 15) & ~size_t(15)) + (tags ? static_cast<size_t>(slice) : 0) + 16 + 16;
+         ((static_cast<size_t>(nw) * rs + 15) & ~size_t(15)) + (fold == 2 ? 4 * static_cast<size_t>(nw) * ht : 0) + 16 + 16;
 }
 
 cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice, cudaStream_t s,
@@ -302,21 +325,33 @@ cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int sli
   if (n_items == 0) return cudaSuccess;
   // 4 images per thread unless that would drop a 512-thread CTA below 2 per SM (when not
   // even 2 images per thread keep 2 per SM, 4)
-  const bool tags = nt == 512 && slice > kSynthSlice;  // the one-CTA class
-  const bool two4 = 2 * synth_smem_bytes(max_order, slice, nt, 4, tags) <= 227 * 1024;
-  const bool two2 = 2 * synth_smem_bytes(max_order, slice, nt, 2, tags) <= 227 * 1024;
-  const bool one4 = synth_smem_bytes(max_order, slice, nt, 4, tags) <= 227 * 1024;
+  static const int fold_big = [] {
+    const char* e = getenv("RSG_K1_FOLD");
+    return e ? atoi(e) : 2;
+  }();
+  static const int fold_sliced = [] {
+    const char* e = getenv("RSG_K1_FOLD_S");
+    return e ? atoi(e) : 2;
+  }();
+  const bool big = nt == 512 && slice > kSynthSlice;  // the one-CTA class
+  const int fold = big ? fold_big : fold_sliced;
+  // claim words per warp: 64 keeps two sliced 512-thread CTAs per SM
+  const int ht = nt == 512 && !big ? 64 : 256;
+  const bool two4 = 2 * synth_smem_bytes(max_order, slice, nt, 4, fold, ht) <= 227 * 1024;
+  const bool two2 = 2 * synth_smem_bytes(max_order, slice, nt, 2, fold, ht) <= 227 * 1024;
+  const bool one4 = synth_smem_bytes(max_order, slice, nt, 4, fold, ht) <= 227 * 1024;
   const int ipt = (nt == 512 && ((!two4 && two2) || !one4)) ? 2 : 4;
-  const size_t smem = synth_smem_bytes(max_order, slice, nt, ipt, tags);
+  const size_t smem = synth_smem_bytes(max_order, slice, nt, ipt, fold, ht);
   auto go = [&](auto kern, int threads) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     kern<<<n_items, threads, smem, s>>>(a, slice);
     return cudaGetLastError();
   };
-  if (nt == 128) return go(rir_synth_kernel<128, 4, false>, 128);
-  if (tags) return ipt == 4 ? go(rir_synth_kernel<512, 4, true>, 512) : go(rir_synth_kernel<512, 2, true>, 512);
-  return ipt == 4 ? go(rir_synth_kernel<512, 4, false>, 512) : go(rir_synth_kernel<512, 2, false>, 512);
+  if (nt == 128) return go(rir_synth_kernel<128, 4, 0>, 128);  // claims measured 6% slower here
+  if (fold == 2 && big) return ipt == 4 ? go(rir_synth_kernel<512, 4, 2>, 512) : go(rir_synth_kernel<512, 2, 2>, 512);
+  if (fold == 2) return ipt == 4 ? go(rir_synth_kernel<512, 4, 2, 64>, 512) : go(rir_synth_kernel<512, 2, 2, 64>, 512);
+  return ipt == 4 ? go(rir_synth_kernel<512, 4, 0>, 512) : go(rir_synth_kernel<512, 2, 0>, 512);
 }
 
 // ============================================================================

@@ -263,7 +263,7 @@ cudaError_t kernels_init();    // smem attributes
 constexpr int kSynthThreads = 512;
 constexpr int kSynthSlice = 10240;  // FP64 bins per K1 CTA (80 KB: two 512-thread CTAs per SM with 4 images/thread)
 constexpr int kSynthBig = 22528;    // FP64 bins of the one-slice class (one 512-thread CTA per SM; + bin tags)
-size_t synth_smem_bytes(int max_order, int slice, int nt, int ipt, bool tags = false);
+size_t synth_smem_bytes(int max_order, int slice, int nt, int ipt, int fold = 0, int ht = 256);
 
 // nt = 512 (16 warps) or 128 (4 warps, small lattices)
 cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int slice,

@@ -436,6 +436,47 @@ def test_render_rirs_bit_exact(rs, ctx, port, cfg, n_utt, seed):
     assert checked == b.n_pairs
 
 
+def test_k1_match_fold_variant():
+    """The 512-thread K1 classes with the match_any fold forced (RSG_K1_FOLD / _S = 0; the
+    default there is the ordered-claims fold) in a fresh process: single RIRs (one slice and
+    sliced) and every pair of a config-5 and a config-4 render, bit for bit."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import numpy as np, oracle\n"
+        "from paper_1712_03439_b200 import roomsim as rs, scenes\n"
+        "ctx = rs.Context(0); port = oracle.port(); rng = np.random.default_rng(12)\n"
+        "u64 = lambda a: np.ascontiguousarray(a, np.float64).view(np.uint64)\n"
+        "for t in range(12):\n"
+        "    room = rng.uniform([3, 3, 2.5], [10, 8, 6]); k = int(rng.integers(0, 30))\n"
+        "    src, mic = rng.uniform(0.5, room - 0.5), rng.uniform(0.5, room - 0.5)\n"
+        "    want = port.synthesize_rir(room, 0.9, k, src, mic, max_taps=30000)\n"
+        "    got = rs.synthesize_rir(room, 0.9, k, src, mic, max_taps=30000, ctx=ctx)\n"
+        "    assert (u64(got) == u64(want)).all(), t\n"
+        "n = 0\n"
+        "for b in (scenes.config5(n_utt=1, seed=27), scenes.config4(n_utt=3, seed=28)):\n"
+        "    g = rs.render_batch(b, ctx=ctx); I, J = np.diff(b.src_begin), np.diff(b.mic_begin)\n"
+        "    for u in range(b.n_utt):\n"
+        "        for i in range(I[u]):\n"
+        "            for j in range(J[u]):\n"
+        "                p = int(b.pair_begin[u] + i * J[u] + j)\n"
+        "                w = port.synthesize_rir(b.room_dims[u], float(b.reflection[u]), int(b.image_order[u]),\n"
+        "                    b.src_pos[b.src_begin[u] + i], b.mic_pos[b.mic_begin[u] + j], fs=float(b.sample_rate[u]),\n"
+        "                    c0=float(b.speed_of_sound[u]), max_taps=int(b.max_taps[u]))\n"
+        "                if b.eta_db > 0: w = port.truncate_rir(w, b.eta_db)[0]\n"
+        "                got = rs.last_pair_rir(p, w.size + 8, ctx=ctx)\n"
+        "                assert got.size == w.size and (u64(got) == u64(w)).all(), p\n"
+        "                n += 1\n"
+        "print(n)\n")
+    env = dict(os.environ, RSG_K1_FOLD="0", RSG_K1_FOLD_S="0")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert int(r.stdout.strip().splitlines()[-1]) > 20
+
+
 def test_render_error_order_matches_reference(rs, ctx):
     """The first error of a render is the one the reference meets first: utterance
     order, then pair order; per pair RoomConfig::validate and the placements inside
