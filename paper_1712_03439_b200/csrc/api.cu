@@ -418,6 +418,9 @@ struct FilterPlan {
   int64_t max_scratch = 0;          // complex elements of the largest batch's scratch
   int64_t spec_total = 0, y_total = 0, part_total = 0;
   double flops = 0;
+  // per pair: the metric's flops, (2B+1) 5 N log2 N of the REFERENCE plan (filled by the caller
+  // when the executed block size differs from it; otherwise by plan_filter from the plans)
+  std::vector<double> alg;
 };
 
 // Sizes that take the four-step path: every M > 16384 (and M = 8192 / 16384 pairs whose
@@ -486,6 +489,65 @@ int k4_variant(int l, int64_t nh) {
   return kVarLarge;  // M >= 8192 whose overlap carry does not fit in shared memory
 }
 
+// ---- executed block size ("re-blocking") ------------------------------------------
+// A pair's output is the linear convolution x * h whatever block size the overlap-add runs
+// at; the reference's plan (N, L, B) is what the API reports (bit-exact), the block size
+// the device EXECUTES is chosen per pair to minimise its modelled K4 time:
+//   (2 B(N') + 1) N' log2 N' / eff(N'),   B(N') = ceil(N_x / (N' - N_h + 1)),
+// eff(N') the measured fraction of the FP32 roofline of the kernel that runs size N'
+// (B200, config-4 render, bench.py by_size).  With the reference's N = bit_ceil(2 N_h) a
+// block yields L in (N/2, 3N/4] new samples per N-point transform pair; at N' = 4096 /
+// 8192 the short filters yield ~0.9 N' and run on the kernels with the best fractions.
+// The choice depends on the pair's (N_x, N_h) only (render invariance).
+// Forced plans (RS_PLAN_FORCED: the caller names the FFT size) execute as given.
+// RSG_REBLOCK=0 executes the reference's plan everywhere; RSG_REBLOCK_EFF="l=e,l=e" overrides eff.
+struct ReblockCfg {
+  bool on = true;
+  double eff[kLargeMaxLog2M + 2];
+};
+const ReblockCfg& reblock_cfg() {
+  static const ReblockCfg cfg = [] {
+    ReblockCfg c;
+    for (double& e : c.eff) e = 0.12;  // four-step sizes
+    //            N =   2     4     8     16    32     64     128    256   512   1024  2048   4096   8192  16384 32768
+    const double m[] = {0.01, 0.01, 0.01, 0.02, 0.075, 0.117, 0.194, 0.24, 0.43, 0.55, 0.507, 0.586, 0.56, 0.50, 0.56};
+    for (int l = 1; l <= 15; ++l) c.eff[l] = m[l - 1];
+    if (const char* e = std::getenv("RSG_REBLOCK")) c.on = std::atoi(e) != 0;
+    if (const char* e = std::getenv("RSG_REBLOCK_EFF")) {
+      int l = 0, used = 0;
+      double v = 0;
+      while (std::sscanf(e, "%d=%lf%n", &l, &v, &used) == 2) {
+        if (l >= 1 && l <= kLargeMaxLog2M + 1 && v > 0) c.eff[l] = v;
+        e += used;
+        if (*e == ',') ++e;
+      }
+    }
+    return c;
+  }();
+  return cfg;
+}
+// log2 of the executed FFT size of a pair whose reference plan is 2^ref_log2n.
+int exec_log2n(size_t nx, size_t nh, int ref_log2n) {
+  const ReblockCfg& c = reblock_cfg();
+  if (!c.on) return ref_log2n;
+  int lmin = 1;
+  while ((size_t(1) << lmin) < nh) ++lmin;  // N' >= N_h: L >= 1
+  const int lmax = std::max(13, std::min(ref_log2n, kLargeMaxLog2M + 1));
+  int best = ref_log2n;
+  double best_cost = -1;
+  for (int l = lmin; l <= lmax; ++l) {
+    const size_t n = size_t(1) << l;
+    const double blocks = static_cast<double>(block_count(nx, nh, n));
+    const double eff = k4_variant(l - 1, static_cast<int64_t>(nh)) == kVarLarge ? c.eff[kLargeMaxLog2M + 1] : c.eff[l];
+    const double cost = (2.0 * blocks + 1.0) * static_cast<double>(n) * l / eff;
+    if (best_cost < 0 || cost < best_cost) {
+      best = l;
+      best_cost = cost;
+    }
+  }
+  return best;
+}
+
 constexpr int64_t kLargeScratchBytes = int64_t(1) << 31;  // per batch (16 M bytes per unit)
 
 // Blocks before a run start whose tails overlap it: ceil((N_h - 1) / L).
@@ -500,12 +562,15 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
   std::vector<std::vector<int32_t>> bucket(NB);
   std::vector<double> work(n_pairs);
   fp.flops = 0;
+  const bool have_alg = static_cast<int64_t>(fp.alg.size()) == n_pairs;
+  if (!have_alg) fp.alg.assign(n_pairs, 0.0);
   for (int64_t p = 0; p < n_pairs; ++p) {
     const int l = plans[p].log2n - 1;
     if (l < 0 || l > kLargeMaxLog2M) return fail(RS_ERR_UNSUPPORTED, "FFT size outside the supported range");
     bucket[l * kVarCount + k4_variant(l, plans[p].nh)].push_back(static_cast<int32_t>(p));
-    work[p] = pair_flops(plans[p]);
-    fp.flops += work[p];
+    work[p] = pair_flops(plans[p]);  // executed plan: scheduling weight
+    if (!have_alg) fp.alg[p] = work[p];
+    fp.flops += fp.alg[p];
   }
   // largest pairs first (LPT) within every one-CTA bucket so each launch's tail is short; the
   // order is scheduling only (a pair's bytes do not depend on it), sorted on host threads
@@ -746,7 +811,7 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
   const bool serial = c->prof_level >= 2;  // diagnostic: one stream, one event pair per span
   auto span_flops = [&](const Span& sp) {
     double f = 0;
-    for (int64_t i = 0; i < sp.list_n; ++i) f += pair_flops(plans[fp.lists[sp.list_off + i]]);
+    for (int64_t i = 0; i < sp.list_n; ++i) f += fp.alg[fp.lists[sp.list_off + i]];
     return f;
   };
   auto span_begin = [&](const Span& sp) {
@@ -858,6 +923,9 @@ struct RenderIO {
   const int64_t* feat_off = nullptr;  // per output channel (utterance-major, then mic), host
 };
 
+// The reference planner's layout of a pair (convolution.hpp:72-161), as reported.
+struct RefLayout { int32_t log2n = 0; int64_t L = 0, B = 0; };
+
 struct Chunk {
   int64_t u0 = 0, u1 = 0, p0 = 0, P = 0;
   std::vector<UttMeta> utt;
@@ -870,7 +938,8 @@ struct Chunk {
   std::vector<uint8_t> empty_sig;        // per pair: N_x == 0 (reported after the RIR's own errors)
   std::vector<int> utt_err;              // per utterance: no target or no mic
   std::vector<std::string> utt_msg;
-  std::vector<PairPlan> plans;
+  std::vector<PairPlan> plans;   // executed plans (device)
+  std::vector<RefLayout> ref;    // the reference's plans (reported)
   std::vector<int32_t> strategy;
   std::vector<int64_t> ulen;
   FilterPlan fp;
@@ -1139,6 +1208,8 @@ int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, cudaStream_t sA
 int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
   RS_CUDA(cudaEventSynchronize(ch.ev_rir));
   ch.plans.assign(ch.P, PairPlan{});
+  ch.ref.assign(ch.P, RefLayout{});
+  ch.fp.alg.assign(ch.P, 0.0);
   ch.strategy.assign(ch.P, RS_OVERLAP_ADD);
   ch.ulen.assign(ch.u1 - ch.u0, 0);
   int64_t spec_off = 0, y_off = 0;
@@ -1181,6 +1252,14 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
       return fail(RS_ERR_UNSUPPORTED, "FFT size " + std::to_string(n) + " not supported by the device kernels");
     ch.strategy[p] = s;
     PairPlan& pl = ch.plans[p];
+    // the reference's plan: reported, and the metric's flops
+    RefLayout& rl = ch.ref[p];
+    rl.log2n = log2_exact(n);
+    rl.L = static_cast<int64_t>(n - nh + 1);
+    rl.B = static_cast<int64_t>(block_count(nx, nh, n));
+    ch.fp.alg[p] = (2.0 * static_cast<double>(rl.B) + 1.0) * 5.0 * static_cast<double>(n) * rl.log2n;
+    // the executed plan (exec_log2n above)
+    if (b->plan_rule != RS_PLAN_FORCED) n = size_t(1) << exec_log2n(nx, nh, rl.log2n);
     pl.log2n = log2_exact(n);
     pl.nh = static_cast<int64_t>(nh);
     pl.L = static_cast<int64_t>(n - nh + 1);
@@ -1523,9 +1602,9 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
         L.rir_len = r.len;
         L.rir_keep = r.keep;
         L.cutoff = b->eta_db > 0.0 ? r.cutoff : -1;
-        L.fft_size = int64_t(1) << ch.plans[p].log2n;
-        L.block_len = ch.plans[p].L;
-        L.n_blocks = ch.plans[p].B;
+        L.fft_size = int64_t(1) << ch.ref[p].log2n;
+        L.block_len = ch.ref[p].L;
+        L.n_blocks = ch.ref[p].B;
         L.out_len = ch.plans[p].out_len;
         L.strategy = ch.strategy[p];
         L.flags = r.flags;
