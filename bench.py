@@ -269,9 +269,13 @@ def ours(args, rank, world, local_rank):
     ctx.set_stream(stream.cuda_stream)
     ctx.set_profiling(True)
 
+    last = [None]
+
     def step():
-        return roomsim.render_batch(batch, ctx=ctx, device_signals_ptr=signals.data_ptr(),
-                                    device_out_ptr=out.data_ptr())
+        # the result arrays (layouts, gains, powers) of the previous step are reused
+        last[0] = roomsim.render_batch(batch, ctx=ctx, device_signals_ptr=signals.data_ptr(),
+                                       device_out_ptr=out.data_ptr(), result=last[0])
+        return last[0]
 
     def barrier():
         if world > 1:

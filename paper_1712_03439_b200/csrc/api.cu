@@ -1387,7 +1387,15 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
 int state_init(rs_ctx* c) {
   if (c->rs) return RS_OK;
   c->rs = new rs_render_state();
-  RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sA, cudaStreamNonBlocking));
+  // Stream A (K1, K2) runs above stream B's priority: chunk k+1's synthesis is enqueued while
+  // chunk k-1's K4 grids still have CTAs waiting; at equal priority it would only start
+  // once those grids had been dispatched, and the host could not plan chunk k+1 in time.
+  {
+    int prio_lo = 0, prio_hi = 0;
+    RS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    static const bool flat = std::getenv("RSG_FLAT_PRIORITY") != nullptr;  // diagnostic
+    RS_CUDA(cudaStreamCreateWithPriority(&c->rs->sA, cudaStreamNonBlocking, flat ? prio_lo : prio_hi));
+  }
   RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sB, cudaStreamNonBlocking));
   RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sH, cudaStreamNonBlocking));
   RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sD, cudaStreamNonBlocking));
@@ -1423,11 +1431,14 @@ void destroy_state(rs_ctx* c) {
 // chunk's upload and the last chunk's download stay short (PCIe-bound).
 constexpr int64_t kChunkPairsDevice = 16384;
 constexpr int64_t kChunkPairsHost = 6144;
+constexpr int64_t kFirstChunkPairs = 4096;
 
 int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const int64_t* out_off,
                 const int64_t* out_stride, int64_t* out_len, rs_pair_layout* layout, double* gains,
                 double* power) {
   if (!b || b->n_utt < 0) return fail(RS_ERR_CONFIG, "invalid scene batch");
+  const auto t_enter = std::chrono::steady_clock::now();
+  static thread_local std::chrono::steady_clock::time_point t_last_return = t_enter;
   RS_TRY(state_init(c));
   rs_render_state& R = *c->rs;
   const int64_t U = b->n_utt;
@@ -1457,9 +1468,18 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
     for (int64_t u = 0; u < U; ++u)
       total += (b->src_begin[u + 1] - b->src_begin[u]) * (b->mic_begin[u + 1] - b->mic_begin[u]);
     int64_t u0 = 0, pairs = 0, done = 0;
+    // Device renders open with a short chunk, so the first filter starts soon after the
+    // call (its K1 and host planning are the pipeline's fill time).
+    static const int64_t first_env = [] {
+      const char* e = std::getenv("RSG_FIRST_CHUNK");  // tuning override (pairs; 0: none)
+      return e ? std::atoll(e) : int64_t(-1);
+    }();
+    const int64_t first_pairs = first_env >= 0 ? first_env : kFirstChunkPairs;
     auto target = [&] {
       const int64_t rem = total - done;
-      if (!host_io) return chunk_pairs;
+      if (!host_io)
+        return done == 0 && !chunk_env && first_pairs > 0 && total > 2 * chunk_pairs ? std::min(first_pairs, chunk_pairs)
+                                                                                  : chunk_pairs;
       if (rem > chunk_pairs) return std::min(chunk_pairs, rem - chunk_pairs);
       return rem > chunk_pairs / 4 ? std::max<int64_t>(rem / 2, chunk_pairs / 4) : rem;
     };
@@ -1495,6 +1515,9 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
     if (!R.tr0) cudaEventCreate(&R.tr0);
     cudaEventRecord(R.tr0, c->stream);
     R.trace_t0 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[trace] host gap since the last render returned %.2f ms, entry to fork %.2f ms\n",
+                 std::chrono::duration<double, std::milli>(t_enter - t_last_return).count(),
+                 std::chrono::duration<double, std::milli>(R.trace_t0 - t_enter).count());
   }
   RS_CUDA(cudaStreamWaitEvent(R.sA, R.ev_start, 0));
   RS_CUDA(cudaStreamWaitEvent(R.sB, R.ev_start, 0));
@@ -1524,19 +1547,57 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
   };
   int status = RS_OK;
   auto t_plan = 0.0;
+  // A chunk's layouts, output lengths and algorithmic bytes come from its plan alone: filled
+  // while its kernels run, so only the gains and powers are left after the final sync.
+  double alg_bytes = 0;
+  R.pair_chunk.assign(Ptot, 0);
+  auto fill_layouts = [&](Chunk& ch) {
+    const int k = static_cast<int>(&ch - R.chunks.data());
+    for (int64_t p = 0; p < ch.P; ++p) {
+      const int64_t gp = ch.p0 + p;
+      R.pair_chunk[gp] = k;
+      if (layout) {
+        rs_pair_layout& L = layout[gp];
+        const PairRir& r = ch.h_rir[p];
+        L.rir_len = r.len;
+        L.rir_keep = r.keep;
+        L.cutoff = b->eta_db > 0.0 ? r.cutoff : -1;
+        L.fft_size = int64_t(1) << ch.ref[p].log2n;
+        L.block_len = ch.ref[p].L;
+        L.n_blocks = ch.ref[p].B;
+        L.out_len = ch.plans[p].out_len;
+        L.strategy = ch.strategy[p];
+        L.flags = r.flags;
+      }
+      alg_bytes += 4.0 * ch.plans[p].nh;
+    }
+    for (int64_t u = ch.u0; u < ch.u1; ++u) {
+      if (out_len) out_len[u] = ch.ulen[u - ch.u0];
+      for (int64_t s = b->src_begin[u]; s < b->src_begin[u + 1]; ++s) alg_bytes += 4.0 * b->sig_len[s];
+      alg_bytes += 4.0 * (b->mic_begin[u + 1] - b->mic_begin[u]) * ch.ulen[u - ch.u0];
+    }
+  };
   // ---- the pipeline: synth(k+1) is enqueued before the host plans chunk k -----------
-  if (nch > 0) {
-    status = prep_chunk(b, R.chunks[0]);
-    if (!status) status = enqueue_synth(c, b, R.chunks[0], R.sA);
+  // Device renders synthesize every chunk's RIRs before the first filter (every chunk owns its
+  // buffers): the K1 launches cover the host's planning of chunk 0, and no K1 runs beside the
+  // K4 launches of earlier chunks.  Host renders (PCIe-bound) keep one chunk of look-ahead.
+  static const int ahead_env = [] {
+    const char* e = std::getenv("RSG_SYNTH_AHEAD");  // tuning override (chunks)
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
+  const int ahead = ahead_env ? ahead_env : (host_io ? 1 : std::max(1, nch));
+  const bool serial = c->prof_level >= 2;
+  for (int j = 0; j < nch && j < (serial ? 1 : ahead) && !status; ++j) {
+    status = prep_chunk(b, R.chunks[j]);
+    if (!status) status = enqueue_synth(c, b, R.chunks[j], R.sA);
   }
   for (int k = 0; k < kSigAhead && !status; ++k) status = enqueue_sig(k);
   // Profiling level 2 (the per-size K4 breakdown) serializes the whole render: chunk k+1's
   // synth waits for chunk k's filter, so no K1 runs beside the K4 launches being timed.
-  const bool serial = c->prof_level >= 2;
   for (int k = 0; k < nch && !status; ++k) {
-    if (k + 1 < nch && !serial) {
-      status = prep_chunk(b, R.chunks[k + 1]);
-      if (!status) status = enqueue_synth(c, b, R.chunks[k + 1], R.sA);
+    if (k + ahead < nch && !serial) {
+      status = prep_chunk(b, R.chunks[k + ahead]);
+      if (!status) status = enqueue_synth(c, b, R.chunks[k + ahead], R.sA);
       if (status) break;
     }
     R.hmark("plan wait " + std::to_string(k));
@@ -1546,6 +1607,7 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
     t_plan += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (status) break;
     status = enqueue_filter(c, b, R.chunks[k], io, out_off, out_stride, R.sB, R.sD);
+    if (!status) fill_layouts(R.chunks[k]);  // host work under the chunk's kernels
     if (serial && !status && k + 1 < nch) {
       RS_CUDA(cudaEventRecord(R.chunks[k].ev_out, R.sB));
       RS_CUDA(cudaStreamWaitEvent(R.sA, R.chunks[k].ev_out, 0));
@@ -1578,8 +1640,7 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
   // ---- results, degenerate-power check, timing --------------------------------------
   c->h_plan.clear();
   c->h_pair.clear();
-  R.pair_chunk.assign(Ptot, 0);
-  double flops = 0, bytes = 0, ola_ms = 0, syn_ms = 0, mix_ms = 0;
+  double flops = 0, ola_ms = 0, syn_ms = 0, mix_ms = 0;
   for (int k = 0; k < nch; ++k) {
     Chunk& ch = R.chunks[k];
     flops += ch.fp.flops;
@@ -1592,33 +1653,12 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
       RS_CUDA(cudaEventElapsedTime(&f, ch.ev_mix0, ch.ev_mix1));
       mix_ms += f;
     }
-    for (int64_t p = 0; p < ch.P; ++p) {
-      const int64_t gp = ch.p0 + p;
-      R.pair_chunk[gp] = k;
+    for (int64_t p = 0; p < ch.P; ++p)
       if (ch.h_flags[p] & 4) return fail(RS_ERR_DEGENERATE, "signal has no energy: SNR gain undefined");
-      if (layout) {
-        rs_pair_layout& L = layout[gp];
-        const PairRir& r = ch.h_rir[p];
-        L.rir_len = r.len;
-        L.rir_keep = r.keep;
-        L.cutoff = b->eta_db > 0.0 ? r.cutoff : -1;
-        L.fft_size = int64_t(1) << ch.ref[p].log2n;
-        L.block_len = ch.ref[p].L;
-        L.n_blocks = ch.ref[p].B;
-        L.out_len = ch.plans[p].out_len;
-        L.strategy = ch.strategy[p];
-        L.flags = r.flags;
-      }
-      if (gains) gains[gp] = ch.h_gain[p];
-      if (power) power[gp] = ch.h_power[p];
-      bytes += 4.0 * ch.plans[p].nh;
-    }
-    for (int64_t u = ch.u0; u < ch.u1; ++u) {
-      if (out_len) out_len[u] = ch.ulen[u - ch.u0];
-      for (int64_t s = b->src_begin[u]; s < b->src_begin[u + 1]; ++s) bytes += 4.0 * b->sig_len[s];
-      bytes += 4.0 * (b->mic_begin[u + 1] - b->mic_begin[u]) * ch.ulen[u - ch.u0];
-    }
+    if (gains) std::memcpy(gains + ch.p0, ch.h_gain, ch.P * sizeof(double));
+    if (power) std::memcpy(power + ch.p0, ch.h_power, ch.P * sizeof(double));
   }
+  const double bytes = alg_bytes;
   c->ola_flops = flops;
   c->alg_bytes = bytes;
   c->ola_ms = ola_ms;
@@ -1630,6 +1670,10 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
   c->stage_ms[4] = ola_ms;
   c->stage_ms[5] = mix_ms;
   c->stage_valid = c->profiling;
+  t_last_return = std::chrono::steady_clock::now();
+  if (R.tracing)
+    std::fprintf(stderr, "[trace] host return at %.2f ms\n",
+                 std::chrono::duration<double, std::milli>(t_last_return - R.trace_t0).count());
   return RS_OK;
 }
 

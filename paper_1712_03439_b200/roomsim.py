@@ -426,8 +426,12 @@ class RenderResult:
 
 
 def render_batch(batch, *, ctx: Optional[Context] = None, out: Optional[np.ndarray] = None,
-                 device_signals_ptr: Optional[int] = None, device_out_ptr: Optional[int] = None) -> RenderResult:
+                 device_signals_ptr: Optional[int] = None, device_out_ptr: Optional[int] = None,
+                 result: Optional[RenderResult] = None) -> RenderResult:
     """Render a ``scenes.SceneBatch``.
+
+    ``result``: a RenderResult of an earlier render of a batch of the same shape, whose
+    layout / gain / power arrays are overwritten and returned (no per-call allocation).
 
     Host mode (default): signals/out are host arrays, H2D/D2H inside the call.
     Device mode: pass ``device_signals_ptr`` and ``device_out_ptr`` (e.g. torch
@@ -438,10 +442,13 @@ def render_batch(batch, *, ctx: Optional[Context] = None, out: Optional[np.ndarr
     b, keep = batch.as_struct(RsSceneBatch, signals_ptr=device_signals_ptr)
     out_off = np.ascontiguousarray(batch.out_off, np.int64)
     out_stride = np.ascontiguousarray(batch.out_stride, np.int64)
-    out_len = np.zeros(batch.n_utt, np.int64)
-    layout = np.zeros(batch.n_pairs, LAYOUT_DTYPE)
-    gains = np.zeros(batch.n_pairs)
-    power = np.zeros(batch.n_pairs)
+    if result is not None and result.layout.shape == (batch.n_pairs,) and result.out_len.shape == (batch.n_utt,):
+        out_len, layout, gains, power = result.out_len, result.layout, result.gains, result.power
+    else:
+        out_len = np.zeros(batch.n_utt, np.int64)
+        layout = np.zeros(batch.n_pairs, LAYOUT_DTYPE)
+        gains = np.zeros(batch.n_pairs)
+        power = np.zeros(batch.n_pairs)
     if device:
         assert device_out_ptr is not None
         st = L.rs_render_batch_device(ctx.h, C.byref(b), C.c_void_p(device_out_ptr), _ptr(out_off),
