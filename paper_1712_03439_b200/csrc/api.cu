@@ -392,7 +392,7 @@ double pair_flops(const PairPlan& p) {
 // Pairs are bucketed by (transform size, variant); buckets run largest work first.
 // Each pair's blocks are split into runs (K4 work items) long enough that the
 // recomputed overlap blocks cost <= ~6%, short enough to fill the GPU.
-enum K4Variant { kVarSmall = 0, kVarIp = 1, kVarOla2 = 2, kVarLarge = 3, kVarCount = 4 };
+enum K4Variant { kVarSmall = 0, kVarIp = 1, kVarOla2 = 2, kVarLarge = 3, kVarIpc = 4, kVarCount = 5 };
 
 struct Span {
   int l;
@@ -480,10 +480,37 @@ bool use_ola2(int log2n) {
   // (ncu launch list, B200); elsewhere K4 is as fast or faster
   return log2n == 8;
 }
+// Real FFT sizes (log2 N) that run two blocks per complex transform (ola_ipc_kernel, big.cu)
+// when the pair's carry fits next to the transform (tuning override RSG_IPC="lo,hi"; "0,0"
+// disables it).
+bool use_ipc(int log2n, int64_t nh) {
+  static const std::pair<int, int> r = [] {
+    const char* e = std::getenv("RSG_IPC");
+    int lo = 12, hi = 13;
+    if (e) std::sscanf(e, "%d,%d", &lo, &hi);
+    return std::make_pair(lo, hi);
+  }();
+  if (log2n < r.first || log2n > r.second) return false;
+  static int64_t cache[kLargeMaxLog2M + 2];
+  static bool init = false;
+  if (!init) {
+    for (int k = 0; k <= kLargeMaxLog2M + 1; ++k) {
+      int64_t lo = 0, hi = int64_t(1) << k;  // largest nh with ipc_supported(k, nh)
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (ipc_supported(k, mid)) lo = mid; else hi = mid - 1;
+      }
+      cache[k] = lo;
+    }
+    init = true;
+  }
+  return nh <= cache[log2n];
+}
 constexpr int kSmallMaxLog2MHost = 12;  // ola_small_kernel<M> sizes (kernels.cu)
 int k4_variant(int l, int64_t nh) {
   if (use_large(l)) return kVarLarge;
   if (use_ola2(l + 1)) return kVarOla2;
+  if (use_ipc(l + 1, nh)) return kVarIpc;
   if (use_ip(l, nh)) return kVarIp;
   if (l <= kSmallMaxLog2MHost) return kVarSmall;
   return kVarLarge;  // M >= 8192 whose overlap carry does not fit in shared memory
@@ -549,6 +576,12 @@ int exec_log2n(size_t nx, size_t nh, int ref_log2n) {
 }
 
 constexpr int64_t kLargeScratchBytes = int64_t(1) << 31;  // per batch (16 M bytes per unit)
+
+// float2 entries of a pair's filter region: M + 1 bins, or all N in ola_ipc_kernel's order.
+int64_t spec_len(int log2n, int64_t nh) {
+  const int64_t n = int64_t(1) << log2n;
+  return k4_variant(log2n - 1, nh) == kVarIpc ? n : n / 2 + 1;
+}
 
 // Blocks before a run start whose tails overlap it: ceil((N_h - 1) / L).
 int64_t pre_blocks(const PairPlan& p) {
@@ -676,8 +709,10 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
       fp.lists.insert(fp.lists.end(), v.begin(), v.end());
       continue;
     }
-    const bool ip = var == kVarIp;
-    const int64_t slots = 148LL * (ip ? ip_resident(l, sp.max_nh) : ola_resident_groups(l));
+    const bool ipc = var == kVarIpc;
+    const bool ip = var == kVarIp || ipc;
+    const int64_t slots = 148LL * (ipc ? ipc_resident(l + 1, sp.max_nh)
+                                       : (ip ? ip_resident(l, sp.max_nh) : ola_resident_groups(l)));
     // work items per resident slot (measured, config 4): the in-place K4 prefers long runs
     // (each item stages its filter and twiddles), ola_small<512> too, the M <= 256 sizes
     // more items (shorter tails)
@@ -689,12 +724,12 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
     // the in-place K4 at M >= 8192: a few long blocks per pair — 2-block power segments and
     // runs down to 2 (pre-)blocks, so even a small bucket fills the SMs (each run recomputes
     // its overlap blocks: up to half the work of a 2-block run, paid only where it buys CTAs)
-    const int seg = (ip && l >= 13) ? kPowerSegLarge : kPowerSeg;
-    const int64_t min_run = (ip && l >= 13) ? 2 * max_pre : 16 * max_pre;
+    const int seg = (ip && !ipc && l >= 13) ? kPowerSegLarge : kPowerSeg;
+    const int64_t min_run = (ip && !ipc && l >= 13) ? 2 * max_pre : 16 * max_pre;
     int64_t run = std::max<int64_t>((total_blocks + run_div * slots - 1) / (run_div * slots), min_run);
     run = (run + seg - 1) / seg * seg;  // runs start on power-segment boundaries
     sp.seg = seg;
-    const int ppb = ip ? ip_parts_per_block(l) : small_parts_per_block(l);
+    const int ppb = ipc ? ipc_parts_per_block(l + 1) : (ip ? ip_parts_per_block(l) : small_parts_per_block(l));
     sp.item_off = static_cast<int64_t>(fp.items.size());
     for (int32_t p : v) {
       PairPlan& pl = plans[p];
@@ -704,7 +739,8 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
       part_acc += pl.npart;
       for (int64_t r0 = 0; r0 < pl.B; r0 += run) {
         const int64_t r1 = std::min<int64_t>(pl.B, r0 + run);
-        const int64_t b0 = r0 == 0 ? 0 : std::max<int64_t>(0, r0 - pre);
+        int64_t b0 = r0 == 0 ? 0 : std::max<int64_t>(0, r0 - pre);
+        if (ipc) b0 &= ~int64_t(1);  // blocks 2j and 2j + 1 always share a transform
         fp.items.push_back(OlaItem{p, static_cast<int32_t>(b0), static_cast<int32_t>(r0), static_cast<int32_t>(r1)});
       }
     }
@@ -715,7 +751,7 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
   fp.part_total = part_acc;
   fp.spec_total = fp.y_total = 0;
   for (const auto& q : plans) {
-    fp.spec_total = std::max<int64_t>(fp.spec_total, q.spec_off + (int64_t(1) << (q.log2n - 1)) + 1);
+    fp.spec_total = std::max<int64_t>(fp.spec_total, q.spec_off + spec_len(q.log2n, q.nh));
     fp.y_total = std::max<int64_t>(fp.y_total, q.y_off + q.out_len);
   }
   return RS_OK;
@@ -790,7 +826,7 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
   for (const Span& sp : fp.spans) {
     if (sp.var == kVarLarge) continue;  // spectrum inside the four-step batches
     SpecArgs a{d_lists + sp.list_off, static_cast<int32_t>(sp.list_n), d_pair, fb.plan.as<PairPlan>(),
-               d_rir, fb.spec.as<float2>(), c->tw[sp.l]};
+               d_rir, fb.spec.as<float2>(), c->tw[sp.l], sp.var == kVarIpc ? ipc_perm(sp.l + 1) : IpcPerm{}};
     RS_CUDA(launch_spectrum(sp.l, a, st));
     ++c->launches;
   }
@@ -857,11 +893,13 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
                  static_cast<int32_t>((sp.max_l + 8 + 3) & ~int64_t(3))};
       RS_CUDA(launch_ola2(sp.l + 1, a, side_for()));
       ++c->launches;
-    } else if (sp.var == kVarSmall || sp.var == kVarIp) {
+    } else if (sp.var == kVarSmall || sp.var == kVarIp || sp.var == kVarIpc) {
       OlaArgs a{fb.olaitems.as<OlaItem>() + sp.item_off, static_cast<int32_t>(sp.item_n), d_pair,
                 fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(), d_part, c->tw[sp.l],
                 sp.seg};
-      if (sp.var == kVarIp)
+      if (sp.var == kVarIpc)
+        RS_CUDA(launch_ola_ipc(sp.l + 1, a, sp.max_nh, side_for()));
+      else if (sp.var == kVarIp)
         RS_CUDA(launch_ola_ip(sp.l, a, sp.max_nh, side_for()));
       else
         RS_CUDA(launch_ola(sp.l, a, side_for()));
@@ -1267,7 +1305,7 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
     pl.out_len = static_cast<int64_t>(nx + nh - 1);
     pl.spec_off = spec_off;
     pl.y_off = y_off;
-    spec_off += static_cast<int64_t>(n / 2 + 1);
+    spec_off += spec_len(pl.log2n, pl.nh);
     y_off += (pl.out_len + 3) & ~int64_t(3);  // 16-byte aligned rows: K6 reads float4
     int64_t& ul = ch.ulen[ch.pair[p].utt];
     ul = std::max(ul, pl.out_len);

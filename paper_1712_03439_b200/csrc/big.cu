@@ -415,6 +415,221 @@ cudaError_t ip_t(const OlaArgs& a, int ccap, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+
+// ============================================================================
+// K4 "two blocks per transform" (ola_ipc_kernel<C>): consecutive OLA blocks 2j and 2j + 1
+// of one pair ride one C = N point COMPLEX transform, z = x_a + i x_b.  h is real, so
+// IFFT(FFT(z) H) = (x_a * h) + i (x_b * h): no untangle / repack step, and the product
+// with H is pointwise — it runs in registers between the last forward pass (stride 1)
+// and the first inverse pass, which share one butterfly's slots.  Per block that is 4
+// reads + 4 writes of N/2 complex in shared memory against 6 + 6 (plus the filter and
+// the pairing table through L1) in ola_ip_kernel<N/2>, which is shared-memory bound.
+// The filter is read from Gp, K3's copy of H / N over all N bins in the order the
+// butterflies want it: Gp[r * (C / R) + u] is the bin of element r of the last pass's
+// butterfly u (IpcPerm), so a warp's loads are contiguous.  Block 2j always pairs with
+// block 2j + 1 (zero past the pair's last block): which blocks share a transform
+// depends on the pair only, whatever the run split (render invariance).
+// Reference: convolve_ola, convolution.hpp:219-255; mean_power, audio_buffer.hpp:66-75.
+// ============================================================================
+#ifndef RSG_IPC_MINB_4096
+#define RSG_IPC_MINB_4096 3
+#endif
+#ifndef RSG_IPC_MINB_8192
+#define RSG_IPC_MINB_8192 2
+#endif
+template <int C>
+struct IpcPlan;
+template <>
+struct IpcPlan<4096> {
+  static constexpr int NP = 3, T = 256, MINB = RSG_IPC_MINB_4096, LS0 = 8;
+  static constexpr bool GS = false;
+  __host__ __device__ static constexpr int radix(int) { return 16; }
+};
+template <>
+struct IpcPlan<8192> {
+  static constexpr int NP = 3, T = 256, MINB = RSG_IPC_MINB_8192, LS0 = 8;
+  static constexpr bool GS = false;
+  __host__ __device__ static constexpr int radix(int p) { return p == 0 ? 32 : 16; }
+};
+
+template <class PL, int C, int P>
+__device__ __forceinline__ void ipc_forward_mid(float2* s, const float2* tws, int t) {
+  if constexpr (P < PL::NP - 1) {
+    ip_pass<PL, C, P, false>(s, tws, t);
+    __syncthreads();
+    ipc_forward_mid<PL, C, P + 1>(s, tws, t);
+  }
+}
+template <class PL, int C, int P>
+__device__ __forceinline__ void ipc_inverse_mid(float2* s, const float2* tws, int t) {
+  if constexpr (P >= 1) {
+    ip_pass<PL, C, P, true>(s, tws, t);
+    __syncthreads();
+    ipc_inverse_mid<PL, C, P - 1>(s, tws, t);
+  }
+}
+
+template <int C>
+__global__ void __launch_bounds__(IpcPlan<C>::T, IpcPlan<C>::MINB) ola_ipc_kernel(OlaArgs a, int ccap) {
+  using PL = IpcPlan<C>;
+  using SH = IpShape<PL, C>;
+  constexpr int T = PL::T;
+  constexpr int R0 = PL::radix(0), S0 = SH::stride(0);
+  constexpr int RL = PL::radix(PL::NP - 1), NBL = C / (RL * T);  // last pass: stride 1
+  static_assert(S0 == T, "passes 0 (forward) and 0 (inverse): one butterfly per thread");
+  static_assert(SH::stride(PL::NP - 1) == 1 && RL == 16 && NBL >= 1, "last pass shape");
+  extern __shared__ __align__(16) float2 smem[];
+  float2* s = smem;
+  float2* tws = smem + SH::SLOTS;
+  float* carry = reinterpret_cast<float*>(tws + ((SH::TWN + 1) & ~1));
+  const int t = threadIdx.x;
+  const OlaItem it = a.items[blockIdx.x];
+  const PairPlan& pl = a.plan[it.pair];
+  const PairMeta& pm = a.pair[it.pair];
+  const float* __restrict__ x = a.signals + pm.sig_off;
+  const long long nx = pm.nx;
+  const float2* __restrict__ Gp = a.spec + pl.spec_off;
+  float* __restrict__ y = a.y + pl.y_off;
+  const int L = static_cast<int>(pl.L);
+  const int B = static_cast<int>(pl.B);
+  const int ovl = C - L;  // N_h - 1 <= ccap
+  const long long own_lo = static_cast<long long>(it.b_own) * L;
+  const long long own_hi = it.b_end == B ? pl.out_len : static_cast<long long>(it.b_end) * L;
+  for (int i = t; i < SH::TWN; i += T) {  // twiddle bases, FP64 sincospi rounded once
+    int p = 0;
+#pragma unroll
+    for (int q = 1; q < PL::NP - 1; ++q)
+      if (i >= SH::tw_off(q)) p = q;
+    const int j = i - SH::tw_off(p);
+    const int span = PL::radix(p) * SH::stride(p);
+    double sn, cs;
+    sincospi(-2.0 * j / span, &sn, &cs);
+    tws[i] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
+  }
+  for (int i = t; i < ovl; i += T) carry[i] = 0.f;
+  if (t == 0) {  // the pair's filter and the run's first two blocks
+    prefetch_l2(Gp, C * sizeof(float2));
+    const long long s0 = static_cast<long long>(it.b_begin) * L;
+    prefetch_l2(x + s0, 4 * (nx - s0 < 2 * L ? nx - s0 : 2 * L));
+  }
+  __syncthreads();
+  double pw = 0.0;  // this lane's Σ y² of the current power segment
+  const int wt = t & ~31;
+#pragma unroll 1
+  for (int b = it.b_begin; b < it.b_end; b += 2) {  // b even: blocks b (real part) and b + 1 (imaginary)
+    const long long start = static_cast<long long>(b) * L;
+    const int take_a = static_cast<int>(nx - start < L ? nx - start : L);
+    const bool has_b = b + 1 < it.b_end;  // false only past the pair's last block
+    const long long rem_b = nx - start - L;
+    const int take_b = has_b ? static_cast<int>(rem_b < 0 ? 0 : (rem_b < L ? rem_b : L)) : 0;
+    const float* xa = x + start;
+    const float* xb = xa + L;
+    if (t == 0 && b + 2 < it.b_end) {  // the next two blocks land in L2 during this transform
+      const long long s1 = start + 2 * static_cast<long long>(L);
+      if (s1 < nx) prefetch_l2(x + s1, 4 * (nx - s1 < 2 * L ? nx - s1 : 2 * L));
+    }
+    {  // forward pass 0 (S_0 = T): z[t + S_0 r] = x_a + i x_b from the signal, zero past the blocks
+      float2 v[R0];
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int n = t + S0 * r, w1 = wt + S0 * r + 32;
+        if (w1 <= take_a && w1 <= take_b) {  // warp-uniform: all 32 samples of both blocks exist
+          v[r].x = __ldg(xa + n);
+          v[r].y = __ldg(xb + n);
+        } else {
+          v[r].x = n < take_a ? __ldg(xa + n) : 0.f;
+          v[r].y = n < take_b ? __ldg(xb + n) : 0.f;
+        }
+      }
+      Dft<R0, false>::run(v);
+      apply_twiddles<R0, false>(v, tws[t]);
+#pragma unroll
+      for (int r = 0; r < R0; ++r) s[ipad<PL>(t) + ip_off<PL, R0, S0, C>(r)] = v[r];
+    }
+    __syncthreads();
+    ipc_forward_mid<PL, C, 1>(s, tws, t);
+    // last forward pass, x H / N, first inverse pass: one butterfly's slots, in registers
+#pragma unroll
+    for (int q = 0; q < NBL; ++q) {
+      const int u = t + q * T;
+      const int pb = ipad<PL>(u * RL);
+      float2 v[RL];
+#pragma unroll
+      for (int r = 0; r < RL; ++r) v[r] = s[pb + ip_off<PL, RL, 1, C>(r)];
+      Dft<RL, false>::run(v);
+#pragma unroll
+      for (int r = 0; r < RL; ++r) v[r] = c_mul(v[r], ld_tw(Gp + r * (C / RL) + u));
+      Dft<RL, true>::run(v);
+#pragma unroll
+      for (int r = 0; r < RL; ++r) s[pb + ip_off<PL, RL, 1, C>(r)] = v[r];
+    }
+    __syncthreads();
+    ipc_inverse_mid<PL, C, PL::NP - 2>(s, tws, t);
+    // inverse pass 0: outputs e = t + S_0 r in registers (.x: block b, .y: block b + 1)
+    float2 v[R0];
+#pragma unroll
+    for (int r = 0; r < R0; ++r) v[r] = s[ipad<PL>(t) + ip_off<PL, R0, S0, C>(r)];
+    apply_twiddles<R0, true>(v, tws[t]);
+    Dft<R0, true>::run(v);
+    // emit block b, then block b + 1 (its head overlaps block b's tail through the carry)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && !has_b) break;
+      const int bb = b + h;
+      const long long st = start + static_cast<long long>(h) * L;
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int e = t + S0 * r;
+        if (e < ovl) (h ? v[r].y : v[r].x) += carry[e];
+      }
+      __syncthreads();  // carry reads (and this transform's smem reads) are done
+      const int lo = static_cast<int>(max(own_lo - st, -1ll));
+      const int hi = static_cast<int>(min(own_hi - st, static_cast<long long>(C)));
+      const int fe = bb == B - 1 ? C : L;  // e < fe: final after this block
+      float* yb = y + st;
+      float p0 = 0.f, p1 = 0.f;
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int e = t + S0 * r;
+        const float val = h ? v[r].y : v[r].x;
+        if (e < fe) {
+          if (e >= lo && e < hi) {
+            yb[e] = val;
+            if (r & 1) p1 = fmaf(val, val, p1); else p0 = fmaf(val, val, p0);
+          }
+        } else {
+          carry[e - L] = val;
+        }
+      }
+      pw += static_cast<double>(p0 + p1);
+      if (closes_segment(bb, it.b_end, a.seg)) {
+        const long long part0 = __ldg(&a.plan[it.pair].part0);
+        store_segment_power<T>(a.part + part0 + static_cast<long long>(bb / a.seg) * parts_per_block_of(T), pw, t,
+                               bb >= it.b_own);
+        pw = 0.0;
+      }
+      __syncthreads();  // carry writes land before the next block reads them
+    }
+  }
+}
+
+template <int C>
+size_t ipc_smem(int ccap) {
+  using SH = IpShape<IpcPlan<C>, C>;
+  return (static_cast<size_t>(SH::SLOTS) + ((SH::TWN + 1) & ~1)) * sizeof(float2) +
+         static_cast<size_t>(ccap) * sizeof(float);
+}
+
+template <int C>
+cudaError_t ipc_t(const OlaArgs& a, int ccap, cudaStream_t st) {
+  const size_t smem = ipc_smem<C>(ccap);
+  cudaError_t e = cudaFuncSetAttribute(ola_ipc_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  ola_ipc_kernel<C><<<a.count, IpcPlan<C>::T, smem, st>>>(a, ccap);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 #define RSG_IP_DISPATCH(L, CALL)                     \
@@ -467,6 +682,61 @@ int ip_parts_per_block(int log2m) {
 cudaError_t launch_ola_ip(int log2m, const OlaArgs& a, int64_t max_nh, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   RSG_IP_DISPATCH(log2m, ip_t<M>(a, ccap_of(max_nh), s))
+  return cudaErrorInvalidValue;
+}
+
+
+// ---- two blocks per transform (ola_ipc_kernel<C>, C = N) --------------------------------
+#define RSG_IPC_DISPATCH(LN, CALL)                   \
+  switch (LN) {                                      \
+    case 12: { constexpr int C = 4096; return CALL; } \
+    case 13: { constexpr int C = 8192; return CALL; } \
+  }
+namespace {
+size_t ipc_smem_of(int log2n, int ccap) {
+  RSG_IPC_DISPATCH(log2n, ipc_smem<C>(ccap))
+  return 0;
+}
+int ipc_minb_of(int log2n) {
+  RSG_IPC_DISPATCH(log2n, IpcPlan<C>::MINB)
+  return 1;
+}
+int ipc_threads_of(int log2n) {
+  RSG_IPC_DISPATCH(log2n, IpcPlan<C>::T)
+  return 0;
+}
+template <int C>
+IpcPerm ipc_perm_t() {
+  using PL = IpcPlan<C>;
+  auto lg = [](int v) { int l = 0; while ((1 << l) < v) ++l; return l; };
+  return IpcPerm{1, lg(PL::radix(0)), lg(PL::radix(1)), lg(PL::radix(2)), lg(C)};
+}
+}  // namespace
+
+bool ipc_supported(int log2n, int64_t max_nh) {
+  if (ipc_threads_of(log2n) == 0) return false;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return ipc_smem_of(log2n, ccap_of(max_nh)) + 1024 <= static_cast<size_t>(optin);
+}
+int ipc_resident(int log2n, int64_t max_nh) {
+  const size_t need = ipc_smem_of(log2n, ccap_of(max_nh)) + 1024;
+  const int by_smem = static_cast<int>((228 * 1024) / need);
+  const int by_threads = 2048 / ipc_threads_of(log2n);
+  return std::max(1, std::min(std::min(by_smem, by_threads), ipc_minb_of(log2n)));
+}
+int ipc_parts_per_block(int log2n) {
+  RSG_IPC_DISPATCH(log2n, parts_per_block_of(IpcPlan<C>::T))
+  return 0;
+}
+IpcPerm ipc_perm(int log2n) {
+  RSG_IPC_DISPATCH(log2n, ipc_perm_t<C>())
+  return IpcPerm{};
+}
+cudaError_t launch_ola_ipc(int log2n, const OlaArgs& a, int64_t max_nh, cudaStream_t s) {
+  if (a.count == 0) return cudaSuccess;
+  RSG_IPC_DISPATCH(log2n, ipc_t<C>(a, ccap_of(max_nh), s))
   return cudaErrorInvalidValue;
 }
 

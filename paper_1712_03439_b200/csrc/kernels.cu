@@ -535,7 +535,13 @@ __global__ void __launch_bounds__(cta_threads_of(Plan<M>::LOG)) rir_spectrum_ker
       const float2 S = c_add(za, zb);
       const float2 D = c_rot<false>(c_sub(za, zb));
       const float2 X2 = c_add(S, c_mul(pair_twiddle<M>(W, k), D));
-      out[k] = c_scale(X2, scale);
+      if (a.perm.on) {  // H / N over all N bins (H(N - k) = conj H(k)), ola_ipc_kernel's order
+        const float2 g = c_scale(X2, 2.0f * scale);
+        out[a.perm.index(k)] = g;
+        if (k != 0 && k != M) out[a.perm.index(2 * M - k)] = c_conj(g);
+      } else {
+        out[k] = c_scale(X2, scale);
+      }
     }
   }
 }

@@ -90,6 +90,19 @@ struct CutArgs {
   double eta_factor;  // pow(10, -eta/10), host std::pow; <= 0: no truncation
 };
 
+// Filter layout of the two-blocks-per-transform K4 (big.cu, ola_ipc_kernel<C>): all C = N
+// bins of H / N, bin k at r * (C / R2) + u with slot(k) = (k mod R0) S0 + ((k / R0) mod R1) S1 +
+// k / (R0 R1) (the in-place transform's digit-reversed slot), u = slot / R2, r = slot mod R2.
+struct IpcPerm {
+  int32_t on = 0;
+  int32_t lr0 = 0, lr1 = 0, lr2 = 0, lc = 0;  // log2 of the radices and of C
+  __host__ __device__ int index(int k) const {
+    const int slot = ((k & ((1 << lr0) - 1)) << (lr1 + lr2)) | (((k >> lr0) & ((1 << lr1) - 1)) << lr2) |
+                     (k >> (lr0 + lr1));
+    return ((slot & ((1 << lr2) - 1)) << (lc - lr2)) | (slot >> lr2);
+  }
+};
+
 struct SpecArgs {
   const int32_t* list;  // pairs of this FFT size
   int32_t count;
@@ -98,6 +111,7 @@ struct SpecArgs {
   const double* rir;
   float2* spec;
   const float2* tw;     // twiddle tables of this M
+  IpcPerm perm;         // on: write H / N over all N bins in ola_ipc_kernel's order
 };
 
 struct OlaArgs {
@@ -250,6 +264,13 @@ int ola2_parts_per_block(int log2n);   // ola2_kernel<N> (per run's block)
 bool ip_supported(int log2m, int64_t max_nh);
 int ip_resident(int log2m, int64_t max_nh);  // CTAs (work items) resident per SM
 cudaError_t launch_ola_ip(int log2m, const OlaArgs& a, int64_t max_nh, cudaStream_t s);
+
+// Two blocks per complex transform (big.cu), N = 4096, 8192; the filter region holds N bins.
+bool ipc_supported(int log2n, int64_t max_nh);
+int ipc_resident(int log2n, int64_t max_nh);
+int ipc_parts_per_block(int log2n);
+IpcPerm ipc_perm(int log2n);
+cudaError_t launch_ola_ipc(int log2n, const OlaArgs& a, int64_t max_nh, cudaStream_t s);
 
 constexpr int kMaxLog2M = 14;  // M <= 16384  (N <= 32768) in one CTA
 int cta_threads(int log2m);

@@ -270,7 +270,7 @@ class Context:
         breakdown (K4 launches serialized — a diagnostic render, not a timed one)."""
         _check(load_library().rs_ctx_set_profiling(self.h, int(on)))
 
-    K4_VARIANTS = ("ola_small", "ola_ip", "ola2", "four_step")
+    K4_VARIANTS = ("ola_small", "ola_ip", "ola2", "four_step", "ola_ipc")
 
     def k4_breakdown(self) -> list:
         """Rows of the last render at profiling level 2: N, variant, pairs, flops, ms."""

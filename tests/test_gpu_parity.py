@@ -216,6 +216,52 @@ def test_k4_variants(env, sizes):
     assert float(r.stdout.strip().splitlines()[-1]) <= WAVE_TOL
 
 
+@pytest.mark.parametrize("n", [4096, 8192])
+def test_two_blocks_per_transform_k4(rs, ctx, port, n):
+    """ola_ipc_kernel (big.cu): blocks 2j and 2j + 1 of a pair share one complex N-point
+    transform.  Odd and even block counts, one block, N_h from 1 to the largest carry that
+    fits, signals that end inside the first / second block of a transform, and runs long
+    enough to be split into several work items (recomputed overlap blocks)."""
+    rng = np.random.default_rng(n)
+    for nh in (1, 2, 57, n // 8 + 1, n // 4 + 3, n // 2, n // 2 + 401):
+        L = n - nh + 1
+        for nx in (1, L - 1, L, L + 1, 2 * L, 2 * L + 1, 3 * L - 5, 7 * L + 13, 150 * L + 77):
+            x, h = rng.standard_normal(nx), rng.standard_normal(nh) * np.exp(-np.arange(nh) / max(nh / 4, 1))
+            want = port.convolve_ola(x, h, n)
+            got = rs.convolve_ola(x, h, n, ctx=ctx)
+            assert got.shape == want.shape
+            assert rel_err(got, want) <= WAVE_TOL, (n, nh, nx)
+
+
+@pytest.mark.parametrize("env", [{"RSG_IPC": "0,0"}, {"RSG_REBLOCK": "0"}, {"RSG_REBLOCK": "0", "RSG_IPC": "0,0"}])
+def test_render_with_reference_blocking_and_without_ipc(env):
+    """The render with the executed block size = the reference's plan (RSG_REBLOCK=0) and
+    with the two-blocks-per-transform K4 off (RSG_IPC=0,0), in fresh processes: both
+    against the reference port, and identical layouts."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import numpy as np, oracle\n"
+        "from paper_1712_03439_b200 import roomsim as rs, scenes\n"
+        "ctx = rs.Context(0); port = oracle.port(); worst = 0.0\n"
+        "for b in (scenes.config4(n_utt=6, seed=41), scenes.config3(n_utt=4, seed=42), scenes.config2(n_utt=2, seed=43)):\n"
+        "    g = rs.render_batch(b, ctx=ctx); o = port.render_batch(b, threads=8)\n"
+        "    for f in ('rir_keep', 'cutoff', 'fft_size', 'block_len', 'n_blocks'):\n"
+        "        assert (g.layout[f] == o[2][f]).all(), f\n"
+        "    assert np.allclose(g.gains, o[3], rtol=1e-5); assert np.allclose(g.power, o[4], rtol=1e-5)\n"
+        "    for u in range(b.n_utt):\n"
+        "        for j in range(int(b.mic_begin[u + 1] - b.mic_begin[u])):\n"
+        "            a_ = b.channel(g.out, u, j, g.out_len[u]); w_ = b.channel(o[0], u, j, o[1][u])\n"
+        "            worst = max(worst, float(np.abs(a_ - w_).max() / np.abs(w_).max()))\n"
+        "print(worst)\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= WAVE_TOL
+
+
 def test_four_step_path_small_sizes(tmp_path):
     """Route every size >= 2^7 through the four-step path (RSG_LARGE_MIN) in a fresh
     process and check it against the oracle at sizes where K4 normally runs."""
