@@ -33,6 +33,7 @@
 // k -> digit-reversed slot, which moves by S_0 per k) is bank-conflict free on 64-bit
 // accesses.
 #include <cmath>
+#include <cstdlib>
 
 #include "fft.cuh"
 #include "kernels.cuh"
@@ -469,8 +470,8 @@ __device__ __forceinline__ void ipc_inverse_mid(float2* s, const float2* tws, in
   }
 }
 
-template <int C>
-__global__ void __launch_bounds__(IpcPlan<C>::T, IpcPlan<C>::MINB) ola_ipc_kernel(OlaArgs a, int ccap) {
+template <int C, int MINB = IpcPlan<C>::MINB>
+__global__ void __launch_bounds__(IpcPlan<C>::T, MINB) ola_ipc_kernel(OlaArgs a, int ccap) {
   using PL = IpcPlan<C>;
   using SH = IpShape<PL, C>;
   constexpr int T = PL::T;
@@ -514,7 +515,6 @@ __global__ void __launch_bounds__(IpcPlan<C>::T, IpcPlan<C>::MINB) ola_ipc_kerne
   }
   __syncthreads();
   double pw = 0.0;  // this lane's Σ y² of the current power segment
-  const int wt = t & ~31;
 #pragma unroll 1
   for (int b = it.b_begin; b < it.b_end; b += 2) {  // b even: blocks b (real part) and b + 1 (imaginary)
     const long long start = static_cast<long long>(b) * L;
@@ -530,16 +530,11 @@ __global__ void __launch_bounds__(IpcPlan<C>::T, IpcPlan<C>::MINB) ola_ipc_kerne
     }
     {  // forward pass 0 (S_0 = T): z[t + S_0 r] = x_a + i x_b from the signal, zero past the blocks
       float2 v[R0];
+      const int ra = take_a - t, rb = take_b - t;
 #pragma unroll
-      for (int r = 0; r < R0; ++r) {
-        const int n = t + S0 * r, w1 = wt + S0 * r + 32;
-        if (w1 <= take_a && w1 <= take_b) {  // warp-uniform: all 32 samples of both blocks exist
-          v[r].x = __ldg(xa + n);
-          v[r].y = __ldg(xb + n);
-        } else {
-          v[r].x = n < take_a ? __ldg(xa + n) : 0.f;
-          v[r].y = n < take_b ? __ldg(xb + n) : 0.f;
-        }
+      for (int r = 0; r < R0; ++r) {  // predicated loads: S_0 r < take - t
+        v[r].x = S0 * r < ra ? __ldg(xa + t + S0 * r) : 0.f;
+        v[r].y = S0 * r < rb ? __ldg(xb + t + S0 * r) : 0.f;
       }
       Dft<R0, false>::run(v);
       apply_twiddles<R0, false>(v, tws[t]);
@@ -577,28 +572,28 @@ __global__ void __launch_bounds__(IpcPlan<C>::T, IpcPlan<C>::MINB) ola_ipc_kerne
       if (h == 1 && !has_b) break;
       const int bb = b + h;
       const long long st = start + static_cast<long long>(h) * L;
+      const int ovl_t = ovl - t;
 #pragma unroll
-      for (int r = 0; r < R0; ++r) {
-        const int e = t + S0 * r;
-        if (e < ovl) (h ? v[r].y : v[r].x) += carry[e];
-      }
+      for (int r = 0; r < R0; ++r)
+        if (S0 * r < ovl_t) (h ? v[r].y : v[r].x) += carry[t + S0 * r];
       __syncthreads();  // carry reads (and this transform's smem reads) are done
       const int lo = static_cast<int>(max(own_lo - st, -1ll));
       const int hi = static_cast<int>(min(own_hi - st, static_cast<long long>(C)));
       const int fe = bb == B - 1 ? C : L;  // e < fe: final after this block
-      float* yb = y + st;
+      float* yb = y + st + t;
+      float* cb = carry + t - L;
       float p0 = 0.f, p1 = 0.f;
+      const int fe_t = fe - t, lo_t = lo - t, hi_t = hi - t;
 #pragma unroll
       for (int r = 0; r < R0; ++r) {
-        const int e = t + S0 * r;
         const float val = h ? v[r].y : v[r].x;
-        if (e < fe) {
-          if (e >= lo && e < hi) {
-            yb[e] = val;
+        if (S0 * r < fe_t) {
+          if (S0 * r >= lo_t && S0 * r < hi_t) {
+            yb[S0 * r] = val;
             if (r & 1) p1 = fmaf(val, val, p1); else p0 = fmaf(val, val, p0);
           }
         } else {
-          carry[e - L] = val;
+          cb[S0 * r] = val;
         }
       }
       pw += static_cast<double>(p0 + p1);
@@ -623,6 +618,14 @@ size_t ipc_smem(int ccap) {
 template <int C>
 cudaError_t ipc_t(const OlaArgs& a, int ccap, cudaStream_t st) {
   const size_t smem = ipc_smem<C>(ccap);
+  static const int minb_env = [] { const char* e = std::getenv("RSG_IPC_MINB"); return e ? std::atoi(e) : 0; }();
+  if (minb_env == IpcPlan<C>::MINB + 1) {  // A/B: one more CTA per SM
+    cudaError_t e = cudaFuncSetAttribute(ola_ipc_kernel<C, IpcPlan<C>::MINB + 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    ola_ipc_kernel<C, IpcPlan<C>::MINB + 1><<<a.count, IpcPlan<C>::T, smem, st>>>(a, ccap);
+    return cudaGetLastError();
+  }
   cudaError_t e = cudaFuncSetAttribute(ola_ipc_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -698,7 +701,8 @@ size_t ipc_smem_of(int log2n, int ccap) {
   return 0;
 }
 int ipc_minb_of(int log2n) {
-  RSG_IPC_DISPATCH(log2n, IpcPlan<C>::MINB)
+  static const int minb_env = [] { const char* e = std::getenv("RSG_IPC_MINB"); return e ? std::atoi(e) : 0; }();
+  RSG_IPC_DISPATCH(log2n, (minb_env == IpcPlan<C>::MINB + 1 ? minb_env : IpcPlan<C>::MINB))
   return 1;
 }
 int ipc_threads_of(int log2n) {
