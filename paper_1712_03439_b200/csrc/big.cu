@@ -470,8 +470,8 @@ __device__ __forceinline__ void ipc_inverse_mid(float2* s, const float2* tws, in
   }
 }
 
-template <int C, int MINB = IpcPlan<C>::MINB>
-__global__ void __launch_bounds__(IpcPlan<C>::T, MINB) ola_ipc_kernel(OlaArgs a, int ccap) {
+template <int C>
+__global__ void __launch_bounds__(IpcPlan<C>::T, IpcPlan<C>::MINB) ola_ipc_kernel(OlaArgs a, int ccap) {
   using PL = IpcPlan<C>;
   using SH = IpShape<PL, C>;
   constexpr int T = PL::T;
@@ -618,14 +618,6 @@ size_t ipc_smem(int ccap) {
 template <int C>
 cudaError_t ipc_t(const OlaArgs& a, int ccap, cudaStream_t st) {
   const size_t smem = ipc_smem<C>(ccap);
-  static const int minb_env = [] { const char* e = std::getenv("RSG_IPC_MINB"); return e ? std::atoi(e) : 0; }();
-  if (minb_env == IpcPlan<C>::MINB + 1) {  // A/B: one more CTA per SM
-    cudaError_t e = cudaFuncSetAttribute(ola_ipc_kernel<C, IpcPlan<C>::MINB + 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    ola_ipc_kernel<C, IpcPlan<C>::MINB + 1><<<a.count, IpcPlan<C>::T, smem, st>>>(a, ccap);
-    return cudaGetLastError();
-  }
   cudaError_t e = cudaFuncSetAttribute(ola_ipc_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -701,8 +693,7 @@ size_t ipc_smem_of(int log2n, int ccap) {
   return 0;
 }
 int ipc_minb_of(int log2n) {
-  static const int minb_env = [] { const char* e = std::getenv("RSG_IPC_MINB"); return e ? std::atoi(e) : 0; }();
-  RSG_IPC_DISPATCH(log2n, (minb_env == IpcPlan<C>::MINB + 1 ? minb_env : IpcPlan<C>::MINB))
+  RSG_IPC_DISPATCH(log2n, IpcPlan<C>::MINB)
   return 1;
 }
 int ipc_threads_of(int log2n) {
