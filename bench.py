@@ -449,25 +449,40 @@ def ours(args, rank, world, local_rank):
             traffic, traffic_src = tj["dram_bytes_per_render"], tj["source"] + "; " + tj["note"]
     except Exception:
         pass
+    ser = None
     if k4_sizes:
         for r in k4_sizes:
             r["tflops"] = r["flops"] / (r["ms"] / 1e3) / 1e12 if r["ms"] > 0 else None
             r["frac"] = r["tflops"] / fp32_peak if r["tflops"] else None
+            r["exec_frac"] = r["exec_flops"] / (r["ms"] / 1e3) / 1e12 / fp32_peak if r["ms"] > 0 else None
+        ms_ser = sum(r["ms"] for r in k4_sizes)
+        if ms_ser > 0:
+            ser = {"ms": ms_ser,
+                   "frac": sum(r["flops"] for r in k4_sizes) / (ms_ser / 1e3) / 1e12 / fp32_peak,
+                   "exec_frac": sum(r["exec_flops"] for r in k4_sizes) / (ms_ser / 1e3) / 1e12 / fp32_peak}
     roofline = {
         "bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
         "frac": achieved / fp32_peak if achieved else None, "traffic": traffic,
         "traffic_unit": "DRAM bytes per step (all K4 launches)", "traffic_source": traffic_src,
-        "kernel": "K4 (ola_small_kernel<M>, ola_ip_kernel<M>, ola2_kernel<N>, four-step stages), all FFT sizes of one render",
+        "kernel": "K4 (ola_ipc_kernel<N>, ola_ip_kernel<M>, ola_small_kernel<M>, ola2_kernel<N>, four-step stages), "
+                  "all FFT sizes of one render",
         "ola_ms_per_step": ola_ms / args.steps,
         "alg_flops_per_step": per_step_flops,
         "alg_bytes_per_step": alg_bytes,
         "hbm_time_ms": alg_bytes / (hbm * 1e9) * 1e3,
         "peak_source": f"derived: {props.multi_processor_count} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz "
                        "(sm_max_mhz of MEASURED_PEAKS.json); FFT flops = 5 N log2 N per real transform",
+        "flops_note": "achieved / frac count the REFERENCE plan's flops, (2B+1) 5 N log2 N with N = the "
+                      "reference's FFT size (SURVEY.md 8d); the device executes each pair's overlap-add at the "
+                      "block size that minimises its modelled time (DESIGN.md 4: re-blocking), reported as "
+                      "exec_flops / exec_frac per executed size in by_size",
+        "serialized": ser,
         "by_size": k4_sizes,
-        "by_size_note": "one extra render with the K4 launches serialized, each timed with CUDA events "
-                        "(algorithmic flops of its pairs / its time); the headline frac is the concurrent "
-                        "launches' aggregate",
+        "by_size_note": "one extra render with the K4 launches serialized, each timed with CUDA events; rows "
+                        "are keyed by the EXECUTED fft_size; `frac` = the rows' reference-plan flops / time / "
+                        "peak, `exec_frac` = the executed plan's; the headline frac is the timed region's "
+                        "concurrent launches (K4 event windows per chunk, which also see the tail of the "
+                        "first chunks' K1 on the other stream); `serialized` sums the rows",
     }
 
     cpu, parity = None, None

@@ -77,12 +77,14 @@ int rs_ctx_stage_times(rs_ctx* ctx, double* ms, int n, double* host_plan_ms);
  * (diagnostic) also serializes the K4 launches of each chunk on one stream and times
  * every (FFT size, kernel variant) span separately: rs_ctx_k4_breakdown. */
 int rs_ctx_set_profiling(rs_ctx* ctx, int enabled);
-/* Per-(log2 N, variant) rows of the last render at profiling level 2 (variant: 0
- * ola_small_kernel, 1 in-place ola_ip_kernel, 2 two-stream ola2_kernel, 3 four-step):
- * pairs, algorithmic FFT flops ((2B+1) 5 N log2 N per pair) and device ms.  Returns the
- * row count (rows beyond `cap` are not written); negative on error. */
+/* Per-(executed log2 N, variant) rows of the last render at profiling level 2 (variant: 0
+ * ola_small_kernel, 1 in-place ola_ip_kernel, 2 two-stream ola2_kernel, 3 four-step, 4 two
+ * blocks per transform ola_ipc_kernel): pairs, algorithmic FFT flops ((2B+1) 5 N log2 N per
+ * pair, N and B of the REFERENCE's plan), device ms, and the same formula on the plan the
+ * device executed (batched renders re-block).  Returns the row count (rows
+ * beyond `cap` are not written); negative on error. */
 int rs_ctx_k4_breakdown(rs_ctx* ctx, int cap, int32_t* log2n, int32_t* variant, int64_t* pairs,
-                        double* flops, double* ms);
+                        double* flops, double* ms, double* exec_flops);
 
 /* ---- host-side planner (convolution.hpp:72-161), exact FP64 mirror -------- */
 double rs_cost_direct(double num_sources, double num_mics, size_t nx, size_t nh);

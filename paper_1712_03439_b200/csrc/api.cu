@@ -316,11 +316,11 @@ struct rs_ctx {
   // profiling level 2: K4 launches serialized on the filter stream, one event pair per
   // (size, variant) span; rows of the last render, merged by (log2 N, variant)
   int prof_level = 0;
-  struct K4Span { int log2n, var; int64_t pairs; double flops; cudaEvent_t a, b; };
+  struct K4Span { int log2n, var; int64_t pairs; double flops, exec_flops; cudaEvent_t a, b; };
   std::vector<K4Span> k4_spans;      // this render's spans (events pending)
   std::vector<cudaEvent_t> ev_pool;  // reusable events
   size_t ev_used = 0;
-  struct K4Row { int log2n, var; int64_t pairs; double flops, ms; };
+  struct K4Row { int log2n, var; int64_t pairs; double flops, ms, exec_flops; };
   std::vector<K4Row> k4_rows;
   cudaEvent_t pool_event() {
     if (ev_used == ev_pool.size()) {
@@ -537,7 +537,7 @@ const ReblockCfg& reblock_cfg() {
     ReblockCfg c;
     for (double& e : c.eff) e = 0.12;  // four-step sizes
     //            N =   2     4     8     16    32     64     128    256   512   1024  2048   4096   8192  16384 32768
-    const double m[] = {0.01, 0.01, 0.01, 0.02, 0.075, 0.117, 0.194, 0.24, 0.43, 0.55, 0.507, 0.586, 0.56, 0.50, 0.56};
+    const double m[] = {0.01, 0.01, 0.01, 0.02, 0.075, 0.117, 0.194, 0.24, 0.40, 0.46, 0.50, 0.66, 0.63, 0.50, 0.56};
     for (int l = 1; l <= 15; ++l) c.eff[l] = m[l - 1];
     if (const char* e = std::getenv("RSG_REBLOCK")) c.on = std::atoi(e) != 0;
     if (const char* e = std::getenv("RSG_REBLOCK_EFF")) {
@@ -852,7 +852,9 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
   };
   auto span_begin = [&](const Span& sp) {
     if (!serial) return;
-    rs_ctx::K4Span k{sp.l + 1, sp.var, sp.list_n, span_flops(sp), c->pool_event(), c->pool_event()};
+    double ef = 0;  // flops of the executed plans
+    for (int64_t i = 0; i < sp.list_n; ++i) ef += pair_flops(plans[fp.lists[sp.list_off + i]]);
+    rs_ctx::K4Span k{sp.l + 1, sp.var, sp.list_n, span_flops(sp), ef, c->pool_event(), c->pool_event()};
     cudaEventRecord(k.a, st);
     c->k4_spans.push_back(k);
   };
@@ -927,10 +929,11 @@ void collect_k4_rows(rs_ctx* c) {
       if (r.log2n == k.log2n && r.var == k.var) {
         r.pairs += k.pairs;
         r.flops += k.flops;
+        r.exec_flops += k.exec_flops;
         r.ms += ms;
         merged = true;
       }
-    if (!merged) c->k4_rows.push_back(rs_ctx::K4Row{k.log2n, k.var, k.pairs, k.flops, ms});
+    if (!merged) c->k4_rows.push_back(rs_ctx::K4Row{k.log2n, k.var, k.pairs, k.flops, ms, k.exec_flops});
   }
   c->k4_spans.clear();
   c->ev_used = 0;
@@ -1845,7 +1848,7 @@ int rs_ctx_set_profiling(rs_ctx* c, int enabled) {
 }
 
 int rs_ctx_k4_breakdown(rs_ctx* c, int cap, int32_t* log2n, int32_t* variant, int64_t* pairs, double* flops,
-                        double* ms) {
+                        double* ms, double* exec_flops) {
   if (!c) return -fail(RS_ERR_CONFIG, "null context");
   const int n = static_cast<int>(c->k4_rows.size());
   for (int i = 0; i < n && i < cap; ++i) {
@@ -1855,6 +1858,7 @@ int rs_ctx_k4_breakdown(rs_ctx* c, int cap, int32_t* log2n, int32_t* variant, in
     if (pairs) pairs[i] = r.pairs;
     if (flops) flops[i] = r.flops;
     if (ms) ms[i] = r.ms;
+    if (exec_flops) exec_flops[i] = r.exec_flops;
   }
   return n;
 }

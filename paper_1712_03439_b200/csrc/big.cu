@@ -8,7 +8,7 @@
 // L-sample block, times H, inverse, overlap-added at b*L; mean_power's Σy²
 // (audio_buffer.hpp:66-75) of the final samples.
 //
-// Why a separate kernel: the Stockham passes of ola_kernel<M> hold a thread's whole
+// Why a separate kernel: the Stockham passes of ola_small_kernel<M> hold a thread's whole
 // E = 32-element share across the barrier between a pass's reads and writes; at one
 // 512-thread CTA per SM (the transform alone is 136 KB of smem) that leaves 128
 // registers and the kernel spills ~1 KB per thread (53 GB of local-memory traffic per

@@ -3,7 +3,7 @@
 //   K1 rir_synth_kernel     synthesize_rir        roomsim/room_model.hpp:141-174 (FP64, bit-exact)
 //   K2 rir_cut_kernel       power_threshold/cutoff_index/truncate_rir  room_model.hpp:177-213
 //   K3 rir_spectrum_kernel  the RIR transform of convolve_ola         convolution.hpp:238-239
-//   K4 ola_kernel           the OLA block loop + Σy^2                 convolution.hpp:242-253,
+//   K4 ola_small_kernel     the OLA block loop + Σy^2                 convolution.hpp:242-253,
 //                                                                     audio_buffer.hpp:66-75
 //   K5 gain_kernel          SPEC compute_gain
 //   K6 mix_kernel           SPEC render sum
@@ -529,19 +529,24 @@ __global__ void __launch_bounds__(cta_threads_of(Plan<M>::LOG)) rir_spectrum_ker
     const float2* W = a.tw + PL::TW_PASS;
     const float scale = 1.0f / (8.0f * M);
     float2* out = a.spec + pl.spec_off;
-    for (int k = t; k <= M; k += PL::T) {
+    auto untangle = [&](int k) {  // 2 H(k) sqrt-free: S + W^k D of the packed transform
       const float2 za = s[PAD(k & (M - 1))];
       const float2 zb = c_conj(s[PAD((M - k) & (M - 1))]);
       const float2 S = c_add(za, zb);
       const float2 D = c_rot<false>(c_sub(za, zb));
-      const float2 X2 = c_add(S, c_mul(pair_twiddle<M>(W, k), D));
-      if (a.perm.on) {  // H / N over all N bins (H(N - k) = conj H(k)), ola_ipc_kernel's order
-        const float2 g = c_scale(X2, 2.0f * scale);
-        out[a.perm.index(k)] = g;
-        if (k != 0 && k != M) out[a.perm.index(2 * M - k)] = c_conj(g);
-      } else {
-        out[k] = c_scale(X2, scale);
+      return c_add(S, c_mul(pair_twiddle<M>(W, k), D));
+    };
+    if (a.perm.on) {
+      // H / N over all N bins (H(N - k) = conj H(k)) in ola_ipc_kernel's order, walked in
+      // OUTPUT order so the stores coalesce (bin order scatters 8-byte stores over 128-byte
+      // lines: K3 was store-bound, 95% L1 throughput)
+      for (int idx = t; idx < 2 * M; idx += PL::T) {
+        const int k = a.perm.bin(idx);
+        const float2 g = c_scale(untangle(k <= M ? k : 2 * M - k), 2.0f * scale);
+        out[idx] = k <= M ? g : c_conj(g);
       }
+    } else {
+      for (int k = t; k <= M; k += PL::T) out[k] = c_scale(untangle(k), scale);
     }
   }
 }

@@ -101,6 +101,11 @@ struct IpcPerm {
                      (k >> (lr0 + lr1));
     return ((slot & ((1 << lr2) - 1)) << (lc - lr2)) | (slot >> lr2);
   }
+  __host__ __device__ int bin(int idx) const {  // inverse of index()
+    const int slot = ((idx & ((1 << (lc - lr2)) - 1)) << lr2) | (idx >> (lc - lr2));
+    return (slot >> (lr1 + lr2)) | (((slot >> lr2) & ((1 << lr1) - 1)) << lr0) |
+           ((slot & ((1 << lr2) - 1)) << (lr0 + lr1));
+  }
 };
 
 struct SpecArgs {

@@ -140,7 +140,7 @@ def load_library() -> C.CDLL:
         "rs_ctx_last_timing": (C.c_int, [vp, dp, dp, dp, C.POINTER(i64)]),
         "rs_ctx_set_profiling": (C.c_int, [vp, C.c_int]),
         "rs_ctx_stage_times": (C.c_int, [vp, dp, C.c_int, dp]),
-        "rs_ctx_k4_breakdown": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp]),
+        "rs_ctx_k4_breakdown": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp, vp]),
         "rs_cost_direct": (d, [d, d, sz, sz]),
         "rs_cost_full_fft": (d, [d, d, sz, sz, sz]),
         "rs_cost_ola": (d, [d, d, sz, sz, sz]),
@@ -273,9 +273,10 @@ class Context:
     K4_VARIANTS = ("ola_small", "ola_ip", "ola2", "four_step", "ola_ipc")
 
     def k4_breakdown(self) -> list:
-        """Rows of the last render at profiling level 2: N, variant, pairs, flops, ms."""
+        """Rows of the last render at profiling level 2: executed N, variant, pairs, algorithmic
+        flops (reference plan), ms, flops of the executed plan."""
         L = load_library()
-        n = L.rs_ctx_k4_breakdown(self.h, 0, None, None, None, None, None)
+        n = L.rs_ctx_k4_breakdown(self.h, 0, None, None, None, None, None, None)
         if n < 0:
             _check(-n)
         lg = np.zeros(n, np.int32)
@@ -283,9 +284,10 @@ class Context:
         pairs = np.zeros(n, np.int64)
         fl = np.zeros(n)
         ms = np.zeros(n)
-        L.rs_ctx_k4_breakdown(self.h, n, _ptr(lg), _ptr(var), _ptr(pairs), _ptr(fl), _ptr(ms))
+        ef = np.zeros(n)
+        L.rs_ctx_k4_breakdown(self.h, n, _ptr(lg), _ptr(var), _ptr(pairs), _ptr(fl), _ptr(ms), _ptr(ef))
         return [{"fft_size": 1 << int(lg[i]), "kernel": self.K4_VARIANTS[int(var[i])], "pairs": int(pairs[i]),
-                 "flops": float(fl[i]), "ms": float(ms[i])} for i in np.argsort(-fl)]
+                 "flops": float(fl[i]), "ms": float(ms[i]), "exec_flops": float(ef[i])} for i in np.argsort(-fl)]
 
     def synchronize(self) -> None:
         _check(load_library().rs_ctx_synchronize(self.h))

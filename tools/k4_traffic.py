@@ -12,7 +12,7 @@ from collections import defaultdict
 
 from launch_summary import SCALE
 
-K4 = re.compile(r"ola_small_kernel|ola_ip_kernel|ola_w_kernel|ola2_kernel|ola_kernel|large_(rows|cols|ola)")
+K4 = re.compile(r"ola_small_kernel|ola_ipc_kernel|ola_ip_kernel|ola2_kernel|large_(rows|cols|ola)")
 
 
 def main(path, renders, source, utts=4096):
@@ -26,7 +26,7 @@ def main(path, renders, source, utts=4096):
     by = sum(m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0) for m in per.values())
     print(json.dumps({
         "workload": "config4", "utterances_per_rank": utts,
-        "kernel": "K4 (ola_small_kernel / ola_ip_kernel / ola2_kernel / four-step stages), all launches of one config-4 render",
+        "kernel": "K4 (ola_ipc_kernel / ola_ip_kernel / ola_small_kernel / ola2_kernel / four-step stages), all launches of one config-4 render",
         "dram_bytes_per_render": by / renders,
         "device_ms_per_render": ms / renders,
         "launches_per_render": len(per) / renders,

@@ -18,9 +18,8 @@ timeout 600 python bench.py --utterances 512 --no-cpu-baseline > $O/${R}_bench_s
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --csv --log-file $O/${R}_launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_list.log 2>&1
 echo "launch list rc=$?"
-for k in "ola_small_kernel<.int.512>" "ola_ip_kernel<.int.1024>" "ola_ip_kernel<.int.2048>" "ola_small_kernel<.int.256>" \
-         "ola_ip_kernel<.int.4096>" "ola2_kernel<.int.256>" "mix_kernel" "rir_synth_kernel<.int.512, .int.4>" \
-         "rir_synth_kernel<.int.128, .int.4>"; do
+for k in "ola_ipc_kernel<.int.4096>" "ola_ipc_kernel<.int.8192>" "ola_small_kernel<.int.512>" "mix_kernel" \
+         "rir_synth_kernel<.int.512, .int.4" "rir_synth_kernel<.int.128, .int.4" "rir_spectrum_kernel<.int.2048>"; do
   n=$(echo "$k" | tr -dc "a-z0-9_")
   timeout 600 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:$k" \
     --launch-skip 2 -c 1 -o $O/${R}_full_$n python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > $O/ncu_$n.log 2>&1
@@ -28,8 +27,11 @@ for k in "ola_small_kernel<.int.512>" "ola_ip_kernel<.int.1024>" "ola_ip_kernel<
   # the copy-back limit is 64 MiB: raw metrics as CSV for every capture, the report itself
   # only for the two largest K4 kernels
   ncu -i $O/${R}_full_$n.ncu-rep --page raw --csv > $O/${R}_full_${n}_raw.csv 2>/dev/null
-  case $n in ola_small_kernelint512|ola_ip_kernelint1024) ;; *) rm -f $O/${R}_full_$n.ncu-rep ;; esac
+  ncu -i $O/${R}_full_$n.ncu-rep --page source --csv > $O/${R}_full_${n}_source.csv 2>/dev/null
+  case $n in ola_ipc_kernelint4096) ;; *) rm -f $O/${R}_full_$n.ncu-rep ;; esac
 done
+# the reference's block sizes executed as planned (RSG_REBLOCK=0): the pre-re-blocking K4 mix
+RSG_REBLOCK=0 timeout 600 python bench.py --no-e2e --no-cpu-baseline > $O/${R}_bench_reblock_off.log 2>&1; echo "reblock-off rc=$?"
 timeout 600 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:ola_ip_kernel<.int.16384>" \
   --launch-skip 2 -c 1 -o $O/${R}_full_ip16384_config5 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --config config5 > $O/ncu_ip16384.log 2>&1
 echo "ip16384 rc=$?"
