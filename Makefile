@@ -5,7 +5,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC,-O2,-ffp-contract=off
 SRC := paper_1712_03439_b200/csrc
 OUT := paper_1712_03439_b200/_lib
-OBJS := $(OUT)/kernels.o $(OUT)/big.o $(OUT)/large.o $(OUT)/ola2.o $(OUT)/sampler.o $(OUT)/features.o $(OUT)/api.o
+OBJS := $(OUT)/kernels.o $(OUT)/big.o $(OUT)/large.o $(OUT)/ola2.o $(OUT)/synth_bound.o $(OUT)/sampler.o $(OUT)/features.o $(OUT)/api.o
 
 REF_INC ?= /root/reference/proj/include
 ADAPTER := tests/cpp/_build/adapter_test
@@ -27,6 +27,10 @@ $(OUT)/big.o: $(SRC)/big.cu $(SRC)/kernels.cuh $(SRC)/power.cuh $(SRC)/fft.cuh
 $(OUT)/ola2.o: $(SRC)/ola2.cu $(SRC)/kernels.cuh $(SRC)/power.cuh $(SRC)/fft.cuh $(SRC)/fft2.cuh $(SRC)/async.cuh
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/ola2.ptxas.log || (cat $(OUT)/ola2.ptxas.log; false)
+
+$(OUT)/synth_bound.o: $(SRC)/synth_bound.cu $(SRC)/kernels.cuh
+	@mkdir -p $(OUT)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/synth_bound.ptxas.log || (cat $(OUT)/synth_bound.ptxas.log; false)
 
 $(OUT)/sampler.o: $(SRC)/sampler.cu $(SRC)/sampler.cuh include/roomsim_gpu.h
 	@mkdir -p $(OUT)

@@ -823,8 +823,11 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
   }
   const int32_t* d_lists = fb.lists.as<int32_t>();
   double* d_part = fb.part.as<double>();
+  // ola_ipc_kernel items transform their pair's RIR themselves (RSG_IPC_K3=1: a K3 launch instead)
+  static const bool ipc_k3 = std::getenv("RSG_IPC_K3") != nullptr;
   for (const Span& sp : fp.spans) {
     if (sp.var == kVarLarge) continue;  // spectrum inside the four-step batches
+    if (sp.var == kVarIpc && !ipc_k3) continue;
     SpecArgs a{d_lists + sp.list_off, static_cast<int32_t>(sp.list_n), d_pair, fb.plan.as<PairPlan>(),
                d_rir, fb.spec.as<float2>(), c->tw[sp.l], sp.var == kVarIpc ? ipc_perm(sp.l + 1) : IpcPerm{}};
     RS_CUDA(launch_spectrum(sp.l, a, st));
@@ -898,7 +901,7 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
     } else if (sp.var == kVarSmall || sp.var == kVarIp || sp.var == kVarIpc) {
       OlaArgs a{fb.olaitems.as<OlaItem>() + sp.item_off, static_cast<int32_t>(sp.item_n), d_pair,
                 fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(), d_part, c->tw[sp.l],
-                sp.seg};
+                sp.seg, (sp.var == kVarIpc && !ipc_k3) ? d_rir : nullptr};
       if (sp.var == kVarIpc)
         RS_CUDA(launch_ola_ipc(sp.l + 1, a, sp.max_nh, side_for()));
       else if (sp.var == kVarIp)
@@ -974,6 +977,8 @@ struct Chunk {
   std::vector<PairMeta> pair;
   std::vector<SynthItem> items;
   std::vector<std::tuple<int64_t, int64_t, int, int>> synth_class;  // (offset, count, slice cap, threads)
+  std::vector<int32_t> bound_pairs;                                  // truncated renders: synth_bound.cu
+  std::vector<std::tuple<int64_t, int64_t, int, int>> bound_class;   // (offset, count, cap, threads)
   std::vector<int> place_err;            // per pair: config / placement error (K1 skips the pair)
   std::vector<std::string> place_msg;
   std::vector<uint8_t> empty_sig;        // per pair: N_x == 0 (reported after the RIR's own errors)
@@ -987,7 +992,7 @@ struct Chunk {
   int max_order = 0, slice = 1;
   int64_t rir_total = 0;
   DevBuf d_chan_feat;
-  DevBuf d_utt, d_pair, d_rg, d_items, d_rir, d_rirout, d_gain, d_power, d_flags, d_snr, d_chan_utt,
+  DevBuf d_utt, d_pair, d_rg, d_items, d_bound, d_rir, d_rirout, d_gain, d_power, d_flags, d_snr, d_chan_utt,
       d_chan_mic, d_chan_out, d_utt_len, d_utt_stride, d_utt_pair0, d_utt_I, d_utt_J;
   FilterBufs fb;
   PinnedArena hA, hB;
@@ -1007,7 +1012,7 @@ struct Chunk {
     return RS_OK;
   }
   void release() {
-    DevBuf* bufs[] = {&d_chan_feat, &d_utt, &d_pair, &d_rg, &d_items, &d_rir, &d_rirout, &d_gain, &d_power, &d_flags,
+    DevBuf* bufs[] = {&d_chan_feat, &d_utt, &d_pair, &d_rg, &d_items, &d_bound, &d_rir, &d_rirout, &d_gain, &d_power, &d_flags,
                       &d_snr, &d_chan_utt, &d_chan_mic, &d_chan_out, &d_utt_len, &d_utt_stride,
                       &d_utt_pair0, &d_utt_I, &d_utt_J, &fb.plan, &fb.lists, &fb.olaitems, &fb.spec,
                       &fb.y, &fb.part, &fb.units, &fb.scratch, &fb.yblk, &fb.olaitems2};
@@ -1180,11 +1185,38 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
   }();
   static const int kClass[4] = {2048, 6144, kSynthSlice, kSynthBig};
   std::vector<SynthItem> cls[2][4];
+  // Truncated renders: the bound pass (synth_bound.cu) finds the prefix of each RIR the cut can
+  // keep, and K1 synthesizes only that — in short slices, since the prefix is typically a few
+  // hundred to a few thousand bins (a slice beyond it exits at once).  RSG_SYNTH_CUT=0: the
+  // whole RIR as for eta = 0.
+  static const bool cut_off = [] {
+    const char* e = std::getenv("RSG_SYNTH_CUT");
+    return e && e[0] == '0';
+  }();
+  static const int kBoundCap[4] = {4096, 8192, 16384, kBoundMaxCap};
+  std::vector<int32_t> bound_cls[2][4];
+  ch.bound_pairs.clear();
+  ch.bound_class.clear();
   for (int64_t p = 0; p < ch.P; ++p) {
     if (ch.place_err[p]) continue;
     const int64_t cap = ch.pair[p].rir_cap;
     const int K = ch.utt[ch.pair[p].utt].order;
-    const int small = K <= 12 ? 1 : 0;  // measured crossover of the 128- and 512-thread K1
+    int small = K <= 12 ? 1 : 0;  // measured crossover of the 128- and 512-thread K1
+    if (b->eta_db > 0.0 && !cut_off && cap <= kBoundMaxCap) {
+      static const int cut_slice = [] { const char* e = std::getenv("RSG_CUT_SLICE"); return e ? std::atoi(e) : kSynthCutSlice; }();
+      static const int cut_small_k = [] { const char* e = std::getenv("RSG_CUT_SMALL_K"); return e ? std::atoi(e) : 40; }();
+      static const int bound_small_k = [] { const char* e = std::getenv("RSG_BOUND_SMALL_K"); return e ? std::atoi(e) : 6; }();
+      int bc = 0;
+      while (cap > kBoundCap[bc]) ++bc;
+      bound_cls[K <= bound_small_k ? 1 : 0][bc].push_back(static_cast<int32_t>(p));
+      small = K <= cut_small_k ? 1 : 0;
+      for (int64_t lo = 0; lo < cap; lo += cut_slice) {
+        const int64_t len = std::min<int64_t>(cut_slice, cap - lo);
+        cls[small][len <= kClass[0] ? 0 : (len <= kClass[1] ? 1 : 2)].push_back(
+            SynthItem{static_cast<int32_t>(p), static_cast<int32_t>(lo), static_cast<int32_t>(len), 0});
+      }
+      continue;
+    }
     if (cap > std::max<int64_t>(kSynthSlice, big.first) && cap <= big.second) {
       cls[small][3].push_back(SynthItem{static_cast<int32_t>(p), 0, static_cast<int32_t>(cap), 0});
       continue;
@@ -1195,6 +1227,13 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
       cls[small][k].push_back(SynthItem{static_cast<int32_t>(p), static_cast<int32_t>(lo), static_cast<int32_t>(len), 0});
     }
   }
+  for (int small = 0; small < 2; ++small)
+    for (int k = 3; k >= 0; --k) {  // large lattices and longest RIRs first
+      if (bound_cls[small][k].empty()) continue;
+      ch.bound_class.emplace_back(static_cast<int64_t>(ch.bound_pairs.size()),
+                                  static_cast<int64_t>(bound_cls[small][k].size()), kBoundCap[k], small ? 128 : 512);
+      ch.bound_pairs.insert(ch.bound_pairs.end(), bound_cls[small][k].begin(), bound_cls[small][k].end());
+    }
   ch.synth_class.clear();
   for (int small = 0; small < 2; ++small)
     for (int k = 3; k >= 0; --k) {  // large lattices and slices first
@@ -1212,6 +1251,7 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
 int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, cudaStream_t sA) {
   RS_TRY(ch.init_events());
   size_t need = staged_bytes(ch.utt) + staged_bytes(ch.pair) + staged_bytes(ch.rg) + staged_bytes(ch.items) +
+                staged_bytes(ch.bound_pairs) +
                 ((std::max<int64_t>(ch.P, 1) * sizeof(PairRir) + 63) & ~size_t(63)) + 64;
   RS_TRY(ch.hA.reserve(need));
   ch.hA.reset();
@@ -1223,6 +1263,16 @@ int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, cudaStream_t sA
   RS_TRY(ch.d_rir.ensure(std::max<int64_t>(ch.rir_total, 1) * sizeof(double)));
   RS_TRY(ch.d_rirout.ensure(std::max<int64_t>(ch.P, 1) * sizeof(PairRir)));
   RS_CUDA(cudaMemsetAsync(ch.d_rirout.p, 0, std::max<int64_t>(ch.P, 1) * sizeof(PairRir), sA));
+  const double eta_factor = b->eta_db > 0.0 ? std::pow(10.0, -b->eta_db / 10.0) : 0.0;
+  if (!ch.bound_pairs.empty()) {  // K1a: the prefix of each RIR the cut can keep
+    RS_TRY(upload_on(ch.d_bound, ch.bound_pairs, sA, &ch.hA));
+    for (const auto& [off, n, cap, nt] : ch.bound_class) {
+      SynthBoundArgs sb{ch.d_utt.as<UttMeta>(), ch.d_pair.as<PairMeta>(), ch.d_rg.as<double>(),
+                        ch.d_bound.as<int32_t>() + off, ch.d_rirout.as<PairRir>(), eta_factor};
+      RS_CUDA(launch_synth_bound(sb, static_cast<int>(n), cap, ch.max_order, sA, nt));
+      ++c->launches;
+    }
+  }
   // one K1 launch per slice-size class, so short RIRs get more CTAs per SM
   for (size_t k = 0; k < ch.synth_class.size(); ++k) {
     const auto& [off, n, cap, nt] = ch.synth_class[k];
@@ -1232,7 +1282,6 @@ int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, cudaStream_t sA
     RS_CUDA(launch_synth(sa, static_cast<int>(n), ch.max_order, cap, sA, nt));
     ++c->launches;
   }
-  const double eta_factor = b->eta_db > 0.0 ? std::pow(10.0, -b->eta_db / 10.0) : 0.0;
   CutArgs ca{ch.d_pair.as<PairMeta>(), ch.d_utt.as<UttMeta>(), ch.d_rir.as<double>(), ch.d_rirout.as<PairRir>(),
              eta_factor};
   RS_CUDA(launch_cut(ca, static_cast<int>(ch.P), sA));
@@ -1312,6 +1361,19 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
     y_off += (pl.out_len + 3) & ~int64_t(3);  // 16-byte aligned rows: K6 reads float4
     int64_t& ul = ch.ulen[ch.pair[p].utt];
     ul = std::max(ul, pl.out_len);
+  }
+  if (std::getenv("RSG_TRACE")) {  // truncated-synthesis statistics of the chunk
+    double sl = 0, se = 0, sk = 0, full = 0, vol = 0, volx = 0;
+    for (int64_t p = 0; p < ch.P; ++p) {
+      const PairRir& r = ch.h_rir[p];
+      const double e = r.exact_len > 0 ? r.exact_len : r.len;
+      sl += r.len; se += e; sk += r.keep; full += r.exact_len > 0 ? 0 : 1;
+      const double W = 2.0 * ch.utt[ch.pair[p].utt].order + 1.0;
+      vol += W * W * W;
+      volx += W * W * W * std::min(1.0, std::pow(e / std::max<double>(r.len, 1), 3.0));
+    }
+    std::fprintf(stderr, "[trace] chunk of %lld pairs: mean len %.0f, exact_len %.0f, keep %.0f; %.0f pairs in full; images %.3g, ~in exact sphere %.3g\n",
+                 static_cast<long long>(ch.P), sl / ch.P, se / ch.P, sk / ch.P, full, vol, volx);
   }
   RS_TRY(utt_check(static_cast<int64_t>(ch.utt_err.size())));  // trailing utterances without pairs
   for (int64_t u = ch.u0; u < ch.u1; ++u)

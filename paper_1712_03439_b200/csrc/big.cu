@@ -489,7 +489,8 @@ __global__ void __launch_bounds__(IpcPlan<C>::T, IpcPlan<C>::MINB) ola_ipc_kerne
   const PairMeta& pm = a.pair[it.pair];
   const float* __restrict__ x = a.signals + pm.sig_off;
   const long long nx = pm.nx;
-  const float2* __restrict__ Gp = a.spec + pl.spec_off;
+  // (not __restrict__ / no read-only path: the item may write the filter itself, below)
+  float2* Gp = const_cast<float2*>(a.spec) + pl.spec_off;
   float* __restrict__ y = a.y + pl.y_off;
   const int L = static_cast<int>(pl.L);
   const int B = static_cast<int>(pl.B);
@@ -508,12 +509,50 @@ __global__ void __launch_bounds__(IpcPlan<C>::T, IpcPlan<C>::MINB) ola_ipc_kerne
     tws[i] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
   }
   for (int i = t; i < ovl; i += T) carry[i] = 0.f;
-  if (t == 0) {  // the pair's filter and the run's first two blocks
-    prefetch_l2(Gp, C * sizeof(float2));
+  if (t == 0) {  // the run's first two blocks (and the pair's filter when K3 wrote it)
+    if (!a.rir) prefetch_l2(Gp, C * sizeof(float2));
     const long long s0 = static_cast<long long>(it.b_begin) * L;
     prefetch_l2(x + s0, 4 * (nx - s0 < 2 * L ? nx - s0 : 2 * L));
   }
   __syncthreads();
+  if (a.rir) {
+    // The filter, by the item itself (K3's work, convolution.hpp:238-239): the forward transform
+    // of the truncated RIR (FP64 taps rounded to FP32, zero-padded to N, imaginary part 0) leaves
+    // H(k) in the digit-reversed slots the product step reads, so after the last pass element r
+    // of butterfly u IS Gp[r (C / RL) + u]: scaled by 1 / N and stored from registers, coalesced.
+    // One forward transform per item (a whole pair's blocks in a batched render: ~3% of its work)
+    // instead of a K3 launch that wrote the same 32 KB per pair through scattered smem reads.
+    const double* __restrict__ h = a.rir + pm.rir_off;
+    const int nh = ovl + 1;
+    {
+      float2 v[R0];
+      const int rh = nh - t;
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        v[r].x = S0 * r < rh ? static_cast<float>(h[t + S0 * r]) : 0.f;
+        v[r].y = 0.f;
+      }
+      Dft<R0, false>::run(v);
+      apply_twiddles<R0, false>(v, tws[t]);
+#pragma unroll
+      for (int r = 0; r < R0; ++r) s[ipad<PL>(t) + ip_off<PL, R0, S0, C>(r)] = v[r];
+    }
+    __syncthreads();
+    ipc_forward_mid<PL, C, 1>(s, tws, t);
+    const float inv_n = 1.0f / static_cast<float>(C);
+#pragma unroll
+    for (int q = 0; q < NBL; ++q) {
+      const int u = t + q * T;
+      const int pb = ipad<PL>(u * RL);
+      float2 v[RL];
+#pragma unroll
+      for (int r = 0; r < RL; ++r) v[r] = s[pb + ip_off<PL, RL, 1, C>(r)];
+      Dft<RL, false>::run(v);
+#pragma unroll
+      for (int r = 0; r < RL; ++r) Gp[r * (C / RL) + u] = c_scale(v[r], inv_n);
+    }
+    __syncthreads();  // the filter (global, this CTA's own writes) and the transform buffer are settled
+  }
   double pw = 0.0;  // this lane's Σ y² of the current power segment
 #pragma unroll 1
   for (int b = it.b_begin; b < it.b_end; b += 2) {  // b even: blocks b (real part) and b + 1 (imaginary)
@@ -553,7 +592,7 @@ __global__ void __launch_bounds__(IpcPlan<C>::T, IpcPlan<C>::MINB) ola_ipc_kerne
       for (int r = 0; r < RL; ++r) v[r] = s[pb + ip_off<PL, RL, 1, C>(r)];
       Dft<RL, false>::run(v);
 #pragma unroll
-      for (int r = 0; r < RL; ++r) v[r] = c_mul(v[r], ld_tw(Gp + r * (C / RL) + u));
+      for (int r = 0; r < RL; ++r) v[r] = c_mul(v[r], __ldcg(Gp + r * (C / RL) + u));
       Dft<RL, true>::run(v);
 #pragma unroll
       for (int r = 0; r < RL; ++r) s[pb + ip_off<PL, RL, 1, C>(r)] = v[r];

@@ -103,7 +103,11 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
     for (int i = threadIdx.x; i < NW * HT; i += NT) cl[i] = 0xffffffffu;
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int lo = it.slice_lo, len = it.slice_len;
+  // Truncated renders (synth_bound.cu): only bins [0, exact_len) are needed
+  const int exact_len = a.out[it.pair].exact_len;
+  const int lo = it.slice_lo;
+  const int len = exact_len > 0 ? min(it.slice_len, exact_len - lo) : it.slice_len;
+  if (len <= 0) return;  // the slice lies beyond the exact range (CTA-uniform)
   // 32-bit shared address of the bins, computed once (laundered through asm: otherwise the
   // compiler re-derives the CTA's shared window, S2UR SR_CgaCtaId, at every use)
   unsigned bins_s;
@@ -121,18 +125,53 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
     ax[idx] = __dmul_rn(diff, diff);                    // :43 v.x * v.x
   }
   for (int g = tid; g <= 3 * K; g += NT) rg[g] = a.rg[um.rg_off + g];
+  // Sub-lattice [x0, x0 + bx) x [y0, y0 + by) x [z0, z0 + bz): the whole lattice, or — when only
+  // bins [0, exact_len) are wanted — the box around the sphere of delay exact_len: an image
+  // outside it has one squared axis offset above (exact_len / spm)^2 (1 + 1e-9), so its delay
+  // is >= exact_len.  Enumeration order within the box is the reference's order restricted to
+  // it (ix -> iy -> iz ascending), so the wanted bins receive the same terms in the same order.
+  __shared__ int s_box[6];
+  if (tid < 6) s_box[tid] = (tid & 1) ? -1 : W;
   __syncthreads();
-
-  const long long V = static_cast<long long>(W) * W * W;
-  // image index i = (ix W + iy) W + iz, advanced incrementally by NT per image slot
-  int iz = tid % W, iy, ix;
-  {
-    const int q = tid / W;
-    iy = q % W;
-    ix = q / W;
+  // squared distance beyond which an image's delay is >= exact_len for certain
+  const double rr = static_cast<double>(exact_len) / spm;
+  const double d2max = exact_len > 0 ? rr * rr * (1.0 + 1e-9) : 1.0e300;
+  if (exact_len > 0) {
+    for (int idx = tid; idx < 3 * W; idx += NT) {
+      const int axis = idx / W, n = idx - axis * W;
+      if (ax[idx] <= d2max) {
+        atomicMin(&s_box[2 * axis], n);
+        atomicMax(&s_box[2 * axis + 1], n);
+      }
+    }
+  } else if (tid < 3) {
+    s_box[2 * tid] = 0;
+    s_box[2 * tid + 1] = W - 1;
   }
-  const int step_z = NT % W, step_q = NT / W;
-  const int step_y = step_q % W, step_x = step_q / W;
+  __syncthreads();
+  const int x0 = s_box[0], y0 = s_box[2], z0 = s_box[4];
+  const int bx = s_box[1] - x0 + 1, by = s_box[3] - y0 + 1, bz = s_box[5] - z0 + 1;
+  if (bx <= 0 || by <= 0 || bz <= 0) {  // no image can land in the range (cannot happen: the direct path does)
+    double* out0 = a.rir + pm.rir_off + lo;
+    for (int l = tid; l < len; l += NT) out0[l] = 0.0;
+    return;
+  }
+
+  const long long V = static_cast<long long>(bx) * by * bz;
+  // image index i = (jx by + jy) bz + jz within the box, advanced incrementally by NT per
+  // image slot; (ix, iy, iz) = (x0 + jx, y0 + jy, z0 + jz)
+  int iz = tid % bz, iy, ix;
+  {
+    const int q = tid / bz;
+    iy = q % by;
+    ix = q / by;
+  }
+  const int step_z = NT % bz, step_q = NT / bz;
+  const int step_y = step_q % by, step_x = step_q / by;
+  const unsigned axx_s = ax_s + 8u * static_cast<unsigned>(x0);
+  const unsigned axy_s = ax_s + 8u * static_cast<unsigned>(W + y0);
+  const unsigned axz_s = ax_s + 8u * static_cast<unsigned>(2 * W + z0);
+  const int kx = K - x0, ky = K - y0, kz = K - z0;
   const unsigned lt = lanemask_lt();
   unsigned long long max_d = 0;
   int geo = 0;
@@ -146,8 +185,11 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
       amp[h] = 0.0;
       if (i < V) {
         // norm: sqrt((x*x + y*y) + z*z), room_model.hpp:43
-        const double d2 = __dadd_rn(__dadd_rn(lds_f64(ax_s + 8u * ix), lds_f64(ax_s + 8u * (W + iy))),
-                                    lds_f64(ax_s + 8u * (2 * W + iz)));
+        const double d2 = __dadd_rn(__dadd_rn(lds_f64(axx_s + 8u * ix), lds_f64(axy_s + 8u * iy)),
+                                    lds_f64(axz_s + 8u * iz));
+        if (d2 > d2max) {  // beyond the exact range (truncated synthesis): no sqrt, no entry
+          // (index advance below)
+        } else {
         const double d = __dsqrt_rn(d2);
         if (d <= 0.0) geo = 1;                     // :157-158
         const double dl = ceil(__dmul_rn(d, spm));  // :159-160
@@ -155,18 +197,19 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
         max_d = D > max_d ? D : max_d;
         const long long rel = static_cast<long long>(D) - lo;
         if (rel >= 0 && rel < len) {
-          const int g = abs(ix - K) + abs(iy - K) + abs(iz - K);
+          const int g = abs(ix - kx) + abs(iy - ky) + abs(iz - kz);
           amp[h] = __ddiv_rn(lds_f64(rg_s + 8u * g), d);  // :161-162 pow(r, g) / d
           rel_bin[h] = static_cast<int>(rel);
+        }
         }
       }
       // advance (ix, iy, iz) by NT images
       iz += step_z;
       int cy = step_y;
-      if (iz >= W) { iz -= W; ++cy; }
+      if (iz >= bz) { iz -= bz; ++cy; }
       iy += cy;
       int cx = step_x;
-      while (iy >= W) { iy -= W; ++cx; }
+      while (iy >= by) { iy -= by; ++cx; }
       ix += cx;
     }
 #ifndef RSG_X_NOSCATTER
@@ -306,7 +349,7 @@ __global__ void __launch_bounds__(NT) rir_synth_kernel(SynthArgs a, int slice_ca
     max_d = other > max_d ? other : max_d;
     geo |= __shfl_xor_sync(0xffffffffu, geo, o);
   }
-  if (lane == 0) {
+  if (lane == 0 && exact_len <= 0) {  // (the bound pass wrote both for a truncated synthesis)
     atomicMax(&a.out[it.pair].max_delay, max_d);
     if (geo) atomicOr(&a.out[it.pair].flags, 1);
   }
@@ -383,8 +426,10 @@ __global__ void __launch_bounds__(256) rir_cut_kernel(CutArgs a) {
     }
     return;
   }
+  // bins at and beyond exact_len were not synthesized: all provably below the threshold
+  const long long scan = (r.exact_len > 0 && r.exact_len < len) ? r.exact_len : len;
   double mx = 0.0;
-  for (long long n = tid; n < len; n += 256) mx = fmax(mx, __dmul_rn(h[n], h[n]));
+  for (long long n = tid; n < scan; n += 256) mx = fmax(mx, __dmul_rn(h[n], h[n]));
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if (lane == 0) red_d[warp] = mx;
   __syncthreads();
@@ -392,7 +437,7 @@ __global__ void __launch_bounds__(256) rir_cut_kernel(CutArgs a) {
   for (int w = 1; w < 8; ++w) mx = fmax(mx, red_d[w]);
   const double th = __dmul_rn(mx, a.eta_factor);  // room_model.hpp:184
   long long last = -1;
-  for (long long n = tid; n < len; n += 256)
+  for (long long n = tid; n < scan; n += 256)
     if (__dmul_rn(h[n], h[n]) >= th) last = n;  // room_model.hpp:193-195
   for (int o = 16; o > 0; o >>= 1) {
     const long long other = __shfl_xor_sync(0xffffffffu, last, o);

@@ -38,7 +38,8 @@ struct PairRir {
   int64_t cutoff;                // n_c
   double threshold;              // p_th (room_model.hpp:184)
   int32_t flags;                 // 1: geometry error (d <= 0), 2: degenerate (all-zero)
-  int32_t pad;
+  int32_t exact_len;             // > 0: K1 synthesizes only bins [0, exact_len) (synth_bound.cu): every
+                                 // later bin is provably below the cut threshold; 0: the whole RIR
 };
 
 // Per pair, written by the host planner (after K2) and consumed by K3/K4/mix.
@@ -81,6 +82,18 @@ struct SynthArgs {
   double* rir;
   PairRir* out;
 };
+
+// K1a (synth_bound.cu): for truncated renders, the prefix of each RIR that truncate_rir can keep.
+struct SynthBoundArgs {
+  const UttMeta* utt;
+  const PairMeta* pair;
+  const double* rg;
+  const int32_t* pairs;  // pairs of this launch
+  PairRir* out;          // exact_len, max_delay, geometry flag
+  double eta_factor;     // pow(10, -eta/10), host std::pow; > 0
+};
+constexpr int kBoundMaxCap = 32768;  // longest RIR (bins) the bound pass takes
+cudaError_t launch_synth_bound(const SynthBoundArgs& a, int n_pairs, int cap, int max_order, cudaStream_t s, int nt);
 
 struct CutArgs {
   const PairMeta* pair;
@@ -130,6 +143,10 @@ struct OlaArgs {
   double* part;         // power partials: segment s, warp w of a pair at plan.part0 + s * ppb + w
   const float2* tw;
   int32_t seg = 16;     // OLA blocks per power segment (power.cuh)
+  // ola_ipc_kernel only: the FP64 RIRs (PairMeta::rir_off).  Non-null: every work item transforms
+  // its pair's truncated RIR itself and writes H / N to `spec` in the butterflies' order before
+  // its first block (no K3 launch for the span); null: `spec` was filled by K3.
+  const double* rir = nullptr;
 };
 
 struct MixArgs {
@@ -288,6 +305,7 @@ cudaError_t kernels_init();    // smem attributes
 
 constexpr int kSynthThreads = 512;
 constexpr int kSynthSlice = 10240;  // FP64 bins per K1 CTA (80 KB: two 512-thread CTAs per SM with 4 images/thread)
+constexpr int kSynthCutSlice = 4096;  // FP64 bins per K1 CTA of a truncated synthesis (synth_bound.cu)
 constexpr int kSynthBig = 22528;    // FP64 bins of the one-slice class (one 512-thread CTA per SM; + bin tags)
 size_t synth_smem_bytes(int max_order, int slice, int nt, int ipt, int fold = 0, int ht = 256);
 

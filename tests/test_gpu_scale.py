@@ -173,6 +173,8 @@ def test_render_invariance(tmp_path):
         "chunk7_dev": _worker(tmp_path, "c7d", {"RSG_CHUNK_PAIRS": "7"}, cfg, n, seed, "device"),
         "chunk50_dev": _worker(tmp_path, "c50d", {"RSG_CHUNK_PAIRS": "50"}, cfg, n, seed, "device"),
         "default_dev": _worker(tmp_path, "dd", {}, cfg, n, seed, "device"),
+        # K1 over the whole RIR instead of the prefix the cut can keep (synth_bound.cu)
+        "full_synth": _worker(tmp_path, "fs", {"RSG_SYNTH_CUT": "0"}, cfg, n, seed, "host"),
     }
     for k, r in runs.items():
         for f in ("out", "out_len", "layout"):
