@@ -296,7 +296,7 @@ def test_config1(rs, ctx, port):
     want = port.convolve_ola(x.astype(np.float64), h, n)
     assert rel_err(got, want) <= WAVE_TOL
     t = ctx.last_timing()
-    assert t["launches"] >= 2
+    assert t["launches"] >= 1  # K4 alone at N = 8192: ola_ipc_kernel transforms the RIR itself (no K3 launch)
 
 
 # ---- the batched render -------------------------------------------------------------
