@@ -2,7 +2,8 @@
 # the test-only checkers under oracle/.
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC,-O2,-ffp-contract=off
+EXTRA ?=
+NVFLAGS := $(ARCH) $(EXTRA) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC,-O2,-ffp-contract=off
 SRC := paper_1712_03439_b200/csrc
 OUT := paper_1712_03439_b200/_lib
 OBJS := $(OUT)/kernels.o $(OUT)/big.o $(OUT)/large.o $(OUT)/ola2.o $(OUT)/synth_bound.o $(OUT)/sampler.o $(OUT)/features.o $(OUT)/api.o
@@ -12,7 +13,7 @@ ADAPTER := tests/cpp/_build/adapter_test
 
 all: $(OUT)/libroomsim_gpu.so oracle adapter
 
-$(OUT)/kernels.o: $(SRC)/kernels.cu $(SRC)/kernels.cuh $(SRC)/power.cuh $(SRC)/fft.cuh $(SRC)/async.cuh
+$(OUT)/kernels.o: $(SRC)/kernels.cu $(SRC)/kernels.cuh $(SRC)/mixfin.cuh $(SRC)/power.cuh $(SRC)/fft.cuh $(SRC)/async.cuh
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/kernels.ptxas.log || (cat $(OUT)/kernels.ptxas.log; false)
 
@@ -20,7 +21,7 @@ $(OUT)/large.o: $(SRC)/large.cu $(SRC)/kernels.cuh $(SRC)/power.cuh $(SRC)/fft.c
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/large.ptxas.log || (cat $(OUT)/large.ptxas.log; false)
 
-$(OUT)/big.o: $(SRC)/big.cu $(SRC)/kernels.cuh $(SRC)/power.cuh $(SRC)/fft.cuh
+$(OUT)/big.o: $(SRC)/big.cu $(SRC)/kernels.cuh $(SRC)/mixfin.cuh $(SRC)/power.cuh $(SRC)/fft.cuh
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OUT)/big.ptxas.log || (cat $(OUT)/big.ptxas.log; false)
 
@@ -36,11 +37,11 @@ $(OUT)/sampler.o: $(SRC)/sampler.cu $(SRC)/sampler.cuh include/roomsim_gpu.h
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(OUT)/features.o: $(SRC)/features.cu $(SRC)/kernels.cuh $(SRC)/power.cuh $(SRC)/fft.cuh
+$(OUT)/features.o: $(SRC)/features.cu $(SRC)/kernels.cuh $(SRC)/mixfin.cuh $(SRC)/power.cuh $(SRC)/fft.cuh
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(OUT)/api.o: $(SRC)/api.cu $(SRC)/kernels.cuh $(SRC)/power.cuh include/roomsim_gpu.h
+$(OUT)/api.o: $(SRC)/api.cu $(SRC)/kernels.cuh $(SRC)/mixfin.cuh $(SRC)/power.cuh include/roomsim_gpu.h
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -Xcompiler -fopenmp -c $< -o $@
 

@@ -312,6 +312,7 @@ def ours(args, rank, world, local_rank):
     clocks = clk.stop()
     ms = e0.elapsed_time(e1) / args.steps
     alg_bytes = ctx.last_timing()["alg_bytes"]
+    mix_fused, mix_channels = ctx.mix_counts()
     ms_max, ola_ms_max = max_over_ranks([ms, ola_ms / args.steps])
     aud = torch.tensor([batch.audio_seconds, batch.n_pairs], device=dev, dtype=torch.float64)
     if world > 1:
@@ -530,6 +531,8 @@ def ours(args, rank, world, local_rank):
             "config": cfg, "roofline": roofline, "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
             "epoch_loop": epoch_loop, "logmel": logmel, "gpu_launches": launches, "clocks": clocks,
             "stage_ms": {k: round(v, 3) for k, v in stages.items()},
+            # output channels mixed inside the K4 launches (the last work item of a channel mixes it)
+            "mix": {"fused_channels": mix_fused, "channels": mix_channels},
         }
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -67,6 +67,10 @@ int rs_ctx_synchronize(rs_ctx* ctx);
  * bytes of that render (SURVEY.md §8d formulas). */
 int rs_ctx_last_timing(rs_ctx* ctx, double* ola_ms, double* ola_flops,
                        double* alg_bytes, int64_t* kernel_launches);
+/* Output channels of the last render mixed inside the K4 launches (the SNR-scaled mix,
+ * SPEC.md:338-356, fused into the overlap-add epilogue: the last work item of a channel
+ * mixes it) and all output channels of that render; the rest went through the mix kernel. */
+int rs_ctx_mix_counts(rs_ctx* ctx, int64_t* fused_channels, int64_t* channels);
 /* Device time (ms) of the stages of the last render (profiling on), summed over
  * the render's chunks: [0] inputs + K1 synth + K2 cut (stream A), [4] K4 OLA,
  * [5] K5 gains + K6 mix (stream B); [1..3] are 0 (the host planner and K3 run

@@ -19,6 +19,7 @@
 
 #include "../../include/roomsim_gpu.h"
 #include "kernels.cuh"
+#include "mixfin.cuh"
 #include "power.cuh"
 
 using namespace rsg;
@@ -305,6 +306,7 @@ struct rs_ctx {
   // timing of the last render
   double ola_ms = 0, ola_flops = 0, alg_bytes = 0;
   int64_t launches = 0;
+  int64_t fused_channels = 0, mixed_channels = 0;  // last render: channels mixed by the K4 epilogue / all
   // side streams: the per-size K4 launches of a chunk run concurrently (fills each
   // launch's tail with another size's CTAs)
   static constexpr int kSide = 4;
@@ -752,7 +754,7 @@ int plan_filter(std::vector<PairPlan>& plans, FilterPlan& fp) {
   fp.spec_total = fp.y_total = 0;
   for (const auto& q : plans) {
     fp.spec_total = std::max<int64_t>(fp.spec_total, q.spec_off + spec_len(q.log2n, q.nh));
-    fp.y_total = std::max<int64_t>(fp.y_total, q.y_off + q.out_len);
+    fp.y_total = std::max<int64_t>(fp.y_total, q.y_off + ((q.out_len + 3) & ~int64_t(3)));  // rows padded to whole quads
   }
   return RS_OK;
 }
@@ -798,9 +800,21 @@ int upload_on(DevBuf& b, const std::vector<T>& v, cudaStream_t st, PinnedArena* 
   return RS_OK;
 }
 
+// K4 variants whose work items run the mix epilogue (mixfin.cuh): the one-CTA-per-item kernels
+// of big.cu.  A channel with a pair on another variant is mixed by mix_kernel.
+// RSG_FUSED_MIX=0: mix_kernel mixes every channel.
+bool fin_variant(int var) { return var == kVarIp || var == kVarIpc; }
+bool fused_mix_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RSG_FUSED_MIX");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<PairPlan>& plans,
                   const PairMeta* d_pair, const double* d_rir, const float* d_signals, cudaStream_t st,
-                  PinnedArena* arena, cudaEvent_t ev_k4a, cudaEvent_t ev_k4b);
+                  PinnedArena* arena, cudaEvent_t ev_k4a, cudaEvent_t ev_k4b, const MixFin* d_fin = nullptr);
 
 template <class T>
 int upload(rs_ctx* c, DevBuf& b, const std::vector<T>& v);
@@ -808,7 +822,7 @@ int upload(rs_ctx* c, DevBuf& b, const std::vector<T>& v);
 // K3 + K4 of a planned set of pairs on stream `st`.
 int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<PairPlan>& plans,
                   const PairMeta* d_pair, const double* d_rir, const float* d_signals, cudaStream_t st,
-                  PinnedArena* arena, cudaEvent_t ev_k4a, cudaEvent_t ev_k4b) {
+                  PinnedArena* arena, cudaEvent_t ev_k4a, cudaEvent_t ev_k4b, const MixFin* d_fin) {
   RS_TRY(upload_on(fb.lists, fp.lists, st, arena));
   RS_TRY(upload_on(fb.plan, plans, st, arena));
   RS_TRY(upload_on(fb.olaitems, fp.items, st, arena));
@@ -901,7 +915,8 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
     } else if (sp.var == kVarSmall || sp.var == kVarIp || sp.var == kVarIpc) {
       OlaArgs a{fb.olaitems.as<OlaItem>() + sp.item_off, static_cast<int32_t>(sp.item_n), d_pair,
                 fb.plan.as<PairPlan>(), d_signals, fb.spec.as<float2>(), fb.y.as<float>(), d_part, c->tw[sp.l],
-                sp.seg, (sp.var == kVarIpc && !ipc_k3) ? d_rir : nullptr};
+                sp.seg, (sp.var == kVarIpc && !ipc_k3) ? d_rir : nullptr,
+                fin_variant(sp.var) ? d_fin : nullptr};
       if (sp.var == kVarIpc)
         RS_CUDA(launch_ola_ipc(sp.l + 1, a, sp.max_nh, side_for()));
       else if (sp.var == kVarIp)
@@ -991,7 +1006,7 @@ struct Chunk {
   FilterPlan fp;
   int max_order = 0, slice = 1;
   int64_t rir_total = 0;
-  DevBuf d_chan_feat;
+  DevBuf d_chan_feat, d_fin, d_chan_left, d_pair_chan, d_chan_utt2, d_chan_mic2, d_chan_out2;
   DevBuf d_utt, d_pair, d_rg, d_items, d_bound, d_rir, d_rirout, d_gain, d_power, d_flags, d_snr, d_chan_utt,
       d_chan_mic, d_chan_out, d_utt_len, d_utt_stride, d_utt_pair0, d_utt_I, d_utt_J;
   FilterBufs fb;
@@ -1012,7 +1027,7 @@ struct Chunk {
     return RS_OK;
   }
   void release() {
-    DevBuf* bufs[] = {&d_chan_feat, &d_utt, &d_pair, &d_rg, &d_items, &d_bound, &d_rir, &d_rirout, &d_gain, &d_power, &d_flags,
+    DevBuf* bufs[] = {&d_chan_feat, &d_fin, &d_chan_left, &d_pair_chan, &d_chan_utt2, &d_chan_mic2, &d_chan_out2, &d_utt, &d_pair, &d_rg, &d_items, &d_bound, &d_rir, &d_rirout, &d_gain, &d_power, &d_flags,
                       &d_snr, &d_chan_utt, &d_chan_mic, &d_chan_out, &d_utt_len, &d_utt_stride,
                       &d_utt_pair0, &d_utt_I, &d_utt_J, &fb.plan, &fb.lists, &fb.olaitems, &fb.spec,
                       &fb.y, &fb.part, &fb.units, &fb.scratch, &fb.yblk, &fb.olaitems2};
@@ -1407,21 +1422,58 @@ int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO
       ch_out.push_back(out_off[u] + j * out_stride[u]);
     }
   }
-  // pair -> source index relative to this chunk's first source (snr table)
-  std::vector<PairMeta>& pm = ch.pair;
-  (void)pm;
+  // ---- fused mix (mixfin.cuh): a channel whose pairs all run on the one-CTA-per-item K4 kernels
+  // is mixed by its last work item inside the K4 launch; the other channels by mix_kernel.
+  const int64_t n_chan = static_cast<int64_t>(ch_utt.size());
+  const bool fuse = fused_mix_enabled() && !io.d_feat && io.d_out;
+  std::vector<int32_t> pair_chan(std::max<int64_t>(ch.P, 1), -1), left(std::max<int64_t>(n_chan, 1), 0);
+  std::vector<int64_t> ch_utt2, ch_out2;  // the channels left to mix_kernel
+  std::vector<int32_t> ch_mic2;
+  {
+    std::vector<int32_t> items_of(ch.P, 0);
+    std::vector<uint8_t> ok(ch.P, 0);
+    if (fuse)
+      for (const Span& sp : ch.fp.spans)
+        if (fin_variant(sp.var))
+          for (int64_t i = sp.item_off; i < sp.item_off + sp.item_n; ++i) {
+            ++items_of[ch.fp.items[i].pair];
+            ok[ch.fp.items[i].pair] = 1;
+          }
+    int64_t cidx = 0;
+    for (int64_t lu = 0; lu < U; ++lu)
+      for (int32_t j = 0; j < uJ[lu]; ++j, ++cidx) {
+        bool all = fuse && uI[lu] >= 1 && uI[lu] <= kMixMaxI;
+        int32_t cnt = 0;
+        for (int32_t i = 0; i < uI[lu] && all; ++i) {
+          const int64_t p = pair0[lu] + static_cast<int64_t>(i) * uJ[lu] + j;
+          all = ok[p] != 0;
+          cnt += items_of[p];
+        }
+        if (all) {
+          left[cidx] = cnt;
+          for (int32_t i = 0; i < uI[lu]; ++i) pair_chan[pair0[lu] + static_cast<int64_t>(i) * uJ[lu] + j] = static_cast<int32_t>(cidx);
+        } else {
+          ch_utt2.push_back(ch_utt[cidx]);
+          ch_mic2.push_back(ch_mic[cidx]);
+          ch_out2.push_back(ch_out[cidx]);
+        }
+      }
+  }
+  const int64_t n_chan2 = static_cast<int64_t>(ch_utt2.size());
+  const bool any_fused = n_chan2 < n_chan;
+  c->fused_channels += n_chan - n_chan2;
+  c->mixed_channels += n_chan;
+  std::vector<MixFin> finv(1);
   size_t need = staged_bytes(ch.fp.lists) + staged_bytes(ch.plans) + staged_bytes(ch.fp.items) +
                 staged_bytes(ch.fp.items2) + staged_bytes(ch.fp.units) +
                 staged_bytes(snr_lin) + staged_bytes(pair0) + staged_bytes(uI) + staged_bytes(uJ) +
                 staged_bytes(ch_utt) + staged_bytes(ch_mic) + staged_bytes(ch_out) + staged_bytes(ch.ulen) +
                 staged_bytes(ustride) + 3 * (((std::max<int64_t>(ch.P, 1) * 8) + 63) & ~size_t(63)) + 256 +
-                (io.d_feat ? staged_bytes(ch_out) : 0);
+                (io.d_feat ? staged_bytes(ch_out) : 0) + staged_bytes(pair_chan) + staged_bytes(left) +
+                staged_bytes(ch_utt2) + staged_bytes(ch_mic2) + staged_bytes(ch_out2) + staged_bytes(finv);
   RS_TRY(ch.hB.reserve(need));
   ch.hB.reset();
-  if (io.h_signals) RS_CUDA(cudaStreamWaitEvent(sB, ch.ev_sig, 0));
-  RS_TRY(launch_filter(c, ch.fb, ch.fp, ch.plans, ch.d_pair.as<PairMeta>(), ch.d_rir.as<double>(), io.d_signals,
-                       sB, &ch.hB, ch.ev_k4a, ch.ev_k4b));
-  if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_mix0, sB));
+  // the mix's metadata goes up before K4: the epilogue reads it
   RS_TRY(upload_on(ch.d_snr, snr_lin, sB, &ch.hB));
   RS_TRY(upload_on(ch.d_utt_pair0, pair0, sB, &ch.hB));
   RS_TRY(upload_on(ch.d_utt_I, uI, sB, &ch.hB));
@@ -1434,16 +1486,41 @@ int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO
   RS_TRY(ch.d_gain.ensure(std::max<int64_t>(ch.P, 1) * sizeof(double)));
   RS_TRY(ch.d_power.ensure(std::max<int64_t>(ch.P, 1) * sizeof(double)));
   RS_TRY(ch.d_flags.ensure(std::max<int64_t>(ch.P, 1) * sizeof(int32_t)));
+  // (launch_filter sizes these three the same way: the pointers below stay valid)
+  RS_TRY(ch.fb.plan.ensure(std::max<size_t>(ch.plans.size(), 1) * sizeof(PairPlan)));
+  RS_TRY(ch.fb.y.ensure(std::max<int64_t>(ch.fp.y_total, 1) * sizeof(float)));
+  RS_TRY(ch.fb.part.ensure(std::max<int64_t>(ch.fp.part_total, 1) * sizeof(double)));
+  MixArgs ma{ch.d_chan_utt.as<int64_t>(), ch.d_chan_mic.as<int32_t>(), ch.d_chan_out.as<int64_t>(),
+             ch.d_utt_len.as<int64_t>(), ch.d_utt_stride.as<int64_t>(), ch.d_utt_pair0.as<int64_t>(),
+             ch.d_utt_I.as<int32_t>(), ch.d_utt_J.as<int32_t>(), ch.fb.plan.as<PairPlan>(), ch.fb.y.as<float>(),
+             ch.d_gain.as<double>(), io.d_out, 4096};
+  const MixFin* d_fin = nullptr;
+  if (any_fused) {
+    RS_TRY(upload_on(ch.d_pair_chan, pair_chan, sB, &ch.hB));
+    RS_TRY(upload_on(ch.d_chan_left, left, sB, &ch.hB));
+    finv[0] = MixFin{ch.d_chan_left.as<int32_t>(), ch.d_pair_chan.as<int32_t>(), ch.d_snr.as<double>() - s_first,
+                     ch.fb.part.as<double>(), ch.d_pair.as<PairMeta>(), ma};
+    RS_TRY(upload_on(ch.d_fin, finv, sB, &ch.hB));
+    d_fin = ch.d_fin.as<MixFin>();
+  }
+  if (io.h_signals) RS_CUDA(cudaStreamWaitEvent(sB, ch.ev_sig, 0));
+  RS_TRY(launch_filter(c, ch.fb, ch.fp, ch.plans, ch.d_pair.as<PairMeta>(), ch.d_rir.as<double>(), io.d_signals,
+                       sB, &ch.hB, ch.ev_k4a, ch.ev_k4b, d_fin));
+  if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_mix0, sB));
   RS_CUDA(cudaMemsetAsync(ch.d_flags.p, 0, std::max<int64_t>(ch.P, 1) * sizeof(int32_t), sB));
   GainArgs ga{ch.d_pair.as<PairMeta>(), ch.fb.plan.as<PairPlan>(), ch.d_utt_pair0.as<int64_t>(),
               ch.d_utt_J.as<int32_t>(), ch.fb.part.as<double>(), ch.d_snr.as<double>() - s_first,
               ch.d_gain.as<double>(), ch.d_power.as<double>(), ch.d_flags.as<int32_t>(), ch.P};
   RS_CUDA(launch_gain(ga, sB));
   c->launches += 2;
-  MixArgs ma{ch.d_chan_utt.as<int64_t>(), ch.d_chan_mic.as<int32_t>(), ch.d_chan_out.as<int64_t>(),
-             ch.d_utt_len.as<int64_t>(), ch.d_utt_stride.as<int64_t>(), ch.d_utt_pair0.as<int64_t>(),
-             ch.d_utt_I.as<int32_t>(), ch.d_utt_J.as<int32_t>(), ch.fb.plan.as<PairPlan>(), ch.fb.y.as<float>(),
-             ch.d_gain.as<double>(), io.d_out, 4096};
+  if (any_fused) {  // mix_kernel: the channels no K4 epilogue mixed
+    RS_TRY(upload_on(ch.d_chan_utt2, ch_utt2, sB, &ch.hB));
+    RS_TRY(upload_on(ch.d_chan_mic2, ch_mic2, sB, &ch.hB));
+    RS_TRY(upload_on(ch.d_chan_out2, ch_out2, sB, &ch.hB));
+    ma.chan_utt = ch.d_chan_utt2.as<int64_t>();
+    ma.chan_mic = ch.d_chan_mic2.as<int32_t>();
+    ma.chan_out = ch.d_chan_out2.as<int64_t>();
+  }
   if (io.d_feat) {  // features mode: mix + log-Mel in one kernel (features.cu)
     std::vector<int64_t> ch_feat(ch_utt.size());
     const int64_t c0 = b->mic_begin[ch.u0];  // global index of the chunk's first channel
@@ -1452,10 +1529,11 @@ int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO
     const MixFeatArgs lf{io.d_feat, ch.d_chan_feat.as<int64_t>(), c->lm_window.as<float>(), c->lm_ptr.as<int32_t>(),
                          c->lm_bin.as<int32_t>(), c->lm_w.as<float>(), c->tw[8], 1e-10f};
     RS_CUDA(launch_mix_logmel(ma, lf, static_cast<int64_t>(ch_utt.size()), max_stride, sB));
-  } else {
-    RS_CUDA(launch_mix(ma, static_cast<int64_t>(ch_utt.size()), max_stride, sB));
+    ++c->launches;
+  } else if (n_chan2 > 0) {
+    RS_CUDA(launch_mix(ma, n_chan2, max_stride, sB));
+    ++c->launches;
   }
-  ++c->launches;
   if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_mix1, sB));
   ch.h_flags = ch.hB.alloc<int32_t>(ch.P);
   ch.h_gain = ch.hB.alloc<double>(ch.P);
@@ -1546,6 +1624,7 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
   rs_render_state& R = *c->rs;
   const int64_t U = b->n_utt;
   c->launches = 0;
+  c->fused_channels = c->mixed_channels = 0;
   g_copy_launches = 0;
   const bool host_io = io.h_signals || io.h_out;
   g_kernel_copies = host_io;
@@ -1775,6 +1854,9 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
   c->stage_valid = c->profiling;
   t_last_return = std::chrono::steady_clock::now();
   if (R.tracing)
+    std::fprintf(stderr, "[trace] %lld of %lld channels mixed by the K4 epilogue\n",
+                 static_cast<long long>(c->fused_channels), static_cast<long long>(c->mixed_channels));
+  if (R.tracing)
     std::fprintf(stderr, "[trace] host return at %.2f ms\n",
                  std::chrono::duration<double, std::milli>(t_last_return - R.trace_t0).count());
   return RS_OK;
@@ -1923,6 +2005,13 @@ int rs_ctx_k4_breakdown(rs_ctx* c, int cap, int32_t* log2n, int32_t* variant, in
     if (exec_flops) exec_flops[i] = r.exec_flops;
   }
   return n;
+}
+
+int rs_ctx_mix_counts(rs_ctx* c, int64_t* fused_channels, int64_t* channels) {
+  if (!c) return fail(RS_ERR_CONFIG, "null context");
+  if (fused_channels) *fused_channels = c->fused_channels;
+  if (channels) *channels = c->mixed_channels;
+  return RS_OK;
 }
 
 int rs_ctx_last_timing(rs_ctx* c, double* ola_ms, double* ola_flops, double* alg_bytes,

@@ -32,11 +32,13 @@
 // below every access of every pass (strides S_p, the S = 1 blocks, and the pairing's
 // k -> digit-reversed slot, which moves by S_0 per k) is bank-conflict free on 64-bit
 // accesses.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
 #include "fft.cuh"
 #include "kernels.cuh"
+#include "mixfin.cuh"
 #include "power.cuh"
 
 namespace rsg {
@@ -239,7 +241,7 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
   constexpr int T = PL::T, N = 2 * M;
   constexpr int R0 = PL::radix(0), S0 = SH::stride(0);
   static_assert(S0 == T, "passes 0 (forward) and 0 (inverse): one butterfly per thread");
-  extern __shared__ __align__(16) float2 smem[];
+  extern __shared__ __align__(128) float2 smem[];
   float2* s = smem;
   float2* tws = smem + SH::SLOTS;
   // sizes up to M = 4096 also stage the pair's G and the pairing table W in smem
@@ -396,6 +398,8 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
       pw = 0.0;
     }
   }
+  // the channel's last work item mixes it (mixfin.cuh); the transform buffer is free by now
+  finish_item<T>(a.fin, it.pair, t, reinterpret_cast<unsigned char*>(smem));
 }
 
 template <int M>
@@ -480,7 +484,7 @@ __global__ void __launch_bounds__(IpcPlan<C>::T, IpcPlan<C>::MINB) ola_ipc_kerne
   static_assert(S0 == T, "passes 0 (forward) and 0 (inverse): one butterfly per thread");
   static_assert(SH::stride(PL::NP - 1) == 1 && RL == 16 && NBL >= 1, "last pass shape");
   constexpr bool DB = PL::DB;  // double-buffered carry
-  extern __shared__ __align__(16) float2 smem[];
+  extern __shared__ __align__(128) float2 smem[];
   float2* s = smem;
   float2* tws = smem + SH::SLOTS;
   float* carry = reinterpret_cast<float*>(tws + ((SH::TWN + 1) & ~1));
@@ -655,6 +659,8 @@ __global__ void __launch_bounds__(IpcPlan<C>::T, IpcPlan<C>::MINB) ola_ipc_kerne
     }
     // (the next transform's passes put barriers between these carry / smem accesses and its own)
   }
+  // the channel's last work item mixes it (mixfin.cuh); the transform buffer is free by now
+  finish_item<T>(a.fin, it.pair, t, reinterpret_cast<unsigned char*>(smem));
 }
 
 template <int C>

@@ -15,6 +15,7 @@
 
 #include "fft.cuh"
 #include "kernels.cuh"
+#include "mixfin.cuh"
 
 namespace rsg {
 namespace {
@@ -176,30 +177,24 @@ __global__ void __launch_bounds__(kFramesPerCta * PLM::T) mix_logmel_kernel(MixA
   // mix [n0, n0 + kTileBuf) into smem (mix_kernel's arithmetic), write [n0, n_out)
   for (int q = threadIdx.x; q < kTileBuf / 4; q += NT) {
     const long long n = n0 + 4 * q;
-    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-    auto add = [&](double g, float4 v) {
-      acc0 = fma(g, static_cast<double>(v.x), acc0);
-      acc1 = fma(g, static_cast<double>(v.y), acc1);
-      acc2 = fma(g, static_cast<double>(v.z), acc2);
-      acc3 = fma(g, static_cast<double>(v.w), acc3);
-    };
+    MixQuadAcc acc;
     if (n < len) {
       int i = 0;
       for (; i + 1 < Ic; i += 2) {
         const float4 va = mix_quad_f(s_row[i], s_len[i], n);
         const float4 vb = mix_quad_f(s_row[i + 1], s_len[i + 1], n);
-        add(s_gain[i], va);
-        add(s_gain[i + 1], vb);
+        acc.add(s_gain[i], va);
+        acc.add(s_gain[i + 1], vb);
       }
-      if (i < Ic) add(s_gain[i], mix_quad_f(s_row[i], s_len[i], n));
+      if (i < Ic) acc.add(s_gain[i], mix_quad_f(s_row[i], s_len[i], n));
       for (i = kFuseMaxI; i < I; ++i) {
         const long long p = pair0 + static_cast<long long>(i) * J + j;
-        add(a.gain[p], mix_quad_f(a.y + a.plan[p].y_off, a.plan[p].out_len, n));
+        acc.add(a.gain[p], mix_quad_f(a.y + a.plan[p].y_off, a.plan[p].out_len, n));
       }
     }
-    const float4 o = make_float4(static_cast<float>(acc0), n + 1 < len ? static_cast<float>(acc1) : 0.f,
-                                 n + 2 < len ? static_cast<float>(acc2) : 0.f,
-                                 n + 3 < len ? static_cast<float>(acc3) : 0.f);
+    const float4 o = make_float4(static_cast<float>(acc.a0), n + 1 < len ? static_cast<float>(acc.a1) : 0.f,
+                                 n + 2 < len ? static_cast<float>(acc.a2) : 0.f,
+                                 n + 3 < len ? static_cast<float>(acc.a3) : 0.f);
     *reinterpret_cast<float4*>(tile + 4 * q) = o;
     if (out && n < n_out) {
       if ((reinterpret_cast<uintptr_t>(out) & 15u) == 0 && n + 3 < n_out) {

@@ -15,6 +15,7 @@
 #include "async.cuh"
 #include "fft.cuh"
 #include "kernels.cuh"
+#include "mixfin.cuh"
 #include "power.cuh"
 
 #ifndef RSG_E
@@ -1078,11 +1079,8 @@ __global__ void __launch_bounds__(256) power_kernel(GainArgs a) {
   const int lane = threadIdx.x & 31;
   if (p >= a.n_pairs) return;  // warp-uniform
   const PairPlan& pl = a.plan[p];
-  const double* part = a.part + pl.part0;
-  double s = 0.0;
-  for (int k = lane; k < pl.npart; k += 32) s += part[k];
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) a.power[p] = s / static_cast<double>(pl.out_len);
+  const double P = pair_power_warp<false>(a.part + pl.part0, pl.npart, pl.out_len, lane);
+  if (lane == 0) a.power[p] = P;
 }
 
 // K5b: gains from the powers; alpha_0j = 1.
@@ -1091,19 +1089,10 @@ __global__ void gain_kernel(GainArgs a) {
   if (p >= a.n_pairs) return;
   const PairMeta& pm = a.pair[p];
   const long long p0 = a.utt_pair0[pm.utt] + pm.mic_local;  // target pair at mic j
-  const double P = a.power[p];
-  if (pm.src_local == 0) {
-    a.gain[p] = 1.0;
-    if (!(P > 0.0)) a.flags[p] |= 4;
-    return;
-  }
-  const double Pt = a.power[p0];
-  if (!(P > 0.0) || !(Pt > 0.0)) {
-    a.flags[p] |= 4;
-    a.gain[p] = 0.0;
-    return;
-  }
-  a.gain[p] = sqrt(Pt / (P * a.snr_lin[pm.src_idx]));
+  const bool target = pm.src_local == 0;
+  bool deg;
+  a.gain[p] = pair_gain(target, a.power[p], target ? 0.0 : a.power[p0], a.snr_lin[pm.src_idx], &deg);
+  if (deg) a.flags[p] |= 4;
 }
 
 cudaError_t launch_gain(const GainArgs& a, cudaStream_t s) {
@@ -1117,18 +1106,6 @@ cudaError_t launch_gain(const GainArgs& a, cudaStream_t s) {
 // K6: the mix y_j[n] = Σ_i alpha_ij (h_ij * x_i)[n], zero-padded, summed in
 // source order in FP64, stored FP32.
 // ============================================================================
-constexpr int kMixMaxI = 8;  // sources whose metadata is cached per CTA (more: read per use)
-
-// One source row's quad at n (zero past the row's end).
-__device__ __forceinline__ float4 mix_quad(const float* row, long long ol, long long n) {
-  if (n + 3 < ol) return __ldcs(reinterpret_cast<const float4*>(row + n));
-  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (n < ol) v.x = row[n];
-  if (n + 1 < ol) v.y = row[n + 1];
-  if (n + 2 < ol) v.z = row[n + 2];
-  return v;
-}
-
 __global__ void __launch_bounds__(256) mix_kernel(MixArgs a) {
   const long long ch = blockIdx.y;
   const long long u = a.chan_utt[ch];
@@ -1159,39 +1136,22 @@ __global__ void __launch_bounds__(256) mix_kernel(MixArgs a) {
   // 16-byte aligned, y_off % 4 == 0), two sources' loads in flight at a time, FP64 sums in
   // source order, one float4 store
   for (long long n = n0 + 4 * threadIdx.x; n < n1; n += 4 * blockDim.x) {
-    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-    auto add = [&](double g, float4 v) {
-      acc0 = fma(g, static_cast<double>(v.x), acc0);
-      acc1 = fma(g, static_cast<double>(v.y), acc1);
-      acc2 = fma(g, static_cast<double>(v.z), acc2);
-      acc3 = fma(g, static_cast<double>(v.w), acc3);
-    };
+    MixQuadAcc acc;
     if (n < len) {
       int i = 0;
       for (; i + 1 < Ic; i += 2) {
-        const float4 va = mix_quad(s_row[i], s_len[i], n);
-        const float4 vb = mix_quad(s_row[i + 1], s_len[i + 1], n);
-        add(s_gain[i], va);
-        add(s_gain[i + 1], vb);
+        const float4 va = mix_quad<false>(s_row[i], s_len[i], n);
+        const float4 vb = mix_quad<false>(s_row[i + 1], s_len[i + 1], n);
+        acc.add(s_gain[i], va);
+        acc.add(s_gain[i + 1], vb);
       }
-      if (i < Ic) add(s_gain[i], mix_quad(s_row[i], s_len[i], n));
+      if (i < Ic) acc.add(s_gain[i], mix_quad<false>(s_row[i], s_len[i], n));
       for (i = kMixMaxI; i < I; ++i) {  // beyond the cached sources
         const long long p = pair0 + static_cast<long long>(i) * J + j;
-        add(a.gain[p], mix_quad(a.y + a.plan[p].y_off, a.plan[p].out_len, n));
+        acc.add(a.gain[p], mix_quad<false>(a.y + a.plan[p].y_off, a.plan[p].out_len, n));
       }
     }
-    // samples in [len, stride) are the zero-filled tail (acc stays 0 there)
-    const float4 o = make_float4(static_cast<float>(acc0), n + 1 < len ? static_cast<float>(acc1) : 0.f,
-                                 n + 2 < len ? static_cast<float>(acc2) : 0.f,
-                                 n + 3 < len ? static_cast<float>(acc3) : 0.f);
-    if (out16 && n + 3 < n1) {
-      __stcs(reinterpret_cast<float4*>(out + n), o);
-    } else {
-      out[n] = o.x;
-      if (n + 1 < n1) out[n + 1] = o.y;
-      if (n + 2 < n1) out[n + 2] = o.z;
-      if (n + 3 < n1) out[n + 3] = o.w;
-    }
+    mix_store(out, out16, n, n1, len, acc);  // [len, stride): the zero-filled tail
   }
 }
 

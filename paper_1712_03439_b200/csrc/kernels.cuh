@@ -147,6 +147,9 @@ struct OlaArgs {
   // its pair's truncated RIR itself and writes H / N to `spec` in the butterflies' order before
   // its first block (no K3 launch for the span); null: `spec` was filled by K3.
   const double* rir = nullptr;
+  // ola_ip_kernel / ola_ipc_kernel: the K4 epilogue's state (mixfin.cuh) — the last work item of
+  // an output channel mixes it.  Null: mix_kernel mixes every channel.
+  const struct MixFin* fin = nullptr;
 };
 
 struct MixArgs {

@@ -180,10 +180,11 @@ class SceneBatch:
 
     @property
     def out_stride(self) -> np.ndarray:
-        """Channel stride per utterance: an upper bound on max_ij(N_x + N_h - 1)."""
+        """Channel stride per utterance: an upper bound on max_ij(N_x + N_h - 1), rounded up to
+        whole quads so every channel starts on a 16-byte boundary (float4 stores in the mix)."""
         nx_max = np.maximum.reduceat(self.sig_len, self.src_begin[:-1])
         cap = np.where(self.max_taps > 0, self.max_taps, self._lattice_bound())
-        return (nx_max + cap - 1).astype(np.int64)
+        return ((nx_max + cap - 1 + 3) // 4 * 4).astype(np.int64)
 
     def _lattice_bound(self) -> np.ndarray:
         ext = (self.image_order[:, None] + 2.0) * self.room_dims

@@ -38,7 +38,7 @@ def main():
         torch.cuda.synchronize()
         out = dout.cpu().numpy()[: b.out_total]
     np.savez(path, out=out.view(np.uint32), out_len=r.out_len, gains=r.gains, power=r.power,
-             layout=r.layout.view(np.uint8))
+             layout=r.layout.view(np.uint8), mix_counts=np.array(ctx.mix_counts(), dtype=np.int64))
     ctx.close()
 
 

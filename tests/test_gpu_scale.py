@@ -175,6 +175,8 @@ def test_render_invariance(tmp_path):
         "default_dev": _worker(tmp_path, "dd", {}, cfg, n, seed, "device"),
         # K1 over the whole RIR instead of the prefix the cut can keep (synth_bound.cu)
         "full_synth": _worker(tmp_path, "fs", {"RSG_SYNTH_CUT": "0"}, cfg, n, seed, "host"),
+        # every channel through mix_kernel instead of the K4 epilogue (mixfin.cuh)
+        "mix_kernel": _worker(tmp_path, "mk", {"RSG_FUSED_MIX": "0"}, cfg, n, seed, "device"),
     }
     for k, r in runs.items():
         for f in ("out", "out_len", "layout"):
@@ -207,6 +209,23 @@ def test_render_invariance(tmp_path):
     lay = r["layout"].view(rs.LAYOUT_DTYPE)
     compare_subset(bs, r["out"].view(np.float32), r["out_len"], lay, r["gains"], r["power"],
                    np.arange(bs.n_utt), want)
+
+
+@pytest.mark.parametrize("cfg,n,seed", [("config4", 48, 5), ("config5", 3, 9), ("config3", 40, 13)])
+def test_fused_mix_matches_mix_kernel(tmp_path, cfg, n, seed):
+    """The mix inside the K4 launches (the last work item of a channel mixes it, mixfin.cuh)
+    and mix_kernel give the same bytes; the epilogue really ran (mix_counts)."""
+    for mode in ("device", "host"):
+        fused = _worker(tmp_path, f"f{mode}", {}, cfg, n, seed, mode)
+        plain = _worker(tmp_path, f"p{mode}", {"RSG_FUSED_MIX": "0"}, cfg, n, seed, mode)
+        small = _worker(tmp_path, f"s{mode}", {"RSG_CHUNK_PAIRS": "30"}, cfg, n, seed, mode)
+        assert plain["mix_counts"][0] == 0 and plain["mix_counts"][1] > 0
+        assert fused["mix_counts"][0] > 0.5 * fused["mix_counts"][1], fused["mix_counts"]
+        for r in (plain, small):
+            for f in ("out", "out_len", "layout"):
+                assert (r[f] == fused[f]).all(), (mode, f)
+            for f in ("gains", "power"):
+                assert (r[f].view(np.uint64) == fused[f].view(np.uint64)).all(), (mode, f)
 
 
 def test_four_step_for_carries_that_do_not_fit(rs, ctx, port):
