@@ -1613,6 +1613,7 @@ void destroy_state(rs_ctx* c) {
 constexpr int64_t kChunkPairsDevice = 16384;
 constexpr int64_t kChunkPairsHost = 6144;
 constexpr int64_t kFirstChunkPairs = 4096;
+constexpr int64_t kFirstChunkPairsSmall = 1024;  // renders of fewer than 2 full chunks
 
 int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const int64_t* out_off,
                 const int64_t* out_stride, int64_t* out_len, rs_pair_layout* layout, double* gains,
@@ -1636,11 +1637,20 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
   int64_t total_pairs = 0;
   for (int64_t u = 0; u < U; ++u)
     total_pairs += (b->src_begin[u + 1] - b->src_begin[u]) * (b->mic_begin[u + 1] - b->mic_begin[u]);
-  // Device renders of fewer than 2 full chunks (e.g. one rank's share under strong scaling)
-  // still get two chunks, so the host planner of one overlaps the other's kernels.
-  const int64_t dev_chunk = total_pairs > 2 * kChunkPairsDevice
-                                ? kChunkPairsDevice
-                                : std::max<int64_t>(2048, (total_pairs + 1) / 2);
+  // Device renders open with a short chunk, so the first filter starts soon after the call (its
+  // K1 and host planning are the pipeline's fill time).  Renders of fewer than 2 full chunks
+  // (e.g. one rank's share under strong scaling) open with a shorter one and split the rest in
+  // two, so the host planner of one chunk overlaps the other's kernels.
+  static const int64_t first_env = [] {
+    const char* e = std::getenv("RSG_FIRST_CHUNK");  // tuning override (pairs; 0: none)
+    return e ? std::atoll(e) : int64_t(-1);
+  }();
+  const bool small_total = total_pairs <= 2 * kChunkPairsDevice;
+  const int64_t first_pairs = first_env >= 0 ? first_env : (small_total ? kFirstChunkPairsSmall : kFirstChunkPairs);
+  const bool open_short = !host_io && !chunk_env && first_pairs > 0 && total_pairs > 3 * first_pairs;
+  const int64_t dev_chunk = small_total
+                                ? std::max<int64_t>(2048, (total_pairs - (open_short ? first_pairs : 0) + 1) / 2)
+                                : kChunkPairsDevice;
   const int64_t chunk_pairs = chunk_env ? chunk_env : (host_io ? kChunkPairsHost : dev_chunk);
   // Host path: the last chunk_pairs are split C/2, C/4, C/4 so the pipeline drains
   // quickly (only the final chunk's filter and download follow the last upload).
@@ -1650,18 +1660,9 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
     for (int64_t u = 0; u < U; ++u)
       total += (b->src_begin[u + 1] - b->src_begin[u]) * (b->mic_begin[u + 1] - b->mic_begin[u]);
     int64_t u0 = 0, pairs = 0, done = 0;
-    // Device renders open with a short chunk, so the first filter starts soon after the
-    // call (its K1 and host planning are the pipeline's fill time).
-    static const int64_t first_env = [] {
-      const char* e = std::getenv("RSG_FIRST_CHUNK");  // tuning override (pairs; 0: none)
-      return e ? std::atoll(e) : int64_t(-1);
-    }();
-    const int64_t first_pairs = first_env >= 0 ? first_env : kFirstChunkPairs;
     auto target = [&] {
       const int64_t rem = total - done;
-      if (!host_io)
-        return done == 0 && !chunk_env && first_pairs > 0 && total > 2 * chunk_pairs ? std::min(first_pairs, chunk_pairs)
-                                                                                  : chunk_pairs;
+      if (!host_io) return done == 0 && open_short ? std::min(first_pairs, chunk_pairs) : chunk_pairs;
       if (rem > chunk_pairs) return std::min(chunk_pairs, rem - chunk_pairs);
       return rem > chunk_pairs / 4 ? std::max<int64_t>(rem / 2, chunk_pairs / 4) : rem;
     };

@@ -234,6 +234,18 @@ __device__ __forceinline__ void prefetch_l2(const void* p, long long bytes) {
   }
 }
 
+// Quads per thread per trip of the K4 epilogue's mix (mixfin.cuh): two where the kernel's launch
+// bounds leave it 128 registers per thread.
+#ifndef RSG_FIN_UN_BIG
+#define RSG_FIN_UN_BIG 2
+#endif
+#ifndef RSG_FIN_UN_SMALL
+#define RSG_FIN_UN_SMALL 1
+#endif
+__host__ __device__ constexpr int fin_un(int threads, int minb) {
+  return threads * minb <= 512 ? RSG_FIN_UN_BIG : RSG_FIN_UN_SMALL;
+}
+
 template <int M>
 __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(OlaArgs a, int ccap) {
   using PL = IpPlan<M>;
@@ -399,7 +411,7 @@ __global__ void __launch_bounds__(IpPlan<M>::T, IpPlan<M>::MINB) ola_ip_kernel(O
     }
   }
   // the channel's last work item mixes it (mixfin.cuh); the transform buffer is free by now
-  finish_item<T>(a.fin, it.pair, t, reinterpret_cast<unsigned char*>(smem));
+  finish_item<T, fin_un(T, PL::MINB)>(a.fin, it.pair, t, reinterpret_cast<unsigned char*>(smem));
 }
 
 template <int M>
@@ -660,7 +672,7 @@ __global__ void __launch_bounds__(IpcPlan<C>::T, IpcPlan<C>::MINB) ola_ipc_kerne
     // (the next transform's passes put barriers between these carry / smem accesses and its own)
   }
   // the channel's last work item mixes it (mixfin.cuh); the transform buffer is free by now
-  finish_item<T>(a.fin, it.pair, t, reinterpret_cast<unsigned char*>(smem));
+  finish_item<T, fin_un(T, PL::MINB)>(a.fin, it.pair, t, reinterpret_cast<unsigned char*>(smem));
 }
 
 template <int C>

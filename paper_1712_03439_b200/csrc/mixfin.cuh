@@ -141,35 +141,28 @@ __device__ __forceinline__ void mix_prefetch_l2(const void* p, long long bytes) 
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(static_cast<unsigned>(a1 - a0)) : "memory");
 }
 
-// One whole channel, samples [0, stride), by the T threads of a CTA.  The CTA has few warps and
-// nothing else hides its instruction latencies, so the main loop is kept to the loads, the
-// FMAs and the store: row pointers and gains live in registers, the trip's offset is uniform,
-// every source's quad is in flight at once, and thread i pulls row i into L2 two tiles ahead
-// with bulk prefetches (the rows were written long before by other SMs: HBM by now).  Trips
-// whose T quads lie inside every row take that loop; the channel's tail takes the checked path.
-// Sums in source order, as mix_kernel.
-template <bool CG, int T>
-__device__ __forceinline__ void mix_channel(const MixChan& mc, int I, float* out, long long len, long long stride,
-                                            int tid) {
-  constexpr int QT = 8;                        // trips per prefetch tile
-  constexpr long long TRIP = 4ll * T;          // samples per trip
-  const bool out16 = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
-  const int Ic = I < kMixMaxI ? I : kMixMaxI;
-  long long full = len < stride ? len : stride;  // samples inside every row
-  for (int i = 0; i < Ic; ++i) full = mc.len[i] < full ? mc.len[i] : full;
-  const int trips = static_cast<int>(full / TRIP);
-  const float4* rp[kMixMaxI];
-  mix_gain_t g[kMixMaxI];
+// Trips [0, trips) of a channel with exactly NI sources: trip `it` covers samples
+// [it UN 4T, (it + 1) UN 4T), UN quads per thread, all NI x UN loads in flight before the sums.
+// Rows are addressed as 32-bit quad indices from `ybase` (one IMAD.WIDE per load, half the
+// registers of pointers); nothing in the loop but the loads, the FMAs and the stores — the CTA
+// shares its SM with K4 CTAs that want every issue slot.
+template <bool CG, int T, int NI, int UN>
+__device__ __forceinline__ void mix_trips(const MixChan& mc, const float* ybase, float* out, bool out16, int trips,
+                                          int tid) {
+  constexpr int QT = 8 / UN;  // trips per prefetch tile (8 x 4T samples)
+  unsigned ri[NI];            // row i's quad index of this thread's first quad
+  mix_gain_t g[NI];
 #pragma unroll
-  for (int i = 0; i < kMixMaxI; ++i) {
-    rp[i] = reinterpret_cast<const float4*>(mc.row[i < Ic ? i : 0]) + tid;
-    g[i] = static_cast<mix_gain_t>(mc.gain[i < Ic ? i : 0]);
+  for (int i = 0; i < NI; ++i) {
+    ri[i] = static_cast<unsigned>((mc.row[i] - ybase) >> 2) + tid;
+    g[i] = static_cast<mix_gain_t>(mc.gain[i]);
   }
+  const float4* yq = reinterpret_cast<const float4*>(ybase);
   float4* op = reinterpret_cast<float4*>(out) + tid;
-  auto prefetch_tile = [&](int k) {  // trips [k QT, (k + 1) QT) of row tid
-    if (tid < Ic) {
-      const long long lo = k * (QT * TRIP), ol = mc.len[tid];
-      if (lo < ol) mix_prefetch_l2(mc.row[tid] + lo, 4 * (ol - lo < QT * TRIP ? ol - lo : QT * TRIP));
+  auto prefetch_tile = [&](int k) {  // samples [k 32T, (k + 1) 32T) of row tid
+    if (tid < NI) {
+      const long long lo = k * (32ll * T), ol = mc.len[tid];
+      if (lo < ol) mix_prefetch_l2(mc.row[tid] + lo, 4 * (ol - lo < 32ll * T ? ol - lo : 32ll * T));
     }
   };
   prefetch_tile(0);
@@ -177,27 +170,56 @@ __device__ __forceinline__ void mix_channel(const MixChan& mc, int I, float* out
 #pragma unroll 1
   for (int it = 0; it < trips; ++it) {
     if ((it & (QT - 1)) == 0) prefetch_tile(it / QT + 2);
-    float4 v[kMixMaxI];
+    const unsigned base = static_cast<unsigned>(it) * (UN * T);
+    float4 v[UN][NI];
 #pragma unroll
-    for (int i = 0; i < kMixMaxI; ++i)
-      if (i < Ic) v[i] = CG ? __ldcg(rp[i] + it * T) : __ldcs(rp[i] + it * T);
-    MixQuadAcc acc;
+    for (int q = 0; q < UN; ++q)
 #pragma unroll
-    for (int i = 0; i < kMixMaxI; ++i)
-      if (i < Ic) acc.add(g[i], v[i]);
-    const float4 o = make_float4(static_cast<float>(acc.a0), static_cast<float>(acc.a1),
-                                 static_cast<float>(acc.a2), static_cast<float>(acc.a3));
-    if (out16) {
-      __stcs(op + it * T, o);
-    } else {  // a channel that does not start on a 16-byte boundary
-      float* os = out + 4ll * (it * T + tid);
-      os[0] = o.x;
-      os[1] = o.y;
-      os[2] = o.z;
-      os[3] = o.w;
+      for (int i = 0; i < NI; ++i)
+        v[q][i] = CG ? __ldcg(yq + (ri[i] + base + q * T)) : __ldcs(yq + (ri[i] + base + q * T));
+#pragma unroll
+    for (int q = 0; q < UN; ++q) {
+      MixQuadAcc acc;
+#pragma unroll
+      for (int i = 0; i < NI; ++i) acc.add(g[i], v[q][i]);
+      const float4 o = make_float4(static_cast<float>(acc.a0), static_cast<float>(acc.a1),
+                                   static_cast<float>(acc.a2), static_cast<float>(acc.a3));
+      if (out16) {
+        __stcs(op + (base + q * T), o);
+      } else {  // a channel that does not start on a 16-byte boundary
+        float* os = out + 4ll * (base + q * T + tid);
+        os[0] = o.x;
+        os[1] = o.y;
+        os[2] = o.z;
+        os[3] = o.w;
+      }
     }
   }
-  for (long long n = trips * TRIP + 4ll * tid; n < stride; n += TRIP) {  // the tail, checked
+}
+
+// One whole channel, samples [0, stride), by the T threads of a CTA.  Trips whose quads lie
+// inside every row take mix_trips; the channel's tail takes the checked path.  Sums in source
+// order, as mix_kernel.  `ybase`: a 16-byte aligned address at or below every row, within 64 GB.
+template <bool CG, int T, int UN>
+__device__ __forceinline__ void mix_channel(const MixChan& mc, int I, const float* ybase, float* out, long long len,
+                                            long long stride, int tid) {
+  constexpr long long TRIP = 4ll * T * UN;  // samples per trip
+  const bool out16 = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+  const int Ic = I < kMixMaxI ? I : kMixMaxI;
+  long long full = len < stride ? len : stride;  // samples inside every row
+  for (int i = 0; i < Ic; ++i) full = mc.len[i] < full ? mc.len[i] : full;
+  const int trips = static_cast<int>(full / TRIP);
+  switch (Ic) {
+    case 1: mix_trips<CG, T, 1, UN>(mc, ybase, out, out16, trips, tid); break;
+    case 2: mix_trips<CG, T, 2, UN>(mc, ybase, out, out16, trips, tid); break;
+    case 3: mix_trips<CG, T, 3, UN>(mc, ybase, out, out16, trips, tid); break;
+    case 4: mix_trips<CG, T, 4, UN>(mc, ybase, out, out16, trips, tid); break;
+    case 5: mix_trips<CG, T, 5, UN>(mc, ybase, out, out16, trips, tid); break;
+    case 6: mix_trips<CG, T, 6, UN>(mc, ybase, out, out16, trips, tid); break;
+    case 7: mix_trips<CG, T, 7, UN>(mc, ybase, out, out16, trips, tid); break;
+    default: mix_trips<CG, T, 8, UN>(mc, ybase, out, out16, trips, tid); break;
+  }
+  for (long long n = trips * TRIP + 4ll * tid; n < stride; n += 4ll * T) {  // the tail, checked
     MixQuadAcc acc;
     if (n < len) {
 #pragma unroll 1
@@ -210,7 +232,7 @@ __device__ __forceinline__ void mix_channel(const MixChan& mc, int I, float* out
 // The channel `ch` by the T threads of the CTA whose work item finished it last.  Not inlined:
 // its registers are allocated apart from the K4 block loop's.  `smem`: the CTA's dynamic shared
 // memory (free after the block loop).
-template <int T>
+template <int T, int UN>
 __device__ __noinline__ void mix_finished_channel(const MixFin* __restrict__ finp, int ch, int t,
                                                   unsigned char* smem) {
   MixChan* mc = reinterpret_cast<MixChan*>(smem);
@@ -243,12 +265,12 @@ __device__ __noinline__ void mix_finished_channel(const MixFin* __restrict__ fin
   __syncthreads();
   if (t < I) mc->gain[t] = g;
   __syncthreads();
-  mix_channel<true, T>(*mc, I, a.out + a.chan_out[ch], a.utt_len[u], a.utt_stride[u], t);
+  mix_channel<true, T, UN>(*mc, I, a.y, a.out + a.chan_out[ch], a.utt_len[u], a.utt_stride[u], t);
 }
 
 // K4 epilogue, called by all T threads of a work item's CTA after its last store.
 // `smem`: the CTA's dynamic shared memory, 128-byte aligned (free after the block loop).
-template <int T>
+template <int T, int UN>
 __device__ __forceinline__ void finish_item(const MixFin* __restrict__ finp, int pair, int t, unsigned char* smem) {
   if (!finp) return;  // uniform over the launch
   int* flag = reinterpret_cast<int*>(smem + sizeof(MixChan));
@@ -265,7 +287,7 @@ __device__ __forceinline__ void finish_item(const MixFin* __restrict__ finp, int
   }
   __syncthreads();
   const int ch = *flag;
-  if (ch >= 0) mix_finished_channel<T>(finp, ch, t, smem);  // uniform over the CTA
+  if (ch >= 0) mix_finished_channel<T, UN>(finp, ch, t, smem);  // uniform over the CTA
 }
 
 }  // namespace rsg
