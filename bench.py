@@ -322,12 +322,19 @@ def ours(args, rank, world, local_rank):
 
     # ---- per-size K4 breakdown: one diagnostic render with the K4 launches serialized and
     # timed one by one (outside the timed region) --------------------------------------
-    k4_sizes = None
+    k4_sizes, k4_alone = None, None
     try:
         ctx.set_profiling(2)
         step()
         k4_sizes = ctx.k4_breakdown()
         ctx.set_profiling(True)
+        # and one with every channel through mix_kernel: K4 alone, the mix alone
+        ctx.set_fused_mix(0)
+        step()
+        st_plain = ctx.stage_times()
+        k4_alone = {"ola_ms": st_plain["ola"], "mix_ms": st_plain["gain_mix"],
+                    "flops": ctx.last_timing()["ola_flops"]}
+        ctx.set_fused_mix(-1)
     except AttributeError:
         pass
 
@@ -466,7 +473,7 @@ def ours(args, rank, world, local_rank):
         "frac": achieved / fp32_peak if achieved else None, "traffic": traffic,
         "traffic_unit": "DRAM bytes per step (all K4 launches)", "traffic_source": traffic_src,
         "kernel": "K4 (ola_ipc_kernel<N>, ola_ip_kernel<M>, ola_small_kernel<M>, ola2_kernel<N>, four-step stages), "
-                  "all FFT sizes of one render",
+                  "all FFT sizes of one render, with the SNR-scaled mix in the launches' epilogue",
         "ola_ms_per_step": ola_ms / args.steps,
         "alg_flops_per_step": per_step_flops,
         "alg_bytes_per_step": alg_bytes,
@@ -478,6 +485,12 @@ def ours(args, rank, world, local_rank):
                       "block size that minimises its modelled time (DESIGN.md 4: re-blocking), reported as "
                       "exec_flops / exec_frac per executed size in by_size",
         "serialized": ser,
+        "without_epilogue": None if not k4_alone else {
+            "ola_ms": k4_alone["ola_ms"], "mix_kernel_ms": k4_alone["mix_ms"],
+            "frac": k4_alone["flops"] / (k4_alone["ola_ms"] / 1e3) / 1e12 / fp32_peak if k4_alone["ola_ms"] > 0 else None,
+            "note": "one extra render with rs_ctx_set_fused_mix(0): K4 without the mix epilogue and the mix "
+                    "kernel it replaces; in the timed region the last work item of every output channel mixes "
+                    "it inside the K4 launches (mixfin.cuh), so ola_ms_per_step and frac above include the mix"},
         "by_size": k4_sizes,
         "by_size_note": "one extra render with the K4 launches serialized, each timed with CUDA events; rows "
                         "are keyed by the EXECUTED fft_size; `frac` = the rows' reference-plan flops / time / "

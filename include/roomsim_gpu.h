@@ -71,6 +71,10 @@ int rs_ctx_last_timing(rs_ctx* ctx, double* ola_ms, double* ola_flops,
  * SPEC.md:338-356, fused into the overlap-add epilogue: the last work item of a channel
  * mixes it) and all output channels of that render; the rest went through the mix kernel. */
 int rs_ctx_mix_counts(rs_ctx* ctx, int64_t* fused_channels, int64_t* channels);
+/* on = 0: every channel of this ctx's renders goes through the mix kernel; 1: the K4 epilogue
+ * mixes the channels it can (the default); -1: the process default (RSG_FUSED_MIX).  The
+ * rendered bytes are the same either way. */
+int rs_ctx_set_fused_mix(rs_ctx* ctx, int on);
 /* Device time (ms) of the stages of the last render (profiling on), summed over
  * the render's chunks: [0] inputs + K1 synth + K2 cut (stream A), [4] K4 OLA,
  * [5] K5 gains + K6 mix (stream B); [1..3] are 0 (the host planner and K3 run

@@ -306,6 +306,7 @@ struct rs_ctx {
   // timing of the last render
   double ola_ms = 0, ola_flops = 0, alg_bytes = 0;
   int64_t launches = 0;
+  int fused_mix = -1;  // rs_ctx_set_fused_mix: 1 / 0, -1 = the process default (RSG_FUSED_MIX)
   int64_t fused_channels = 0, mixed_channels = 0;  // last render: channels mixed by the K4 epilogue / all
   // side streams: the per-size K4 launches of a chunk run concurrently (fills each
   // launch's tail with another size's CTAs)
@@ -1425,7 +1426,7 @@ int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO
   // ---- fused mix (mixfin.cuh): a channel whose pairs all run on the one-CTA-per-item K4 kernels
   // is mixed by its last work item inside the K4 launch; the other channels by mix_kernel.
   const int64_t n_chan = static_cast<int64_t>(ch_utt.size());
-  const bool fuse = fused_mix_enabled() && !io.d_feat && io.d_out;
+  const bool fuse = (c->fused_mix < 0 ? fused_mix_enabled() : c->fused_mix != 0) && !io.d_feat && io.d_out;
   std::vector<int32_t> pair_chan(std::max<int64_t>(ch.P, 1), -1), left(std::max<int64_t>(n_chan, 1), 0);
   std::vector<int64_t> ch_utt2, ch_out2;  // the channels left to mix_kernel
   std::vector<int32_t> ch_mic2;
@@ -2008,6 +2009,12 @@ int rs_ctx_k4_breakdown(rs_ctx* c, int cap, int32_t* log2n, int32_t* variant, in
     if (exec_flops) exec_flops[i] = r.exec_flops;
   }
   return n;
+}
+
+int rs_ctx_set_fused_mix(rs_ctx* c, int on) {
+  if (!c) return fail(RS_ERR_CONFIG, "null context");
+  c->fused_mix = on < 0 ? -1 : (on != 0);
+  return RS_OK;
 }
 
 int rs_ctx_mix_counts(rs_ctx* c, int64_t* fused_channels, int64_t* channels) {

@@ -71,6 +71,9 @@ __device__ __forceinline__ float4 mix_quad(const float* row, long long ol, long 
 // < 4e-7 of the peak for 6 sources, against the 1e-5 bar.  (FP64 sums cost a conversion and a
 // DFMA per sample and source; the FP64 pipe issues a warp instruction every ~4 cycles per SM,
 // which bound mix_kernel — not HBM — and made a one-CTA channel mix 3x slower than its loads.)
+#ifndef RSG_FIN_AHEAD
+#define RSG_FIN_AHEAD 2  // 32-KB tiles of every row the K4 epilogue's mix keeps ahead in L2
+#endif
 #ifndef RSG_MIX_FP64
 #define RSG_MIX_FP64 0
 #endif
@@ -165,11 +168,11 @@ __device__ __forceinline__ void mix_trips(const MixChan& mc, const float* ybase,
       if (lo < ol) mix_prefetch_l2(mc.row[tid] + lo, 4 * (ol - lo < 32ll * T ? ol - lo : 32ll * T));
     }
   };
-  prefetch_tile(0);
-  prefetch_tile(1);
+#pragma unroll
+  for (int k = 0; k < RSG_FIN_AHEAD; ++k) prefetch_tile(k);
 #pragma unroll 1
   for (int it = 0; it < trips; ++it) {
-    if ((it & (QT - 1)) == 0) prefetch_tile(it / QT + 2);
+    if ((it & (QT - 1)) == 0) prefetch_tile(it / QT + RSG_FIN_AHEAD);
     const unsigned base = static_cast<unsigned>(it) * (UN * T);
     float4 v[UN][NI];
 #pragma unroll

@@ -93,7 +93,7 @@ LAYOUT_DTYPE = np.dtype([("rir_len", np.int64), ("rir_keep", np.int64), ("cutoff
 # Every symbol include/roomsim_gpu.h declares (checked by tests/test_abi.py).
 ABI_SYMBOLS = [
     "rs_last_error", "rs_version", "rs_ctx_create", "rs_ctx_destroy", "rs_ctx_set_stream",
-    "rs_ctx_synchronize", "rs_ctx_last_timing", "rs_ctx_mix_counts", "rs_ctx_stage_times", "rs_ctx_set_profiling",
+    "rs_ctx_synchronize", "rs_ctx_last_timing", "rs_ctx_mix_counts", "rs_ctx_set_fused_mix", "rs_ctx_stage_times", "rs_ctx_set_profiling",
     "rs_ctx_k4_breakdown", "rs_cost_direct",
     "rs_cost_full_fft", "rs_cost_ola", "rs_ola_block_count", "rs_plan_for", "rs_choose_plan",
     "rs_rfft_forward", "rs_rfft_inverse", "rs_synthesize_rir", "rs_truncate_rir",
@@ -139,6 +139,7 @@ def load_library() -> C.CDLL:
         "rs_ctx_synchronize": (C.c_int, [vp]),
         "rs_ctx_last_timing": (C.c_int, [vp, dp, dp, dp, C.POINTER(i64)]),
         "rs_ctx_mix_counts": (C.c_int, [vp, C.POINTER(i64), C.POINTER(i64)]),
+        "rs_ctx_set_fused_mix": (C.c_int, [vp, C.c_int]),
         "rs_ctx_set_profiling": (C.c_int, [vp, C.c_int]),
         "rs_ctx_stage_times": (C.c_int, [vp, dp, C.c_int, dp]),
         "rs_ctx_k4_breakdown": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp, vp]),
@@ -309,6 +310,10 @@ class Context:
         n = C.c_int64()
         _check(load_library().rs_ctx_last_timing(self.h, C.byref(ms), C.byref(fl), C.byref(by), C.byref(n)))
         return {"ola_ms": ms.value, "ola_flops": fl.value, "alg_bytes": by.value, "launches": n.value}
+
+    def set_fused_mix(self, on: int):
+        """1 / 0: the K4 epilogue mixes the channels it can / mix_kernel mixes all; -1: process default."""
+        _check(load_library().rs_ctx_set_fused_mix(self.h, int(on)))
 
     def mix_counts(self):
         """(channels of the last render mixed by the K4 epilogue, all its channels)."""

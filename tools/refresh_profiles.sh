@@ -18,7 +18,7 @@ timeout 600 python bench.py --utterances 512 --no-cpu-baseline > $O/${R}_bench_s
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --csv --log-file $O/${R}_launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_list.log 2>&1
 echo "launch list rc=$?"
-for k in "ola_ipc_kernel<.int.4096>" "ola_ipc_kernel<.int.8192>" "mix_kernel" \
+for k in "ola_ipc_kernel<.int.4096>" "ola_ipc_kernel<.int.8192>" \
          "rir_synth_kernel<.int.128, .int.4" "rir_bound_kernel<.int.512"; do
   n=$(echo "$k" | tr -dc "a-z0-9_")
   timeout 600 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:$k" \
