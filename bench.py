@@ -59,6 +59,8 @@ def parse(argv=None):
                     help="CPU only (gloo): spawn / shard / max-over-ranks logic without rendering")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-breakdown", action="store_true",
+                    help="skip the diagnostic renders after the timed region (per-size K4, K4 without the mix epilogue)")
     ap.add_argument("--cpu-sample-utts", type=int, default=0)
     ap.add_argument("--seed", type=int, default=4)
     return ap.parse_args(argv)
@@ -324,6 +326,8 @@ def ours(args, rank, world, local_rank):
     # timed one by one (outside the timed region) --------------------------------------
     k4_sizes, k4_alone = None, None
     try:
+        if args.no_breakdown:
+            raise AttributeError
         ctx.set_profiling(2)
         step()
         k4_sizes = ctx.k4_breakdown()

@@ -234,13 +234,15 @@ __device__ __forceinline__ void prefetch_l2(const void* p, long long bytes) {
   }
 }
 
-// Quads per thread per trip of the K4 epilogue's mix (mixfin.cuh): two where the kernel's launch
-// bounds leave it 128 registers per thread.
+// Quads per thread per trip of the K4 epilogue's mix (mixfin.cuh).  The mix loop waits on its
+// loads (long-scoreboard stalls are 2/3 of its samples), so bytes in flight are its speed: two
+// quads of every source per thread, also at 80 registers (12-16 bytes of spills in the epilogue
+// only; config 4 measured 26.9-27.1 ms vs 27.3-27.8 ms with one).
 #ifndef RSG_FIN_UN_BIG
 #define RSG_FIN_UN_BIG 2
 #endif
 #ifndef RSG_FIN_UN_SMALL
-#define RSG_FIN_UN_SMALL 1
+#define RSG_FIN_UN_SMALL 2
 #endif
 __host__ __device__ constexpr int fin_un(int threads, int minb) {
   return threads * minb <= 512 ? RSG_FIN_UN_BIG : RSG_FIN_UN_SMALL;
