@@ -340,6 +340,42 @@ def test_render_config4_subset(rs, ctx, port):
     _check_render(b, g, o)
 
 
+def test_mix_epilogue_edges(rs, ctx, port):
+    """The mix in the K4 epilogue (mixfin.cuh) at its edges: utterances with more sources than it
+    caches (10 > 8: mix_kernel mixes them), channels that do not start on 16-byte boundaries
+    (scalar stores), and the per-context toggle — same bytes with the epilogue on and off."""
+    import dataclasses
+
+    from paper_1712_03439_b200 import scenes
+
+    wide = scenes.make_batch(dataclasses.replace(scenes.spec_config4(33), num_noises=9), 3, eta_db=20.0,
+                             plan_rule=scenes.PLAN_POW2_TWICE, name="wide")
+    g, o = _render_both(rs, ctx, port, wide)
+    _check_render(wide, g, o)
+    assert ctx.mix_counts() == (0, int(np.diff(wide.mic_begin).sum()))
+
+    b = scenes.config4(n_utt=5, seed=34)
+    base = type(b)
+
+    class OddStrides(base):
+        out_stride = property(lambda self: base.out_stride.fget(self) + 1)
+
+    b.__class__ = OddStrides
+    assert (b.out_stride % 4 != 0).any()
+    g, o = _render_both(rs, ctx, port, b)
+    _check_render(b, g, o)
+    fused, total = ctx.mix_counts()
+    assert fused == total > 0
+    try:
+        ctx.set_fused_mix(0)
+        g0 = rs.render_batch(b, ctx=ctx)
+        assert ctx.mix_counts() == (0, total)
+    finally:
+        ctx.set_fused_mix(-1)
+    assert (g0.out.view(np.uint32) == g.out.view(np.uint32)).all()
+    assert (g0.gains.view(np.uint64) == g.gains.view(np.uint64)).all()
+
+
 def test_render_config2_subset(rs, ctx, port):
     from paper_1712_03439_b200 import scenes
 
