@@ -310,9 +310,11 @@ struct rs_ctx {
   int64_t fused_channels = 0, mixed_channels = 0;  // last render: channels mixed by the K4 epilogue / all
   // side streams: the per-size K4 launches of a chunk run concurrently (fills each
   // launch's tail with another size's CTAs)
-  static constexpr int kSide = 4;
-  cudaStream_t side[kSide] = {};
-  cudaEvent_t side_fork = nullptr, side_join[kSide] = {};
+  // K4 side streams: two lanes of kSide (consecutive render chunks alternate lanes, so a chunk's
+  // K4 launches do not queue behind the previous chunk's and fill its tail)
+  static constexpr int kSide = 4, kLanes = 2;
+  cudaStream_t side[kLanes * kSide] = {};
+  cudaEvent_t side_fork[kLanes] = {}, side_join[kLanes * kSide] = {};
   // log-Mel front end tables (built on first use)
   DevBuf lm_window, lm_ptr, lm_bin, lm_w, lm_tiles;
   bool lm_ready = false;
@@ -344,11 +346,11 @@ int ctx_init(rs_ctx* c) {
   RS_CUDA(cudaEventCreate(&c->ev0));
   RS_CUDA(cudaEventCreate(&c->ev1));
   for (auto& e : c->st) RS_CUDA(cudaEventCreate(&e));
-  for (int i = 0; i < rs_ctx::kSide; ++i) {
+  for (int i = 0; i < rs_ctx::kLanes * rs_ctx::kSide; ++i) {
     RS_CUDA(cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking));
     RS_CUDA(cudaEventCreateWithFlags(&c->side_join[i], cudaEventDisableTiming));
   }
-  RS_CUDA(cudaEventCreateWithFlags(&c->side_fork, cudaEventDisableTiming));
+  for (auto& e : c->side_fork) RS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   RS_CUDA(kernels_init());
   size_t total = 0;
   size_t off[kMaxLog2M + 1], off2[kOla2MaxLog2N + 1][2] = {};
@@ -815,7 +817,8 @@ bool fused_mix_enabled() {
 
 int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<PairPlan>& plans,
                   const PairMeta* d_pair, const double* d_rir, const float* d_signals, cudaStream_t st,
-                  PinnedArena* arena, cudaEvent_t ev_k4a, cudaEvent_t ev_k4b, const MixFin* d_fin = nullptr);
+                  PinnedArena* arena, cudaEvent_t ev_k4a, cudaEvent_t ev_k4b, const MixFin* d_fin = nullptr,
+                  int lane = 0);
 
 template <class T>
 int upload(rs_ctx* c, DevBuf& b, const std::vector<T>& v);
@@ -823,7 +826,7 @@ int upload(rs_ctx* c, DevBuf& b, const std::vector<T>& v);
 // K3 + K4 of a planned set of pairs on stream `st`.
 int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<PairPlan>& plans,
                   const PairMeta* d_pair, const double* d_rir, const float* d_signals, cudaStream_t st,
-                  PinnedArena* arena, cudaEvent_t ev_k4a, cudaEvent_t ev_k4b, const MixFin* d_fin) {
+                  PinnedArena* arena, cudaEvent_t ev_k4a, cudaEvent_t ev_k4b, const MixFin* d_fin, int lane) {
   RS_TRY(upload_on(fb.lists, fp.lists, st, arena));
   RS_TRY(upload_on(fb.plan, plans, st, arena));
   RS_TRY(upload_on(fb.olaitems, fp.items, st, arena));
@@ -851,16 +854,18 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
   if (ev_k4a) RS_CUDA(cudaEventRecord(ev_k4a, st));
   // fork: each size's K4 launch on its own side stream (the four-step batches share one
   // scratch, so they stay in order on one stream), joined back into `st` below
-  RS_CUDA(cudaEventRecord(c->side_fork, st));
+  cudaStream_t* side = c->side + lane * rs_ctx::kSide;
+  cudaEvent_t* side_join = c->side_join + lane * rs_ctx::kSide;
+  RS_CUDA(cudaEventRecord(c->side_fork[lane], st));
   bool used[rs_ctx::kSide] = {};
   int next_side = 0;
   std::function<cudaStream_t()> side_for = [&]() -> cudaStream_t {
     const int i = next_side++ % rs_ctx::kSide;
     if (!used[i]) {
-      cudaStreamWaitEvent(c->side[i], c->side_fork, 0);
+      cudaStreamWaitEvent(side[i], c->side_fork[lane], 0);
       used[i] = true;
     }
-    return c->side[i];
+    return side[i];
   };
   const bool serial = c->prof_level >= 2;  // diagnostic: one stream, one event pair per span
   auto span_flops = [&](const Span& sp) {
@@ -930,8 +935,8 @@ int launch_filter(rs_ctx* c, FilterBufs& fb, FilterPlan& fp, const std::vector<P
   }
   for (int i = 0; i < rs_ctx::kSide; ++i)  // join
     if (used[i]) {
-      RS_CUDA(cudaEventRecord(c->side_join[i], c->side[i]));
-      RS_CUDA(cudaStreamWaitEvent(st, c->side_join[i], 0));
+      RS_CUDA(cudaEventRecord(side_join[i], side[i]));
+      RS_CUDA(cudaStreamWaitEvent(st, side_join[i], 0));
     }
   if (ev_k4b) RS_CUDA(cudaEventRecord(ev_k4b, st));
   return RS_OK;
@@ -1049,8 +1054,9 @@ struct rs_render_state {
   std::vector<int64_t> pair_chunk;  // global pair -> chunk
   // sA: K1/K2 and RIR summaries; sB: K3-K6; sH/sD: host<->device copies of the
   // signals and outputs, so the PCIe transfers run back to back under the kernels.
-  cudaStream_t sA = nullptr, sB = nullptr, sH = nullptr, sD = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_endA = nullptr, ev_endB = nullptr, ev_endH = nullptr, ev_endD = nullptr;
+  cudaStream_t sA = nullptr, sB = nullptr, sB2 = nullptr, sH = nullptr, sD = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_endA = nullptr, ev_endB = nullptr, ev_endB2 = nullptr, ev_endH = nullptr,
+              ev_endD = nullptr;
   // RSG_TRACE=1: per-chunk timeline of the pipeline (device events + host marks) on stderr
   bool tracing = false;
   cudaEvent_t tr0 = nullptr;
@@ -1399,7 +1405,7 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
 
 // Stream B: K3, K4, K5, K6 (+ output download on the host path).
 int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO& io, const int64_t* out_off,
-                   const int64_t* out_stride, cudaStream_t sB, cudaStream_t sD) {
+                   const int64_t* out_stride, cudaStream_t sB, cudaStream_t sD, int lane) {
   const int64_t U = ch.u1 - ch.u0;
   std::vector<double> snr_lin(b->src_begin[ch.u1] - b->src_begin[ch.u0]);
   const int64_t s_first = b->src_begin[ch.u0];
@@ -1506,7 +1512,7 @@ int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO
   }
   if (io.h_signals) RS_CUDA(cudaStreamWaitEvent(sB, ch.ev_sig, 0));
   RS_TRY(launch_filter(c, ch.fb, ch.fp, ch.plans, ch.d_pair.as<PairMeta>(), ch.d_rir.as<double>(), io.d_signals,
-                       sB, &ch.hB, ch.ev_k4a, ch.ev_k4b, d_fin));
+                       sB, &ch.hB, ch.ev_k4a, ch.ev_k4b, d_fin, lane));
   if (c->profiling) RS_CUDA(cudaEventRecord(ch.ev_mix0, sB));
   RS_CUDA(cudaMemsetAsync(ch.d_flags.p, 0, std::max<int64_t>(ch.P, 1) * sizeof(int32_t), sB));
   GainArgs ga{ch.d_pair.as<PairMeta>(), ch.fb.plan.as<PairPlan>(), ch.d_utt_pair0.as<int64_t>(),
@@ -1579,9 +1585,11 @@ int state_init(rs_ctx* c) {
     RS_CUDA(cudaStreamCreateWithPriority(&c->rs->sA, cudaStreamNonBlocking, flat ? prio_lo : prio_hi));
   }
   RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sB, cudaStreamNonBlocking));
+  RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sB2, cudaStreamNonBlocking));
   RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sH, cudaStreamNonBlocking));
   RS_CUDA(cudaStreamCreateWithFlags(&c->rs->sD, cudaStreamNonBlocking));
-  cudaEvent_t* evs[] = {&c->rs->ev_start, &c->rs->ev_endA, &c->rs->ev_endB, &c->rs->ev_endH, &c->rs->ev_endD};
+  cudaEvent_t* evs[] = {&c->rs->ev_start, &c->rs->ev_endA, &c->rs->ev_endB, &c->rs->ev_endB2, &c->rs->ev_endH,
+                        &c->rs->ev_endD};
   for (auto* e : evs) RS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   return RS_OK;
 }
@@ -1589,7 +1597,7 @@ int state_init(rs_ctx* c) {
 void destroy_state(rs_ctx* c) {
   if (!c->rs) return;
   rs_render_state* r = c->rs;
-  cudaStream_t ss[] = {r->sA, r->sB, r->sH, r->sD};
+  cudaStream_t ss[] = {r->sA, r->sB, r->sB2, r->sH, r->sD};
   for (auto st : ss)
     if (st) cudaStreamSynchronize(st);
   for (auto& ch : r->chunks) ch.release();
@@ -1599,7 +1607,7 @@ void destroy_state(rs_ctx* c) {
   for (DevBuf* b : bufs) b->release();
   for (auto st : ss)
     if (st) cudaStreamDestroy(st);
-  cudaEvent_t evs[] = {r->ev_start, r->ev_endA, r->ev_endB, r->ev_endH, r->ev_endD};
+  cudaEvent_t evs[] = {r->ev_start, r->ev_endA, r->ev_endB, r->ev_endB2, r->ev_endH, r->ev_endD};
   for (auto e : evs)
     if (e) cudaEventDestroy(e);
   delete r;
@@ -1707,6 +1715,7 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
   }
   RS_CUDA(cudaStreamWaitEvent(R.sA, R.ev_start, 0));
   RS_CUDA(cudaStreamWaitEvent(R.sB, R.ev_start, 0));
+  RS_CUDA(cudaStreamWaitEvent(R.sB2, R.ev_start, 0));
   RS_CUDA(cudaStreamWaitEvent(R.sH, R.ev_start, 0));
   RS_CUDA(cudaStreamWaitEvent(R.sD, R.ev_start, 0));
   if (c->profiling) RS_CUDA(cudaEventRecord(c->st[0], c->stream));
@@ -1792,15 +1801,21 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
     R.hmark("plan done " + std::to_string(k));
     t_plan += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (status) break;
-    status = enqueue_filter(c, b, R.chunks[k], io, out_off, out_stride, R.sB, R.sD);
+    // Consecutive chunks alternate between two filter streams (and two lanes of K4 side streams):
+    // chunks share nothing, so chunk k + 1's K4 CTAs fill the tail of chunk k's launches instead
+    // of waiting behind them (RSG_ONE_LANE: one stream, the launches in chunk order).
+    static const bool one_lane = std::getenv("RSG_ONE_LANE") != nullptr;
+    const int lane = one_lane ? 0 : (k & 1);
+    cudaStream_t sBk = lane ? R.sB2 : R.sB;
+    status = enqueue_filter(c, b, R.chunks[k], io, out_off, out_stride, sBk, R.sD, lane);
     if (!status) fill_layouts(R.chunks[k]);  // host work under the chunk's kernels
     if (serial && !status && k + 1 < nch) {
-      RS_CUDA(cudaEventRecord(R.chunks[k].ev_out, R.sB));
+      RS_CUDA(cudaEventRecord(R.chunks[k].ev_out, sBk));
       RS_CUDA(cudaStreamWaitEvent(R.sA, R.chunks[k].ev_out, 0));
       status = prep_chunk(b, R.chunks[k + 1]);
       if (!status) status = enqueue_synth(c, b, R.chunks[k + 1], R.sA);
     }
-    R.mark(R.sB, "filter+mix enq-end " + std::to_string(k));
+    R.mark(sBk, "filter+mix enq-end " + std::to_string(k));
     R.mark(R.sD, "d2h done " + std::to_string(k));
     R.mark(R.sA, "sA at " + std::to_string(k));
     if (!status) status = enqueue_sig(k + kSigAhead);
@@ -1808,10 +1823,12 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
   // ---- join back into the caller's stream -------------------------------------------
   cudaEventRecord(R.ev_endA, R.sA);
   cudaEventRecord(R.ev_endB, R.sB);
+  cudaEventRecord(R.ev_endB2, R.sB2);
   cudaEventRecord(R.ev_endH, R.sH);
   cudaEventRecord(R.ev_endD, R.sD);
   cudaStreamWaitEvent(c->stream, R.ev_endA, 0);
   cudaStreamWaitEvent(c->stream, R.ev_endB, 0);
+  cudaStreamWaitEvent(c->stream, R.ev_endB2, 0);
   cudaStreamWaitEvent(c->stream, R.ev_endH, 0);
   cudaStreamWaitEvent(c->stream, R.ev_endD, 0);
   if (c->profiling) cudaEventRecord(c->st[6], c->stream);
@@ -1954,11 +1971,12 @@ int rs_ctx_destroy(rs_ctx* c) {
                     &c->scratch_a, &c->scratch_b};
   for (DevBuf* b : bufs) b->release();
   destroy_state(c);
-  for (int i = 0; i < rs_ctx::kSide; ++i) {
+  for (int i = 0; i < rs_ctx::kLanes * rs_ctx::kSide; ++i) {
     if (c->side[i]) cudaStreamDestroy(c->side[i]);
     if (c->side_join[i]) cudaEventDestroy(c->side_join[i]);
   }
-  if (c->side_fork) cudaEventDestroy(c->side_fork);
+  for (auto e : c->side_fork)
+    if (e) cudaEventDestroy(e);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
