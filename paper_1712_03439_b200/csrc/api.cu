@@ -1622,9 +1622,11 @@ void destroy_state(rs_ctx* c) {
 constexpr int64_t kChunkPairsDevice = 16384;
 constexpr int64_t kChunkPairsHost = 6144;
 constexpr int64_t kFirstChunkPairs = 4096;
-constexpr int64_t kFirstChunkPairsSmall = 0;  // renders of fewer than 2 full chunks: two equal chunks
-// (measured, 512 utterances: opening chunks of 512 / 1024 / 2048 pairs 4.59 / 4.54 / 4.48 ms vs 4.38 ms —
-// a short K4 launch underfills the GPU and the later chunks wait behind it)
+// Renders of fewer than 2 full chunks open with a quarter of their pairs and split the rest in
+// two (measured, 512 utterances = 6144 pairs, chunks alternating between the two filter streams:
+// opening chunks of 768 / 1024 / 1536 / 2048 pairs 4.38 / 4.40 / 4.16 / 4.20 ms vs 4.24 ms for two
+// equal chunks — a shorter K4 launch underfills the GPU).
+constexpr int64_t kFirstChunkDivSmall = 4;
 
 int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const int64_t* out_off,
                 const int64_t* out_stride, int64_t* out_len, rs_pair_layout* layout, double* gains,
@@ -1650,14 +1652,17 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
     total_pairs += (b->src_begin[u + 1] - b->src_begin[u]) * (b->mic_begin[u + 1] - b->mic_begin[u]);
   // Device renders open with a short chunk, so the first filter starts soon after the call (its
   // K1 and host planning are the pipeline's fill time).  Renders of fewer than 2 full chunks
-  // (e.g. one rank's share under strong scaling) are split in two equal chunks, so the host
-  // planner of one chunk overlaps the other's kernels.
+  // (e.g. one rank's share under strong scaling) open with a quarter of their pairs and split the
+  // rest in two, so the host planner of one chunk overlaps the others' kernels.
   static const int64_t first_env = [] {
     const char* e = std::getenv("RSG_FIRST_CHUNK");  // tuning override (pairs; 0: none)
     return e ? std::atoll(e) : int64_t(-1);
   }();
   const bool small_total = total_pairs <= 2 * kChunkPairsDevice;
-  const int64_t first_pairs = first_env >= 0 ? first_env : (small_total ? kFirstChunkPairsSmall : kFirstChunkPairs);
+  const int64_t first_pairs =
+      first_env >= 0 ? first_env
+                     : (small_total ? (total_pairs / kFirstChunkDivSmall >= 1024 ? total_pairs / kFirstChunkDivSmall : 0)
+                                    : kFirstChunkPairs);
   const bool open_short = !host_io && !chunk_env && first_pairs > 0 && total_pairs > 3 * first_pairs;
   const int64_t dev_chunk = small_total
                                 ? std::max<int64_t>(2048, (total_pairs - (open_short ? first_pairs : 0) + 1) / 2)
