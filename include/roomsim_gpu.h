@@ -76,8 +76,10 @@ int rs_ctx_mix_counts(rs_ctx* ctx, int64_t* fused_channels, int64_t* channels);
  * rendered bytes are the same either way. */
 int rs_ctx_set_fused_mix(rs_ctx* ctx, int on);
 /* Device time (ms) of the stages of the last render (profiling on), summed over
- * the render's chunks: [0] inputs + K1 synth + K2 cut (stream A), [4] K4 OLA,
- * [5] K5 gains + K6 mix (stream B); [1..3] are 0 (the host planner and K3 run
+ * the render's chunks: [0] inputs + K1 synth + K2 cut (stream A), [4] K4 OLA
+ * (with the mix of the channels its epilogue covers), [5] K5 gains + K6 mix of the remaining
+ * channels (filter stream; with chunks alternating between two filter streams the window
+ * also sees the wait for SMs under the next chunk's K4); [1..3] are 0 (the host planner and K3 run
  * overlapped with the other stream); host_plan_ms = host wall time of the
  * planner.  Entries are -1 when unavailable. */
 int rs_ctx_stage_times(rs_ctx* ctx, double* ms, int n, double* host_plan_ms);
