@@ -46,7 +46,7 @@ $(OUT)/api.o: $(SRC)/api.cu $(SRC)/kernels.cuh $(SRC)/mixfin.cuh $(SRC)/power.cu
 	$(NVCC) $(NVFLAGS) -Xcompiler -fopenmp -c $< -o $@
 
 $(OUT)/libroomsim_gpu.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -lgomp
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -lgomp -ldl
 
 oracle:
 	$(MAKE) -s -C oracle

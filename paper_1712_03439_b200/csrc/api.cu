@@ -17,6 +17,8 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/roomsim_gpu.h"
 #include "kernels.cuh"
 #include "mixfin.cuh"
@@ -55,6 +57,15 @@ namespace {
     int st_ = (call);             \
     if (st_ != RS_OK) return st_; \
   } while (0)
+
+// NVTX range over a host phase of the render (nsys / ncu timelines; header-only NVTX3, a no-op
+// without a profiler attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Device buffer that only grows (the ctx's arena).
 struct DevBuf {
@@ -1095,6 +1106,7 @@ int state_init(rs_ctx* c);
 
 // Host metadata of chunk k (validation with the reference's messages).
 int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
+  NvtxRange nv("roomsim: prep chunk (host metadata, K1 classes)");
   ch.items.clear();
   ch.max_order = 0; ch.slice = 1; ch.rir_total = 0;
   const int64_t U = ch.u1 - ch.u0;
@@ -1271,6 +1283,7 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
 
 // Stream A: inputs, K1, K2, RIR summary -> pinned host.
 int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, cudaStream_t sA) {
+  NvtxRange nv("roomsim: enqueue K1a / K1 / K2");
   RS_TRY(ch.init_events());
   size_t need = staged_bytes(ch.utt) + staged_bytes(ch.pair) + staged_bytes(ch.rg) + staged_bytes(ch.items) +
                 staged_bytes(ch.bound_pairs) +
@@ -1318,6 +1331,7 @@ int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, cudaStream_t sA
 
 // Host: errors in reference order and the planner (after chunk k's RIR summary).
 int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
+  NvtxRange nv("roomsim: plan chunk (wait for the RIR summary, reference planner)");
   RS_CUDA(cudaEventSynchronize(ch.ev_rir));
   ch.plans.assign(ch.P, PairPlan{});
   ch.ref.assign(ch.P, RefLayout{});
@@ -1406,6 +1420,7 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
 // Stream B: K3, K4, K5, K6 (+ output download on the host path).
 int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO& io, const int64_t* out_off,
                    const int64_t* out_stride, cudaStream_t sB, cudaStream_t sD, int lane) {
+  NvtxRange nv("roomsim: enqueue K3 / K4 + mix epilogue / K5 / K6");
   const int64_t U = ch.u1 - ch.u0;
   std::vector<double> snr_lin(b->src_begin[ch.u1] - b->src_begin[ch.u0]);
   const int64_t s_first = b->src_begin[ch.u0];
@@ -1639,6 +1654,7 @@ int render_impl(rs_ctx* c, const rs_scene_batch* b, const RenderIO& io, const in
                 const int64_t* out_stride, int64_t* out_len, rs_pair_layout* layout, double* gains,
                 double* power) {
   if (!b || b->n_utt < 0) return fail(RS_ERR_CONFIG, "invalid scene batch");
+  NvtxRange nv_render("roomsim: render_batch");
   const auto t_enter = std::chrono::steady_clock::now();
   static thread_local std::chrono::steady_clock::time_point t_last_return = t_enter;
   RS_TRY(state_init(c));
