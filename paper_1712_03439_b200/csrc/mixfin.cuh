@@ -10,7 +10,7 @@
 // its last block, makes its stores visible (__threadfence) and decrements its channel's
 // counter; the item that brings it to zero computes the channel's powers and gains and mixes
 // the channel — inside the K4 launch, on an SM whose other resident CTAs keep transforming.
-// The arithmetic is the same code K5 / K6 run (pair_power_warp, pair_gain, mix_span), so the
+// The arithmetic is the same code K5 / K6 run (pair_power_warp, pair_gain, MixQuadAcc), so the
 // bytes do not depend on which item finished last, nor on whether a channel was mixed here or
 // by mix_kernel (render invariance).
 #pragma once
