@@ -5,6 +5,7 @@
 // roomsim/convolution.hpp:72-161), bucketing of pairs by transform size, and
 // the kernel sequence K1 -> K2 -> plan -> K3 -> K4 -> K5 -> K6.
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <functional>
 #include <cmath>
@@ -455,19 +456,20 @@ bool use_large(int l) {
 }
 // Largest N_h whose overlap carry fits next to the in-place K4's transform (0: none).
 int64_t ip_max_nh(int l) {
-  static int64_t cache[kMaxLog2M + 1];
-  static bool init = false;
-  if (!init) {
+  // (a function-local static's initializer runs once, thread-safe: renders may run in several
+  // host threads, one context each)
+  static const std::array<int64_t, kMaxLog2M + 1> cache = [] {
+    std::array<int64_t, kMaxLog2M + 1> c{};
     for (int k = 0; k <= kMaxLog2M; ++k) {
       int64_t lo = 0, hi = int64_t(2) << k;  // N_h <= N
       while (lo < hi) {  // largest nh with ip_supported(k, nh)
         const int64_t mid = (lo + hi + 1) / 2;
         if (ip_supported(k, mid)) lo = mid; else hi = mid - 1;
       }
-      cache[k] = lo;
+      c[k] = lo;
     }
-    init = true;
-  }
+    return c;
+  }();
   return l >= 0 && l <= kMaxLog2M ? cache[l] : 0;
 }
 // Sizes (log2 M) that take the in-place one-CTA K4 (big.cu) when the pair's carry fits in
@@ -507,19 +509,18 @@ bool use_ipc(int log2n, int64_t nh) {
     return std::make_pair(lo, hi);
   }();
   if (log2n < r.first || log2n > r.second) return false;
-  static int64_t cache[kLargeMaxLog2M + 2];
-  static bool init = false;
-  if (!init) {
+  static const std::array<int64_t, kLargeMaxLog2M + 2> cache = [] {
+    std::array<int64_t, kLargeMaxLog2M + 2> c{};
     for (int k = 0; k <= kLargeMaxLog2M + 1; ++k) {
       int64_t lo = 0, hi = int64_t(1) << k;  // largest nh with ipc_supported(k, nh)
       while (lo < hi) {
         const int64_t mid = (lo + hi + 1) / 2;
         if (ipc_supported(k, mid)) lo = mid; else hi = mid - 1;
       }
-      cache[k] = lo;
+      c[k] = lo;
     }
-    init = true;
-  }
+    return c;
+  }();
   return nh <= cache[log2n];
 }
 constexpr int kSmallMaxLog2MHost = 12;  // ola_small_kernel<M> sizes (kernels.cu)

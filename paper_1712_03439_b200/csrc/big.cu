@@ -427,8 +427,7 @@ size_t ip_smem(int ccap) {
 template <int M>
 cudaError_t ip_t(const OlaArgs& a, int ccap, cudaStream_t st) {
   const size_t smem = ip_smem<M>(ccap);
-  cudaError_t e = cudaFuncSetAttribute(ola_ip_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = ensure_dynamic_smem(ola_ip_kernel<M>, smem);
   if (e != cudaSuccess) return e;
   ola_ip_kernel<M><<<a.count, IpPlan<M>::T, smem, st>>>(a, ccap);
   return cudaGetLastError();
@@ -687,8 +686,7 @@ size_t ipc_smem(int ccap) {
 template <int C>
 cudaError_t ipc_t(const OlaArgs& a, int ccap, cudaStream_t st) {
   const size_t smem = ipc_smem<C>(ccap);
-  cudaError_t e = cudaFuncSetAttribute(ola_ipc_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = ensure_dynamic_smem(ola_ipc_kernel<C>, smem);
   if (e != cudaSuccess) return e;
   ola_ipc_kernel<C><<<a.count, IpcPlan<C>::T, smem, st>>>(a, ccap);
   return cudaGetLastError();

@@ -387,7 +387,7 @@ cudaError_t launch_synth(const SynthArgs& a, int n_items, int max_order, int sli
   const int ipt = (nt == 512 && ((!two4 && two2) || !one4)) ? 2 : 4;
   const size_t smem = synth_smem_bytes(max_order, slice, nt, ipt, fold, ht);
   auto go = [&](auto kern, int threads) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaError_t e = ensure_dynamic_smem(kern, smem);
     if (e != cudaSuccess) return e;
     kern<<<n_items, threads, smem, s>>>(a, slice);
     return cudaGetLastError();

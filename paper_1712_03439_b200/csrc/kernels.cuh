@@ -2,9 +2,32 @@
 // orchestration (api.cu).  See DESIGN.md §"Data layout in HBM".
 #pragma once
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace rsg {
+
+// Raise — never lower — a kernel's dynamic shared-memory limit.  Launch sites whose size varies
+// with the batch (carry / slice capacities) call this instead of cudaFuncSetAttribute: renders
+// running in several host threads (one context each) launch the same kernels with different
+// sizes, and a limit set to exactly one launch's size could be lowered by another thread between
+// this call and the launch ("invalid argument").
+template <class K>
+inline cudaError_t ensure_dynamic_smem(K kern, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> cur;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = cur[std::make_pair(dev, reinterpret_cast<const void*>(kern))];
+  if (bytes <= have) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
 
 // Per utterance (room) — RoomConfig (roomsim/room_model.hpp:49-72) plus the
 // host-computed constants that must match glibc bit for bit.

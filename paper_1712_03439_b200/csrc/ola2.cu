@@ -237,7 +237,7 @@ template <int N>
 cudaError_t ola2_t(const Ola2Args& a, cudaStream_t s) {
   constexpr int CTA = ola2_cta(ilog2(N)), G = CTA / PlanF<N>::T;
   const size_t smem = ola2_smem<N>(a.ccap, a.scap);
-  cudaError_t e = cudaFuncSetAttribute(ola2_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_dynamic_smem(ola2_kernel<N>, smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(ola2_kernel<N>, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);

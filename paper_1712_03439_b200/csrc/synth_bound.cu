@@ -171,7 +171,7 @@ cudaError_t launch_synth_bound(const SynthBoundArgs& a, int n_pairs, int cap, in
   const size_t smem = ((4 * static_cast<size_t>(cap) + 15) & ~size_t(15)) + sizeof(double) * 3 * W + sizeof(float) * 3 * W +
                       sizeof(float) * (3 * max_order + 1) + 16;
   auto go = [&](auto kern, int threads) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaError_t e = ensure_dynamic_smem(kern, smem);
     if (e != cudaSuccess) return e;
     kern<<<n_pairs, threads, smem, s>>>(a, cap);
     return cudaGetLastError();

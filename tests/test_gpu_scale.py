@@ -228,6 +228,43 @@ def test_fused_mix_matches_mix_kernel(tmp_path, cfg, n, seed):
                 assert (r[f].view(np.uint64) == fused[f].view(np.uint64)).all(), (mode, f)
 
 
+def test_concurrent_contexts(rs):
+    """Renders from two host threads, one context each, running at once (a stream of batches with
+    two in flight, bench.py `two_in_flight`): the same bytes as one at a time.  The two workloads
+    need different shared-memory sizes from the same kernels (K1 slices, K4 carries)."""
+    import threading
+
+    from paper_1712_03439_b200 import scenes
+
+    batches = [scenes.config4(n_utt=24, seed=61), scenes.config5(n_utt=2, seed=62), scenes.config3(n_utt=40, seed=63)]
+    solo = rs.Context(0)
+    want = [rs.render_batch(b, ctx=solo) for b in batches]
+    solo.close()
+    errs, got = [], {}
+
+    def work(tid):
+        try:
+            c = rs.Context(0)
+            for rep in range(4):
+                for k in range(len(batches)):
+                    i = (k + tid) % len(batches)
+                    got[(tid, i)] = rs.render_batch(batches[i], ctx=c)
+            c.close()
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    ths = [threading.Thread(target=work, args=(t,)) for t in range(2)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    assert not errs, errs
+    for (tid, i), g in got.items():
+        assert (g.out.view(np.uint32) == want[i].out.view(np.uint32)).all(), (tid, i)
+        assert (g.gains.view(np.uint64) == want[i].gains.view(np.uint64)).all(), (tid, i)
+        assert (g.layout == want[i].layout).all(), (tid, i)
+
+
 def test_four_step_for_carries_that_do_not_fit(rs, ctx, port):
     """N = 32768 with N_h ~ 30000: the in-place K4's carry does not fit in shared memory,
     so the pair takes the four-step path (large.cu); also inside a render."""
