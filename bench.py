@@ -474,6 +474,19 @@ def ours(args, rank, world, local_rank):
         e1.record(stream)
         torch.cuda.synchronize(dev)
         ms_f = max_over_ranks([e0.elapsed_time(e1) / args.steps])[0]
+        # features and waveforms: the mix in the K4 epilogue, the log-Mel reading the channels back
+        wstep = lambda: roomsim.render_features(batch, device_signals_ptr=signals.data_ptr(),  # noqa: E731
+                                                feat_ptr=fused.data_ptr(), feat_off=foff,
+                                                device_out_ptr=out.data_ptr(), ctx=ctx)
+        wstep()
+        barrier()
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(args.steps):
+            wstep()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms_w = max_over_ranks([e0.elapsed_time(e1) / args.steps])[0]
         logmel = {"ms_per_step": lm_ms / args.steps, "channels": int(ch_len.size), "frames": frames,
                   "stacked_vectors": int(S.sum()),
                   "frames_per_s": frames / (lm_ms / args.steps / 1e3) if lm_ms > 0 else None,
@@ -483,7 +496,11 @@ def ours(args, rank, world, local_rank):
                       "ms_per_step": ms_f, "value": total_audio / (ms_f / 1e3), "unit": UNIT,
                       "vs_render_plus_logmel_ms": ms_max + lm_ms / args.steps,
                       "what": "rs_render_features_device: the whole render with the log-Mel computed inside the "
-                              "mix kernel from shared memory; waveforms not written (features only)"}}
+                              "mix kernel from shared memory; waveforms not written (features only)"},
+                  "render_features_with_waveforms": {
+                      "ms_per_step": ms_w, "value": total_audio / (ms_w / 1e3), "unit": UNIT,
+                      "what": "rs_render_features_device with an output buffer: waveforms mixed in the K4 "
+                              "epilogue, the log-Mel kernel reads them back; features bit-identical"}}
         del feat, fused
 
     # ---- roofline of the OLA filter kernels (K4) -------------------------------------

@@ -293,8 +293,10 @@ int rs_logmel_device(rs_ctx* ctx, const float* wave_dev, int64_t n_chan, const i
  * output tile is mixed into shared memory and the frames starting in it are featurized
  * there): rs_render_batch_device's arguments plus feat_dev / feat_off (per output channel,
  * utterance-major then mic; capacity from rs_logmel_shape(out_stride[u])).  out_dev may be
- * NULL: the waveforms are then never written to HBM.  Features are bit-identical to
- * rs_logmel_device on the rendered channels. */
+ * NULL: the waveforms are then never written to HBM (the fused kernel).  With out_dev the
+ * waveforms are mixed in the overlap-add launches' epilogue and the log-Mel reads them back
+ * (measured faster than the fused kernel when the waveforms are wanted anyway).  Features are
+ * bit-identical to rs_logmel_device on the rendered channels either way. */
 int rs_render_features_device(rs_ctx* ctx, const rs_scene_batch* batch, float* out_dev,
                               const int64_t* out_off, const int64_t* out_stride, int64_t* out_len,
                               rs_pair_layout* layout, double* gains, double* power, float* feat_dev,

@@ -2427,19 +2427,23 @@ int rs_logmel_device(rs_ctx* c, const float* wave_dev, int64_t n_chan, const int
                      const int64_t* chan_len, float* feat_dev, const int64_t* feat_off) {
   RS_TRY(check_ctx(c));
   RS_TRY(logmel_tables(c));
-  std::vector<LogMelTile> tiles;
+  // per-channel table only: the kernel derives a tile (8 frames) from its index
+  std::vector<LogMelChan> chans(static_cast<size_t>(std::max<int64_t>(n_chan, 0)) + 1);
+  int64_t n_tiles = 0;
   for (int64_t ch = 0; ch < n_chan; ++ch) {
     int64_t F, S;
     rs_logmel_shape(chan_len[ch], &F, &S);
     const int64_t used = S > 0 ? 3 * (S - 1) + 4 : 0;  // frames that reach a stacked vector
-    for (int64_t f0 = 0; f0 < used; f0 += 8)
-      tiles.push_back(LogMelTile{chan_off[ch], feat_off[ch], static_cast<int32_t>(f0),
-                                 static_cast<int32_t>(std::min<int64_t>(8, used - f0)), static_cast<int32_t>(S), 0});
+    chans[ch] = LogMelChan{chan_off[ch], feat_off[ch], static_cast<int32_t>(n_tiles), static_cast<int32_t>(S)};
+    n_tiles += (used + 7) / 8;
   }
+  if (n_tiles > INT32_MAX) return fail(RS_ERR_UNSUPPORTED, "too many log-Mel frames in one call");
+  chans[n_chan] = LogMelChan{0, 0, static_cast<int32_t>(n_tiles), 0};
   c->launches = 0;
-  if (tiles.empty()) return RS_OK;
-  RS_TRY(upload(c, c->lm_tiles, tiles));
-  LogMelArgs a{wave_dev, feat_dev, c->lm_tiles.as<LogMelTile>(), static_cast<int32_t>(tiles.size()),
+  if (n_tiles == 0) return RS_OK;
+  RS_TRY(upload(c, c->lm_tiles, chans));
+  LogMelArgs a{wave_dev, feat_dev, c->lm_tiles.as<LogMelChan>(), static_cast<int32_t>(n_chan),
+               static_cast<int32_t>(n_tiles),
                c->lm_window.as<float>(), c->lm_ptr.as<int32_t>(), c->lm_bin.as<int32_t>(), c->lm_w.as<float>(),
                c->tw[8], 1e-10f};
   if (c->profiling) RS_CUDA(cudaEventRecord(c->ev0, c->stream));
@@ -2462,6 +2466,30 @@ int rs_render_features_device(rs_ctx* c, const rs_scene_batch* b, float* out_dev
   if (!b) return fail(RS_ERR_CONFIG, "invalid scene batch");
   if (!feat_dev || !feat_off) return fail(RS_ERR_CONFIG, "features mode needs a feature buffer and offsets");
   RS_TRY(logmel_tables(c));
+  if (out_dev) {
+    // The waveforms are wanted too: they are mixed in the K4 launches' epilogue (mixfin.cuh) and
+    // the log-Mel reads them back — measured faster than the mix + log-Mel kernel, which keeps the
+    // whole mix out of the K4 launches (config 4: 26.9 + 10.9 ms vs 42.2 ms); same bytes
+    // (test_fused_mix_logmel_matches_separate).  Without an output buffer the fused kernel runs
+    // and no waveform is written.
+    RenderIO io{b->signals, out_dev, nullptr, nullptr};
+    std::vector<int64_t> len_tmp(static_cast<size_t>(std::max<int64_t>(b->n_utt, 1)));
+    int64_t* ol = out_len ? out_len : len_tmp.data();
+    RS_TRY(render_impl(c, b, io, out_off, out_stride, ol, layout, gains, power));
+    const int64_t launches = c->launches;
+    const double ola_ms = c->ola_ms;
+    std::vector<int64_t> ch_off, ch_len;
+    for (int64_t u = 0; u < b->n_utt; ++u)
+      for (int64_t j = 0; j < b->mic_begin[u + 1] - b->mic_begin[u]; ++j) {
+        ch_off.push_back(out_off[u] + j * out_stride[u]);
+        ch_len.push_back(ol[u]);
+      }
+    RS_TRY(rs_logmel_device(c, out_dev, static_cast<int64_t>(ch_off.size()), ch_off.data(), ch_len.data(), feat_dev,
+                            feat_off));
+    c->launches += launches;
+    c->ola_ms = ola_ms;
+    return RS_OK;
+  }
   RenderIO io{b->signals, out_dev, nullptr, nullptr};
   io.d_feat = feat_dev;
   io.feat_off = feat_off;

@@ -104,20 +104,40 @@ __global__ void __launch_bounds__(kFramesPerCta * PLM::T) logmel_kernel(LogMelAr
   }
   __syncthreads();
   const int g = threadIdx.x / T, t = threadIdx.x % T;
-  for (int tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
-    const LogMelTile tl = a.tiles[tile];
-    if (g >= tl.nfr) continue;  // warp-uniform
-    const int f = tl.f0 + g;
-    const float* src = a.wave + tl.wave_off + static_cast<long long>(f) * kHop;
-    frame_logmel(src, (reinterpret_cast<uintptr_t>(src) & 15u) == 0, f, tl.feat_off, tl.nstack, win, mptr, mbin,
+  // a contiguous range of tiles per CTA: the first tile's channel by a 32-ary search of the warp
+  // (the largest ch with tile_begin[ch] <= tile), the following ones by stepping forward
+  const int tile_lo = static_cast<int>(static_cast<long long>(a.n_tiles) * blockIdx.x / gridDim.x);
+  const int tile_hi = static_cast<int>(static_cast<long long>(a.n_tiles) * (blockIdx.x + 1) / gridDim.x);
+  int lo = 0;
+  {
+    int n = a.n_chan;  // tile_begin[lo] <= tile_lo < tile_begin[lo + n]
+    while (n > 1) {
+      const int step = (n + 31) / 32;
+      const int idx = lo + t * step;
+      const bool le = idx < lo + n && __ldg(&a.chans[idx].tile_begin) <= tile_lo;
+      const int k = 31 - __clz(__ballot_sync(0xffffffffu, le));  // lane 0 always holds
+      const int hi = lo + n;
+      lo += k * step;
+      n = min(step, hi - lo);
+    }
+  }
+  for (int tile = tile_lo; tile < tile_hi; ++tile) {
+    while (__ldg(&a.chans[lo + 1].tile_begin) <= tile) ++lo;  // (chans[n_chan].tile_begin = n_tiles > tile)
+    const LogMelChan chn = a.chans[lo];
+    const int f0 = 8 * (tile - chn.tile_begin);
+    const int used = chn.nstack > 0 ? 3 * (chn.nstack - 1) + 4 : 0;  // frames that reach a stacked vector
+    if (f0 + g >= used) continue;  // warp-uniform
+    const int f = f0 + g;
+    const float* src = a.wave + chn.wave_off + static_cast<long long>(f) * kHop;
+    frame_logmel(src, (reinterpret_cast<uintptr_t>(src) & 15u) == 0, f, chn.feat_off, chn.nstack, win, mptr, mbin,
                  mw, a.tw, a.log_floor, xw[g], fft[g], a.feat, t);
   }
 }
 
 // ---- mix + log-Mel in one kernel (the render's features mode) --------------------------
 // One CTA per (channel, tile of kMixTile output samples): it mixes the tile plus the
-// kFrame - 1 samples its last frames reach into (the exact arithmetic of mix_kernel:
-// FP64 accumulation in source order, stored FP32), writes the tile to the output
+// kFrame - 1 samples its last frames reach into (the arithmetic of mix_kernel, MixQuadAcc:
+// FP32 FMAs in source order), writes the tile to the output
 // channel when one is given, and computes from shared memory the log-Mel of every
 // stacked-vector frame that starts in the tile.  The waveform never has to be re-read
 // from HBM, and with no output channel it is never written at all.

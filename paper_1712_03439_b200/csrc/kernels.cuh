@@ -235,17 +235,20 @@ void ola2_fill_twiddles(int log2n, bool rev, float2* host);
 cudaError_t launch_ola2(int log2n, const Ola2Args& a, cudaStream_t s);
 
 // log-Mel front end (features.cu).
-struct LogMelTile {
-  int64_t wave_off;  // channel start in `wave`
-  int64_t feat_off;  // channel start in `feat` (stacked vectors of 512 floats)
-  int32_t f0, nfr;   // first frame of the tile, frames in the tile (<= 8)
-  int32_t nstack;    // stacked vectors of the channel
-  int32_t pad;
+// Per channel; a tile is 8 consecutive frames of one channel, tiles are numbered channel by
+// channel (tile_begin) and the kernel finds a tile's channel by a warp-wide 32-ary search — the
+// host never lists the ~10^6 tiles of a batch.
+struct LogMelChan {
+  int64_t wave_off;    // channel start in `wave`
+  int64_t feat_off;    // channel start in `feat` (stacked vectors of 512 floats)
+  int32_t tile_begin;  // first tile of the channel
+  int32_t nstack;      // stacked vectors of the channel; frames that reach one: 3 (nstack - 1) + 4
 };
 struct LogMelArgs {
   const float* wave;
   float* feat;
-  const LogMelTile* tiles;
+  const LogMelChan* chans;  // n_chan + 1 entries: the last one's tile_begin = n_tiles
+  int32_t n_chan;
   int32_t n_tiles;
   const float* window;    // [512] periodic Hann
   const int32_t* mel_ptr; // [129] CSR rows of the filterbank
