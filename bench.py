@@ -59,6 +59,9 @@ def parse(argv=None):
                     help="CPU only (gloo): spawn / shard / max-over-ranks logic without rendering")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gather", action="store_true",
+                    help="after the timed region: gather every rank's mixed outputs on rank 0 (NCCL; optional, "
+                         "not on the render path)")
     ap.add_argument("--no-breakdown", action="store_true",
                     help="skip the diagnostic renders after the timed region (per-size K4, K4 without the mix epilogue)")
     ap.add_argument("--cpu-sample-utts", type=int, default=0)
@@ -321,6 +324,27 @@ def ours(args, rank, world, local_rank):
         dist.all_reduce(aud, op=dist.ReduceOp.SUM)
     total_audio, total_pairs = float(aud[0]), int(aud[1])
     value = total_audio / (ms_max / 1e3)
+
+    # ---- optional final gather of the mixed outputs on rank 0 (north star: NCCL only here) -----
+    gather = None
+    if args.gather:
+        from paper_1712_03439_b200 import shard
+
+        res = step()
+        torch.cuda.synchronize(dev)
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        got = shard.gather_outputs(out, batch.ids, res.out_len)
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms_g = max_over_ranks([g0.elapsed_time(g1)])[0]
+        if rank == 0:
+            gather = {"ms": ms_g, "bytes": int(sum(4 * o.numel() for _, _, o in got)), "ranks": len(got),
+                      "utterances": int(sum(len(i) for i, _, _ in got)),
+                      "what": "shard.gather_outputs: every rank's output buffer, utterance ids and lengths to "
+                              "rank 0 (torch.distributed gather over NCCL), after the timed region"}
+        del got
 
     # ---- two renders in flight (steady-state stream of batches: the paper's on-the-fly data
     # generation) — a second context on its own streams and buffers renders the same batch into a
@@ -613,7 +637,7 @@ def ours(args, rank, world, local_rank):
             "stage_ms": {k: round(v, 3) for k, v in stages.items()},
             # output channels mixed inside the K4 launches (the last work item of a channel mixes it)
             "mix": {"fused_channels": mix_fused, "channels": mix_channels},
-            "two_in_flight": in_flight2,
+            "two_in_flight": in_flight2, "gather": gather,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

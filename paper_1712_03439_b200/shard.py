@@ -45,3 +45,46 @@ def shard_batch(batch, rank: int, world: int):
         return batch, np.arange(batch.n_utt)
     part = lpt_partition(predicted_work(batch), world)[rank]
     return batch.subset(part), part
+
+
+def gather_outputs(out, ids, out_len, dst: int = 0):
+    """The optional final gather (north star: "NCCL only for an optional final gather"): every
+    rank's mixed output buffer, its utterance ids and output lengths to rank `dst`, over the
+    process group's backend (NCCL on GPUs: device-to-device over NVLink; gloo on CPU).  Not on
+    the render path — ranks share nothing until here.
+
+    out: this rank's 1-D float32 tensor (device or CPU); ids / out_len: 1-D int64 arrays.
+    Returns on `dst` a list of (ids, out_len, out) per rank, `out` trimmed to the rank's size;
+    None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    ids_t = torch.as_tensor(np.asarray(ids, np.int64))
+    len_t = torch.as_tensor(np.asarray(out_len, np.int64))
+    if world == 1:
+        return [(ids_t.numpy(), len_t.numpy(), out)]
+    rank = dist.get_rank()
+    dev = out.device
+    # sizes first (buffers are padded to the largest: gather needs equal shapes)
+    sizes = torch.tensor([out.numel(), ids_t.numel()], dtype=torch.int64, device=dev)
+    all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
+    dist.all_gather(all_sizes, sizes)
+    n_out = int(max(int(s[0]) for s in all_sizes))
+    n_ids = int(max(int(s[1]) for s in all_sizes))
+    pad_out = torch.zeros(n_out, dtype=out.dtype, device=dev)
+    pad_out[: out.numel()] = out
+    meta = torch.zeros(2 * n_ids, dtype=torch.int64, device=dev)
+    meta[: ids_t.numel()] = ids_t.to(dev)
+    meta[n_ids: n_ids + len_t.numel()] = len_t.to(dev)
+    outs = [torch.empty_like(pad_out) for _ in range(world)] if rank == dst else None
+    metas = [torch.empty_like(meta) for _ in range(world)] if rank == dst else None
+    dist.gather(pad_out, outs, dst=dst)
+    dist.gather(meta, metas, dst=dst)
+    if rank != dst:
+        return None
+    res = []
+    for r in range(world):
+        no, ni = int(all_sizes[r][0]), int(all_sizes[r][1])
+        res.append((metas[r][:ni].cpu().numpy(), metas[r][n_ids: n_ids + ni].cpu().numpy(), outs[r][:no]))
+    return res

@@ -40,6 +40,22 @@ def _worker(rank, world, port, q):
         per_utt[int(u)] = [sub.channel(out, k, j, out_len[k]).copy() for j in range(J)]
     gathered = [None] * world
     dist.all_gather_object(gathered, per_utt)
+    # the optional final gather of the output buffers themselves (shard.gather_outputs)
+    got = shard.gather_outputs(torch.from_numpy(np.ascontiguousarray(out)), ids, out_len)
+    if rank == 0:
+        assert len(got) == world
+        for r, (g_ids, g_len, g_out) in enumerate(got):
+            sub_r, ids_r = shard.shard_batch(full, r, world)
+            assert (g_ids == ids_r).all()
+            if r == rank:
+                assert (g_len == out_len).all() and (g_out.numpy() == out).all()
+            for k, u in enumerate(g_ids):
+                J = int(np.diff(sub_r.mic_begin)[k])
+                for j in range(J):
+                    ch = sub_r.channel(g_out.numpy(), k, j, g_len[k])
+                    assert (ch == gathered[r][int(u)][j]).all()
+    else:
+        assert got is None
     # bench.py's timing reduction: max over ranks
     t = torch.tensor([float(rank + 1)], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
