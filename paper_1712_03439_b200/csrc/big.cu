@@ -449,6 +449,12 @@ cudaError_t ip_t(const OlaArgs& a, int ccap, cudaStream_t st) {
 // depends on the pair only, whatever the run split (render invariance).
 // Reference: convolve_ola, convolution.hpp:219-255; mean_power, audio_buffer.hpp:66-75.
 // ============================================================================
+// The product step reads the pair's H through L1 (the CTA re-reads the same 32-64 KB every
+// transform; written by this CTA before its first block, or by K3 in an earlier launch): K4
+// alone 19.7-20.1 -> 19.4-19.5 ms per config-4 render against L2-only loads.
+#ifndef RSG_IPC_H_L1
+#define RSG_IPC_H_L1 1
+#endif
 #ifndef RSG_IPC_MINB_4096
 #define RSG_IPC_MINB_4096 3
 #endif
@@ -610,7 +616,13 @@ __global__ void __launch_bounds__(IpcPlan<C>::T, IpcPlan<C>::MINB) ola_ipc_kerne
       for (int r = 0; r < RL; ++r) v[r] = s[pb + ip_off<PL, RL, 1, C>(r)];
       Dft<RL, false>::run(v);
 #pragma unroll
-      for (int r = 0; r < RL; ++r) v[r] = c_mul(v[r], __ldcg(Gp + r * (C / RL) + u));
+      for (int r = 0; r < RL; ++r) {
+#if RSG_IPC_H_L1
+        v[r] = c_mul(v[r], Gp[r * (C / RL) + u]);  // through L1: the CTA re-reads its pair's H every trip
+#else
+        v[r] = c_mul(v[r], __ldcg(Gp + r * (C / RL) + u));
+#endif
+      }
       Dft<RL, true>::run(v);
 #pragma unroll
       for (int r = 0; r < RL; ++r) s[pb + ip_off<PL, RL, 1, C>(r)] = v[r];
