@@ -3,7 +3,8 @@
 // host-computed constants that must match glibc (r^g, 10^(-eta/10),
 // 10^(snr/10)), the FFT-size planner (an exact mirror of
 // roomsim/convolution.hpp:72-161), bucketing of pairs by transform size, and
-// the kernel sequence K1 -> K2 -> plan -> K3 -> K4 -> K5 -> K6.
+// the kernel sequence K1a -> K1 -> K2 -> plan -> K3 -> K4 (with the mix in its epilogue,
+// mixfin.cuh) -> K5 -> K6 (the channels the epilogue does not cover).
 #include <algorithm>
 #include <array>
 #include <chrono>
@@ -988,9 +989,10 @@ int finish_timing(rs_ctx* c) {
 // Utterances are processed in chunks.  Stream A runs chunk k's input upload,
 // K1 (synth) and K2 (cut) and returns the per-pair RIR summary to pinned host
 // memory; the host plans chunk k (reference planner) while the GPU is busy
-// with chunk k-1's filter on stream B; stream B then runs K3, K4, K5, K6 and
-// the output download of chunk k.  Chunks are independent (utterances share
-// nothing), so results do not depend on the chunking.
+// with chunk k-1's filter on a filter stream, which then runs K3, K4 (the last
+// work item of an output channel mixes it), K5, K6 for the channels K4 left,
+// and the output download of chunk k.  Chunks are independent (utterances
+// share nothing), so results do not depend on the chunking.
 struct RenderIO {
   const float* d_signals;  // device signals (sig_off indexes them)
   float* d_out;            // device output base (out_off indexes it); null: features only
@@ -1064,7 +1066,7 @@ struct rs_render_state {
   FilterBufs conv;                  // single-pair convolve path
   std::vector<Chunk> chunks;
   std::vector<int64_t> pair_chunk;  // global pair -> chunk
-  // sA: K1/K2 and RIR summaries; sB: K3-K6; sH/sD: host<->device copies of the
+  // sA: K1/K2 and RIR summaries; sB / sB2: K3-K6 (the filter streams); sH/sD: host<->device copies of the
   // signals and outputs, so the PCIe transfers run back to back under the kernels.
   cudaStream_t sA = nullptr, sB = nullptr, sB2 = nullptr, sH = nullptr, sD = nullptr;
   cudaEvent_t ev_start = nullptr, ev_endA = nullptr, ev_endB = nullptr, ev_endB2 = nullptr, ev_endH = nullptr,
@@ -1395,7 +1397,7 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
     pl.spec_off = spec_off;
     pl.y_off = y_off;
     spec_off += spec_len(pl.log2n, pl.nh);
-    y_off += (pl.out_len + 3) & ~int64_t(3);  // 16-byte aligned rows: K6 reads float4
+    y_off += (pl.out_len + 3) & ~int64_t(3);  // 16-byte aligned rows: the mix reads float4
     int64_t& ul = ch.ulen[ch.pair[p].utt];
     ul = std::max(ul, pl.out_len);
   }
@@ -1418,7 +1420,7 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
   return plan_filter(ch.plans, ch.fp);
 }
 
-// Stream B: K3, K4, K5, K6 (+ output download on the host path).
+// Filter stream: K3, K4 + mix epilogue, K5, K6 (+ output download on the host path).
 int enqueue_filter(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, const RenderIO& io, const int64_t* out_off,
                    const int64_t* out_stride, cudaStream_t sB, cudaStream_t sD, int lane) {
   NvtxRange nv("roomsim: enqueue K3 / K4 + mix epilogue / K5 / K6");

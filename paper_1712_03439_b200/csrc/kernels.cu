@@ -6,7 +6,7 @@
 //   K4 ola_small_kernel     the OLA block loop + Σy^2                 convolution.hpp:242-253,
 //                                                                     audio_buffer.hpp:66-75
 //   K5 gain_kernel          SPEC compute_gain
-//   K6 mix_kernel           SPEC render sum
+//   K6 mix_kernel           SPEC render sum (channels K4's epilogue leaves)
 //   rfft_*_kernel           RealFftEngine seam                        fft.hpp:38-49
 #include <cmath>
 #include <cstdio>
@@ -1104,7 +1104,9 @@ cudaError_t launch_gain(const GainArgs& a, cudaStream_t s) {
 
 // ============================================================================
 // K6: the mix y_j[n] = Σ_i alpha_ij (h_ij * x_i)[n], zero-padded, summed in
-// source order in FP64, stored FP32.
+// source order by FP32 FMAs (MixQuadAcc, mixfin.cuh) — for the
+// channels the K4 epilogue does not mix (a pair on a K4 variant without it, more than
+// 8 sources, RSG_FUSED_MIX=0); the epilogue runs the same arithmetic.
 // ============================================================================
 __global__ void __launch_bounds__(256) mix_kernel(MixArgs a) {
   const long long ch = blockIdx.y;
