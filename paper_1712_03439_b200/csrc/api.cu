@@ -1241,7 +1241,11 @@ int prep_chunk(const rs_scene_batch* b, Chunk& ch) {
     int small = K <= 12 ? 1 : 0;  // measured crossover of the 128- and 512-thread K1
     if (b->eta_db > 0.0 && !cut_off && cap <= kBoundMaxCap) {
       static const int cut_slice = [] { const char* e = std::getenv("RSG_CUT_SLICE"); return e ? std::atoi(e) : kSynthCutSlice; }();
-      static const int cut_small_k = [] { const char* e = std::getenv("RSG_CUT_SMALL_K"); return e ? std::atoi(e) : 40; }();
+      // largest K on the 128-thread exact kernel: 40 in a full chunk (the best K1 + K1a throughput);
+      // 12 in a small chunk, whose K1 launches do not fill the GPU — the launch then lasts as long
+      // as its longest CTA, and 512 threads shorten that (512 utterances: K1 windows 2.2 -> 1.7 ms)
+      static const int cut_small_k_env = [] { const char* e = std::getenv("RSG_CUT_SMALL_K"); return e ? std::atoi(e) : -1; }();
+      const int cut_small_k = cut_small_k_env >= 0 ? cut_small_k_env : (ch.P < 8192 ? 12 : 40);
       static const int bound_small_k = [] { const char* e = std::getenv("RSG_BOUND_SMALL_K"); return e ? std::atoi(e) : 6; }();
       int bc = 0;
       while (cap > kBoundCap[bc]) ++bc;
