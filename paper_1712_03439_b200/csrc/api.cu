@@ -1339,7 +1339,11 @@ int enqueue_synth(rs_ctx* c, const rs_scene_batch* b, Chunk& ch, cudaStream_t sA
 // Host: errors in reference order and the planner (after chunk k's RIR summary).
 int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
   NvtxRange nv("roomsim: plan chunk (wait for the RIR summary, reference planner)");
+  const auto t_wait0 = std::chrono::steady_clock::now();
   RS_CUDA(cudaEventSynchronize(ch.ev_rir));
+  if (std::getenv("RSG_TRACE"))
+    std::fprintf(stderr, "[trace] chunk of %lld pairs waited %.3f ms for its RIR summary\n", static_cast<long long>(ch.P),
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_wait0).count());
   ch.plans.assign(ch.P, PairPlan{});
   ch.ref.assign(ch.P, RefLayout{});
   ch.fp.alg.assign(ch.P, 0.0);
@@ -1353,9 +1357,13 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
       if (ch.utt_err[next_utt]) return fail(ch.utt_err[next_utt], ch.utt_msg[next_utt]);
     return RS_OK;
   };
-  for (int64_t p = 0; p < ch.P; ++p) {
-    RS_TRY(utt_check(ch.pair[p].utt + 1));
-    if (ch.place_err[p]) return fail(ch.place_err[p], ch.place_msg[p]);
+  // Per pair, on the host threads (a small render's first plan is on its critical path: ~160 ns
+  // per pair serially): the pair's own checks in the reference's order and its plans, everything
+  // but the offsets.  A failing pair records its status and message (fail() writes the worker
+  // thread's g_err); the serial pass below reports the first error in utterance / pair order.
+  std::vector<int> pair_err(ch.P, RS_OK);
+  std::vector<std::string> pair_msg(ch.P);
+  auto plan_pair = [&](int64_t p) -> int {
     const PairRir& r = ch.h_rir[p];
     if (r.flags & 1) return fail(RS_ERR_GEOMETRY, "microphone coincides with an image source");
     if (r.flags & 8) return fail(RS_ERR_CUDA, "internal: device RIR length exceeds the host bound");
@@ -1398,6 +1406,22 @@ int plan_chunk(const rs_scene_batch* b, Chunk& ch, const int64_t* out_stride) {
     pl.L = static_cast<int64_t>(n - nh + 1);
     pl.B = static_cast<int64_t>(block_count(nx, nh, n));
     pl.out_len = static_cast<int64_t>(nx + nh - 1);
+    return RS_OK;
+  };
+  constexpr int64_t kPlanBlock = 256;  // pairs per parallel iteration
+  host_parallel_for((ch.P + kPlanBlock - 1) / kPlanBlock, [&](int64_t blk) {
+    const int64_t hi = std::min<int64_t>(ch.P, (blk + 1) * kPlanBlock);
+    for (int64_t p = blk * kPlanBlock; p < hi; ++p) {
+      if (ch.place_err[p]) continue;  // reported below; its RIR summary is not meaningful
+      pair_err[p] = plan_pair(p);
+      if (pair_err[p]) pair_msg[p] = g_err;  // g_err is thread-local
+    }
+  }, 2);
+  for (int64_t p = 0; p < ch.P; ++p) {  // serial: errors in order, offsets
+    RS_TRY(utt_check(ch.pair[p].utt + 1));
+    if (ch.place_err[p]) return fail(ch.place_err[p], ch.place_msg[p]);
+    if (pair_err[p]) return fail(pair_err[p], pair_msg[p]);
+    PairPlan& pl = ch.plans[p];
     pl.spec_off = spec_off;
     pl.y_off = y_off;
     spec_off += spec_len(pl.log2n, pl.nh);
